@@ -1,0 +1,176 @@
+/*
+ * xmc_head.h -- C ABI of the B200-native ELMO extreme-classification head.
+ *
+ * Drop-in boundary for the reference's hot path (lpxmc, pure Python/numpy):
+ * every entry point below replaces one reference function, cited as
+ * /root/reference/pkg/src/lpxmc/<file>:<line>.  Plain pointers and sizes only;
+ * device pointers are CUDA global-memory addresses, `stream` is a cudaStream_t.
+ * The library never frees caller memory; the caller (the Python host module,
+ * via torch) owns W, X, positives, outputs and the workspace.
+ *
+ * Error convention (mirrors the reference's exceptions, head.py / formats.py /
+ * optimizers.py): every call returns an xmc_status; xmc_last_error() gives a
+ * message.  Device-detected errors (non-finite input/gradient, sample index
+ * out of range) are latched in the handle and reported by xmc_head_check()
+ * or by the next call, and make every later kernel of the step a no-op.
+ */
+#ifndef XMC_HEAD_H_
+#define XMC_HEAD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  XMC_OK = 0,
+  XMC_ERR_ARG = 1,         /* ValueError: bad config / argument     */
+  XMC_ERR_SHAPE = 2,       /* ValueError: dimension mismatch        */
+  XMC_ERR_NONFINITE = 3,   /* ValueError: non-finite input/gradient */
+  XMC_ERR_INDEX = 4,       /* IndexError: sample index out of range */
+  XMC_ERR_LABEL = 5,       /* ValueError: label outside chunk range */
+  XMC_ERR_CUDA = 6,        /* RuntimeError: CUDA failure            */
+  XMC_ERR_UNSUPPORTED = 7, /* NotImplementedError                   */
+  XMC_ERR_CAPACITY = 8     /* workspace too small for this call     */
+} xmc_status;
+
+/* Storage / grid formats (formats.py:139-143).  Native storage: fp32 = 4 B,
+ * bf16 = 2 B (torch.bfloat16 bits), e4m3 = 1 B (float8_e4m3fn bits, identical
+ * to encode_grid_bits, head.py:317-338), e5m2 = 1 B. */
+typedef enum { XMC_FMT_FP32 = 0, XMC_FMT_BF16 = 1, XMC_FMT_FP16 = 2, XMC_FMT_E4M3 = 3, XMC_FMT_E5M2 = 4 } xmc_fmt;
+
+/* SgdSrConfig.rounding (optimizers.py:28-41).  SR_EXACT draws u from the
+ * reference's splitmix64 keyed generator (rng.py:36-57) and compares in fp64
+ * exactly like round_stochastic (formats.py:209-225): bit-identical decisions.
+ * SR_FAST uses Philox4x32-10 bits with the hardware cvt.rs conversion. */
+typedef enum { XMC_ROUND_NEAREST = 0, XMC_ROUND_SR_EXACT = 1, XMC_ROUND_SR_FAST = 2 } xmc_rounding;
+
+/* Head geometry: ChunkedHead (head.py:69-112) restricted to one rank's label
+ * shard [label_offset, label_offset + num_labels_local) of num_labels_global. */
+typedef struct {
+  int64_t num_labels_global; /* L                                        */
+  int64_t label_offset;      /* first global label owned by this rank     */
+  int64_t num_labels_local;  /* labels owned by this rank                 */
+  int32_t dim;               /* d (multiple of 128 for e4m3, 64 for bf16) */
+  int32_t fmt;               /* xmc_fmt of W: XMC_FMT_E4M3 or XMC_FMT_BF16 */
+  int32_t num_chunks;        /* k: chunks = partition(num_labels_local, k) (head.py:51-57) */
+  int32_t max_batch;         /* B capacity of the workspace               */
+  int64_t max_positives;     /* nnz capacity of the workspace             */
+  int32_t num_sms;           /* persistent-grid size (0 = device SM count)*/
+  int32_t reserved;
+} xmc_head_desc;
+
+typedef struct xmc_head* xmc_head_t;
+
+/* Per-step hyper-parameters (SgdSrConfig + RoundingRng + step). */
+typedef struct {
+  float lr;            /* > 0                                   */
+  float weight_decay;  /* >= 0                                  */
+  int32_t rounding;    /* xmc_rounding                          */
+  int32_t reserved;
+  uint64_t seed;       /* RoundingRng(seed)                     */
+  uint64_t step;       /* step index keying the draws           */
+  uint64_t tensor_id;  /* ChunkedHead.tensor_id (HEAD_WEIGHTS_TAG) */
+} xmc_step_args;
+
+const char* xmc_last_error(void);
+const char* xmc_version(void);
+
+/* Workspace bytes needed for `desc` (G chunk buffer, Xq/Xq^T, grad_X partials,
+ * positive lists, status words). */
+xmc_status xmc_head_workspace_size(const xmc_head_desc* desc, size_t* bytes);
+
+/* Bind a handle to a device workspace of >= workspace_size bytes. */
+xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace, size_t workspace_bytes,
+                           xmc_head_t* out);
+xmc_status xmc_head_destroy(xmc_head_t h);
+
+/* head_update (head.py:254-298): one full step over all chunks of this shard.
+ *   W          device, num_labels_local x dim in desc.fmt, updated in place
+ *   X          device fp32, B x dim (rounded once to the head grid, head.py:265)
+ *   pos_sample / pos_label: device int32 COO of positives, nnz entries, any
+ *              order; labels are GLOBAL ids, those outside this shard are
+ *              ignored (as the reference ignores labels outside every chunk)
+ *   grad_x     device fp32 B x dim: the (shard-partial) input gradient,
+ *              overwritten (head.py:266, 290)
+ *   stats      device fp32[2] or NULL: [0] = sum |G| of the step, [1] unused
+ */
+xmc_status xmc_head_step(xmc_head_t h, void* W, const float* X, int32_t B, const int32_t* pos_sample,
+                         const int32_t* pos_label, int64_t nnz, const xmc_step_args* args,
+                         float* grad_x, float* stats, void* stream);
+
+/* Synchronise `stream` and report a latched device error (and clear it). */
+xmc_status xmc_head_check(xmc_head_t h, void* stream);
+
+/* ---- unfused pieces, for parity isolation (same kernels as the step) ---- */
+
+/* head_forward_logits (head.py:164-178): logits[r][s] = sum_c W[row0+r][c] Xq[s][c],
+ * for local rows [row0, row1), fp32 out with leading dimension ld (>= B).
+ * Also ChunkedHead.scores (head.py:109-112) transposed. */
+xmc_status xmc_head_logits(xmc_head_t h, const void* W, const float* X, int32_t B, int64_t row0,
+                           int64_t row1, float* logits, int64_t ld, void* stream);
+
+/* logit_gradient (head.py:181-196): G = clip(sigmoid(logits)) - Y, elementwise fp32.
+ * Labels are chunk-relative GLOBAL ids in [chunk_start, chunk_start + rows). */
+xmc_status xmc_logit_gradient(const float* logits, int64_t rows, int32_t B, int64_t ld,
+                              const int32_t* pos_sample, const int32_t* pos_label, int64_t nnz,
+                              int64_t chunk_start, float* G, void* stream);
+
+/* input_gradient_accumulate (head.py:199-209) and/or fused_weight_update
+ * (head.py:212-251) on local rows [row0, row1) from an fp32 G (rows x B, ld):
+ * G is rounded to the backward operand format (e4m3 x 2^8 or bf16) and run
+ * through the same tcgen05 kernel as the step.  acc (B x dim fp32) += when
+ * accumulate_gx != 0; W updated in place when update != 0. */
+xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, int64_t ld, const float* X,
+                             int32_t B, int64_t row0, int64_t row1, float* acc, int32_t accumulate_gx,
+                             int32_t update, const xmc_step_args* args, void* stream);
+
+/* ---- elementwise numeric core (formats.py / optimizers.py), bit-exact ---- */
+
+/* Grid of an emulated (exp_bits, man_bits) format, formats.py:49-137.
+ * extended_range < 0 selects the reference default (e4m3 only). */
+typedef struct {
+  int32_t exp_bits;
+  int32_t man_bits;
+  int32_t extended_range;
+  int32_t reserved;
+} xmc_grid;
+
+/* round_nearest (formats.py:197-206): out[i] = RTN(x[i]) as fp32 on-grid values. */
+xmc_status xmc_round_nearest(xmc_grid g, const float* x, float* out, int64_t n, void* stream);
+
+/* round_stochastic (formats.py:209-225) with RoundingRng(seed).uniform(step,
+ * tensor_id, index[i]) (rng.py:54-57); index may be NULL (then i). */
+xmc_status xmc_round_stochastic(xmc_grid g, const float* x, float* out, int64_t n, uint64_t seed,
+                                uint64_t step, uint64_t tensor_id, const uint64_t* index, void* stream);
+
+/* sgd_sr_step (optimizers.py:51-74) on fp32 on-grid weights:
+ * w[i] <- ROUND(w - lr*(grad + wd*w)), keys index[i] (NULL -> i). Sets a
+ * latched non-finite error through the return of the NEXT xmc_sync_status. */
+xmc_status xmc_sgd_sr_step(xmc_grid g, float* w, const float* grad, int64_t n, float lr, float wd,
+                           int32_t rounding, uint64_t seed, uint64_t step, uint64_t tensor_id,
+                           const uint64_t* index, int32_t* status, void* stream);
+
+/* Kahan-compensated SGD on the head grid (kahan_add
+ * formats.py:246-263 composed with sgd_sr_step): fp32 on-grid w, fp32 comp. */
+xmc_status xmc_kahan_sgd_step(xmc_grid g, float* w, float* comp, const float* grad, int64_t n, float lr,
+                              float wd, int32_t rounding, uint64_t seed, uint64_t step,
+                              uint64_t tensor_id, const uint64_t* index, int32_t* status, void* stream);
+
+/* Native-storage RTN cast, e.g. X -> e4m3 bytes (head.py:265). */
+xmc_status xmc_cast_rn(const float* x, void* out, int64_t n, int32_t fmt, int32_t* status, void* stream);
+
+/* ---- measurement (no reference counterpart; used by bench.py) ---- */
+/* Bracket every logits+G (fwd) and grad_X+update (bwd) launch with CUDA
+ * events on its stream; xmc_profile_read syncs them, returns summed device ms
+ * and launch counts since the previous read, and clears the record. */
+xmc_status xmc_profile_enable(int32_t on);
+xmc_status xmc_profile_read(double* ms_fwd, int64_t* n_fwd, double* ms_bwd, int64_t* n_bwd);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* XMC_HEAD_H_ */

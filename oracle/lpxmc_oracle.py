@@ -451,9 +451,22 @@ def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None):
                     head.tensor_id, idx)
 
 
+def quantize_g_operand(G, fmt):
+    """The GPU consumes G in the backward tensor-core operand format: an e4m3
+    head uses e4m3(G * 2^8) * 2^-8 (exact power-of-two scale), a bf16 head
+    uses bf16(G); both RTN.  This is a documented B200 design choice (not in
+    the reference), so parity tests can isolate it by applying it here."""
+    G = np.asarray(G, dtype=np.float32)
+    if fmt.name == "e4m3":
+        return (round_nearest(E4M3, G * np.float32(256.0)) * np.float32(1.0 / 256.0)).astype(np.float32)
+    return round_nearest(fmt, G)
+
+
 def head_update(head, X, sample_idx, label_idx, cfg, rng, step, comp=None,
-                probe=None):
-    """One head step over all chunks; returns grad_X (b, d).  head.py:254-298."""
+                probe=None, g_quant=False):
+    """One head step over all chunks; returns grad_X (b, d).  head.py:254-298.
+    ``g_quant=True`` applies quantize_g_operand to each chunk's G before the
+    backward (the GPU's operand precision)."""
     X = np.asarray(X, dtype=np.float32)
     sample_idx = np.asarray(sample_idx, dtype=np.int64)
     label_idx = np.asarray(label_idx, dtype=np.int64)
@@ -469,6 +482,8 @@ def head_update(head, X, sample_idx, label_idx, cfg, rng, step, comp=None,
         del logits
         if probe is not None:
             probe(step, chunk, G)
+        if g_quant:
+            G = quantize_g_operand(G, head.fmt)
         input_gradient_accumulate(acc, G, head, chunk, rng, step)
         fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp)
     return acc

@@ -1,0 +1,967 @@
+// C-ABI implementation: workspace layout, TMA descriptor encoding, the small
+// per-step kernels (X cast, positive-list bucketing, grad_X reduction), the
+// bit-exact elementwise numeric core, and launch orchestration of the two
+// tcgen05 kernels per chunk (xmc_fwd.cuh, xmc_bwd.cuh).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/xmc_head.h"
+#include "xmc_bwd.cuh"
+#include "xmc_fwd.cuh"
+#include "xmc_ptx.cuh"
+#include "xmc_round.cuh"
+
+using namespace xmc;
+
+// ============================================================== errors
+static thread_local std::string g_err;
+
+static xmc_status fail(xmc_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return fail(XMC_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),    \
+                  __FILE__, __LINE__);                                                     \
+  } while (0)
+
+#define XMC_TRY(expr)              \
+  do {                             \
+    xmc_status s_ = (expr);        \
+    if (s_ != XMC_OK) return s_;   \
+  } while (0)
+
+extern "C" const char* xmc_last_error(void) { return g_err.c_str(); }
+extern "C" const char* xmc_version(void) { return "xmc-b200 0.1 (sm_100a tcgen05)"; }
+
+// ============================================================== TMA maps
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major tensor [rows][cols] of `eb`-byte elements, box [box_rows][128 B], 128-B swizzle.
+static xmc_status make_map(CUtensorMap* m, const void* base, int eb, uint64_t cols, uint64_t rows,
+                           uint64_t ld_elems, uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(XMC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const CUtensorMapDataType dt = eb == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld_elems * eb};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / eb), box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(XMC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) cols=%llu rows=%llu", (int)r,
+                (unsigned long long)cols, (unsigned long long)rows);
+  return XMC_OK;
+}
+
+// ============================================================== profiling
+// Optional CUDA-event bracketing of every fwd / bwd launch on its own stream
+// (bench.py reads per-kernel device time of the timed region from here).
+struct ProfRec {
+  int kind;  // 0 = fwd, 1 = bwd
+  cudaEvent_t a, b;
+};
+static bool g_prof = false;
+static std::vector<ProfRec> g_prof_recs;
+
+static void prof_begin(int kind, cudaStream_t st, ProfRec* r) {
+  r->kind = kind;
+  r->a = r->b = nullptr;
+  if (!g_prof) return;
+  cudaEventCreate(&r->a);
+  cudaEventCreate(&r->b);
+  cudaEventRecord(r->a, st);
+}
+static void prof_end(cudaStream_t st, ProfRec* r) {
+  if (!g_prof || !r->a) return;
+  cudaEventRecord(r->b, st);
+  g_prof_recs.push_back(*r);
+}
+
+extern "C" xmc_status xmc_profile_enable(int32_t on) {
+  g_prof = on != 0;
+  return XMC_OK;
+}
+
+// Sum of device milliseconds and launch counts per kernel kind since the last
+// read (synchronises on the recorded events, then clears them).
+extern "C" xmc_status xmc_profile_read(double* ms_fwd, int64_t* n_fwd, double* ms_bwd, int64_t* n_bwd) {
+  double t[2] = {0, 0};
+  int64_t n[2] = {0, 0};
+  for (auto& r : g_prof_recs) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+      t[r.kind] += ms;
+      n[r.kind] += 1;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof_recs.clear();
+  if (ms_fwd) *ms_fwd = t[0];
+  if (n_fwd) *n_fwd = n[0];
+  if (ms_bwd) *ms_bwd = t[1];
+  if (n_bwd) *n_bwd = n[1];
+  return XMC_OK;
+}
+
+// ============================================================== helpers
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static inline size_t align_up(size_t a, size_t b) { return (a + b - 1) / b * b; }
+
+static int elem_bytes(int fmt) { return fmt == XMC_FMT_E4M3 || fmt == XMC_FMT_E5M2 ? 1 : (fmt == XMC_FMT_FP32 ? 4 : 2); }
+
+// padded batch = N of the logits MMA = G leading dimension
+static int padded_batch(int eb, int B) {
+  const int opts1[] = {128, 256};
+  const int opts2[] = {64, 128, 256, 512};
+  if (eb == 1) {
+    for (int o : opts1) if (B <= o) return o;
+  } else {
+    for (int o : opts2) if (B <= o) return o;
+  }
+  return -1;
+}
+
+static std::vector<std::pair<int64_t, int64_t>> partition(int64_t total, int64_t parts) {
+  std::vector<std::pair<int64_t, int64_t>> out;  // head.py:51-57
+  for (int64_t i = 0; i < parts; ++i) {
+    const int64_t a = (i * total) / parts, b = ((i + 1) * total) / parts;
+    if (b > a) out.emplace_back(a, b);
+  }
+  return out;
+}
+
+// ============================================================== handle
+struct xmc_head {
+  xmc_head_desc desc;
+  int eb;              // W / X / G element bytes
+  int max_bp;          // padded batch capacity
+  int num_sms;
+  int dtiles;
+  std::vector<std::pair<int64_t, int64_t>> chunks;  // local row ranges
+  std::vector<int32_t> tile_base;                   // per chunk, plus total at the end
+  int64_t total_tiles;
+  int64_t max_chunk_rows;
+  // workspace carve-up (device pointers)
+  uint8_t* xq;         // [max_bp][d]
+  uint8_t* xqt;        // [d][max_bp]
+  uint8_t* gbuf;       // [max_chunk_rows][max_bp]
+  float* gx_ws;        // [R][d][256]
+  int32_t* tile_cnt;   // [total_tiles + 1]
+  int32_t* tile_ptr;   // [total_tiles + 1]
+  uint32_t* entries;   // [max_positives]
+  int64_t* chunk_dev;  // [k+1] chunk starts (local rows) + [k+1] tile bases
+  int32_t* status;     // [4]
+  int R;               // bwd CTAs per d-tile
+};
+
+struct Layout {
+  size_t xq, xqt, gbuf, gx, cnt, ptr, ent, chunk, status, total;
+};
+
+static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out, int* bp_out, int* R_out,
+                                 int64_t* tiles_out, int64_t* maxrows_out, int num_sms) {
+  if (!d) return fail(XMC_ERR_ARG, "null desc");
+  if (d->fmt != XMC_FMT_E4M3 && d->fmt != XMC_FMT_BF16)
+    return fail(XMC_ERR_UNSUPPORTED, "head format must be e4m3 or bf16 (got %d)", d->fmt);
+  const int eb = elem_bytes(d->fmt);
+  if (d->dim <= 0 || d->dim % 128 != 0)
+    return fail(XMC_ERR_SHAPE, "dim must be a positive multiple of 128 (got %d)", d->dim);
+  if (d->num_chunks < 1) return fail(XMC_ERR_ARG, "num_chunks must be >= 1");
+  if (d->num_labels_local < 1 || d->label_offset < 0 ||
+      d->label_offset + d->num_labels_local > d->num_labels_global)
+    return fail(XMC_ERR_ARG, "bad label shard [%lld, +%lld) of %lld", (long long)d->label_offset,
+                (long long)d->num_labels_local, (long long)d->num_labels_global);
+  if (d->max_batch < 1 || d->max_batch > 65535) return fail(XMC_ERR_ARG, "max_batch out of range");
+  const int bp = padded_batch(eb, d->max_batch);
+  if (bp < 0) return fail(XMC_ERR_UNSUPPORTED, "batch %d too large for format", d->max_batch);
+  auto ch = partition(d->num_labels_local, d->num_chunks);
+  int64_t tiles = 0, maxrows = 0;
+  for (auto& c : ch) {
+    tiles += cdiv(c.second - c.first, 128);
+    maxrows = std::max(maxrows, c.second - c.first);
+  }
+  const int dtiles = d->dim / 128;
+  int R = std::max(1, num_sms / dtiles);
+  const int64_t D = d->dim;
+  L->xq = 0;
+  L->xqt = align_up(L->xq + (size_t)bp * D * eb, 1024);
+  L->gbuf = align_up(L->xqt + (size_t)bp * D * eb, 1024);
+  L->gx = align_up(L->gbuf + (size_t)(maxrows + 128) * bp * eb, 1024);
+  L->cnt = align_up(L->gx + (size_t)R * D * 256 * 4, 256);
+  L->ptr = align_up(L->cnt + (size_t)(tiles + 1) * 4, 256);
+  L->ent = align_up(L->ptr + (size_t)(tiles + 1) * 4, 256);
+  L->chunk = align_up(L->ent + (size_t)std::max<int64_t>(d->max_positives, 1) * 4, 256);
+  L->status = align_up(L->chunk + (size_t)(2 * (ch.size() + 1)) * 8, 256);
+  L->total = align_up(L->status + 64, 1024);
+  *eb_out = eb;
+  *bp_out = bp;
+  *R_out = R;
+  *tiles_out = tiles;
+  *maxrows_out = maxrows;
+  return XMC_OK;
+}
+
+static int device_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+extern "C" xmc_status xmc_head_workspace_size(const xmc_head_desc* desc, size_t* bytes) {
+  Layout L;
+  int eb, bp, R;
+  int64_t t, m;
+  const int sms = desc && desc->num_sms > 0 ? desc->num_sms : device_sms();
+  XMC_TRY(compute_layout(desc, &L, &eb, &bp, &R, &t, &m, sms));
+  *bytes = L.total;
+  return XMC_OK;
+}
+
+template <int EB, int BN>
+static void set_fwd_attr() {
+  cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       FwdCfg<EB, BN>::kSmemBytes);
+}
+template <int EB, bool XR, int KC>
+static void set_bwd_attr() {
+  cudaFuncSetAttribute(xmc_bwd_kernel<EB, XR, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       BwdCfg<EB, XR, KC>::kSmemBytes);
+}
+
+extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace, size_t workspace_bytes,
+                                      xmc_head_t* out) {
+  if (!out) return fail(XMC_ERR_ARG, "null out");
+  Layout L;
+  int eb, bp, R;
+  int64_t tiles, maxrows;
+  const int sms = desc && desc->num_sms > 0 ? desc->num_sms : device_sms();
+  XMC_TRY(compute_layout(desc, &L, &eb, &bp, &R, &tiles, &maxrows, sms));
+  if (!workspace || workspace_bytes < L.total)
+    return fail(XMC_ERR_CAPACITY, "workspace too small: need %zu bytes", L.total);
+  if (reinterpret_cast<uintptr_t>(workspace) % 1024 != 0)
+    return fail(XMC_ERR_ARG, "workspace must be 1024-byte aligned");
+  xmc_head* h = new xmc_head();
+  h->desc = *desc;
+  h->eb = eb;
+  h->max_bp = bp;
+  h->num_sms = sms;
+  h->dtiles = desc->dim / 128;
+  h->R = R;
+  h->chunks = partition(desc->num_labels_local, desc->num_chunks);
+  h->total_tiles = tiles;
+  h->max_chunk_rows = maxrows;
+  uint8_t* w = static_cast<uint8_t*>(workspace);
+  h->xq = w + L.xq;
+  h->xqt = w + L.xqt;
+  h->gbuf = w + L.gbuf;
+  h->gx_ws = reinterpret_cast<float*>(w + L.gx);
+  h->tile_cnt = reinterpret_cast<int32_t*>(w + L.cnt);
+  h->tile_ptr = reinterpret_cast<int32_t*>(w + L.ptr);
+  h->entries = reinterpret_cast<uint32_t*>(w + L.ent);
+  h->chunk_dev = reinterpret_cast<int64_t*>(w + L.chunk);
+  h->status = reinterpret_cast<int32_t*>(w + L.status);
+  std::vector<int64_t> host(2 * (h->chunks.size() + 1));
+  int64_t tb = 0;
+  for (size_t c = 0; c < h->chunks.size(); ++c) {
+    host[c] = h->chunks[c].first;
+    host[h->chunks.size() + 1 + c] = tb;
+    h->tile_base.push_back(static_cast<int32_t>(tb));
+    tb += cdiv(h->chunks[c].second - h->chunks[c].first, 128);
+  }
+  host[h->chunks.size()] = desc->num_labels_local;
+  host[2 * h->chunks.size() + 1] = tb;
+  h->tile_base.push_back(static_cast<int32_t>(tb));
+  cudaError_t e1 = cudaMemcpy(h->chunk_dev, host.data(), host.size() * 8, cudaMemcpyHostToDevice);
+  cudaError_t e2 = cudaMemset(h->status, 0, 64);
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    delete h;
+    return fail(XMC_ERR_CUDA, "workspace init failed: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+  }
+  set_fwd_attr<1, 128>();
+  set_fwd_attr<1, 256>();
+  set_fwd_attr<2, 64>();
+  set_fwd_attr<2, 128>();
+  set_fwd_attr<2, 256>();
+  set_fwd_attr<2, 512>();
+  set_bwd_attr<1, true, 1>();
+  set_bwd_attr<1, true, 2>();
+  set_bwd_attr<2, true, 1>();
+  set_bwd_attr<2, true, 2>();
+  set_bwd_attr<2, true, 4>();
+  set_bwd_attr<2, false, 8>();
+  *out = h;
+  return XMC_OK;
+}
+
+extern "C" xmc_status xmc_head_destroy(xmc_head_t h) {
+  delete h;
+  return XMC_OK;
+}
+
+// ============================================================== small kernels
+// X fp32 [B][d] -> Xq [Bp][d] and Xq^T [d][Bp] on the head grid (RTN,
+// head.py:265 / formats.py:197-206); padding rows/cols are zero.
+template <int EB>
+__global__ void x_prep_kernel(const float* __restrict__ X, int B, int Bp, int d, uint8_t* __restrict__ xq,
+                              uint8_t* __restrict__ xqt, int32_t* status) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+  bool bad = false;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int s = s0 + i, c = c0 + threadIdx.x;
+    float v = 0.f;
+    if (s < B) {
+      v = X[(int64_t)s * d + c];
+      bad |= !isfinite(v);
+    }
+    float q;
+    if (EB == 1) q = dec_e4m3(enc_e4m3(v));
+    else q = dec_bf16(enc_bf16(v));
+    tile[i][threadIdx.x] = q;
+    if (EB == 1) xq[(int64_t)s * d + c] = enc_e4m3(v);
+    else reinterpret_cast<uint16_t*>(xq)[(int64_t)s * d + c] = enc_bf16(v);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, s = s0 + threadIdx.x;
+    const float q = tile[threadIdx.x][i];
+    if (EB == 1) xqt[(int64_t)c * Bp + s] = enc_e4m3(q);
+    else reinterpret_cast<uint16_t*>(xqt)[(int64_t)c * Bp + s] = enc_bf16(q);
+  }
+  if (bad) atomicOr(status, ST_NONFINITE_X);
+}
+
+struct PosGeom {
+  const int64_t* chunk_start;  // [k+1]
+  const int64_t* tile_base;    // [k+1]
+  int32_t k;
+  int64_t label_offset;
+  int64_t num_local;
+  int32_t B;
+};
+
+__device__ __forceinline__ int64_t pos_tile(const PosGeom& g, int64_t local, int32_t* row_in_tile) {
+  // chunk c with chunk_start[c] <= local < chunk_start[c+1]; bounds are i*n/k
+  int c = static_cast<int>((local * g.k) / g.num_local);
+  if (c >= g.k) c = g.k - 1;
+  while (c > 0 && g.chunk_start[c] > local) --c;
+  while (c + 1 < g.k && g.chunk_start[c + 1] <= local) ++c;
+  const int64_t off = local - g.chunk_start[c];
+  *row_in_tile = static_cast<int32_t>(off & 127);
+  return g.tile_base[c] + (off >> 7);
+}
+
+__global__ void pos_count_kernel(PosGeom g, const int32_t* __restrict__ ps, const int32_t* __restrict__ pl,
+                                 int64_t nnz, int32_t* __restrict__ cnt, int32_t* status) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = ps[i];
+    if (s < 0 || s >= g.B) {
+      atomicOr(status, ST_BAD_SAMPLE);
+      continue;
+    }
+    const int64_t local = static_cast<int64_t>(pl[i]) - g.label_offset;
+    if (local < 0 || local >= g.num_local) continue;
+    int32_t r;
+    atomicAdd(&cnt[pos_tile(g, local, &r)], 1);
+  }
+}
+
+// exclusive scan of cnt[0..n) into ptr[0..n]; cnt becomes the scatter cursor
+__global__ void pos_scan_kernel(int32_t* cnt, int32_t* ptr, int64_t n) {
+  __shared__ int32_t warp_sums[32];
+  __shared__ int32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const int32_t v = i < n ? cnt[i] : 0;
+    int32_t x = v;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int32_t ws = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, ws, o);
+        if (lane >= o) ws += y;
+      }
+      warp_sums[lane] = ws;
+    }
+    __syncthreads();
+    const int32_t excl = carry + (w > 0 ? warp_sums[w - 1] : 0) + x - v;
+    if (i < n) {
+      ptr[i] = excl;
+      cnt[i] = excl;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ptr[n] = carry;
+}
+
+__global__ void pos_scatter_kernel(PosGeom g, const int32_t* __restrict__ ps, const int32_t* __restrict__ pl,
+                                   int64_t nnz, int32_t* __restrict__ cursor, uint32_t* __restrict__ entries) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = ps[i];
+    if (s < 0 || s >= g.B) continue;
+    const int64_t local = static_cast<int64_t>(pl[i]) - g.label_offset;
+    if (local < 0 || local >= g.num_local) continue;
+    int32_t r;
+    const int64_t t = pos_tile(g, local, &r);
+    const int32_t slot = atomicAdd(&cursor[t], 1);
+    entries[slot] = (static_cast<uint32_t>(r) << 16) | static_cast<uint32_t>(s);
+  }
+}
+
+// grad_x[s][c] += sum_r ws[r][c][s - col0]   (fixed r order: deterministic)
+__global__ void gx_reduce_kernel(const float* __restrict__ ws, int R, int d, int ld, int col0, int ncols, int B,
+                                 float* __restrict__ gx) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, sl = s0 + threadIdx.x;
+    float acc = 0.f;
+    if (sl < ncols)
+      for (int r = 0; r < R; ++r) acc += ws[((int64_t)r * d + c) * ld + sl];
+    tile[i][threadIdx.x] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int sl = s0 + i, c = c0 + threadIdx.x;
+    const int s = col0 + sl;
+    if (sl < ncols && s < B) gx[(int64_t)s * d + c] += tile[threadIdx.x][i];
+  }
+}
+
+// fp32 G (rows x B, ld) -> backward operand format (e4m3 x scale or bf16), [rows][Bp]
+template <int EB>
+__global__ void g_quant_kernel(const float* __restrict__ G, int64_t ld, int64_t rows, int B, int Bp, float scale,
+                               uint8_t* __restrict__ out, int32_t* status) {
+  const int64_t n = rows * Bp;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / Bp;
+    const int s = static_cast<int>(i - r * Bp);
+    float v = 0.f;
+    if (s < B) {
+      v = G[r * ld + s];
+      bad |= !isfinite(v);
+    }
+    if (EB == 1) out[i] = enc_e4m3(v * scale);
+    else reinterpret_cast<uint16_t*>(out)[i] = enc_bf16(v);
+  }
+  if (bad) atomicOr(status, ST_NONFINITE_GRAD);
+}
+
+// ============================================================== launches
+static xmc_status launch_x_prep(xmc_head* h, const float* X, int B, int Bp, cudaStream_t st) {
+  dim3 grid(h->desc.dim / 32, Bp / 32), block(32, 8);
+  if (h->eb == 1) x_prep_kernel<1><<<grid, block, 0, st>>>(X, B, Bp, h->desc.dim, h->xq, h->xqt, h->status);
+  else x_prep_kernel<2><<<grid, block, 0, st>>>(X, B, Bp, h->desc.dim, h->xq, h->xqt, h->status);
+  CUDA_TRY(cudaGetLastError());
+  return XMC_OK;
+}
+
+template <int EB, int BN>
+static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtensorMap& tx, const FwdParams& p,
+                               cudaStream_t st) {
+  const int grid = static_cast<int>(std::min<int64_t>(h->num_sms, p.num_tiles));
+  if (grid <= 0) return XMC_OK;
+  ProfRec pr;
+  prof_begin(0, st, &pr);
+  xmc_fwd_kernel<EB, BN><<<grid, kFwdThreads, FwdCfg<EB, BN>::kSmemBytes, st>>>(tw, tx, p);
+  CUDA_TRY(cudaGetLastError());
+  prof_end(st, &pr);
+  return XMC_OK;
+}
+
+// rows [row0, row0+rows) of W (local), mode 0 -> G into gbuf, mode 1 -> fp32 logits
+static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t rows, int B, int Bp, int mode,
+                             const int32_t* tile_ptr, void* out, int64_t ld, float* stats, cudaStream_t st) {
+  const int eb = h->eb, D = h->desc.dim;
+  CUtensorMap tw, tx;
+  XMC_TRY(make_map(&tw, static_cast<const uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 128));
+  XMC_TRY(make_map(&tx, h->xq, eb, D, Bp, D, std::min(Bp, 256)));
+  FwdParams p{};
+  p.rows = static_cast<int32_t>(rows);
+  p.B = B;
+  p.d = D;
+  p.num_tiles = static_cast<int32_t>(cdiv(rows, 128));
+  p.mode = mode;
+  p.g_fmt = eb == 1 ? FMT_E4M3 : FMT_BF16;
+  p.g_scale = eb == 1 ? 256.0f : 1.0f;
+  p.tile_ptr = tile_ptr;
+  p.entries = h->entries;
+  p.out = out;
+  p.ld = ld;
+  p.stats = stats;
+  p.status = h->status;
+  if (eb == 1) {
+    if (Bp == 128) return launch_fwd_t<1, 128>(h, tw, tx, p, st);
+    if (Bp == 256) return launch_fwd_t<1, 256>(h, tw, tx, p, st);
+  } else {
+    if (Bp == 64) return launch_fwd_t<2, 64>(h, tw, tx, p, st);
+    if (Bp == 128) return launch_fwd_t<2, 128>(h, tw, tx, p, st);
+    if (Bp == 256) return launch_fwd_t<2, 256>(h, tw, tx, p, st);
+    if (Bp == 512) return launch_fwd_t<2, 512>(h, tw, tx, p, st);
+  }
+  return fail(XMC_ERR_UNSUPPORTED, "no forward kernel for padded batch %d", Bp);
+}
+
+template <int EB, bool XR, int KC>
+static xmc_status launch_bwd_t(int grid, const CUtensorMap& tw, const CUtensorMap& tg, const CUtensorMap& tx,
+                               const BwdParams& p, cudaStream_t st) {
+  ProfRec pr;
+  prof_begin(1, st, &pr);
+  xmc_bwd_kernel<EB, XR, KC><<<grid, kBwdThreads, BwdCfg<EB, XR, KC>::kSmemBytes, st>>>(tw, tg, tx, p);
+  CUDA_TRY(cudaGetLastError());
+  prof_end(st, &pr);
+  return XMC_OK;
+}
+
+// one bwd pass over local rows [row0, row0+rows), G from gbuf; optional grad_X into acc
+static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, int B, int Bp, bool update,
+                             int gx_kc0, int gx_kc_count, const xmc_step_args* a, float* acc, cudaStream_t st) {
+  const int eb = h->eb, D = h->desc.dim;
+  const int box_k = 128 / eb;
+  CUtensorMap tw, tg, tx;
+  XMC_TRY(make_map(&tw, static_cast<uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 128));
+  XMC_TRY(make_map(&tg, h->gbuf, eb, Bp, rows, Bp, 128));
+  XMC_TRY(make_map(&tx, h->xqt, eb, Bp, D, Bp, 128));
+  const int64_t tiles = cdiv(rows, 128);
+  const int R = static_cast<int>(std::min<int64_t>(h->R, tiles));
+  BwdParams p{};
+  p.rows = static_cast<int32_t>(rows);
+  p.d = D;
+  p.num_tiles = static_cast<int32_t>(tiles);
+  p.dtiles = h->dtiles;
+  p.kc_count = Bp / box_k;
+  p.do_update = update ? 1 : 0;
+  p.gx_kc0 = gx_kc0;
+  p.gx_kc_count = gx_kc_count;
+  p.W = static_cast<uint8_t*>(W) + row0 * D * eb;
+  p.row0_global = h->desc.label_offset + row0;
+  p.lr = a ? a->lr : 0.f;
+  p.wd = a ? a->weight_decay : 0.f;
+  p.dw_scale = eb == 1 ? (1.0f / 256.0f) : 1.0f;
+  p.rounding = a ? a->rounding : 0;
+  p.rng_base = a ? sm64_base(a->seed, a->step, a->tensor_id) : 0;
+  p.gx_ws = h->gx_ws;
+  p.gx_ld = gx_kc_count * box_k;
+  p.status = h->status;
+  const int grid = R * h->dtiles;
+  xmc_status s;
+  if (eb == 1) {
+    if (Bp == 128) s = launch_bwd_t<1, true, 1>(grid, tw, tg, tx, p, st);
+    else if (Bp == 256) s = launch_bwd_t<1, true, 2>(grid, tw, tg, tx, p, st);
+    else return fail(XMC_ERR_UNSUPPORTED, "no backward kernel for padded batch %d", Bp);
+  } else {
+    if (Bp == 64) s = launch_bwd_t<2, true, 1>(grid, tw, tg, tx, p, st);
+    else if (Bp == 128) s = launch_bwd_t<2, true, 2>(grid, tw, tg, tx, p, st);
+    else if (Bp == 256) s = launch_bwd_t<2, true, 4>(grid, tw, tg, tx, p, st);
+    else if (Bp == 512) s = launch_bwd_t<2, false, 8>(grid, tw, tg, tx, p, st);
+    else return fail(XMC_ERR_UNSUPPORTED, "no backward kernel for padded batch %d", Bp);
+  }
+  if (s != XMC_OK) return s;
+  if (gx_kc_count > 0 && acc) {
+    dim3 g(D / 32, (p.gx_ld + 31) / 32), b(32, 8);
+    gx_reduce_kernel<<<g, b, 0, st>>>(h->gx_ws, R, D, p.gx_ld, gx_kc0 * box_k, p.gx_ld, B, acc);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return XMC_OK;
+}
+
+// grad_X + update for one chunk whose G is in gbuf (handles Bp = 512 in two passes)
+static xmc_status run_backward(xmc_head* h, void* W, int64_t row0, int64_t rows, int B, int Bp, bool gx,
+                               bool update, const xmc_step_args* a, float* acc, cudaStream_t st) {
+  const int kcs = Bp * h->eb / 128;
+  const int per = 256 * h->eb / 128;   // k-chunks whose grad_X columns fit 256 TMEM columns
+  if (!gx) return launch_bwd(h, W, row0, rows, B, Bp, update, 0, 0, a, nullptr, st);
+  // passes over grad_X column groups; the update rides on the LAST pass so
+  // every grad_X pass reads the pre-update weights (head.py:290-291)
+  const int groups = (kcs + per - 1) / per;
+  for (int gi = groups - 1; gi >= 0; --gi) {
+    const int kc0 = gi * per;
+    const int cnt = std::min(per, kcs - kc0);
+    XMC_TRY(launch_bwd(h, W, row0, rows, B, Bp, update && gi == 0, kc0, cnt, a, acc, st));
+  }
+  return XMC_OK;
+}
+
+static xmc_status check_args(const xmc_step_args* a) {
+  if (!a) return fail(XMC_ERR_ARG, "null step args");
+  if (!(a->lr > 0.0f)) return fail(XMC_ERR_ARG, "lr must be positive");
+  if (!(a->weight_decay >= 0.0f)) return fail(XMC_ERR_ARG, "weight_decay must be non-negative");
+  if (a->rounding < 0 || a->rounding > 2) return fail(XMC_ERR_ARG, "unknown rounding mode %d", a->rounding);
+  return XMC_OK;
+}
+
+static xmc_status prepare_positives(xmc_head* h, const int32_t* ps, const int32_t* pl, int64_t nnz, int B,
+                                    cudaStream_t st) {
+  if (nnz > h->desc.max_positives)
+    return fail(XMC_ERR_CAPACITY, "%lld positives exceed workspace capacity %lld", (long long)nnz,
+                (long long)h->desc.max_positives);
+  CUDA_TRY(cudaMemsetAsync(h->tile_cnt, 0, (h->total_tiles + 1) * 4, st));
+  PosGeom g{h->chunk_dev, h->chunk_dev + h->chunks.size() + 1, static_cast<int32_t>(h->chunks.size()),
+            h->desc.label_offset, h->desc.num_labels_local, B};
+  if (nnz > 0) {
+    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(nnz, 256), 1184));
+    pos_count_kernel<<<blocks, 256, 0, st>>>(g, ps, pl, nnz, h->tile_cnt, h->status);
+    CUDA_TRY(cudaGetLastError());
+  }
+  pos_scan_kernel<<<1, 1024, 0, st>>>(h->tile_cnt, h->tile_ptr, h->total_tiles);
+  CUDA_TRY(cudaGetLastError());
+  if (nnz > 0) {
+    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(nnz, 256), 1184));
+    pos_scatter_kernel<<<blocks, 256, 0, st>>>(g, ps, pl, nnz, h->tile_cnt, h->entries);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return XMC_OK;
+}
+
+static xmc_status read_status(xmc_head* h, cudaStream_t st, bool clear) {
+  int32_t s = 0;
+  CUDA_TRY(cudaMemcpyAsync(&s, h->status, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (s != 0 && clear) CUDA_TRY(cudaMemsetAsync(h->status, 0, 4, st));
+  if (s & ST_NONFINITE_X) return fail(XMC_ERR_NONFINITE, "non-finite input to rounding operation");
+  if (s & ST_BAD_SAMPLE) return fail(XMC_ERR_INDEX, "positive sample index out of range");
+  if (s & ST_LABEL_OUTSIDE) return fail(XMC_ERR_LABEL, "label outside chunk range");
+  if (s & ST_NONFINITE_GRAD) return fail(XMC_ERR_NONFINITE, "non-finite values in fused scratch block");
+  return XMC_OK;
+}
+
+extern "C" xmc_status xmc_head_check(xmc_head_t h, void* stream) {
+  if (!h) return fail(XMC_ERR_ARG, "null handle");
+  return read_status(h, static_cast<cudaStream_t>(stream), true);
+}
+
+extern "C" xmc_status xmc_head_step(xmc_head_t h, void* W, const float* X, int32_t B, const int32_t* pos_sample,
+                                    const int32_t* pos_label, int64_t nnz, const xmc_step_args* args,
+                                    float* grad_x, float* stats, void* stream) {
+  if (!h || !W || !X || !grad_x) return fail(XMC_ERR_ARG, "null argument");
+  XMC_TRY(check_args(args));
+  if (B < 1 || B > h->desc.max_batch) return fail(XMC_ERR_SHAPE, "batch %d outside [1, %d]", B, h->desc.max_batch);
+  if (nnz < 0 || (nnz > 0 && (!pos_sample || !pos_label))) return fail(XMC_ERR_ARG, "bad positives");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int Bp = padded_batch(h->eb, B);
+  XMC_TRY(launch_x_prep(h, X, B, Bp, st));
+  XMC_TRY(prepare_positives(h, pos_sample, pos_label, nnz, B, st));
+  CUDA_TRY(cudaMemsetAsync(grad_x, 0, (size_t)B * h->desc.dim * 4, st));
+  if (stats) CUDA_TRY(cudaMemsetAsync(stats, 0, 8, st));
+  for (size_t c = 0; c < h->chunks.size(); ++c) {
+    const int64_t r0 = h->chunks[c].first, rows = h->chunks[c].second - h->chunks[c].first;
+    XMC_TRY(launch_fwd(h, W, r0, rows, B, Bp, 0, h->tile_ptr + h->tile_base[c], h->gbuf, Bp, stats, st));
+    XMC_TRY(run_backward(h, W, r0, rows, B, Bp, true, true, args, grad_x, st));
+  }
+  return XMC_OK;
+}
+
+extern "C" xmc_status xmc_head_logits(xmc_head_t h, const void* W, const float* X, int32_t B, int64_t row0,
+                                      int64_t row1, float* logits, int64_t ld, void* stream) {
+  if (!h || !W || !X || !logits) return fail(XMC_ERR_ARG, "null argument");
+  if (B < 1 || B > h->desc.max_batch) return fail(XMC_ERR_SHAPE, "batch %d outside [1, %d]", B, h->desc.max_batch);
+  if (row0 < 0 || row1 > h->desc.num_labels_local || row1 <= row0) return fail(XMC_ERR_ARG, "bad row range");
+  if (ld < B) return fail(XMC_ERR_ARG, "ld < B");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int Bp = padded_batch(h->eb, B);
+  XMC_TRY(launch_x_prep(h, X, B, Bp, st));
+  return launch_fwd(h, W, row0, row1 - row0, B, Bp, 1, nullptr, logits, ld, nullptr, st);
+}
+
+extern "C" xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, int64_t ld, const float* X,
+                                        int32_t B, int64_t row0, int64_t row1, float* acc, int32_t accumulate_gx,
+                                        int32_t update, const xmc_step_args* args, void* stream) {
+  if (!h || !W || !G || (update && !X)) return fail(XMC_ERR_ARG, "null argument");
+  if (update) XMC_TRY(check_args(args));
+  if (B < 1 || B > h->desc.max_batch) return fail(XMC_ERR_SHAPE, "batch %d outside [1, %d]", B, h->desc.max_batch);
+  if (row0 < 0 || row1 > h->desc.num_labels_local || row1 <= row0) return fail(XMC_ERR_ARG, "bad row range");
+  if (row1 - row0 > h->max_chunk_rows + 128) return fail(XMC_ERR_CAPACITY, "row range exceeds the G buffer");
+  if (accumulate_gx && !acc) return fail(XMC_ERR_ARG, "null acc");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int Bp = padded_batch(h->eb, B);
+  if (X) XMC_TRY(launch_x_prep(h, X, B, Bp, st));
+  const int64_t rows = row1 - row0;
+  const int blocks = static_cast<int>(std::min<int64_t>(cdiv(rows * Bp, 256), 4096));
+  if (h->eb == 1) g_quant_kernel<1><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, 256.0f, h->gbuf, h->status);
+  else g_quant_kernel<2><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, 1.0f, h->gbuf, h->status);
+  CUDA_TRY(cudaGetLastError());
+  return run_backward(h, W, row0, rows, B, Bp, accumulate_gx != 0, update != 0, args, acc, st);
+}
+
+// ============================================================== elementwise core
+static GridFmt grid_from(xmc_grid g, xmc_status* s) {
+  GridFmt f{};
+  if (g.exp_bits < 2 || g.exp_bits > 8 || g.man_bits < 0 || g.man_bits > 23) {
+    *s = fail(XMC_ERR_ARG, "bad format e%dm%d", g.exp_bits, g.man_bits);
+    return f;
+  }
+  const bool ext = g.extended_range < 0 ? (g.exp_bits == 4 && g.man_bits == 3) : g.extended_range != 0;
+  if (ext && g.man_bits == 0) {
+    *s = fail(XMC_ERR_ARG, "extended range needs at least one mantissa bit");
+    return f;
+  }
+  const int bias = (1 << (g.exp_bits - 1)) - 1;
+  f.man_bits = g.man_bits;
+  f.min_normal_exp = 1 - bias;
+  f.max_exp = ext ? bias + 1 : bias;
+  const double top = ext ? 2.0 - std::ldexp(1.0, 1 - g.man_bits) : 2.0 - std::ldexp(1.0, -g.man_bits);
+  f.max_finite = std::ldexp(top, f.max_exp);
+  *s = XMC_OK;
+  return f;
+}
+
+__global__ void finite_check_kernel(const float* __restrict__ x, int64_t n, int32_t* status, int32_t bit) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    bad |= !isfinite(x[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, bit);
+}
+
+__global__ void round_kernel(GridFmt f, const float* __restrict__ x, float* __restrict__ out, int64_t n, int mode,
+                             uint64_t base, const uint64_t* __restrict__ index, const int32_t* status) {
+  if (*status != 0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    if (mode == 0) out[i] = grid_round_nearest(f, v);
+    else out[i] = grid_round_stochastic(f, v, sm64_uniform(base, index ? index[i] : static_cast<uint64_t>(i)));
+  }
+}
+
+// sgd_sr_step (optimizers.py:51-74); kahan=1 -> head-Kahan composition (A8k)
+__global__ void sgd_kernel(GridFmt f, bool working_precision, float* __restrict__ w, float* __restrict__ comp,
+                           const float* __restrict__ grad, int64_t n, float lr, float wd, int rounding,
+                           uint64_t base, const uint64_t* __restrict__ index, const int32_t* status) {
+  if (*status != 0) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float s = w[i];
+    const float g = wd != 0.0f ? __fadd_rn(grad[i], __fmul_rn(wd, s)) : grad[i];
+    const uint64_t key = index ? index[i] : static_cast<uint64_t>(i);
+    if (comp == nullptr) {
+      const float upd = __fsub_rn(s, __fmul_rn(lr, g));
+      w[i] = rounding == 0 ? grid_round_nearest(f, upd) : grid_round_stochastic(f, upd, sm64_uniform(base, key));
+    } else {
+      const float v = -__fmul_rn(lr, g);
+      if (working_precision) {
+        w[i] = __fadd_rn(s, v);
+        continue;
+      }
+      const float c = comp[i];
+      const float y = __fsub_rn(v, c);
+      const float x = __fadd_rn(s, y);
+      const float t = rounding == 0 ? grid_round_nearest(f, x) : grid_round_stochastic(f, x, sm64_uniform(base, key));
+      comp[i] = __fsub_rn(__fsub_rn(t, s), y);
+      w[i] = t;
+    }
+  }
+}
+
+static int ew_blocks(int64_t n) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 8192))); }
+
+static int32_t* scratch_status() {
+  static int32_t* p = nullptr;
+  if (!p) cudaMalloc(&p, 64);
+  return p;
+}
+
+static xmc_status status_to_error(int32_t s) {
+  if (s & ST_NONFINITE_X) return fail(XMC_ERR_NONFINITE, "non-finite input to rounding operation");
+  if (s & ST_NONFINITE_GRAD) return fail(XMC_ERR_NONFINITE, "non-finite gradient entry");
+  return XMC_OK;
+}
+
+// run a finite check then the op; sync and report (the reference raises before writing)
+static xmc_status checked_elementwise(const float* chk, int64_t n, int32_t bit, int32_t* status, cudaStream_t st) {
+  CUDA_TRY(cudaMemsetAsync(status, 0, 4, st));
+  finite_check_kernel<<<ew_blocks(n), 256, 0, st>>>(chk, n, status, bit);
+  CUDA_TRY(cudaGetLastError());
+  return XMC_OK;
+}
+
+static xmc_status finish_elementwise(int32_t* status, cudaStream_t st) {
+  int32_t s = 0;
+  CUDA_TRY(cudaMemcpyAsync(&s, status, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return status_to_error(s);
+}
+
+extern "C" xmc_status xmc_round_nearest(xmc_grid g, const float* x, float* out, int64_t n, void* stream) {
+  xmc_status s;
+  const GridFmt f = grid_from(g, &s);
+  XMC_TRY(s);
+  if (n <= 0) return XMC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t* status = scratch_status();
+  XMC_TRY(checked_elementwise(x, n, ST_NONFINITE_X, status, st));
+  round_kernel<<<ew_blocks(n), 256, 0, st>>>(f, x, out, n, 0, 0, nullptr, status);
+  CUDA_TRY(cudaGetLastError());
+  return finish_elementwise(status, st);
+}
+
+extern "C" xmc_status xmc_round_stochastic(xmc_grid g, const float* x, float* out, int64_t n, uint64_t seed,
+                                           uint64_t step, uint64_t tensor_id, const uint64_t* index, void* stream) {
+  xmc_status s;
+  const GridFmt f = grid_from(g, &s);
+  XMC_TRY(s);
+  if (n <= 0) return XMC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t* status = scratch_status();
+  XMC_TRY(checked_elementwise(x, n, ST_NONFINITE_X, status, st));
+  round_kernel<<<ew_blocks(n), 256, 0, st>>>(f, x, out, n, 1, sm64_base(seed, step, tensor_id), index, status);
+  CUDA_TRY(cudaGetLastError());
+  return finish_elementwise(status, st);
+}
+
+static xmc_status sgd_common(xmc_grid g, float* w, float* comp, const float* grad, int64_t n, float lr, float wd,
+                             int32_t rounding, uint64_t seed, uint64_t step, uint64_t tensor_id,
+                             const uint64_t* index, int32_t* status, void* stream) {
+  xmc_status s;
+  const GridFmt f = grid_from(g, &s);
+  XMC_TRY(s);
+  if (!(lr > 0.0f)) return fail(XMC_ERR_ARG, "lr must be positive");
+  if (!(wd >= 0.0f)) return fail(XMC_ERR_ARG, "weight_decay must be non-negative");
+  if (rounding != 0 && rounding != 1) return fail(XMC_ERR_ARG, "elementwise SGD supports nearest / exact SR");
+  if (n <= 0) return XMC_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t* stw = status ? status : scratch_status();
+  XMC_TRY(checked_elementwise(grad, n, ST_NONFINITE_GRAD, stw, st));
+  const bool wp = g.exp_bits == 8 && g.man_bits == 23;
+  sgd_kernel<<<ew_blocks(n), 256, 0, st>>>(f, wp, w, comp, grad, n, lr, wd, rounding, sm64_base(seed, step, tensor_id),
+                                           index, stw);
+  CUDA_TRY(cudaGetLastError());
+  return finish_elementwise(stw, st);
+}
+
+extern "C" xmc_status xmc_sgd_sr_step(xmc_grid g, float* w, const float* grad, int64_t n, float lr, float wd,
+                                      int32_t rounding, uint64_t seed, uint64_t step, uint64_t tensor_id,
+                                      const uint64_t* index, int32_t* status, void* stream) {
+  return sgd_common(g, w, nullptr, grad, n, lr, wd, rounding, seed, step, tensor_id, index, status, stream);
+}
+
+extern "C" xmc_status xmc_kahan_sgd_step(xmc_grid g, float* w, float* comp, const float* grad, int64_t n, float lr,
+                                         float wd, int32_t rounding, uint64_t seed, uint64_t step, uint64_t tensor_id,
+                                         const uint64_t* index, int32_t* status, void* stream) {
+  if (!comp) return fail(XMC_ERR_ARG, "null compensation buffer");
+  return sgd_common(g, w, comp, grad, n, lr, wd, rounding, seed, step, tensor_id, index, status, stream);
+}
+
+__global__ void cast_kernel(const float* __restrict__ x, void* __restrict__ out, int64_t n, int fmt, int32_t* status) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    bad |= !isfinite(v);
+    if (fmt == FMT_E4M3) static_cast<uint8_t*>(out)[i] = enc_e4m3(v);
+    else if (fmt == FMT_E5M2) static_cast<uint8_t*>(out)[i] = enc_e5m2(v);
+    else static_cast<uint16_t*>(out)[i] = enc_bf16(v);
+  }
+  if (bad && status) atomicOr(status, ST_NONFINITE_X);
+}
+
+extern "C" xmc_status xmc_cast_rn(const float* x, void* out, int64_t n, int32_t fmt, int32_t* status, void* stream) {
+  if (fmt != XMC_FMT_E4M3 && fmt != XMC_FMT_E5M2 && fmt != XMC_FMT_BF16)
+    return fail(XMC_ERR_UNSUPPORTED, "cast target must be e4m3, e5m2 or bf16");
+  if (n <= 0) return XMC_OK;
+  cast_kernel<<<ew_blocks(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(x, out, n, fmt, status);
+  CUDA_TRY(cudaGetLastError());
+  return XMC_OK;
+}
+
+// logit_gradient (head.py:181-196): accurate expf + IEEE division like numpy fp32
+__global__ void sigmoid_clip_kernel(const float* __restrict__ z, int64_t rows, int B, int64_t ld, float* __restrict__ G) {
+  const int64_t n = rows * B;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / B;
+    const int s = static_cast<int>(i - r * B);
+    float g = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z[r * ld + s])));
+    g = g < 5.9604644775390625e-08f ? 5.9604644775390625e-08f : g;
+    g = g > 0.99999994039535522461f ? 0.99999994039535522461f : g;
+    G[r * ld + s] = g;
+  }
+}
+
+__global__ void positives_apply_kernel(const float* __restrict__ z, int64_t rows, int B, int64_t ld,
+                                       const int32_t* __restrict__ ps, const int32_t* __restrict__ pl, int64_t nnz,
+                                       int64_t start, float* __restrict__ G, int32_t* status) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = static_cast<int64_t>(pl[i]) - start;
+    const int s = ps[i];
+    if (r < 0 || r >= rows) {
+      atomicOr(status, ST_LABEL_OUTSIDE);
+      continue;
+    }
+    if (s < 0 || s >= B) {
+      atomicOr(status, ST_BAD_SAMPLE);
+      continue;
+    }
+    float g = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z[r * ld + s])));
+    g = g < 5.9604644775390625e-08f ? 5.9604644775390625e-08f : g;
+    g = g > 0.99999994039535522461f ? 0.99999994039535522461f : g;
+    G[r * ld + s] = __fsub_rn(g, 1.0f);
+  }
+}
+
+extern "C" xmc_status xmc_logit_gradient(const float* logits, int64_t rows, int32_t B, int64_t ld,
+                                         const int32_t* pos_sample, const int32_t* pos_label, int64_t nnz,
+                                         int64_t chunk_start, float* G, void* stream) {
+  if (!logits || !G || rows < 0 || B < 1 || ld < B) return fail(XMC_ERR_ARG, "bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t* status = scratch_status();
+  CUDA_TRY(cudaMemsetAsync(status, 0, 4, st));
+  if (rows > 0) {
+    sigmoid_clip_kernel<<<ew_blocks(rows * B), 256, 0, st>>>(logits, rows, B, ld, G);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (nnz > 0) {
+    positives_apply_kernel<<<ew_blocks(nnz), 256, 0, st>>>(logits, rows, B, ld, pos_sample, pos_label, nnz,
+                                                          chunk_start, G, status);
+    CUDA_TRY(cudaGetLastError());
+  }
+  int32_t s = 0;
+  CUDA_TRY(cudaMemcpyAsync(&s, status, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (s & ST_LABEL_OUTSIDE) return fail(XMC_ERR_LABEL, "label outside chunk range");
+  if (s & ST_BAD_SAMPLE) return fail(XMC_ERR_INDEX, "positive sample index out of range");
+  return XMC_OK;
+}

@@ -1,0 +1,391 @@
+// Kernel 2 of a head chunk: input-gradient accumulation and the gradient-fused
+// SGD update, both on tcgen05, reading the chunk's G once per d-tile.
+//
+//   grad_X^T[j] += W_old[t, j]^T . G[t]         (M = 128 d, N = samples, K = 128 labels)
+//   dW[t, j]     = G[t] . Xq[:, j]               (M = 128 labels, N = 128 d, K = samples)
+//   W[t, j]      = ROUND(W_old - lr (dW + wd W_old))   in place, RTN / SR
+//
+// Reference: input_gradient_accumulate head.py:199-209 (pre-update W, called
+// before the update head.py:290-291), fused_weight_update head.py:212-251,
+// sgd_sr_step optimizers.py:51-74, round_nearest / round_stochastic
+// formats.py:197-225, keys = global flat index r*d + c (head.py:244-247).
+//
+// Work decomposition: CTA c owns d-tile j = c % dtiles and walks label tiles
+// t = c / dtiles + k * R.  Its grad_X^T[j] partial stays in TMEM for the whole
+// launch and is flushed once to a workspace (deterministic reduce afterwards).
+// The dW accumulator is double-buffered in TMEM so the update epilogue of tile
+// i overlaps the MMAs of tile i+1.  dW never leaves TMEM/registers.
+#pragma once
+
+#include "xmc_ptx.cuh"
+#include "xmc_round.cuh"
+
+namespace xmc {
+
+constexpr int kBwdEpiWarps = 8;
+constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32;
+
+enum StatusBits : int32_t {
+  ST_NONFINITE_X = 1,
+  ST_BAD_SAMPLE = 2,
+  ST_NONFINITE_GRAD = 4,
+  ST_LABEL_OUTSIDE = 8,
+  ST_CAPACITY = 16,
+};
+
+struct BwdParams {
+  int32_t rows;          // labels in this chunk
+  int32_t d;             // feature dim
+  int32_t num_tiles;     // ceil(rows / 128)
+  int32_t dtiles;        // d / 128
+  int32_t kc_count;      // sample k-chunks (Bp * EB / 128)
+  int32_t do_update;     // dW + SGD + rounding, W written in place
+  int32_t gx_kc0;        // first sample k-chunk accumulated into grad_X
+  int32_t gx_kc_count;   // 0 = no grad_X
+  uint8_t* W;            // chunk base (row-major rows x d, EB bytes/elem)
+  int64_t row0_global;   // global label of chunk row 0 (RNG key)
+  float lr, wd, dw_scale;
+  int32_t rounding;      // ROUND_NEAREST / ROUND_SR_EXACT / ROUND_SR_FAST
+  uint64_t rng_base;     // splitmix64 base(seed, step, tensor_id)
+  float* gx_ws;          // [R][d][gx_ld] fp32 partials
+  int32_t gx_ld;
+  int32_t* status;
+};
+
+template <int EB, bool XT_RES, int KCMAX>
+struct BwdCfg {
+  static constexpr int kBoxK = 128 / EB;             // elements per 128-B atom row
+  static constexpr int kBox = 128 * 128;             // one [128 rows x 128 B] box
+  static constexpr int kWBoxes = EB;                 // d-tile of 128 elements
+  static constexpr int kWBytes = kWBoxes * kBox;
+  static constexpr int kWStages = 2;
+  static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
+  static constexpr int kKStages = 4;
+  static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
+  static constexpr int kSmemBytes = 1024 + kXtBytes + kWStages * kWBytes + kKStages * kKSlot + 512;
+  static constexpr int kKmma = 32 / EB;              // K per MMA instruction (elements)
+};
+
+template <int EB>
+XMC_DEV void bwd_update_row_chunk(const BwdParams& p, const float (&dw)[32], const uint8_t* wsm_row_base,
+                                  int row_sw, int c0_local, int64_t grow, int64_t gcol0, bool row_ok,
+                                  bool& bad, uint8_t* gdst);
+
+template <int EB, bool XT_RES, int KCMAX>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
+                   const __grid_constant__ CUtensorMap tm_xt, BwdParams p) {
+  using C = BwdCfg<EB, XT_RES, KCMAX>;
+  if (*p.status != 0) return;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* xt_s = smem;
+  uint8_t* w_s = smem + C::kXtBytes;
+  uint8_t* k_s = w_s + C::kWStages * C::kWBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(k_s + C::kKStages * C::kKSlot);
+  uint64_t* w_full = bars;                       // [2]
+  uint64_t* w_empty = bars + 2;                  // [2]
+  uint64_t* k_full = bars + 4;                   // [4]
+  uint64_t* k_empty = bars + 8;                  // [4]
+  uint64_t* t_full = bars + 12;                  // [2]
+  uint64_t* t_empty = bars + 14;                 // [2]
+  uint64_t* xt_full = bars + 16;
+  uint64_t* gx_full = bars + 17;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+
+  const uint32_t warp = warp_id_sync();
+  const int j = blockIdx.x % p.dtiles;
+  const int R = gridDim.x / p.dtiles;
+  const int r0 = blockIdx.x / p.dtiles;
+  const bool do_gx = p.gx_kc_count > 0;
+
+  if (warp == 0 && elect_one()) {
+    prefetch_tmap(&tm_w);
+    prefetch_tmap(&tm_g);
+    prefetch_tmap(&tm_xt);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], 1 + kBwdEpiWarps);
+      mbar_init(&t_full[s], 1);
+      mbar_init(&t_empty[s], kBwdEpiWarps);
+    }
+    for (int s = 0; s < C::kKStages; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    mbar_init(xt_full, 1);
+    mbar_init(gx_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_gx = tmem_base + 256;   // cols [256, 512): grad_X^T partial
+  // cols [0,128) and [128,256): the two dW buffers
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      const uint64_t pol_stream = policy_evict_first();
+      const uint64_t pol_keep = policy_evict_last();
+      if constexpr (XT_RES) {
+        mbar_arrive_expect_tx(xt_full, p.kc_count * C::kBox);
+        for (int kc = 0; kc < p.kc_count; ++kc)
+          tma_load_2d_hint(xt_s + kc * C::kBox, &tm_xt, xt_full, kc * C::kBoxK, j * 128, pol_keep);
+      }
+      int ws = 0, ks = 0;
+      uint32_t wph = 0, kph = 0;
+      for (int tile = r0; tile < p.num_tiles; tile += R) {
+        mbar_wait(&w_empty[ws], wph ^ 1);
+        mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
+#pragma unroll
+        for (int b = 0; b < C::kWBoxes; ++b)
+          tma_load_2d_hint(w_s + ws * C::kWBytes + b * C::kBox, &tm_w, &w_full[ws],
+                           j * 128 + b * C::kBoxK, tile * 128, pol_stream);
+        if (++ws == 2) { ws = 0; wph ^= 1; }
+        for (int kc = 0; kc < p.kc_count; ++kc) {
+          mbar_wait(&k_empty[ks], kph ^ 1);
+          uint8_t* slot = k_s + ks * C::kKSlot;
+          mbar_arrive_expect_tx(&k_full[ks], C::kKSlot);
+          tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
+          if constexpr (!XT_RES)
+            tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], kc * C::kBoxK, j * 128, pol_keep);
+          if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    constexpr uint32_t fa = EB == 1 ? 0u : 1u;   // e4m3 : bf16
+    constexpr uint32_t idesc_dw = umma_idesc(fa, fa, false, false, 128, 128);
+    constexpr uint32_t idesc_gx = umma_idesc(fa, fa, true, true, 128, C::kBoxK);
+    if constexpr (XT_RES) mbar_wait(xt_full, 0);
+    int ws = 0, ks = 0, ds = 0;
+    uint32_t wph = 0, kph = 0, dph = 0;
+    int it = 0;
+    for (int tile = r0; tile < p.num_tiles; tile += R, ++it) {
+      mbar_wait(&w_full[ws], wph);
+      mbar_wait(&t_empty[ds], dph ^ 1);
+      tc_fence_after();
+      const uint32_t w_addr = smem_u32(w_s + ws * C::kWBytes);
+      const uint32_t d_dw = tmem_base + ds * 128;
+      for (int kc = 0; kc < p.kc_count; ++kc) {
+        mbar_wait(&k_full[ks], kph);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t g_addr = smem_u32(k_s + ks * C::kKSlot);
+          const uint32_t x_addr = XT_RES ? smem_u32(xt_s + kc * C::kBox) : g_addr + C::kBox;
+          if (p.do_update) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t ad = umma_desc_sw128(g_addr + k * 32, 16, 1024);
+              const uint64_t bd = umma_desc_sw128(x_addr + k * 32, 16, 1024);
+              if constexpr (EB == 1) mma_f8(d_dw, ad, bd, idesc_dw, (kc | k) != 0);
+              else mma_f16(d_dw, ad, bd, idesc_dw, (kc | k) != 0);
+            }
+          }
+          const int gk = kc - p.gx_kc0;
+          if (do_gx && gk >= 0 && gk < p.gx_kc_count) {
+            const uint32_t d_gx = tmem_gx + gk * C::kBoxK;
+#pragma unroll
+            for (int k = 0; k < 128 / C::kKmma; ++k) {
+              const uint64_t ad = umma_desc_sw128(w_addr + k * C::kKmma * 128, C::kBox, 1024);
+              const uint64_t bd = umma_desc_sw128(g_addr + k * C::kKmma * 128, C::kBox, 1024);
+              if constexpr (EB == 1) mma_f8(d_gx, ad, bd, idesc_gx, (it | k) != 0);
+              else mma_f16(d_gx, ad, bd, idesc_gx, (it | k) != 0);
+            }
+          }
+          mma_commit(&k_empty[ks]);
+        }
+        __syncwarp();
+        if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
+      }
+      if (elect_one()) {
+        mma_commit(&t_full[ds]);
+        mma_commit(&w_empty[ws]);
+      }
+      __syncwarp();
+      if (++ws == 2) { ws = 0; wph ^= 1; }
+      if (++ds == 2) { ds = 0; dph ^= 1; }
+    }
+    if (elect_one()) mma_commit(gx_full);
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    const int row = q * 32 + lane_id();
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    bool bad = false;
+    int ws = 0, ds = 0;
+    uint32_t wph = 0, dph = 0;
+    for (int tile = r0; tile < p.num_tiles; tile += R) {
+      mbar_wait(&t_full[ds], dph);
+      mbar_wait(&w_full[ws], wph);
+      tc_fence_after();
+      if (p.do_update) {
+        const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
+        const bool row_ok = grow < p.rows;
+        const uint8_t* wsm = w_s + ws * C::kWBytes;
+        uint8_t* gdst = p.W + grow * p.d * EB;
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c0 = half * 64 + cc * 32;          // column within the d-tile
+          uint32_t r[32];
+          tmem_ld32(tmem_base + lane_off + ds * 128 + c0, r);
+          tmem_ld_wait();
+          float dw[32];
+#pragma unroll
+          for (int k = 0; k < 32; ++k) dw[k] = __uint_as_float(r[k]) * p.dw_scale;
+          bwd_update_row_chunk<EB>(p, dw, wsm, row, c0, grow, static_cast<int64_t>(j) * 128 + c0,
+                                   row_ok, bad, gdst);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) {
+        mbar_arrive(&t_empty[ds]);
+        mbar_arrive(&w_empty[ws]);
+      }
+      if (++ws == 2) { ws = 0; wph ^= 1; }
+      if (++ds == 2) { ds = 0; dph ^= 1; }
+    }
+    if (bad) atomicOr(p.status, ST_NONFINITE_GRAD);
+    if (do_gx) {
+      mbar_wait(gx_full, 0);
+      tc_fence_after();
+      const int ncols = p.gx_kc_count * C::kBoxK;
+      const int per_half = ncols / 2;
+      float* dst = p.gx_ws + (static_cast<int64_t>(r0) * p.d + j * 128 + row) * p.gx_ld;
+#pragma unroll 1
+      for (int c0 = half * per_half; c0 < (half + 1) * per_half; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_gx + lane_off + c0, r);
+        tmem_ld_wait();
+        uint4* o = reinterpret_cast<uint4*>(dst + c0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// One thread: 32 consecutive columns [c0, c0+32) of its row.
+// W_old comes from the swizzled smem tile, W_new goes straight to HBM.
+template <int EB>
+XMC_DEV void bwd_update_row_chunk(const BwdParams& p, const float (&dw)[32], const uint8_t* wsm,
+                                  int row, int c0, int64_t grow, int64_t gcol0, bool row_ok, bool& bad,
+                                  uint8_t* gdst) {
+  float w[32];
+  if constexpr (EB == 1) {
+    // 32 bytes = two 16-B chunks of the 128-B swizzled row
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cidx = (c0 >> 4) + h;
+      const uint4 v = *reinterpret_cast<const uint4*>(wsm + row * 128 + ((cidx ^ (row & 7)) << 4));
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 a = dec_e4m3x2(static_cast<uint16_t>(wv[k] & 0xFFFF));
+        const float2 b = dec_e4m3x2(static_cast<uint16_t>(wv[k] >> 16));
+        w[h * 16 + 4 * k + 0] = a.x;
+        w[h * 16 + 4 * k + 1] = a.y;
+        w[h * 16 + 4 * k + 2] = b.x;
+        w[h * 16 + 4 * k + 3] = b.y;
+      }
+    }
+  } else {
+    // bf16: columns [c0, c0+32) live in box c0/64, 64 B = four 16-B chunks
+    const uint8_t* box = wsm + (c0 >> 6) * (128 * 128);
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int cidx = ((c0 & 63) >> 3) + h;
+      const uint4 v = *reinterpret_cast<const uint4*>(box + row * 128 + ((cidx ^ (row & 7)) << 4));
+      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        w[h * 8 + 2 * k + 0] = __uint_as_float(wv[k] << 16);
+        w[h * 8 + 2 * k + 1] = __uint_as_float(wv[k] & 0xFFFF0000u);
+      }
+    }
+  }
+
+  // updated = w - lr * (g + wd * w), fp32, one rounding (optimizers.py:71-73)
+  float u[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    bad |= !(fabsf(dw[k]) <= 3.4028234663852886e38f);
+    const float g = p.wd != 0.0f ? __fadd_rn(dw[k], __fmul_rn(p.wd, w[k])) : dw[k];
+    u[k] = __fsub_rn(w[k], __fmul_rn(p.lr, g));
+  }
+  if (!row_ok) return;
+
+  const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + gcol0;
+  if (p.rounding == ROUND_SR_EXACT) {
+    const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      u[k] = grid_round_stochastic(gf, u[k], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + k)));
+  }
+
+  if constexpr (EB == 1) {
+    uint32_t pk[8];
+    if (p.rounding == ROUND_SR_FAST) {
+      const uint32_t k0 = static_cast<uint32_t>(p.rng_base), k1 = static_cast<uint32_t>(p.rng_base >> 32);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint64_t ctr = static_cast<uint64_t>(flat0 + 16 * h) >> 4;
+        const U4 rb = philox4x32_10(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), 0u, 0u}, k0, k1);
+        const uint32_t rr[4] = {rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int e = h * 16 + 4 * k;
+          pk[h * 4 + k] = cvt_e4m3x4_rs(u[e + 3], u[e + 2], u[e + 1], u[e + 0], rr[k]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t lo = cvt_e4m3x2_rn(u[4 * k + 1], u[4 * k + 0]);
+        const uint32_t hi = cvt_e4m3x2_rn(u[4 * k + 3], u[4 * k + 2]);
+        pk[k] = lo | (hi << 16);
+      }
+    }
+    uint4* o = reinterpret_cast<uint4*>(gdst + gcol0);
+    o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+  } else {
+    uint32_t pk[16];
+    if (p.rounding == ROUND_SR_FAST) {
+      const uint32_t k0 = static_cast<uint32_t>(p.rng_base), k1 = static_cast<uint32_t>(p.rng_base >> 32);
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const uint64_t ctr = static_cast<uint64_t>(flat0 + 8 * h) >> 3;
+        const U4 rb = philox4x32_10(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), 1u, 0u}, k0, k1);
+        const uint32_t rr[4] = {rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) pk[h * 4 + k] = cvt_bf16x2_rs(u[h * 8 + 2 * k + 1], u[h * 8 + 2 * k], rr[k]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) pk[k] = cvt_bf16x2_rn(u[2 * k + 1], u[2 * k]);
+    }
+    uint4* o = reinterpret_cast<uint4*>(gdst + gcol0 * 2);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+  }
+}
+
+}  // namespace xmc

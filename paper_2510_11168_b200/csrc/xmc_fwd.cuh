@@ -1,0 +1,258 @@
+// Kernel 1 of a head chunk: logits S = W_c . Xq^T on tcgen05 (TMEM accumulator),
+// fused epilogue G = clip(sigmoid(S), 2^-24, 1-2^-24) - Y (positives from the
+// per-tile label-sorted list), written once to the chunk's G buffer in the
+// backward operand format.  Reference: head_forward_logits head.py:164-178 and
+// logit_gradient head.py:181-196 (also the plain-logits mode used by
+// ChunkedHead.scores head.py:109-112).
+//
+// Warp roles (persistent, one CTA per SM):
+//   warp 0      TMA producer  (W k-chunk + Xq k-chunk per stage)
+//   warp 1      MMA issuer    (one elected lane), owns the TMEM allocation
+//   warps 2..9  epilogue      (2 warps per TMEM sub-partition, each half the columns)
+#pragma once
+
+#include "xmc_ptx.cuh"
+#include "xmc_round.cuh"
+
+namespace xmc {
+
+constexpr int kFwdEpiWarps = 8;
+constexpr int kFwdThreads = 64 + kFwdEpiWarps * 32;
+
+struct FwdParams {
+  int32_t rows;        // labels in this chunk
+  int32_t B;           // valid samples
+  int32_t d;           // feature dim (multiple of 128 B / elem)
+  int32_t num_tiles;   // ceil(rows / 128)
+  int32_t mode;        // 0: write quantized G; 1: write fp32 logits
+  int32_t g_fmt;       // FMT_E4M3 (scaled by g_scale) or FMT_BF16
+  float g_scale;       // 256 for e4m3 G, 1 for bf16 G
+  const int32_t* tile_ptr;   // [num_tiles + 1] into entries (chunk-local tiles)
+  const uint32_t* entries;   // (row_in_tile << 16) | sample
+  void* out;                 // G [rows][ld] or logits fp32 [rows][ld]
+  int64_t ld;                // leading dimension (elements) of out
+  float* stats;              // [0] += sum |G| over valid entries
+  const int32_t* status;     // nonzero abort bits -> no-op
+};
+
+template <int EB, int BN>
+struct FwdCfg {
+  static constexpr int kBoxK = 128 / EB;                  // K elements per 128-B swizzle atom
+  static constexpr int kWBytes = 128 * 128;               // W box: 128 rows x 128 B
+  static constexpr int kXBoxRows = BN > 256 ? 256 : BN;
+  static constexpr int kXBoxes = BN / kXBoxRows;
+  static constexpr int kXBytes = BN * 128;
+  static constexpr int kStageBytes = kWBytes + kXBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
+  static constexpr int kAccStages = (2 * BN <= 512) ? 2 : 1;
+  static constexpr int kTmemCols = (BN * kAccStages) <= 128 ? 128 : ((BN * kAccStages) <= 256 ? 256 : 512);
+  static constexpr int kWordsPerRow = BN / 32;
+  static constexpr int kBitmapBytes = 128 * kWordsPerRow * 4;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 2 * kBitmapBytes + 256;
+  static constexpr int kMmaN = BN > 256 ? 256 : BN;
+};
+
+template <int EB, int BN>
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    xmc_fwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                   FwdParams p) {
+  using C = FwdCfg<EB, BN>;
+  if (*p.status != 0) return;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* stage_base = smem;
+  uint32_t* bitmaps = reinterpret_cast<uint32_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + 2 * C::kBitmapBytes);
+  uint64_t* full = bars;                          // [kStages]
+  uint64_t* empty = bars + C::kStages;            // [kStages]
+  uint64_t* tfull = bars + 2 * C::kStages;        // [kAccStages]
+  uint64_t* tempty = tfull + C::kAccStages;       // [kAccStages]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kAccStages);
+
+  const uint32_t warp = warp_id_sync();
+  const int kc_count = p.d / C::kBoxK;
+
+  if (warp == 0 && elect_one()) {
+    prefetch_tmap(&tm_w);
+    prefetch_tmap(&tm_x);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < C::kAccStages; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kFwdEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      const uint64_t pol_w = policy_evict_first();
+      const uint64_t pol_x = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        for (int kc = 0; kc < kc_count; ++kc) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sb = stage_base + stage * C::kStageBytes;
+          mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+          tma_load_2d_hint(sb, &tm_w, &full[stage], kc * C::kBoxK, tile * 128, pol_w);
+#pragma unroll
+          for (int xb = 0; xb < C::kXBoxes; ++xb)
+            tma_load_2d_hint(sb + C::kWBytes + xb * C::kXBoxRows * 128, &tm_x, &full[stage],
+                             kc * C::kBoxK, xb * C::kXBoxRows, pol_x);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = (EB == 1) ? umma_idesc(0, 0, false, false, 128, C::kMmaN)
+                                         : umma_idesc(1, 1, false, false, 128, C::kMmaN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kc = 0; kc < kc_count; ++kc) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(stage_base + stage * C::kStageBytes);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = umma_desc_sw128(sa + k * 32, 16, 1024);
+#pragma unroll
+            for (int xb = 0; xb < C::kXBoxes; ++xb) {
+              const uint64_t bd = umma_desc_sw128(sa + C::kWBytes + xb * C::kXBoxRows * 128 + k * 32, 16, 1024);
+              if constexpr (EB == 1)
+                mma_f8(d_tmem + xb * 256, ad, bd, idesc, (kc | k) != 0);
+              else
+                mma_f16(d_tmem + xb * 256, ad, bd, idesc, (kc | k) != 0);
+            }
+          }
+          mma_commit(&empty[stage]);
+          if (kc == kc_count - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+      }
+      if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 2;                 // 0..7
+    const int q = warp & 3;                  // TMEM sub-partition of this warp
+    const int half = ew >> 2;                // column half
+    const int row = q * 32 + lane_id();      // row within the 128-label tile
+    const int etid = ew * 32 + lane_id();    // 0..255
+    constexpr int kHalfCols = BN / 2;
+    constexpr int kChunks = kHalfCols / 32;
+    const float SIG_LO = 5.9604644775390625e-08f;        // 2^-24
+    const float SIG_HI = 0.99999994039535522461f;        // 1 - 2^-24
+    float abs_sum = 0.f;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
+      // positives of this tile -> bitmap (rows x BN bits)
+      uint32_t* bm = bitmaps + (it & 1) * (128 * C::kWordsPerRow);
+      for (int w = etid; w < 128 * C::kWordsPerRow; w += kFwdEpiWarps * 32) bm[w] = 0u;
+      named_bar_sync(1, kFwdEpiWarps * 32);
+      if (p.mode == 0 && p.tile_ptr != nullptr) {
+        const int e0 = p.tile_ptr[tile], e1 = p.tile_ptr[tile + 1];
+        for (int e = e0 + etid; e < e1; e += kFwdEpiWarps * 32) {
+          const uint32_t v = p.entries[e];
+          const uint32_t r = v >> 16, s = v & 0xFFFFu;
+          atomicOr(&bm[r * C::kWordsPerRow + (s >> 5)], 1u << (s & 31));
+        }
+      }
+      named_bar_sync(1, kFwdEpiWarps * 32);
+
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
+      const bool row_ok = grow < p.rows;
+#pragma unroll 1
+      for (int cc = 0; cc < kChunks; ++cc) {
+        const int col0 = half * kHalfCols + cc * 32;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, r);
+        tmem_ld_wait();
+        if (p.mode == 1) {
+          if (row_ok) {
+            float* o = reinterpret_cast<float*>(p.out) + grow * p.ld;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < p.B) o[col0 + j] = __uint_as_float(r[j]);
+          }
+          continue;
+        }
+        const uint32_t pos = bm[row * C::kWordsPerRow + (col0 >> 5)];
+        float g[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float z = __uint_as_float(r[j]);
+          // 1 / (1 + exp(-z)) with ex2.approx / rcp.approx (rel. err ~2^-22)
+          float sg = fast_rcp(1.0f + fast_ex2(-z * 1.4426950408889634f));
+          sg = sg < SIG_LO ? SIG_LO : sg;  // NaN propagates like np.clip
+          sg = sg > SIG_HI ? SIG_HI : sg;
+          if ((pos >> j) & 1u) sg -= 1.0f;
+          sg = (col0 + j < p.B) ? sg : 0.0f;
+          abs_sum += row_ok ? fabsf(sg) : 0.0f;
+          g[j] = sg * p.g_scale;
+        }
+        if (row_ok) {
+          if (p.g_fmt == FMT_E4M3) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t lo = cvt_e4m3x2_rn(g[4 * j + 1], g[4 * j + 0]);
+              const uint32_t hi = cvt_e4m3x2_rn(g[4 * j + 3], g[4 * j + 2]);
+              pk[j] = lo | (hi << 16);
+            }
+            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out) + grow * p.ld + col0);
+            o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          } else {
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pk[j] = cvt_bf16x2_rn(g[2 * j + 1], g[2 * j]);
+            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + grow * p.ld + col0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
+    }
+    // one atomic per warp per CTA
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) abs_sum += __shfl_xor_sync(0xffffffffu, abs_sum, o);
+    if (lane_id() == 0 && p.stats != nullptr && p.mode == 0) atomicAdd(p.stats, abs_sum);
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace xmc

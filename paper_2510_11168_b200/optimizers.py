@@ -1,0 +1,88 @@
+"""SGD with one rounding onto the storage grid -- mirror of lpxmc.optimizers.
+
+``SgdSrConfig`` keeps the reference fields and validation
+(optimizers.py:28-41) and adds ``sr_impl``: the draw generator used when
+``rounding == "stochastic"``.
+
+* ``"philox"`` (default, the fast product path): Philox4x32-10 random bits
+  fed to the sm_100a hardware stochastic-rounding conversion (cvt.rs).  SR
+  decisions match the reference in distribution (unbiased, same variance).
+* ``"splitmix64"``: the reference's own keyed generator (rng.py:36-57) and
+  fp64 neighbour/probability comparison (formats.py:209-225).  Given the same
+  fp32 update value the decision is bit-identical to the reference.
+
+``sgd_sr_step`` (optimizers.py:51-74) runs elementwise on the GPU on
+float32 on-grid values, bit-exact with the reference for both rounding modes.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from .formats import FP32, FloatFormat, _f32_cuda, _index_tensor
+
+
+@dataclass
+class SgdSrConfig:
+    lr: float
+    weight_decay: float = 0.0
+    fmt: FloatFormat = field(default_factory=lambda: FP32)
+    rounding: str = "stochastic"  # or "nearest"
+    sr_impl: str = "philox"       # or "splitmix64" (bit-exact reference draws)
+
+    def __post_init__(self):
+        if self.lr <= 0:
+            raise ValueError("lr must be positive")
+        if self.weight_decay < 0:
+            raise ValueError("weight_decay must be non-negative")
+        if self.rounding not in ("stochastic", "nearest"):
+            raise ValueError(f"unknown rounding mode {self.rounding!r}")
+        if self.sr_impl not in ("philox", "splitmix64"):
+            raise ValueError(f"unknown SR generator {self.sr_impl!r}")
+
+    @property
+    def rounding_code(self) -> int:
+        if self.rounding == "nearest":
+            return _lib.ROUND_NEAREST
+        return _lib.ROUND_SR_FAST if self.sr_impl == "philox" else _lib.ROUND_SR_EXACT
+
+
+def sgd_sr_step(w: torch.Tensor, grad, cfg: SgdSrConfig, rng, step: int, tensor_id: int = 0,
+                global_index=None) -> torch.Tensor:
+    """w <- ROUND(w - lr*(grad + wd*w)), in place on a float32 CUDA tensor of
+    on-grid values (optimizers.py:51-74).  Stochastic rounding always uses the
+    reference's splitmix64 keys here (bit-exact)."""
+    if not (w.is_cuda and w.dtype == torch.float32 and w.is_contiguous()):
+        raise ValueError("w must be a contiguous float32 CUDA tensor")
+    g = _f32_cuda(grad)
+    if tuple(g.shape) != tuple(w.shape):
+        raise ValueError(f"shape mismatch: weights {tuple(w.shape)}, grad {tuple(g.shape)}")
+    idx = _index_tensor(global_index, w.numel(), w.device)
+    rmode = _lib.ROUND_NEAREST if cfg.rounding == "nearest" else _lib.ROUND_SR_EXACT
+    _lib.check(_lib.load().xmc_sgd_sr_step(
+        cfg.fmt.grid(), w.data_ptr(), g.data_ptr(), w.numel(), cfg.lr, cfg.weight_decay, rmode,
+        rng.seed, step & (2**64 - 1), tensor_id & (2**64 - 1), _lib.ptr(idx), None,
+        _lib.stream_ptr()))
+    return w
+
+
+def kahan_sgd_step(w: torch.Tensor, comp: torch.Tensor, grad, cfg: SgdSrConfig, rng, step: int,
+                   tensor_id: int = 0, global_index=None):
+    """Head-Kahan SGD: kahan_add (formats.py:246-263) of the
+    SGD update onto the grid, ROUND = RTN or keyed SR; float32 w and comp."""
+    for t in (w, comp):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise ValueError("w and comp must be contiguous float32 CUDA tensors")
+    g = _f32_cuda(grad)
+    if tuple(g.shape) != tuple(w.shape) or tuple(comp.shape) != tuple(w.shape):
+        raise ValueError("shape mismatch")
+    idx = _index_tensor(global_index, w.numel(), w.device)
+    rmode = _lib.ROUND_NEAREST if cfg.rounding == "nearest" else _lib.ROUND_SR_EXACT
+    _lib.check(_lib.load().xmc_kahan_sgd_step(
+        cfg.fmt.grid(), w.data_ptr(), comp.data_ptr(), g.data_ptr(), w.numel(), cfg.lr,
+        cfg.weight_decay, rmode, rng.seed, step & (2**64 - 1), tensor_id & (2**64 - 1),
+        _lib.ptr(idx), None, _lib.stream_ptr()))
+    return w, comp

@@ -116,7 +116,7 @@ def main():
     cases = [("bf16", "nearest", 1, 0.0, 0.0), ("bf16", "stochastic", 3, 1e-4, 0.0),
              ("e4m3", "nearest", 2, 1e-4, 0.0), ("e4m3", "stochastic", 1, 0.0, 0.0),
              ("e4m3", "stochastic", 4, 1e-4, 0.0), ("bf16", "stochastic", 1, 0.0, 0.1)]
-    L, d, b = 300, 64, 16
+    L, d, b = 300, 128, 16
     for ci, (name, rmode, k, wd, p) in enumerate(cases):
         fmt = F.parse_format(name)
         head = H.ChunkedHead.create(L, d, fmt, seed=ci, num_chunks=k, dropout_p=p)
