@@ -1,0 +1,380 @@
+"""Benchmark of the ELMO head step on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[3]): Amazon-3M shape,
+L = 2,812,281 labels, d = 768, batch 256, FP8 e4m3 weights, SR on (Philox +
+cvt.rs), lr 0.05, wd 1e-4, dropout 0, synthetic data: W0 ~ N(0, 0.02^2) RTN to
+e4m3, X ~ N(0, 1), positives per sample max(1, Poisson(36.17)) distinct labels
+drawn Zipf(1.0).  Labels are sharded contiguously across ranks (strong
+scaling: the 3M-label problem is fixed, each rank owns L/N rows).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints one JSON line (rank 0).  `value` is device-timed samples/s with inputs
+resident in HBM (W = 2.16 GB >> L2, so no flush is needed); `e2e` is the same
+metric through the public API with host inputs copied in and grad_X copied
+out every step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_MEAN_LABELS = {2_812_281: 36.17, 670_091: 5.45, 131_073: 5.15, 8_623_847: 9.03}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--labels", type=int, default=2_812_281)
+    ap.add_argument("--dim", type=int, default=768)
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--fmt", default="e4m3")
+    ap.add_argument("--chunks", type=int, default=8)
+    ap.add_argument("--rounding", default="stochastic")
+    ap.add_argument("--sr-impl", default="philox")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-labels", type=int, default=8192)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------- synthetic data
+
+def synthetic_positives(num_labels, batch, mean_labels, seed=0):
+    """max(1, Poisson(mean)) distinct labels per sample, Zipf(1.0) over [0, L)."""
+    rng = np.random.default_rng(seed)
+    p = 1.0 / np.arange(1, num_labels + 1, dtype=np.float64)
+    cdf = np.cumsum(p)
+    cdf /= cdf[-1]
+    rows, cols = [], []
+    for i in range(batch):
+        n = min(max(1, int(rng.poisson(mean_labels))), num_labels)
+        chosen = set()
+        while len(chosen) < n:
+            for lab in np.minimum(np.searchsorted(cdf, rng.random(2 * n), side="right"), num_labels - 1):
+                if len(chosen) < n:
+                    chosen.add(int(lab))
+        for lab in sorted(chosen):
+            rows.append(i)
+            cols.append(lab)
+    return np.array(rows, np.int64), np.array(cols, np.int64)
+
+
+# ------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- peaks
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    if os.path.exists(path):
+        with open(path) as f:
+            peaks.update(json.load(f))
+        peaks["source"] = "measured"
+    fp8 = os.path.join(ROOT, "profiles", "fp8_peak.json")
+    if os.path.exists(fp8):
+        with open(fp8) as f:
+            peaks["fp8"] = json.load(f)
+    return peaks
+
+
+# ------------------------------------------------------------- CPU baseline
+
+def cpu_baseline(a, seconds):
+    """The reference algorithm (oracle/lpxmc_oracle.py, numpy restatement of
+    lpxmc.head.head_update) on a bounded label slice of the same workload,
+    extrapolated linearly in L (time is linear in L)."""
+    from oracle import lpxmc_oracle as O
+    Ls = min(a.cpu_labels, a.labels)
+    fmt = O.parse_format(a.fmt)
+    rs = np.random.default_rng(0)
+    W = O.round_nearest(fmt, rs.normal(scale=0.02, size=(Ls, a.dim)).astype(np.float32))
+    X = rs.normal(size=(a.batch, a.dim)).astype(np.float32)
+    mean = PAPER_MEAN_LABELS.get(a.labels, 5.0)
+    si, li = synthetic_positives(a.labels, a.batch, mean, seed=1)
+    keep = li < Ls
+    head = O.OracleHead(W, fmt, max(1, round(a.chunks * Ls / a.labels)))
+    cfg = O.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt, rounding=a.rounding)
+    rng = O.RoundingRng(0)
+    O.head_update(head, X, si[keep], li[keep], cfg, rng, 0)  # warm-up
+    times, step = [], 1
+    t_end = time.perf_counter() + seconds
+    while time.perf_counter() < t_end or len(times) < 2:
+        t0 = time.perf_counter()
+        O.head_update(head, X, si[keep], li[keep], cfg, rng, step)
+        times.append(time.perf_counter() - t0)
+        step += 1
+    t_slice = statistics.median(times)
+    t_full = t_slice * a.labels / Ls
+    return {"value": a.batch / t_full, "unit": "samples/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"oracle head_update on {Ls} of {a.labels} labels (d={a.dim}, B={a.batch}, {a.fmt}, "
+                      f"{a.rounding}), median of {len(times)} steps = {t_slice:.3f} s, x{a.labels / Ls:.1f} "
+                      f"linear in L; numpy/OpenBLAS on {os.cpu_count()} host threads",
+            "s_per_step_full": t_full}
+
+
+# ------------------------------------------------------------- main
+
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    metric = "head train samples/sec at 3M labels FP8"
+    config = {"workload": f"Amazon-3M head step: L={a.labels}, d={a.dim}, B={a.batch}, {a.fmt} weights, "
+                          f"k={a.chunks} chunks, SR={a.rounding}/{a.sr_impl}, lr=0.05, wd=1e-4",
+              "labels": a.labels, "dim": a.dim, "global_batch": a.batch, "chunks": a.chunks,
+              "parallelism": f"label-shard x{world}", "l2": "inputs larger than L2 (W >> 126 MB)"}
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_baseline(a, a.cpu_seconds)
+        out = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": "samples/s",
+               "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": a.fmt, "data": "synthetic",
+               "config": config, "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+               "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2510_11168_b200 as xmc
+    from paper_2510_11168_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    lo, hi = xmc.partition(a.labels, world)[rank]
+    fmt = xmc.parse_format(a.fmt)
+
+    # weights: N(0, 0.02^2) generated on device in blocks and RTN-cast to the grid
+    W = torch.empty((hi - lo, a.dim), dtype=fmt.torch_dtype, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    blk = 262_144
+    for r0 in range(0, hi - lo, blk):
+        r1 = min(r0 + blk, hi - lo)
+        W[r0:r1] = xmc.cast_native(torch.randn((r1 - r0, a.dim), generator=g, device=dev) * 0.02, fmt)
+    head = xmc.ChunkedHead(xmc.QuantizedMatrix(W, fmt), num_chunks=a.chunks, num_labels_global=a.labels,
+                           label_offset=lo)
+    rs = np.random.default_rng(0)
+    Xh = rs.normal(size=(a.batch, a.dim)).astype(np.float32)
+    si, li = synthetic_positives(a.labels, a.batch, PAPER_MEAN_LABELS.get(a.labels, 5.0), seed=1)
+    cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt, rounding=a.rounding, sr_impl=a.sr_impl)
+    rng = xmc.RoundingRng(0)
+    Xd = torch.from_numpy(Xh).to(dev)
+    sid = torch.from_numpy(si.astype(np.int32)).to(dev)
+    lid = torch.from_numpy(li.astype(np.int32)).to(dev)
+    batch_dev = xmc.BatchInput(Xd, sid, lid)
+    gx = torch.empty((a.batch, a.dim), dtype=torch.float32, device=dev)
+
+    def step_fn(s, batch, out):
+        r = xmc.head_update(head, batch, cfg, rng, s, check=False, grad_out=out)
+        if world > 1:
+            dist.all_reduce(r)
+        return r
+
+    torch.cuda.reset_peak_memory_stats(dev)
+    mem0 = torch.cuda.memory_allocated(dev)
+    for s in range(a.warmup):
+        step_fn(s, batch_dev, gx)
+    _lib.check(_lib.load().xmc_head_check(head.handle(a.batch, len(si)).h, _lib.stream_ptr()))
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device-resident inputs)
+    stream = torch.cuda.current_stream()
+    clocks = ClockSampler(local)
+    _lib.profile_read()
+    _lib.profile_enable(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for s in range(a.steps):
+        step_fn(a.warmup + s, batch_dev, gx)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    _lib.profile_enable(False)
+    ms_fwd, n_fwd, ms_bwd, n_bwd = _lib.profile_read()
+    t_ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_ms = float(t.item())
+    peak_mem = torch.cuda.max_memory_allocated(dev) - mem0 + W.numel() * W.element_size()
+    _lib.check(_lib.load().xmc_head_check(head.handle(a.batch, len(si)).h, _lib.stream_ptr()))
+
+    # ---------------- end-to-end through the public API, host buffers
+    Xp = torch.from_numpy(Xh).pin_memory()
+    sip = torch.from_numpy(si.astype(np.int32)).pin_memory()
+    lip = torch.from_numpy(li.astype(np.int32)).pin_memory()
+    gxh = torch.empty((a.batch, a.dim), dtype=torch.float32).pin_memory()
+    Xe = torch.empty_like(Xd)
+    sie = torch.empty_like(sid)
+    lie = torch.empty_like(lid)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for s in range(a.e2e_steps):
+        Xe.copy_(Xp, non_blocking=True)
+        sie.copy_(sip, non_blocking=True)
+        lie.copy_(lip, non_blocking=True)
+        r = step_fn(10_000 + s, xmc.BatchInput(Xe, sie, lie), gx)
+        gxh.copy_(r, non_blocking=True)
+        stream.synchronize()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item()) / a.e2e_steps
+
+    # ---------------- roofline of the dominant kernel
+    peaks = load_peaks()
+    L_r, B, D = hi - lo, a.batch, a.dim
+    eb = 1 if a.fmt == "e4m3" else 2
+    Bp = 128 if (eb == 1 and B <= 128) else (256 if eb == 1 else max(64, 1 << (B - 1).bit_length()))
+    per_step = {"fwd": (ms_fwd / max(a.steps, 1), n_fwd // max(a.steps, 1)),
+                "bwd": (ms_bwd / max(a.steps, 1), n_bwd // max(a.steps, 1))}
+    dom = "bwd" if ms_bwd >= ms_fwd else "fwd"
+    n_launch = max(per_step[dom][1], 1)
+    ms_launch = per_step[dom][0] / n_launch
+    rows_launch = L_r / n_launch
+    if dom == "bwd":   # grad_X + dW GEMMs, W read+write, G read once per d-tile group
+        flops = 4.0 * B * rows_launch * D
+        bytes_ = 2.0 * rows_launch * D * eb + rows_launch * Bp * eb
+    else:              # logits GEMM, W read, G write
+        flops = 2.0 * B * rows_launch * D
+        bytes_ = rows_launch * D * eb + rows_launch * Bp * eb
+    # kernels are timed inside a long step loop -> the SUSTAINED peaks apply
+    fp8 = peaks.get("fp8", {})
+    tc_peak = (fp8.get("tflops_sustained") if eb == 1 and fp8 else None)
+    tc_src = ("measured fp8 sustained: " + fp8.get("how", "")) if tc_peak else ""
+    if tc_peak is None:
+        tc_peak = peaks["bf16_tflops_sustained"] * (2.0 if eb == 1 else 1.0)
+        tc_src = ("2x measured bf16 sustained (no measured fp8)" if eb == 1 else "measured bf16 sustained") \
+            + f" [{peaks['source']}]"
+    t_tc = flops / (tc_peak * 1e12)
+    t_hbm = bytes_ / (peaks["hbm_gbs"] * 1e9)
+    bound = "tensor" if t_tc >= t_hbm else "hbm"
+    if bound == "tensor":
+        achieved = flops / (ms_launch * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+                "frac": achieved / tc_peak}
+    else:
+        achieved = bytes_ / (ms_launch * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"]}
+    roof.update({"kernel": "xmc_bwd_kernel (grad_X + dW + SGD/SR update)" if dom == "bwd"
+                 else "xmc_fwd_kernel (logits + sigmoid - Y)", "traffic": None,
+                 "ms_per_launch": ms_launch, "launches_per_step": n_launch,
+                 "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": bytes_,
+                 "peak_source": tc_src if bound == "tensor" else f"hbm {peaks['source']}",
+                 "step_kernel_ms": {"fwd": per_step["fwd"][0], "bwd": per_step["bwd"][0]}})
+    step_flops = 6.0 * B * a.labels * D
+    ms_step = t_ms / a.steps
+    value = B * a.steps / (t_ms * 1e-3)
+    out = {"metric": metric, "value": value, "unit": "samples/s", "n_gpus": world, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": a.fmt, "data": "synthetic", "config": config,
+           "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "samples/s",
+                   "h2d_bytes_per_step": int(Xh.nbytes + 8 * len(si)),
+                   "d2h_bytes_per_step": int(B * D * 4), "ms_per_step": e2e_ms},
+           "roofline": roof,
+           "step_tflops": step_flops / (ms_step * 1e-3) / 1e12,
+           "step_frac_of_tc_peak": step_flops / (ms_step * 1e-3) / 1e12 / (tc_peak * world),
+           "peak_hbm_gib_per_gpu": peak_mem / 2**30,
+           "gpu_launches": (4 + 3 * a.chunks) * a.steps,
+           "clocks": clk}
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cb = cpu_baseline(a, a.cpu_seconds)
+        out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -456,7 +456,7 @@ __global__ void pos_scatter_kernel(PosGeom g, const int32_t* __restrict__ ps, co
 }
 
 // grad_x[s][c] += sum_r ws[r][c][s - col0]   (fixed r order: deterministic)
-__global__ void gx_reduce_kernel(const float* __restrict__ ws, int R, int d, int ld, int col0, int ncols, int B,
+__global__ void gx_reduce_kernel(const float* __restrict__ ws, int R, int d, int ld, int col0, int ncols, int B, float scale,
                                  float* __restrict__ gx) {
   __shared__ float tile[32][33];
   const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
@@ -465,7 +465,7 @@ __global__ void gx_reduce_kernel(const float* __restrict__ ws, int R, int d, int
     float acc = 0.f;
     if (sl < ncols)
       for (int r = 0; r < R; ++r) acc += ws[((int64_t)r * d + c) * ld + sl];
-    tile[i][threadIdx.x] = acc;
+    tile[i][threadIdx.x] = acc * scale;
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -607,7 +607,7 @@ static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, i
   if (s != XMC_OK) return s;
   if (gx_kc_count > 0 && acc) {
     dim3 g(D / 32, (p.gx_ld + 31) / 32), b(32, 8);
-    gx_reduce_kernel<<<g, b, 0, st>>>(h->gx_ws, R, D, p.gx_ld, gx_kc0 * box_k, p.gx_ld, B, acc);
+    gx_reduce_kernel<<<g, b, 0, st>>>(h->gx_ws, R, D, p.gx_ld, gx_kc0 * box_k, p.gx_ld, B, p.dw_scale, acc);
     CUDA_TRY(cudaGetLastError());
   }
   return XMC_OK;

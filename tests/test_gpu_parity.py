@@ -37,6 +37,24 @@ def ulp_dist(a, b, fmt):
     return np.abs(a - b) / O._ulp_of(fmt, np.maximum(np.abs(a), np.abs(b)))
 
 
+def assert_update_within_bound(got, ref, fmt, lr, Xq, G_gpu, G_ref=None, wd=0.0):
+    """Per-element bound for W_new = ROUND(w - lr (G.Xq + wd w)) computed from
+    two gradients: one grid ulp (RTN / SR with the same draw) plus lr times
+    the dW difference, i.e. |G_gpu - G_ref| . |Xq| (operand quantisation) and
+    an fp32 accumulation-order term 2^-17 |G| . |Xq| (tensor-core vs BLAS
+    summation order; it dominates only where dW cancels to ~0)."""
+    Xa = np.abs(np.asarray(Xq, np.float64))
+    Ga = np.abs(np.asarray(G_gpu, np.float64))
+    err = 2.0 ** -17 * (Ga @ Xa)
+    if G_ref is not None:
+        err += np.abs(np.asarray(G_gpu, np.float64) - np.asarray(G_ref, np.float64)) @ Xa
+    ulp = O._ulp_of(fmt, np.maximum(np.abs(got), np.abs(ref)).astype(np.float64))
+    bound = ulp + lr * err * 1.01 + 1e-30
+    diff = np.abs(np.asarray(got, np.float64) - np.asarray(ref, np.float64))
+    bad = diff > bound
+    assert not bad.any(), (int(bad.sum()), float((diff / bound).max()))
+
+
 # ------------------------------------------------------------ numeric core
 
 @pytest.mark.parametrize("name", ["bf16", "e4m3", "e5m2", "fp16", "e3m2", "e2m1"])
@@ -201,9 +219,9 @@ def test_fused_update_matches_oracle_on_operand_G(xmc, fmt_name, B, rmode, impl)
     ref = oh.values
     same = np.mean(bits(got) == bits(ref))
     # fp32 dot products differ from numpy only in accumulation order: rare
-    # one-ulp flips at rounding boundaries, never more than one ulp
+    # one-ulp flips at rounding boundaries (bounded as documented above)
     assert same > 0.995, same
-    assert ulp_dist(got, ref, fmt).max() <= 1.0 + 1e-9
+    assert_update_within_bound(got, ref, fmt, 0.05, Xq, Gq)
 
 
 @pytest.mark.parametrize("ci", range(6))
@@ -227,12 +245,16 @@ def test_head_update_matches_reference_golden(xmc, ci):
     np.testing.assert_allclose(gx.cpu().numpy(), gx_o, rtol=1e-4, atol=1e-4)
     got = head.weights.values.float().cpu().numpy()
     assert np.mean(bits(got) == bits(oh.values)) > 0.99
-    assert ulp_dist(got, oh.values, ofmt).max() <= 1.0 + 1e-9
-    # (b) against the reference's own fp32-G result: G quantisation tolerance
-    ref = GOLD[p + "W1"]
-    assert ulp_dist(got, ref, ofmt).max() <= 1.0 + 1e-9
-    g_tol = 0.1 if c["fmt"] == "e4m3" else 0.02
-    np.testing.assert_allclose(gx.cpu().numpy(), GOLD[p + "gradX1"], rtol=g_tol, atol=g_tol)
+    Xq = O.round_nearest(ofmt, GOLD[p + "X"])
+    W0 = GOLD[p + "W0"]
+    G = O.logit_gradient(W0 @ Xq.T, GOLD[p + "sample_idx"], GOLD[p + "label_idx"], (0, W0.shape[0]))
+    Gq = O.quantize_g_operand(G, ofmt)
+    assert_update_within_bound(got, oh.values, ofmt, c["lr"], Xq, Gq)
+    # (b) against the reference's own fp32-G result: the bound adds the
+    # G operand-quantisation term |Gq - G| . |Xq|
+    assert_update_within_bound(got, GOLD[p + "W1"], ofmt, c["lr"], Xq, Gq, G_ref=G)
+    gx_bound = np.abs(Gq - G).T @ np.abs(W0) + 1e-4
+    assert np.all(np.abs(gx.cpu().numpy() - GOLD[p + "gradX1"]) <= gx_bound * 1.01)
 
 
 @pytest.mark.parametrize("fmt_name,B", [("e4m3", 256), ("bf16", 128)])
