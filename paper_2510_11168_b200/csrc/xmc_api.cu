@@ -531,7 +531,6 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t r
   p.num_tiles = static_cast<int32_t>(cdiv(rows, 128));
   p.mode = mode;
   p.g_fmt = eb == 1 ? FMT_E4M3 : FMT_BF16;
-  p.g_scale = eb == 1 ? 256.0f : 1.0f;
   p.tile_ptr = tile_ptr;
   p.entries = h->entries;
   p.out = out;
@@ -581,7 +580,6 @@ static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, i
   p.do_update = update ? 1 : 0;
   p.gx_kc0 = gx_kc0;
   p.gx_kc_count = gx_kc_count;
-  p.W = static_cast<uint8_t*>(W) + row0 * D * eb;
   p.row0_global = h->desc.label_offset + row0;
   p.lr = a ? a->lr : 0.f;
   p.wd = a ? a->weight_decay : 0.f;

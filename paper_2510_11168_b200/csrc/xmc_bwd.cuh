@@ -15,6 +15,13 @@
 // launch and is flushed once to a workspace (deterministic reduce afterwards).
 // The dW accumulator is double-buffered in TMEM so the update epilogue of tile
 // i overlaps the MMAs of tile i+1.  dW never leaves TMEM/registers.
+//
+// Warp roles: warp 0 TMA producer, warp 1 MMA issuer (+ TMEM owner),
+// warps 2..17 update epilogue: 4 warps per TMEM sub-partition, each owning 32
+// of the tile's 128 d-columns for its 32 label rows.  Per tile the epilogue
+// reads W_old and draws its random bits while the MMA is still running,
+// releases the dW buffer right after tcgen05.ld, writes W_new back into the
+// same swizzled smem tile and one thread TMA-stores the tile to HBM.
 #pragma once
 
 #include "xmc_ptx.cuh"
@@ -22,7 +29,7 @@
 
 namespace xmc {
 
-constexpr int kBwdEpiWarps = 8;
+constexpr int kBwdEpiWarps = 16;
 constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32;
 
 enum StatusBits : int32_t {
@@ -42,11 +49,10 @@ struct BwdParams {
   int32_t do_update;     // dW + SGD + rounding, W written in place
   int32_t gx_kc0;        // first sample k-chunk accumulated into grad_X
   int32_t gx_kc_count;   // 0 = no grad_X
-  uint8_t* W;            // chunk base (row-major rows x d, EB bytes/elem)
   int64_t row0_global;   // global label of chunk row 0 (RNG key)
   float lr, wd, dw_scale;
   int32_t rounding;      // ROUND_NEAREST / ROUND_SR_EXACT / ROUND_SR_FAST
-  uint64_t rng_base;     // splitmix64 base(seed, step, tensor_id)
+  uint64_t rng_base;     // splitmix64 base(seed, step, tensor_id); Philox key
   float* gx_ws;          // [R][d][gx_ld] fp32 partials
   int32_t gx_ld;
   int32_t* status;
@@ -58,41 +64,141 @@ struct BwdCfg {
   static constexpr int kBox = 128 * 128;             // one [128 rows x 128 B] box
   static constexpr int kWBoxes = EB;                 // d-tile of 128 elements
   static constexpr int kWBytes = kWBoxes * kBox;
-  static constexpr int kWStages = 2;
+  static constexpr int kWStages = EB == 1 ? 5 : 3;
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
-  static constexpr int kKStages = 4;
+  static constexpr int kKStages = EB == 1 ? 6 : 4;
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
-  static constexpr int kSmemBytes = 1024 + kXtBytes + kWStages * kWBytes + kKStages * kKSlot + 512;
+  static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2) + 16;
+  static constexpr int kSmemBytes = 1024 + kXtBytes + kWStages * kWBytes + kKStages * kKSlot + kBarBytes;
   static constexpr int kKmma = 32 / EB;              // K per MMA instruction (elements)
+  static constexpr int kChunks16 = 2 * EB;           // 16-B smem chunks per thread (32 elements)
+  static constexpr int kRandWords = 8 * EB;          // cvt.rs words per 32 elements
 };
 
+// byte offset of 16-B chunk `h` of this thread's 32 columns [c0, c0+32) in the
+// 128-B-swizzled W tile (one [128 x 128 B] box per 128 / EB columns)
 template <int EB>
-XMC_DEV void bwd_update_row_chunk(const BwdParams& p, const float (&dw)[32], const uint8_t* wsm_row_base,
-                                  int row_sw, int c0_local, int64_t grow, int64_t gcol0, bool row_ok,
-                                  bool& bad, uint8_t* gdst);
+XMC_DEV uint32_t w_chunk_off(int row, int c0, int h) {
+  if constexpr (EB == 1) {
+    const int cidx = (c0 >> 4) + h;
+    return row * 128 + ((cidx ^ (row & 7)) << 4);
+  } else {
+    const int cidx = ((c0 & 63) >> 3) + h;
+    return (c0 >> 6) * (128 * 128) + row * 128 + ((cidx ^ (row & 7)) << 4);
+  }
+}
+
+template <int EB>
+XMC_DEV void w_decode(const uint4 (&raw)[2 * EB], float (&w)[32]) {
+  if constexpr (EB == 1) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t wv[4] = {raw[h].x, raw[h].y, raw[h].z, raw[h].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 a = dec_e4m3x2(static_cast<uint16_t>(wv[k] & 0xFFFF));
+        const float2 b = dec_e4m3x2(static_cast<uint16_t>(wv[k] >> 16));
+        w[h * 16 + 4 * k + 0] = a.x;
+        w[h * 16 + 4 * k + 1] = a.y;
+        w[h * 16 + 4 * k + 2] = b.x;
+        w[h * 16 + 4 * k + 3] = b.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const uint32_t wv[4] = {raw[h].x, raw[h].y, raw[h].z, raw[h].w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        w[h * 8 + 2 * k + 0] = __uint_as_float(wv[k] << 16);
+        w[h * 8 + 2 * k + 1] = __uint_as_float(wv[k] & 0xFFFF0000u);
+      }
+    }
+  }
+}
+
+// Philox4x32-10 words for 32 elements starting at flat index flat0 (multiple
+// of 32).  e4m3: one word per cvt.rs.e4m3x4 (4 elements, 16 random bits per
+// lane, see profiles/r1_probe_cvt_rs.txt); bf16: one word per bf16x2.
+template <int EB>
+XMC_DEV void sr_words(uint64_t key, int64_t flat0, uint32_t (&rw)[8 * EB]) {
+  const uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
+#pragma unroll
+  for (int h = 0; h < 2 * EB; ++h) {
+    const uint64_t ctr = static_cast<uint64_t>(flat0) / (16 / EB) + h;
+    const U4 r = philox4x32_10(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), EB - 1u, 0u}, k0, k1);
+    rw[4 * h + 0] = r.x;
+    rw[4 * h + 1] = r.y;
+    rw[4 * h + 2] = r.z;
+    rw[4 * h + 3] = r.w;
+  }
+}
+
+// updated = w (1 - lr wd) - (lr * dw_scale) acc  (SGD with wd folded,
+// optimizers.py:71-73, one rounding), rounded and packed into the tile's
+// storage bytes.  FMA contraction moves the fp32 update by <= 1 fp32 ulp,
+// far below the tensor-core accumulation noise of acc.
+template <int EB>
+XMC_DEV void w_update_pack(const BwdParams& p, const uint32_t (&acc)[32], const float (&w)[32],
+                           const uint32_t (&rw)[8 * EB], int64_t flat0, uint4 (&out)[2 * EB]) {
+  const float a_lr = -p.lr * p.dw_scale;
+  const float c_wd = 1.0f - p.lr * p.wd;
+  float u[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) u[k] = fmaf(a_lr, __uint_as_float(acc[k]), w[k] * c_wd);
+  if (p.rounding == ROUND_SR_EXACT) {
+    const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      u[k] = grid_round_stochastic(gf, u[k], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + k)));
+  }
+  uint32_t pk[8 * EB];
+  if constexpr (EB == 1) {
+    if (p.rounding == ROUND_SR_FAST) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pk[k] = cvt_e4m3x4_rs(u[4 * k + 3], u[4 * k + 2], u[4 * k + 1], u[4 * k], rw[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        pk[k] = cvt_e4m3x2_rn(u[4 * k + 1], u[4 * k]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(u[4 * k + 3], u[4 * k + 2])) << 16);
+    }
+  } else {
+    if (p.rounding == ROUND_SR_FAST) {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) pk[k] = cvt_bf16x2_rs(u[2 * k + 1], u[2 * k], rw[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) pk[k] = cvt_bf16x2_rn(u[2 * k + 1], u[2 * k]);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
+}
 
 template <int EB, bool XT_RES, int KCMAX>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
                    const __grid_constant__ CUtensorMap tm_xt, BwdParams p) {
   using C = BwdCfg<EB, XT_RES, KCMAX>;
+  constexpr int WS = C::kWStages;
+  constexpr int KS = C::kKStages;
   if (*p.status != 0) return;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* xt_s = smem;
   uint8_t* w_s = smem + C::kXtBytes;
-  uint8_t* k_s = w_s + C::kWStages * C::kWBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(k_s + C::kKStages * C::kKSlot);
-  uint64_t* w_full = bars;                       // [2]
-  uint64_t* w_empty = bars + 2;                  // [2]
-  uint64_t* k_full = bars + 4;                   // [4]
-  uint64_t* k_empty = bars + 8;                  // [4]
-  uint64_t* t_full = bars + 12;                  // [2]
-  uint64_t* t_empty = bars + 14;                 // [2]
-  uint64_t* xt_full = bars + 16;
-  uint64_t* gx_full = bars + 17;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint8_t* k_s = w_s + WS * C::kWBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(k_s + KS * C::kKSlot);
+  uint64_t* w_full = bars;                 // [WS]
+  uint64_t* w_empty = w_full + WS;         // [WS]
+  uint64_t* k_full = w_empty + WS;         // [KS]
+  uint64_t* k_empty = k_full + KS;         // [KS]
+  uint64_t* t_full = k_empty + KS;         // [2]
+  uint64_t* t_empty = t_full + 2;          // [2]
+  uint64_t* xt_full = t_empty + 2;
+  uint64_t* gx_full = xt_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gx_full + 1);
 
   const uint32_t warp = warp_id_sync();
   const int j = blockIdx.x % p.dtiles;
@@ -104,15 +210,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     prefetch_tmap(&tm_w);
     prefetch_tmap(&tm_g);
     prefetch_tmap(&tm_xt);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < WS; ++s) {
       mbar_init(&w_full[s], 1);
-      mbar_init(&w_empty[s], 1 + kBwdEpiWarps);
-      mbar_init(&t_full[s], 1);
-      mbar_init(&t_empty[s], kBwdEpiWarps);
+      mbar_init(&w_empty[s], 2);   // MMA commit + the W-tile store thread
     }
-    for (int s = 0; s < C::kKStages; ++s) {
+    for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&t_full[s], 1);
+      mbar_init(&t_empty[s], kBwdEpiWarps);
     }
     mbar_init(xt_full, 1);
     mbar_init(gx_full, 1);
@@ -145,7 +253,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int b = 0; b < C::kWBoxes; ++b)
           tma_load_2d_hint(w_s + ws * C::kWBytes + b * C::kBox, &tm_w, &w_full[ws],
                            j * 128 + b * C::kBoxK, tile * 128, pol_stream);
-        if (++ws == 2) { ws = 0; wph ^= 1; }
+        if (++ws == WS) { ws = 0; wph ^= 1; }
         for (int kc = 0; kc < p.kc_count; ++kc) {
           mbar_wait(&k_empty[ks], kph ^ 1);
           uint8_t* slot = k_s + ks * C::kKSlot;
@@ -153,7 +261,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
           if constexpr (!XT_RES)
             tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], kc * C::kBoxK, j * 128, pol_keep);
-          if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
+          if (++ks == KS) { ks = 0; kph ^= 1; }
         }
       }
     }
@@ -202,72 +310,94 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           mma_commit(&k_empty[ks]);
         }
         __syncwarp();
-        if (++ks == C::kKStages) { ks = 0; kph ^= 1; }
+        if (++ks == KS) { ks = 0; kph ^= 1; }
       }
       if (elect_one()) {
         mma_commit(&t_full[ds]);
         mma_commit(&w_empty[ws]);
       }
       __syncwarp();
-      if (++ws == 2) { ws = 0; wph ^= 1; }
+      if (++ws == WS) { ws = 0; wph ^= 1; }
       if (++ds == 2) { ds = 0; dph ^= 1; }
     }
     if (elect_one()) mma_commit(gx_full);
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 2;
-    const int q = warp & 3;
-    const int half = ew >> 2;
+    const int ew = warp - 2;                 // 0..15
+    const int q = warp & 3;                  // TMEM sub-partition
+    const int quarter = ew >> 2;             // which 32 of the 128 d-columns
     const int row = q * 32 + lane_id();
+    const int c0 = quarter * 32;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    bool bad = false;
-    int ws = 0, ds = 0;
+    const bool storer = (ew == 0) && lane_id() == 0;
+    int ws = 0, ds = 0, prev_ws = -1;
     uint32_t wph = 0, dph = 0;
     for (int tile = r0; tile < p.num_tiles; tile += R) {
-      mbar_wait(&t_full[ds], dph);
+      uint8_t* wt = w_s + ws * C::kWBytes;
       mbar_wait(&w_full[ws], wph);
-      tc_fence_after();
       if (p.do_update) {
         const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
-        const bool row_ok = grow < p.rows;
-        const uint8_t* wsm = w_s + ws * C::kWBytes;
-        uint8_t* gdst = p.W + grow * p.d * EB;
-#pragma unroll 1
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c0 = half * 64 + cc * 32;          // column within the d-tile
-          uint32_t r[32];
-          tmem_ld32(tmem_base + lane_off + ds * 128 + c0, r);
-          tmem_ld_wait();
-          float dw[32];
+        const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + c0;
+        // --- independent of dW: W_old and random bits, overlapping the MMAs
+        uint4 raw[C::kChunks16];
 #pragma unroll
-          for (int k = 0; k < 32; ++k) dw[k] = __uint_as_float(r[k]) * p.dw_scale;
-          bwd_update_row_chunk<EB>(p, dw, wsm, row, c0, grow, static_cast<int64_t>(j) * 128 + c0,
-                                   row_ok, bad, gdst);
+        for (int h = 0; h < C::kChunks16; ++h)
+          raw[h] = *reinterpret_cast<const uint4*>(wt + w_chunk_off<EB>(row, c0, h));
+        uint32_t rw[C::kRandWords];
+        if (p.rounding == ROUND_SR_FAST) sr_words<EB>(p.rng_base, flat0, rw);
+        float w[32];
+        w_decode<EB>(raw, w);
+        // --- dW from TMEM, then release the accumulator buffer at once
+        mbar_wait(&t_full[ds], dph);
+        tc_fence_after();
+        uint32_t acc[32];
+        tmem_ld32(tmem_base + lane_off + ds * 128 + c0, acc);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&t_empty[ds]);
+        uint4 out[C::kChunks16];
+        w_update_pack<EB>(p, acc, w, rw, flat0, out);
+#pragma unroll
+        for (int h = 0; h < C::kChunks16; ++h) *reinterpret_cast<uint4*>(wt + w_chunk_off<EB>(row, c0, h)) = out[h];
+        fence_proxy_async_smem();
+        named_bar_sync(1, kBwdEpiWarps * 32);
+        if (storer) {
+#pragma unroll
+          for (int b = 0; b < C::kWBoxes; ++b) tma_store_2d(&tm_w, wt + b * C::kBox, j * 128 + b * C::kBoxK, tile * 128);
+          bulk_commit();
+          // release the previous tile's slot once its store has read smem
+          bulk_wait_read<1>();
+          if (prev_ws >= 0) mbar_arrive(&w_empty[prev_ws]);
         }
+        prev_ws = ws;
+      } else {
+        mbar_wait(&t_full[ds], dph);
+        tc_fence_after();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&t_empty[ds]);
+        if (storer) mbar_arrive(&w_empty[ws]);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) {
-        mbar_arrive(&t_empty[ds]);
-        mbar_arrive(&w_empty[ws]);
-      }
-      if (++ws == 2) { ws = 0; wph ^= 1; }
+      if (++ws == WS) { ws = 0; wph ^= 1; }
       if (++ds == 2) { ds = 0; dph ^= 1; }
     }
-    if (bad) atomicOr(p.status, ST_NONFINITE_GRAD);
+    if (storer && p.do_update) {
+      bulk_wait<0>();
+      if (prev_ws >= 0) mbar_arrive(&w_empty[prev_ws]);
+    }
     if (do_gx) {
       mbar_wait(gx_full, 0);
       tc_fence_after();
-      const int ncols = p.gx_kc_count * C::kBoxK;
-      const int per_half = ncols / 2;
+      const int nchunks = p.gx_kc_count * C::kBoxK / 32;
       float* dst = p.gx_ws + (static_cast<int64_t>(r0) * p.d + j * 128 + row) * p.gx_ld;
 #pragma unroll 1
-      for (int c0 = half * per_half; c0 < (half + 1) * per_half; c0 += 32) {
+      for (int cch = quarter; cch < nchunks; cch += 4) {
         uint32_t r[32];
-        tmem_ld32(tmem_gx + lane_off + c0, r);
+        tmem_ld32(tmem_gx + lane_off + cch * 32, r);
         tmem_ld_wait();
-        uint4* o = reinterpret_cast<uint4*>(dst + c0);
+        uint4* o = reinterpret_cast<uint4*>(dst + cch * 32);
 #pragma unroll
         for (int k = 0; k < 8; ++k) o[k] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
       }
@@ -279,112 +409,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
-  }
-}
-
-// One thread: 32 consecutive columns [c0, c0+32) of its row.
-// W_old comes from the swizzled smem tile, W_new goes straight to HBM.
-template <int EB>
-XMC_DEV void bwd_update_row_chunk(const BwdParams& p, const float (&dw)[32], const uint8_t* wsm,
-                                  int row, int c0, int64_t grow, int64_t gcol0, bool row_ok, bool& bad,
-                                  uint8_t* gdst) {
-  float w[32];
-  if constexpr (EB == 1) {
-    // 32 bytes = two 16-B chunks of the 128-B swizzled row
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int cidx = (c0 >> 4) + h;
-      const uint4 v = *reinterpret_cast<const uint4*>(wsm + row * 128 + ((cidx ^ (row & 7)) << 4));
-      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 a = dec_e4m3x2(static_cast<uint16_t>(wv[k] & 0xFFFF));
-        const float2 b = dec_e4m3x2(static_cast<uint16_t>(wv[k] >> 16));
-        w[h * 16 + 4 * k + 0] = a.x;
-        w[h * 16 + 4 * k + 1] = a.y;
-        w[h * 16 + 4 * k + 2] = b.x;
-        w[h * 16 + 4 * k + 3] = b.y;
-      }
-    }
-  } else {
-    // bf16: columns [c0, c0+32) live in box c0/64, 64 B = four 16-B chunks
-    const uint8_t* box = wsm + (c0 >> 6) * (128 * 128);
-#pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const int cidx = ((c0 & 63) >> 3) + h;
-      const uint4 v = *reinterpret_cast<const uint4*>(box + row * 128 + ((cidx ^ (row & 7)) << 4));
-      const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        w[h * 8 + 2 * k + 0] = __uint_as_float(wv[k] << 16);
-        w[h * 8 + 2 * k + 1] = __uint_as_float(wv[k] & 0xFFFF0000u);
-      }
-    }
-  }
-
-  // updated = w - lr * (g + wd * w), fp32, one rounding (optimizers.py:71-73)
-  float u[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    bad |= !(fabsf(dw[k]) <= 3.4028234663852886e38f);
-    const float g = p.wd != 0.0f ? __fadd_rn(dw[k], __fmul_rn(p.wd, w[k])) : dw[k];
-    u[k] = __fsub_rn(w[k], __fmul_rn(p.lr, g));
-  }
-  if (!row_ok) return;
-
-  const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + gcol0;
-  if (p.rounding == ROUND_SR_EXACT) {
-    const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-      u[k] = grid_round_stochastic(gf, u[k], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + k)));
-  }
-
-  if constexpr (EB == 1) {
-    uint32_t pk[8];
-    if (p.rounding == ROUND_SR_FAST) {
-      const uint32_t k0 = static_cast<uint32_t>(p.rng_base), k1 = static_cast<uint32_t>(p.rng_base >> 32);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint64_t ctr = static_cast<uint64_t>(flat0 + 16 * h) >> 4;
-        const U4 rb = philox4x32_10(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), 0u, 0u}, k0, k1);
-        const uint32_t rr[4] = {rb.x, rb.y, rb.z, rb.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int e = h * 16 + 4 * k;
-          pk[h * 4 + k] = cvt_e4m3x4_rs(u[e + 3], u[e + 2], u[e + 1], u[e + 0], rr[k]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint32_t lo = cvt_e4m3x2_rn(u[4 * k + 1], u[4 * k + 0]);
-        const uint32_t hi = cvt_e4m3x2_rn(u[4 * k + 3], u[4 * k + 2]);
-        pk[k] = lo | (hi << 16);
-      }
-    }
-    uint4* o = reinterpret_cast<uint4*>(gdst + gcol0);
-    o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-  } else {
-    uint32_t pk[16];
-    if (p.rounding == ROUND_SR_FAST) {
-      const uint32_t k0 = static_cast<uint32_t>(p.rng_base), k1 = static_cast<uint32_t>(p.rng_base >> 32);
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        const uint64_t ctr = static_cast<uint64_t>(flat0 + 8 * h) >> 3;
-        const U4 rb = philox4x32_10(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), 1u, 0u}, k0, k1);
-        const uint32_t rr[4] = {rb.x, rb.y, rb.z, rb.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) pk[h * 4 + k] = cvt_bf16x2_rs(u[h * 8 + 2 * k + 1], u[h * 8 + 2 * k], rr[k]);
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) pk[k] = cvt_bf16x2_rn(u[2 * k + 1], u[2 * k]);
-    }
-    uint4* o = reinterpret_cast<uint4*>(gdst + gcol0 * 2);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) o[k] = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
   }
 }
 

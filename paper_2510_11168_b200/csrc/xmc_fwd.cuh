@@ -1,6 +1,6 @@
 // Kernel 1 of a head chunk: logits S = W_c . Xq^T on tcgen05 (TMEM accumulator),
 // fused epilogue G = clip(sigmoid(S), 2^-24, 1-2^-24) - Y (positives from the
-// per-tile label-sorted list), written once to the chunk's G buffer in the
+// per-tile label-bucketed list), written once to the chunk's G buffer in the
 // backward operand format.  Reference: head_forward_logits head.py:164-178 and
 // logit_gradient head.py:181-196 (also the plain-logits mode used by
 // ChunkedHead.scores head.py:109-112).
@@ -9,6 +9,12 @@
 //   warp 0      TMA producer  (W k-chunk + Xq k-chunk per stage)
 //   warp 1      MMA issuer    (one elected lane), owns the TMEM allocation
 //   warps 2..9  epilogue      (2 warps per TMEM sub-partition, each half the columns)
+//
+// Epilogue numerics.  sigmoid = rcp(1 + ex2(-z log2 e)) (MUFU, rel. err ~2^-21).
+// e4m3 G is stored as e4m3(256 g): the 2^8 scale is folded into the reciprocal
+// (256 / (1 + e) = rcp(2^-8 + 2^-8 e)) and the [2^-24, 1-2^-24] clip is dropped
+// because it is below e4m3 resolution at that scale (both clip edges round to
+// the same code, 0 / 256, as the unclipped value).  bf16 G keeps the clip.
 #pragma once
 
 #include "xmc_ptx.cuh"
@@ -25,14 +31,13 @@ struct FwdParams {
   int32_t d;           // feature dim (multiple of 128 B / elem)
   int32_t num_tiles;   // ceil(rows / 128)
   int32_t mode;        // 0: write quantized G; 1: write fp32 logits
-  int32_t g_fmt;       // FMT_E4M3 (scaled by g_scale) or FMT_BF16
-  float g_scale;       // 256 for e4m3 G, 1 for bf16 G
+  int32_t g_fmt;       // FMT_E4M3 (scaled by 256) or FMT_BF16
   const int32_t* tile_ptr;   // [num_tiles + 1] into entries (chunk-local tiles)
   const uint32_t* entries;   // (row_in_tile << 16) | sample
   void* out;                 // G [rows][ld] or logits fp32 [rows][ld]
   int64_t ld;                // leading dimension (elements) of out
-  float* stats;              // [0] += sum |G| over valid entries
-  const int32_t* status;     // nonzero abort bits -> no-op
+  float* stats;              // [0] += sum |G| over valid entries (optional)
+  int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
 };
 
 template <int EB, int BN>
@@ -48,7 +53,7 @@ struct FwdCfg {
   static constexpr int kTmemCols = (BN * kAccStages) <= 128 ? 128 : ((BN * kAccStages) <= 256 ? 256 : 512);
   static constexpr int kWordsPerRow = BN / 32;
   static constexpr int kBitmapBytes = 128 * kWordsPerRow * 4;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + 2 * kBitmapBytes + 256;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kBitmapBytes + 256;
   static constexpr int kMmaN = BN > 256 ? 256 : BN;
 };
 
@@ -62,8 +67,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_base = smem;
-  uint32_t* bitmaps = reinterpret_cast<uint32_t*>(smem + C::kStages * C::kStageBytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + 2 * C::kBitmapBytes);
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kBitmapBytes);
   uint64_t* full = bars;                          // [kStages]
   uint64_t* empty = bars + C::kStages;            // [kStages]
   uint64_t* tfull = bars + 2 * C::kStages;        // [kAccStages]
@@ -160,26 +165,28 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int etid = ew * 32 + lane_id();    // 0..255
     constexpr int kHalfCols = BN / 2;
     constexpr int kChunks = kHalfCols / 32;
-    const float SIG_LO = 5.9604644775390625e-08f;        // 2^-24
-    const float SIG_HI = 0.99999994039535522461f;        // 1 - 2^-24
+    const bool want_stats = p.stats != nullptr && p.mode == 0;
+    const bool pad_cols = p.B < BN;
     float abs_sum = 0.f;
+    bool nan_seen = false;
     int acc = 0;
     uint32_t acc_phase = 0;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++it) {
-      // positives of this tile -> bitmap (rows x BN bits)
-      uint32_t* bm = bitmaps + (it & 1) * (128 * C::kWordsPerRow);
-      for (int w = etid; w < 128 * C::kWordsPerRow; w += kFwdEpiWarps * 32) bm[w] = 0u;
-      named_bar_sync(1, kFwdEpiWarps * 32);
-      if (p.mode == 0 && p.tile_ptr != nullptr) {
-        const int e0 = p.tile_ptr[tile], e1 = p.tile_ptr[tile + 1];
+    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      // positives of this tile -> bitmap, only when the tile has any (uniform)
+      const int e0 = (p.mode == 0 && p.tile_ptr) ? p.tile_ptr[tile] : 0;
+      const int e1 = (p.mode == 0 && p.tile_ptr) ? p.tile_ptr[tile + 1] : 0;
+      const bool has_pos = e1 > e0;
+      if (has_pos) {
+        named_bar_sync(1, kFwdEpiWarps * 32);   // previous users of the bitmap are done
+        for (int w = etid; w < 128 * C::kWordsPerRow; w += kFwdEpiWarps * 32) bitmap[w] = 0u;
+        named_bar_sync(1, kFwdEpiWarps * 32);
         for (int e = e0 + etid; e < e1; e += kFwdEpiWarps * 32) {
           const uint32_t v = p.entries[e];
           const uint32_t r = v >> 16, s = v & 0xFFFFu;
-          atomicOr(&bm[r * C::kWordsPerRow + (s >> 5)], 1u << (s & 31));
+          atomicOr(&bitmap[r * C::kWordsPerRow + (s >> 5)], 1u << (s & 31));
         }
+        named_bar_sync(1, kFwdEpiWarps * 32);
       }
-      named_bar_sync(1, kFwdEpiWarps * 32);
 
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -200,22 +207,44 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
           continue;
         }
-        const uint32_t pos = bm[row * C::kWordsPerRow + (col0 >> 5)];
+        const uint32_t pos = has_pos ? bitmap[row * C::kWordsPerRow + (col0 >> 5)] : 0u;
         float g[32];
+        if constexpr (EB == 1) {
+          // g256 = 256 sigmoid(z) - 256 y
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float z = __uint_as_float(r[j]);
-          // 1 / (1 + exp(-z)) with ex2.approx / rcp.approx (rel. err ~2^-22)
-          float sg = fast_rcp(1.0f + fast_ex2(-z * 1.4426950408889634f));
-          sg = sg < SIG_LO ? SIG_LO : sg;  // NaN propagates like np.clip
-          sg = sg > SIG_HI ? SIG_HI : sg;
-          if ((pos >> j) & 1u) sg -= 1.0f;
-          sg = (col0 + j < p.B) ? sg : 0.0f;
-          abs_sum += row_ok ? fabsf(sg) : 0.0f;
-          g[j] = sg * p.g_scale;
+          for (int j = 0; j < 32; ++j) {
+            const float e = fast_ex2(__uint_as_float(r[j]) * -1.4426950408889634f);
+            g[j] = fast_rcp(fmaf(e, 0.00390625f, 0.00390625f));
+          }
+        } else {
+          const float SIG_LO = 5.9604644775390625e-08f;   // 2^-24  (head.py:47-48)
+          const float SIG_HI = 0.99999994039535522461f;   // 1 - 2^-24
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float z = __uint_as_float(r[j]);
+            nan_seen |= (z != z);
+            float sg = fast_rcp(1.0f + fast_ex2(z * -1.4426950408889634f));
+            sg = sg < SIG_LO ? SIG_LO : sg;   // NaN propagates like np.clip
+            g[j] = sg > SIG_HI ? SIG_HI : sg;
+          }
+        }
+        const float one = EB == 1 ? 256.0f : 1.0f;
+        if (pos != 0u) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if ((pos >> j) & 1u) g[j] -= one;
+        }
+        if (pad_cols) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j >= p.B) g[j] = 0.0f;
+        }
+        if (want_stats && row_ok) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) abs_sum += fabsf(g[j]);
         }
         if (row_ok) {
-          if (p.g_fmt == FMT_E4M3) {
+          if constexpr (EB == 1) {
             uint32_t pk[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -241,10 +270,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       if (lane_id() == 0) mbar_arrive(&tempty[acc]);
       if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
     }
-    // one atomic per warp per CTA
+    if (want_stats) {
+      abs_sum *= (EB == 1) ? 0.00390625f : 1.0f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) abs_sum += __shfl_xor_sync(0xffffffffu, abs_sum, o);
-    if (lane_id() == 0 && p.stats != nullptr && p.mode == 0) atomicAdd(p.stats, abs_sum);
+      for (int o = 16; o > 0; o >>= 1) abs_sum += __shfl_xor_sync(0xffffffffu, abs_sum, o);
+      if (lane_id() == 0) atomicAdd(p.stats, abs_sum);
+    }
+    if (__any_sync(0xffffffffu, nan_seen) && lane_id() == 0) atomicOr(p.status, 4 /*ST_NONFINITE_GRAD*/);
   }
 
   tc_fence_before();

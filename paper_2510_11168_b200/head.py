@@ -126,6 +126,7 @@ class ChunkedHead:
         self.label_offset = label_offset
         self._handle = None
         self.last_stats = None
+        self.collect_stats = False   # True: head_update also returns sum|G| in last_stats[0]
 
     # -- construction -------------------------------------------------------
     @classmethod
@@ -270,8 +271,11 @@ def head_update(head: ChunkedHead, batch: BatchInput, cfg: SgdSrConfig, rng: Rou
             return _head_update_unfused(head, X, si, li, cfg, rng, step, tracker, probe)
         h = head.handle(b, si.numel())
         gx = grad_out if grad_out is not None else torch.empty((b, head.dim), dtype=torch.float32, device=dev)
-        if head.last_stats is None or head.last_stats.device != dev:
-            head.last_stats = torch.zeros(2, dtype=torch.float32, device=dev)
+        stats_ptr = None
+        if head.collect_stats:  # sum |G| of the step (trainer divergence proxy)
+            if head.last_stats is None or head.last_stats.device != dev:
+                head.last_stats = torch.zeros(2, dtype=torch.float32, device=dev)
+            stats_ptr = head.last_stats.data_ptr()
         args = _step_args(cfg, rng, step, head.tensor_id)
         lhs = []
         if tracker is not None:
@@ -279,8 +283,7 @@ def head_update(head: ChunkedHead, batch: BatchInput, cfg: SgdSrConfig, rng: Rou
                 lhs.append(tracker.alloc("chunk_logits", "logits", (e - s) * b * 2))
         _lib.check(_lib.load().xmc_head_step(
             h.h, head.weights.values.data_ptr(), X.data_ptr(), b, si.data_ptr(), li.data_ptr(),
-            si.numel(), ctypes.byref(args), gx.data_ptr(), head.last_stats.data_ptr(),
-            _lib.stream_ptr()))
+            si.numel(), ctypes.byref(args), gx.data_ptr(), stats_ptr, _lib.stream_ptr()))
         for lh in lhs:
             tracker.free(lh)
         if check:
