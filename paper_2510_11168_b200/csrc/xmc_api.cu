@@ -222,7 +222,7 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   L->xqt = align_up(L->xq + (size_t)bp * D * eb, 1024);
   L->gbuf = align_up(L->xqt + (size_t)bp * D * eb, 1024);
   L->gx = align_up(L->gbuf + (size_t)(maxrows + 128) * bp * eb, 1024);
-  L->cnt = align_up(L->gx + (size_t)R * D * 256 * 4, 256);
+  L->cnt = align_up(L->gx + (size_t)R * D * bp * 4, 256);
   L->ptr = align_up(L->cnt + (size_t)(tiles + 1) * 4, 256);
   L->ent = align_up(L->ptr + (size_t)(tiles + 1) * 4, 256);
   L->chunk = align_up(L->ent + (size_t)std::max<int64_t>(d->max_positives, 1) * 4, 256);
@@ -456,22 +456,24 @@ __global__ void pos_scatter_kernel(PosGeom g, const int32_t* __restrict__ ps, co
 }
 
 // grad_x[s][c] += sum_r ws[r][c][s - col0]   (fixed r order: deterministic)
-__global__ void gx_reduce_kernel(const float* __restrict__ ws, int R, int d, int ld, int col0, int ncols, int B, float scale,
-                                 float* __restrict__ gx) {
+__global__ void gx_reduce_kernel(const float* __restrict__ ws, int R, int d, int ld, int B, float scale,
+                                 int accumulate, float* __restrict__ gx) {
   __shared__ float tile[32][33];
   const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int c = c0 + i, sl = s0 + threadIdx.x;
+    const int c = c0 + i, s = s0 + threadIdx.x;
     float acc = 0.f;
-    if (sl < ncols)
-      for (int r = 0; r < R; ++r) acc += ws[((int64_t)r * d + c) * ld + sl];
+    if (s < B)
+      for (int r = 0; r < R; ++r) acc += ws[((int64_t)r * d + c) * ld + s];
     tile[i][threadIdx.x] = acc * scale;
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int sl = s0 + i, c = c0 + threadIdx.x;
-    const int s = col0 + sl;
-    if (sl < ncols && s < B) gx[(int64_t)s * d + c] += tile[threadIdx.x][i];
+    const int s = s0 + i, c = c0 + threadIdx.x;
+    if (s < B) {
+      float* o = gx + (int64_t)s * d + c;
+      *o = accumulate ? *o + tile[threadIdx.x][i] : tile[threadIdx.x][i];
+    }
   }
 }
 
@@ -551,22 +553,24 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t r
 
 template <int EB, bool XR, int KC>
 static xmc_status launch_bwd_t(int grid, const CUtensorMap& tw, const CUtensorMap& tg, const CUtensorMap& tx,
-                               const BwdParams& p, cudaStream_t st) {
+                               const CUtensorMap& tws, const BwdParams& p, cudaStream_t st) {
   ProfRec pr;
   prof_begin(1, st, &pr);
-  xmc_bwd_kernel<EB, XR, KC><<<grid, kBwdThreads, BwdCfg<EB, XR, KC>::kSmemBytes, st>>>(tw, tg, tx, p);
+  xmc_bwd_kernel<EB, XR, KC><<<grid, kBwdThreads, BwdCfg<EB, XR, KC>::kSmemBytes, st>>>(tw, tg, tx, tws, p);
   CUDA_TRY(cudaGetLastError());
   prof_end(st, &pr);
   return XMC_OK;
 }
 
-// one bwd pass over local rows [row0, row0+rows), G from gbuf; optional grad_X into acc
-static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, int B, int Bp, bool update,
-                             int gx_kc0, int gx_kc_count, const xmc_step_args* a, float* acc, cudaStream_t st) {
+// one bwd pass over local rows [row0, row0+rows), G from gbuf; grad_X partials
+// accumulate into the [R][d][Bp] workspace (zeroed by the caller per step)
+static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, int Bp, bool update, int gx_kc0,
+                             int gx_kc_count, const xmc_step_args* a, cudaStream_t st) {
   const int eb = h->eb, D = h->desc.dim;
   const int box_k = 128 / eb;
-  CUtensorMap tw, tg, tx;
+  CUtensorMap tw, tg, tx, tws;
   XMC_TRY(make_map(&tw, static_cast<uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 128));
+  XMC_TRY(make_map(&tws, static_cast<uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 32));
   XMC_TRY(make_map(&tg, h->gbuf, eb, Bp, rows, Bp, 128));
   XMC_TRY(make_map(&tx, h->xqt, eb, Bp, D, Bp, 128));
   const int64_t tiles = cdiv(rows, 128);
@@ -580,6 +584,7 @@ static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, i
   p.do_update = update ? 1 : 0;
   p.gx_kc0 = gx_kc0;
   p.gx_kc_count = gx_kc_count;
+  p.W = static_cast<uint8_t*>(W) + row0 * D * eb;
   p.row0_global = h->desc.label_offset + row0;
   p.lr = a ? a->lr : 0.f;
   p.wd = a ? a->weight_decay : 0.f;
@@ -587,44 +592,51 @@ static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, i
   p.rounding = a ? a->rounding : 0;
   p.rng_base = a ? sm64_base(a->seed, a->step, a->tensor_id) : 0;
   p.gx_ws = h->gx_ws;
-  p.gx_ld = gx_kc_count * box_k;
+  p.gx_ld = Bp;
+  p.gx_accumulate = 1;
   p.status = h->status;
   const int grid = R * h->dtiles;
-  xmc_status s;
   if (eb == 1) {
-    if (Bp == 128) s = launch_bwd_t<1, true, 1>(grid, tw, tg, tx, p, st);
-    else if (Bp == 256) s = launch_bwd_t<1, true, 2>(grid, tw, tg, tx, p, st);
-    else return fail(XMC_ERR_UNSUPPORTED, "no backward kernel for padded batch %d", Bp);
+    if (Bp == 128) return launch_bwd_t<1, true, 1>(grid, tw, tg, tx, tws, p, st);
+    if (Bp == 256) return launch_bwd_t<1, true, 2>(grid, tw, tg, tx, tws, p, st);
   } else {
-    if (Bp == 64) s = launch_bwd_t<2, true, 1>(grid, tw, tg, tx, p, st);
-    else if (Bp == 128) s = launch_bwd_t<2, true, 2>(grid, tw, tg, tx, p, st);
-    else if (Bp == 256) s = launch_bwd_t<2, true, 4>(grid, tw, tg, tx, p, st);
-    else if (Bp == 512) s = launch_bwd_t<2, false, 8>(grid, tw, tg, tx, p, st);
-    else return fail(XMC_ERR_UNSUPPORTED, "no backward kernel for padded batch %d", Bp);
+    if (Bp == 64) return launch_bwd_t<2, true, 1>(grid, tw, tg, tx, tws, p, st);
+    if (Bp == 128) return launch_bwd_t<2, true, 2>(grid, tw, tg, tx, tws, p, st);
+    if (Bp == 256) return launch_bwd_t<2, true, 4>(grid, tw, tg, tx, tws, p, st);
+    if (Bp == 512) return launch_bwd_t<2, false, 8>(grid, tw, tg, tx, tws, p, st);
   }
-  if (s != XMC_OK) return s;
-  if (gx_kc_count > 0 && acc) {
-    dim3 g(D / 32, (p.gx_ld + 31) / 32), b(32, 8);
-    gx_reduce_kernel<<<g, b, 0, st>>>(h->gx_ws, R, D, p.gx_ld, gx_kc0 * box_k, p.gx_ld, B, p.dw_scale, acc);
-    CUDA_TRY(cudaGetLastError());
-  }
-  return XMC_OK;
+  return fail(XMC_ERR_UNSUPPORTED, "no backward kernel for padded batch %d", Bp);
 }
 
-// grad_X + update for one chunk whose G is in gbuf (handles Bp = 512 in two passes)
-static xmc_status run_backward(xmc_head* h, void* W, int64_t row0, int64_t rows, int B, int Bp, bool gx,
-                               bool update, const xmc_step_args* a, float* acc, cudaStream_t st) {
+// grad_X partials + update for one chunk whose G is in gbuf (Bp = 512 takes two passes)
+static xmc_status run_backward(xmc_head* h, void* W, int64_t row0, int64_t rows, int Bp, bool gx, bool update,
+                               const xmc_step_args* a, cudaStream_t st) {
   const int kcs = Bp * h->eb / 128;
   const int per = 256 * h->eb / 128;   // k-chunks whose grad_X columns fit 256 TMEM columns
-  if (!gx) return launch_bwd(h, W, row0, rows, B, Bp, update, 0, 0, a, nullptr, st);
+  if (!gx) return launch_bwd(h, W, row0, rows, Bp, update, 0, 0, a, st);
   // passes over grad_X column groups; the update rides on the LAST pass so
   // every grad_X pass reads the pre-update weights (head.py:290-291)
   const int groups = (kcs + per - 1) / per;
   for (int gi = groups - 1; gi >= 0; --gi) {
     const int kc0 = gi * per;
     const int cnt = std::min(per, kcs - kc0);
-    XMC_TRY(launch_bwd(h, W, row0, rows, B, Bp, update && gi == 0, kc0, cnt, a, acc, st));
+    XMC_TRY(launch_bwd(h, W, row0, rows, Bp, update && gi == 0, kc0, cnt, a, st));
   }
+  return XMC_OK;
+}
+
+// acc[s][c] (+)= scale * sum_r ws[r][c][s]  -- one deterministic reduction per step
+static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumulate, cudaStream_t st) {
+  const int D = h->desc.dim;
+  dim3 g(D / 32, (Bp + 31) / 32), b(32, 8);
+  gx_reduce_kernel<<<g, b, 0, st>>>(h->gx_ws, h->R, D, Bp, B, h->eb == 1 ? (1.0f / 256.0f) : 1.0f,
+                                     accumulate ? 1 : 0, acc);
+  CUDA_TRY(cudaGetLastError());
+  return XMC_OK;
+}
+
+static xmc_status zero_gx_ws(xmc_head* h, int Bp, cudaStream_t st) {
+  CUDA_TRY(cudaMemsetAsync(h->gx_ws, 0, (size_t)h->R * h->desc.dim * Bp * 4, st));
   return XMC_OK;
 }
 
@@ -687,14 +699,14 @@ extern "C" xmc_status xmc_head_step(xmc_head_t h, void* W, const float* X, int32
   const int Bp = padded_batch(h->eb, B);
   XMC_TRY(launch_x_prep(h, X, B, Bp, st));
   XMC_TRY(prepare_positives(h, pos_sample, pos_label, nnz, B, st));
-  CUDA_TRY(cudaMemsetAsync(grad_x, 0, (size_t)B * h->desc.dim * 4, st));
+  XMC_TRY(zero_gx_ws(h, Bp, st));
   if (stats) CUDA_TRY(cudaMemsetAsync(stats, 0, 8, st));
   for (size_t c = 0; c < h->chunks.size(); ++c) {
     const int64_t r0 = h->chunks[c].first, rows = h->chunks[c].second - h->chunks[c].first;
     XMC_TRY(launch_fwd(h, W, r0, rows, B, Bp, 0, h->tile_ptr + h->tile_base[c], h->gbuf, Bp, stats, st));
-    XMC_TRY(run_backward(h, W, r0, rows, B, Bp, true, true, args, grad_x, st));
+    XMC_TRY(run_backward(h, W, r0, rows, Bp, true, true, args, st));
   }
-  return XMC_OK;
+  return reduce_gx(h, B, Bp, grad_x, false, st);
 }
 
 extern "C" xmc_status xmc_head_logits(xmc_head_t h, const void* W, const float* X, int32_t B, int64_t row0,
@@ -726,7 +738,10 @@ extern "C" xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, i
   if (h->eb == 1) g_quant_kernel<1><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, 256.0f, h->gbuf, h->status);
   else g_quant_kernel<2><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, 1.0f, h->gbuf, h->status);
   CUDA_TRY(cudaGetLastError());
-  return run_backward(h, W, row0, rows, B, Bp, accumulate_gx != 0, update != 0, args, acc, st);
+  if (accumulate_gx) XMC_TRY(zero_gx_ws(h, Bp, st));
+  XMC_TRY(run_backward(h, W, row0, rows, Bp, accumulate_gx != 0, update != 0, args, st));
+  if (accumulate_gx) XMC_TRY(reduce_gx(h, B, Bp, acc, true, st));
+  return XMC_OK;
 }
 
 // ============================================================== elementwise core

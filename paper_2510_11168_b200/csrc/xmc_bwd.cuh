@@ -49,12 +49,14 @@ struct BwdParams {
   int32_t do_update;     // dW + SGD + rounding, W written in place
   int32_t gx_kc0;        // first sample k-chunk accumulated into grad_X
   int32_t gx_kc_count;   // 0 = no grad_X
+  uint8_t* W;            // chunk base (row-major rows x d, EB bytes/elem), written in place
   int64_t row0_global;   // global label of chunk row 0 (RNG key)
   float lr, wd, dw_scale;
   int32_t rounding;      // ROUND_NEAREST / ROUND_SR_EXACT / ROUND_SR_FAST
   uint64_t rng_base;     // splitmix64 base(seed, step, tensor_id); Philox key
-  float* gx_ws;          // [R][d][gx_ld] fp32 partials
+  float* gx_ws;          // [R][d][gx_ld] fp32 partials (gx_ld = padded batch)
   int32_t gx_ld;
+  int32_t gx_accumulate; // 1: add into the partial slot, 0: overwrite it
   int32_t* status;
 };
 
@@ -117,7 +119,7 @@ XMC_DEV void w_decode(const uint4 (&raw)[2 * EB], float (&w)[32]) {
   }
 }
 
-// Philox4x32-10 words for 32 elements starting at flat index flat0 (multiple
+// Philox4x32-7 words for 32 elements starting at flat index flat0 (multiple
 // of 32).  e4m3: one word per cvt.rs.e4m3x4 (4 elements, 16 random bits per
 // lane, see profiles/r1_probe_cvt_rs.txt); bf16: one word per bf16x2.
 template <int EB>
@@ -126,7 +128,8 @@ XMC_DEV void sr_words(uint64_t key, int64_t flat0, uint32_t (&rw)[8 * EB]) {
 #pragma unroll
   for (int h = 0; h < 2 * EB; ++h) {
     const uint64_t ctr = static_cast<uint64_t>(flat0) / (16 / EB) + h;
-    const U4 r = philox4x32_10(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), EB - 1u, 0u}, k0, k1);
+    const U4 r = philox4x32<kPhiloxRounds>(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), EB - 1u, 0u},
+                                           k0, k1);
     rw[4 * h + 0] = r.x;
     rw[4 * h + 1] = r.y;
     rw[4 * h + 2] = r.z;
@@ -143,9 +146,23 @@ XMC_DEV void w_update_pack(const BwdParams& p, const uint32_t (&acc)[32], const 
                            const uint32_t (&rw)[8 * EB], int64_t flat0, uint4 (&out)[2 * EB]) {
   const float a_lr = -p.lr * p.dw_scale;
   const float c_wd = 1.0f - p.lr * p.wd;
+  const uint64_t A2 = f2pack(a_lr, a_lr), C2 = f2pack(c_wd, c_wd);
   float u[32];
+  if (p.wd != 0.0f) {
 #pragma unroll
-  for (int k = 0; k < 32; ++k) u[k] = fmaf(a_lr, __uint_as_float(acc[k]), w[k] * c_wd);
+    for (int k = 0; k < 16; ++k) {
+      const uint64_t r = ffma2(f2pack(__uint_as_float(acc[2 * k]), __uint_as_float(acc[2 * k + 1])), A2,
+                               fmul2(f2pack(w[2 * k], w[2 * k + 1]), C2));
+      f2unpack(r, u[2 * k], u[2 * k + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const uint64_t r = ffma2(f2pack(__uint_as_float(acc[2 * k]), __uint_as_float(acc[2 * k + 1])), A2,
+                               f2pack(w[2 * k], w[2 * k + 1]));
+      f2unpack(r, u[2 * k], u[2 * k + 1]);
+    }
+  }
   if (p.rounding == ROUND_SR_EXACT) {
     const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
 #pragma unroll
@@ -178,7 +195,8 @@ XMC_DEV void w_update_pack(const BwdParams& p, const uint32_t (&acc)[32], const 
 template <int EB, bool XT_RES, int KCMAX>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
-                   const __grid_constant__ CUtensorMap tm_xt, BwdParams p) {
+                   const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
+                   BwdParams p) {
   using C = BwdCfg<EB, XT_RES, KCMAX>;
   constexpr int WS = C::kWStages;
   constexpr int KS = C::kKStages;
@@ -212,7 +230,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     prefetch_tmap(&tm_xt);
     for (int s = 0; s < WS; ++s) {
       mbar_init(&w_full[s], 1);
-      mbar_init(&w_empty[s], 2);   // MMA commit + the W-tile store thread
+      mbar_init(&w_empty[s], 5);   // MMA commit + one store thread per TMEM sub-partition
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -270,7 +288,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ---------------------------------------------------------- MMA issuer
     constexpr uint32_t fa = EB == 1 ? 0u : 1u;   // e4m3 : bf16
     constexpr uint32_t idesc_dw = umma_idesc(fa, fa, false, false, 128, 128);
-    constexpr uint32_t idesc_gx = umma_idesc(fa, fa, true, true, 128, C::kBoxK);
+    const uint32_t idesc_gx = umma_idesc(fa, fa, true, true, 128, p.gx_kc_count * C::kBoxK);
     if constexpr (XT_RES) mbar_wait(xt_full, 0);
     int ws = 0, ks = 0, ds = 0;
     uint32_t wph = 0, kph = 0, dph = 0;
@@ -296,18 +314,24 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               else mma_f16(d_dw, ad, bd, idesc_dw, (kc | k) != 0);
             }
           }
+          // grad_X^T: one MMA group with N = all samples of the pass, issued
+          // once its G boxes (contiguous ring slots, LBO = slot pitch) landed;
+          // W (A operand) is then read from smem once per tile.
           const int gk = kc - p.gx_kc0;
-          if (do_gx && gk >= 0 && gk < p.gx_kc_count) {
-            const uint32_t d_gx = tmem_gx + gk * C::kBoxK;
+          const bool in_gx = do_gx && gk >= 0 && gk < p.gx_kc_count;
+          if (in_gx && gk == p.gx_kc_count - 1) {
+            const uint32_t g0 = smem_u32(k_s + (ks - gk) * C::kKSlot);
 #pragma unroll
             for (int k = 0; k < 128 / C::kKmma; ++k) {
               const uint64_t ad = umma_desc_sw128(w_addr + k * C::kKmma * 128, C::kBox, 1024);
-              const uint64_t bd = umma_desc_sw128(g_addr + k * C::kKmma * 128, C::kBox, 1024);
-              if constexpr (EB == 1) mma_f8(d_gx, ad, bd, idesc_gx, (it | k) != 0);
-              else mma_f16(d_gx, ad, bd, idesc_gx, (it | k) != 0);
+              const uint64_t bd = umma_desc_sw128(g0 + k * C::kKmma * 128, C::kKSlot, 1024);
+              if constexpr (EB == 1) mma_f8(tmem_gx, ad, bd, idesc_gx, (it | k) != 0);
+              else mma_f16(tmem_gx, ad, bd, idesc_gx, (it | k) != 0);
             }
+            for (int s = ks - gk; s <= ks; ++s) mma_commit(&k_empty[s]);
+          } else if (!in_gx) {
+            mma_commit(&k_empty[ks]);
           }
-          mma_commit(&k_empty[ks]);
         }
         __syncwarp();
         if (++ks == KS) { ks = 0; kph ^= 1; }
@@ -330,7 +354,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int row = q * 32 + lane_id();
     const int c0 = quarter * 32;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-    const bool storer = (ew == 0) && lane_id() == 0;
+    // the 4 warps of sub-partition q own rows [32q, 32q+32) of every tile;
+    // they sync among themselves and one lane TMA-stores their 32-row slab
+    const bool storer = (quarter == 0) && lane_id() == 0;
     int ws = 0, ds = 0, prev_ws = -1;
     uint32_t wph = 0, dph = 0;
     for (int tile = r0; tile < p.num_tiles; tile += R) {
@@ -359,13 +385,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (lane_id() == 0) mbar_arrive(&t_empty[ds]);
         uint4 out[C::kChunks16];
         w_update_pack<EB>(p, acc, w, rw, flat0, out);
+        // W_new back into the same swizzled smem tile, then one TMA store per
+        // 32-row slab (full 128-B lines to HBM, no LSU traffic)
 #pragma unroll
         for (int h = 0; h < C::kChunks16; ++h) *reinterpret_cast<uint4*>(wt + w_chunk_off<EB>(row, c0, h)) = out[h];
         fence_proxy_async_smem();
-        named_bar_sync(1, kBwdEpiWarps * 32);
+        named_bar_sync(1 + q, 128);
         if (storer) {
 #pragma unroll
-          for (int b = 0; b < C::kWBoxes; ++b) tma_store_2d(&tm_w, wt + b * C::kBox, j * 128 + b * C::kBoxK, tile * 128);
+          for (int b = 0; b < C::kWBoxes; ++b)
+            tma_store_2d(&tm_ws, wt + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK, tile * 128 + q * 32);
           bulk_commit();
           // release the previous tile's slot once its store has read smem
           bulk_wait_read<1>();
@@ -390,16 +419,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (do_gx) {
       mbar_wait(gx_full, 0);
       tc_fence_after();
+      // this CTA's slot of the [R][d][Bp] partial buffer; chunks of one step
+      // accumulate into it (stream-ordered, one owner per slot: deterministic)
       const int nchunks = p.gx_kc_count * C::kBoxK / 32;
-      float* dst = p.gx_ws + (static_cast<int64_t>(r0) * p.d + j * 128 + row) * p.gx_ld;
+      float* dst = p.gx_ws + (static_cast<int64_t>(r0) * p.d + j * 128 + row) * p.gx_ld + p.gx_kc0 * C::kBoxK;
 #pragma unroll 1
       for (int cch = quarter; cch < nchunks; cch += 4) {
         uint32_t r[32];
         tmem_ld32(tmem_gx + lane_off + cch * 32, r);
         tmem_ld_wait();
-        uint4* o = reinterpret_cast<uint4*>(dst + cch * 32);
+        float4* o = reinterpret_cast<float4*>(dst + cch * 32);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+        for (int k = 0; k < 8; ++k) {
+          float4 v = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                                 __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+          if (p.gx_accumulate) {
+            const float4 old = o[k];
+            v.x += old.x;
+            v.y += old.y;
+            v.z += old.z;
+            v.w += old.w;
+          }
+          o[k] = v;
+        }
       }
     }
   }

@@ -70,6 +70,23 @@ struct U4 {
   uint32_t x, y, z, w;
 };
 
+// Philox4x32-R (Salmon et al., SC'11).  The update epilogue uses R = 7, the
+// smallest round count the Random123 authors report as BigCrush-clean for
+// Philox4x32 ("Philox4x32-7"); R = 10 is their default safety margin.
+template <int ROUNDS>
+XMC_DEV U4 philox4x32(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int i = 0; i < ROUNDS; ++i) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+constexpr int kPhiloxRounds = 7;
+
 XMC_DEV U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
