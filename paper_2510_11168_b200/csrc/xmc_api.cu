@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -184,13 +185,15 @@ struct xmc_head {
   int32_t* tile_cnt;   // [total_tiles + 1]
   int32_t* tile_ptr;   // [total_tiles + 1]
   uint32_t* entries;   // [max_positives]
+  uint32_t* tmp_tile;  // [max_positives] tile id per positive (bucketing scratch)
+  uint32_t* tmp_entry; // [max_positives] packed entry per positive
   int64_t* chunk_dev;  // [k+1] chunk starts (local rows) + [k+1] tile bases
   int32_t* status;     // [4]
   int R;               // bwd CTAs per d-tile
 };
 
 struct Layout {
-  size_t xq, xqt, gbuf, gx, cnt, ptr, ent, chunk, status, total;
+  size_t xq, xqt, gbuf, gx, cnt, ptr, ent, tmp, chunk, status, total;
 };
 
 static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out, int* bp_out, int* R_out,
@@ -225,7 +228,8 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   L->cnt = align_up(L->gx + (size_t)R * D * bp * 4, 256);
   L->ptr = align_up(L->cnt + (size_t)(tiles + 1) * 4, 256);
   L->ent = align_up(L->ptr + (size_t)(tiles + 1) * 4, 256);
-  L->chunk = align_up(L->ent + (size_t)std::max<int64_t>(d->max_positives, 1) * 4, 256);
+  L->tmp = align_up(L->ent + (size_t)std::max<int64_t>(d->max_positives, 1) * 4, 256);
+  L->chunk = align_up(L->tmp + (size_t)std::max<int64_t>(d->max_positives, 1) * 8, 256);
   L->status = align_up(L->chunk + (size_t)(2 * (ch.size() + 1)) * 8, 256);
   L->total = align_up(L->status + 64, 1024);
   *eb_out = eb;
@@ -293,6 +297,8 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->tile_cnt = reinterpret_cast<int32_t*>(w + L.cnt);
   h->tile_ptr = reinterpret_cast<int32_t*>(w + L.ptr);
   h->entries = reinterpret_cast<uint32_t*>(w + L.ent);
+  h->tmp_tile = reinterpret_cast<uint32_t*>(w + L.tmp);
+  h->tmp_entry = h->tmp_tile + std::max<int64_t>(desc->max_positives, 1);
   h->chunk_dev = reinterpret_cast<int64_t*>(w + L.chunk);
   h->status = reinterpret_cast<int32_t*>(w + L.status);
   std::vector<int64_t> host(2 * (h->chunks.size() + 1));
@@ -376,8 +382,10 @@ struct PosGeom {
 };
 
 __device__ __forceinline__ int64_t pos_tile(const PosGeom& g, int64_t local, int32_t* row_in_tile) {
-  // chunk c with chunk_start[c] <= local < chunk_start[c+1]; bounds are i*n/k
-  int c = static_cast<int>((local * g.k) / g.num_local);
+  // chunk c with chunk_start[c] <= local < chunk_start[c+1]; bounds are i*n/k,
+  // so a float estimate is off by at most one and the loops fix it up
+  int c = static_cast<int>(static_cast<float>(local) * (static_cast<float>(g.k) / static_cast<float>(g.num_local)));
+  c = c < 0 ? 0 : c;
   if (c >= g.k) c = g.k - 1;
   while (c > 0 && g.chunk_start[c] > local) --c;
   while (c + 1 < g.k && g.chunk_start[c + 1] <= local) ++c;
@@ -386,93 +394,276 @@ __device__ __forceinline__ int64_t pos_tile(const PosGeom& g, int64_t local, int
   return g.tile_base[c] + (off >> 7);
 }
 
-__global__ void pos_count_kernel(PosGeom g, const int32_t* __restrict__ ps, const int32_t* __restrict__ pl,
-                                 int64_t nnz, int32_t* __restrict__ cnt, int32_t* status) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t s = ps[i];
-    if (s < 0 || s >= g.B) {
-      atomicOr(status, ST_BAD_SAMPLE);
-      continue;
+// grad_x[s][c] += sum_r ws[r][c][s - col0]   (fixed r order: deterministic)
+// one thread per output element (block 32 x 32): R independent coalesced loads
+// in flight per thread, fixed summation order r = 0..R-1 (deterministic)
+__global__ void __launch_bounds__(1024) gx_reduce_kernel(const float* __restrict__ ws, int R, int d, int ld, int B,
+                                                         float scale, int accumulate, float* __restrict__ gx) {
+  __shared__ float tile[32][33];
+  const int c = blockIdx.x * 32 + threadIdx.y, s = blockIdx.y * 32 + threadIdx.x;
+  float acc = 0.f;
+  if (s < B) {
+    const float* p = ws + (int64_t)c * ld + s;
+    const int64_t stride = (int64_t)d * ld;
+    float v[8];
+    int r = 0;
+    for (; r + 8 <= R; r += 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldg(p + (r + k) * stride);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += v[k];
     }
-    const int64_t local = static_cast<int64_t>(pl[i]) - g.label_offset;
-    if (local < 0 || local >= g.num_local) continue;
-    int32_t r;
-    atomicAdd(&cnt[pos_tile(g, local, &r)], 1);
+    for (; r < R; ++r) acc += __ldg(p + r * stride);
+  }
+  tile[threadIdx.y][threadIdx.x] = acc * scale;
+  __syncthreads();
+  const int s2 = blockIdx.y * 32 + threadIdx.y, c2 = blockIdx.x * 32 + threadIdx.x;
+  if (s2 < B) {
+    float* o = gx + (int64_t)s2 * d + c2;
+    *o = accumulate ? *o + tile[threadIdx.x][threadIdx.y] : tile[threadIdx.x][threadIdx.y];
   }
 }
 
-// exclusive scan of cnt[0..n) into ptr[0..n]; cnt becomes the scatter cursor
-__global__ void pos_scan_kernel(int32_t* cnt, int32_t* ptr, int64_t n) {
-  __shared__ int32_t warp_sums[32];
-  __shared__ int32_t carry;
-  if (threadIdx.x == 0) carry = 0;
+// Bitonic sort of 32 (key, value) pairs across a warp (15 shuffle exchanges).
+__device__ __forceinline__ void warp_sort_pairs(uint32_t& key, uint32_t& val) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t ok = __shfl_xor_sync(0xffffffffu, key, j);
+      const uint32_t ov = __shfl_xor_sync(0xffffffffu, val, j);
+      const bool asc = (lane & k) == 0, lower = (lane & j) == 0;
+      const bool take = (lower == asc) ? (ok < key) : (ok > key);
+      if (take) {
+        key = ok;
+        val = ov;
+      }
+    }
+  }
+}
+
+// After warp_sort_pairs: start lane of this lane's run of equal keys and the
+// run length (valid on the run's first lane).
+__device__ __forceinline__ void warp_runs(uint32_t key, int* start, int* len) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = lane == 0 || prev != key;
+  const uint32_t heads = __ballot_sync(0xffffffffu, head);
+  *start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
+  const uint32_t above = heads & ~(0xffffffffu >> (31 - lane));
+  *len = (above ? __ffs(above) - 1 : 32) - lane;
+}
+
+// ---- multi-CTA positive bucketing: count -> scan -> scatter -------------
+// K1: tile id per positive (kept for K3) + warp-aggregated global counts
+__global__ void __launch_bounds__(256) pos_count_kernel(PosGeom g, const int32_t* __restrict__ ps,
+                                                        const int32_t* __restrict__ pl, int64_t nnz,
+                                                        int32_t* __restrict__ cnt, uint32_t* __restrict__ tmp_tile,
+                                                        uint32_t* __restrict__ tmp_entry, int32_t* status) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  uint32_t key = 0xffffffffu, val = 0;
+  bool bad = false;
+  if (i < nnz) {
+    const int32_t s = ps[i];
+    const int64_t local = static_cast<int64_t>(pl[i]) - g.label_offset;
+    if (s < 0 || s >= g.B) bad = true;
+    else if (local >= 0 && local < g.num_local) {
+      int32_t r;
+      key = static_cast<uint32_t>(pos_tile(g, local, &r));
+      val = (static_cast<uint32_t>(r) << 16) | static_cast<uint32_t>(s);
+    }
+    tmp_tile[i] = key;
+    tmp_entry[i] = val;
+  }
+  if (bad) atomicOr(status, ST_BAD_SAMPLE);
+  warp_sort_pairs(key, val);
+  int st, len;
+  warp_runs(key, &st, &len);
+  if (key != 0xffffffffu && (threadIdx.x & 31) == st) atomicAdd(&cnt[key], len);
+}
+
+// K2: exclusive scan of the T tile counters (one CTA; smem-staged segments)
+__global__ void __launch_bounds__(1024) pos_scan_kernel(int32_t* __restrict__ cnt, int32_t* __restrict__ ptr, int32_t T) {
+  extern __shared__ int32_t sc[];   // [T]
+  __shared__ int32_t wsum[32];
+  const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, w = tid >> 5;
+  for (int i = tid; i < T; i += nth) sc[i] = cnt[i];
   __syncthreads();
-  for (int64_t base = 0; base < n; base += blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const int32_t v = i < n ? cnt[i] : 0;
+  const int per = (T + nth - 1) / nth;
+  const int a = min(T, tid * per), b = min(T, a + per);
+  int32_t run = 0;
+  for (int i = a; i < b; ++i) run += sc[i];
+  int32_t x = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int32_t v = lane < (nth >> 5) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    wsum[lane] = v;
+  }
+  __syncthreads();
+  int32_t pre = (w > 0 ? wsum[w - 1] : 0) + x - run;
+  for (int i = a; i < b; ++i) {
+    const int32_t c = sc[i];
+    sc[i] = pre;
+    pre += c;
+  }
+  if (tid == nth - 1) ptr[T] = pre;
+  __syncthreads();
+  for (int i = tid; i < T; i += nth) {
+    ptr[i] = sc[i];
+    cnt[i] = sc[i];   // becomes the scatter cursor
+  }
+}
+
+// K3: scatter packed entries to their tile buckets (warp-aggregated cursors)
+__global__ void __launch_bounds__(256) pos_scatter_kernel(int64_t nnz, const uint32_t* __restrict__ tmp_tile,
+                                                          const uint32_t* __restrict__ tmp_entry,
+                                                          int32_t* __restrict__ cursor, uint32_t* __restrict__ entries) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  uint32_t key = 0xffffffffu, val = 0;
+  if (i < nnz) {
+    key = tmp_tile[i];
+    val = tmp_entry[i];
+  }
+  warp_sort_pairs(key, val);
+  int st, len;
+  warp_runs(key, &st, &len);
+  const int lane = threadIdx.x & 31;
+  int32_t b = 0;
+  if (key != 0xffffffffu && lane == st) b = atomicAdd(&cursor[key], len);
+  b = __shfl_sync(0xffffffffu, b, st);
+  if (key != 0xffffffffu) entries[b + (lane - st)] = val;
+}
+
+// Whole positive-list bucketing in one CTA with shared-memory counters:
+// count per (chunk, 128-label tile) -> exclusive scan -> scatter.  Used when
+// the tile count fits shared memory (every BASELINE config per rank).
+constexpr int kPosMaxTiles = 48 * 1024;
+__global__ void __launch_bounds__(1024) pos_bucket_kernel(PosGeom g, const int32_t* __restrict__ ps,
+                                                          const int32_t* __restrict__ pl, int64_t nnz, int32_t T,
+                                                          int32_t* __restrict__ tile_ptr,
+                                                          uint32_t* __restrict__ entries, int32_t* status) {
+  constexpr int kPer = 16;            // positives held in registers per thread per batch
+  extern __shared__ int32_t cnt[];    // [T]
+  __shared__ int64_t cs[65], tb[65];
+  __shared__ int32_t wsum[32];
+  __shared__ int32_t carry;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, w = tid >> 5, nw = nth >> 5;
+  for (int i = tid; i <= g.k; i += nth) {
+    cs[i] = g.chunk_start[i];
+    tb[i] = g.tile_base[i];
+  }
+  const int T4 = (T + 3) / 4;
+  for (int i = tid; i < T4; i += nth) reinterpret_cast<int4*>(cnt)[i] = make_int4(0, 0, 0, 0);
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  PosGeom sg = g;
+  sg.chunk_start = cs;
+  sg.tile_base = tb;
+  // positives of this thread: i = tid + k * nth (all loads issued up front)
+  const int64_t per_pass = static_cast<int64_t>(nth) * kPer;
+  bool bad = false;
+  for (int64_t base0 = 0; base0 < nnz; base0 += per_pass) {
+    int32_t t[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int64_t i = base0 + tid + static_cast<int64_t>(k) * nth;
+      t[k] = -1;
+      if (i < nnz) {
+        const int32_t s = ps[i];
+        const int64_t local = static_cast<int64_t>(pl[i]) - g.label_offset;
+        if (s < 0 || s >= g.B) bad = true;
+        else if (local >= 0 && local < g.num_local) {
+          int32_t r;
+          t[k] = static_cast<int32_t>(pos_tile(sg, local, &r));
+        }
+      }
+    }
+    // Zipf labels pile onto a few low tiles: sort each warp's 32 tile ids and
+    // issue one shared atomic per run of equal tiles
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      uint32_t key = t[k] >= 0 ? static_cast<uint32_t>(t[k]) : 0xffffffffu, val = 0;
+      warp_sort_pairs(key, val);
+      int st, len;
+      warp_runs(key, &st, &len);
+      if (key != 0xffffffffu && lane == st) atomicAdd(&cnt[key], len);
+    }
+  }
+  if (bad) atomicOr(status, ST_BAD_SAMPLE);
+  __syncthreads();
+  // exclusive scan in coalesced rounds of nth counters
+  for (int base = 0; base < T; base += nth) {
+    const int i = base + tid;
+    const int32_t v = i < T ? cnt[i] : 0;
     int32_t x = v;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    if (lane == 31) warp_sums[w] = x;
+    if (lane == 31) wsum[w] = x;
     __syncthreads();
     if (w == 0) {
-      int32_t ws = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+      int32_t s = lane < nw ? wsum[lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, ws, o);
-        if (lane >= o) ws += y;
+        const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
       }
-      warp_sums[lane] = ws;
+      wsum[lane] = s;
     }
     __syncthreads();
-    const int32_t excl = carry + (w > 0 ? warp_sums[w - 1] : 0) + x - v;
-    if (i < n) {
-      ptr[i] = excl;
-      cnt[i] = excl;
+    const int32_t excl = carry + (w > 0 ? wsum[w - 1] : 0) + x - v;
+    if (i < T) {
+      tile_ptr[i] = excl;
+      cnt[i] = excl;   // becomes the scatter cursor
     }
     __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    if (tid == nth - 1) carry = excl + v;
     __syncthreads();
   }
-  if (threadIdx.x == 0) ptr[n] = carry;
-}
-
-__global__ void pos_scatter_kernel(PosGeom g, const int32_t* __restrict__ ps, const int32_t* __restrict__ pl,
-                                   int64_t nnz, int32_t* __restrict__ cursor, uint32_t* __restrict__ entries) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t s = ps[i];
-    if (s < 0 || s >= g.B) continue;
-    const int64_t local = static_cast<int64_t>(pl[i]) - g.label_offset;
-    if (local < 0 || local >= g.num_local) continue;
-    int32_t r;
-    const int64_t t = pos_tile(g, local, &r);
-    const int32_t slot = atomicAdd(&cursor[t], 1);
-    entries[slot] = (static_cast<uint32_t>(r) << 16) | static_cast<uint32_t>(s);
-  }
-}
-
-// grad_x[s][c] += sum_r ws[r][c][s - col0]   (fixed r order: deterministic)
-__global__ void gx_reduce_kernel(const float* __restrict__ ws, int R, int d, int ld, int B, float scale,
-                                 int accumulate, float* __restrict__ gx) {
-  __shared__ float tile[32][33];
-  const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int c = c0 + i, s = s0 + threadIdx.x;
-    float acc = 0.f;
-    if (s < B)
-      for (int r = 0; r < R; ++r) acc += ws[((int64_t)r * d + c) * ld + s];
-    tile[i][threadIdx.x] = acc * scale;
-  }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int s = s0 + i, c = c0 + threadIdx.x;
-    if (s < B) {
-      float* o = gx + (int64_t)s * d + c;
-      *o = accumulate ? *o + tile[threadIdx.x][i] : tile[threadIdx.x][i];
+  if (tid == 0) tile_ptr[T] = carry;
+  for (int64_t base0 = 0; base0 < nnz; base0 += per_pass) {
+    int32_t t[kPer];
+    uint32_t e[kPer];
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int64_t i = base0 + tid + static_cast<int64_t>(k) * nth;
+      t[k] = -1;
+      e[k] = 0;
+      if (i < nnz) {
+        const int32_t s = ps[i];
+        const int64_t local = static_cast<int64_t>(pl[i]) - g.label_offset;
+        if (s >= 0 && s < g.B && local >= 0 && local < g.num_local) {
+          int32_t r;
+          t[k] = static_cast<int32_t>(pos_tile(sg, local, &r));
+          e[k] = (static_cast<uint32_t>(r) << 16) | static_cast<uint32_t>(s);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      uint32_t key = t[k] >= 0 ? static_cast<uint32_t>(t[k]) : 0xffffffffu, val = e[k];
+      warp_sort_pairs(key, val);
+      int st, len;
+      warp_runs(key, &st, &len);
+      int32_t b = 0;
+      if (key != 0xffffffffu && lane == st) b = atomicAdd(&cnt[key], len);
+      b = __shfl_sync(0xffffffffu, b, st);
+      if (key != 0xffffffffu) entries[b + (lane - st)] = val;
     }
   }
 }
@@ -513,7 +704,7 @@ static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtenso
   if (grid <= 0) return XMC_OK;
   ProfRec pr;
   prof_begin(0, st, &pr);
-  xmc_fwd_kernel<EB, BN><<<grid, kFwdThreads, FwdCfg<EB, BN>::kSmemBytes, st>>>(tw, tx, p);
+  xmc_fwd_kernel<EB, BN><<<grid, FwdCfg<EB, BN>::kThreads, FwdCfg<EB, BN>::kSmemBytes, st>>>(tw, tx, p);
   CUDA_TRY(cudaGetLastError());
   prof_end(st, &pr);
   return XMC_OK;
@@ -565,7 +756,7 @@ static xmc_status launch_bwd_t(int grid, const CUtensorMap& tw, const CUtensorMa
 // one bwd pass over local rows [row0, row0+rows), G from gbuf; grad_X partials
 // accumulate into the [R][d][Bp] workspace (zeroed by the caller per step)
 static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, int Bp, bool update, int gx_kc0,
-                             int gx_kc_count, const xmc_step_args* a, cudaStream_t st) {
+                             int gx_kc_count, bool gx_overwrite, const xmc_step_args* a, cudaStream_t st) {
   const int eb = h->eb, D = h->desc.dim;
   const int box_k = 128 / eb;
   CUtensorMap tw, tg, tx, tws;
@@ -593,7 +784,9 @@ static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, i
   p.rng_base = a ? sm64_base(a->seed, a->step, a->tensor_id) : 0;
   p.gx_ws = h->gx_ws;
   p.gx_ld = Bp;
-  p.gx_accumulate = 1;
+  p.gx_accumulate = gx_overwrite ? 0 : 1;
+  static const int dbg = getenv("XMC_DEBUG_BWD") ? atoi(getenv("XMC_DEBUG_BWD")) : 0;
+  p.debug = dbg;
   p.status = h->status;
   const int grid = R * h->dtiles;
   if (eb == 1) {
@@ -610,17 +803,17 @@ static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, i
 
 // grad_X partials + update for one chunk whose G is in gbuf (Bp = 512 takes two passes)
 static xmc_status run_backward(xmc_head* h, void* W, int64_t row0, int64_t rows, int Bp, bool gx, bool update,
-                               const xmc_step_args* a, cudaStream_t st) {
+                               bool gx_overwrite, const xmc_step_args* a, cudaStream_t st) {
   const int kcs = Bp * h->eb / 128;
   const int per = 256 * h->eb / 128;   // k-chunks whose grad_X columns fit 256 TMEM columns
-  if (!gx) return launch_bwd(h, W, row0, rows, Bp, update, 0, 0, a, st);
+  if (!gx) return launch_bwd(h, W, row0, rows, Bp, update, 0, 0, false, a, st);
   // passes over grad_X column groups; the update rides on the LAST pass so
   // every grad_X pass reads the pre-update weights (head.py:290-291)
   const int groups = (kcs + per - 1) / per;
   for (int gi = groups - 1; gi >= 0; --gi) {
     const int kc0 = gi * per;
     const int cnt = std::min(per, kcs - kc0);
-    XMC_TRY(launch_bwd(h, W, row0, rows, Bp, update && gi == 0, kc0, cnt, a, st));
+    XMC_TRY(launch_bwd(h, W, row0, rows, Bp, update && gi == 0, kc0, cnt, gx_overwrite, a, st));
   }
   return XMC_OK;
 }
@@ -628,7 +821,7 @@ static xmc_status run_backward(xmc_head* h, void* W, int64_t row0, int64_t rows,
 // acc[s][c] (+)= scale * sum_r ws[r][c][s]  -- one deterministic reduction per step
 static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumulate, cudaStream_t st) {
   const int D = h->desc.dim;
-  dim3 g(D / 32, (Bp + 31) / 32), b(32, 8);
+  dim3 g(D / 32, (Bp + 31) / 32), b(32, 32);
   gx_reduce_kernel<<<g, b, 0, st>>>(h->gx_ws, h->R, D, Bp, B, h->eb == 1 ? (1.0f / 256.0f) : 1.0f,
                                      accumulate ? 1 : 0, acc);
   CUDA_TRY(cudaGetLastError());
@@ -653,21 +846,32 @@ static xmc_status prepare_positives(xmc_head* h, const int32_t* ps, const int32_
   if (nnz > h->desc.max_positives)
     return fail(XMC_ERR_CAPACITY, "%lld positives exceed workspace capacity %lld", (long long)nnz,
                 (long long)h->desc.max_positives);
-  CUDA_TRY(cudaMemsetAsync(h->tile_cnt, 0, (h->total_tiles + 1) * 4, st));
   PosGeom g{h->chunk_dev, h->chunk_dev + h->chunks.size() + 1, static_cast<int32_t>(h->chunks.size()),
             h->desc.label_offset, h->desc.num_labels_local, B};
-  if (nnz > 0) {
-    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(nnz, 256), 1184));
-    pos_count_kernel<<<blocks, 256, 0, st>>>(g, ps, pl, nnz, h->tile_cnt, h->status);
-    CUDA_TRY(cudaGetLastError());
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pos_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPosMaxTiles * 4);
+    cudaFuncSetAttribute(pos_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPosMaxTiles * 4);
+    attr = true;
   }
-  pos_scan_kernel<<<1, 1024, 0, st>>>(h->tile_cnt, h->tile_ptr, h->total_tiles);
+  const int32_t T = static_cast<int32_t>(h->total_tiles);
+  if (T > kPosMaxTiles || h->chunks.size() > 64)
+    return fail(XMC_ERR_UNSUPPORTED, "%d label tiles per rank exceed the bucketing capacity %d; use more ranks", T,
+                kPosMaxTiles);
+  if (nnz <= 2048) {
+    // tiny batches: one launch, everything in one CTA's shared memory
+    pos_bucket_kernel<<<1, 1024, T * 4, st>>>(g, ps, pl, nnz, T, h->tile_ptr, h->entries, h->status);
+    CUDA_TRY(cudaGetLastError());
+    return XMC_OK;
+  }
+  CUDA_TRY(cudaMemsetAsync(h->tile_cnt, 0, (h->total_tiles + 1) * 4, st));
+  const int blocks = static_cast<int>(cdiv(nnz, 256));
+  pos_count_kernel<<<blocks, 256, 0, st>>>(g, ps, pl, nnz, h->tile_cnt, h->tmp_tile, h->tmp_entry, h->status);
   CUDA_TRY(cudaGetLastError());
-  if (nnz > 0) {
-    const int blocks = static_cast<int>(std::min<int64_t>(cdiv(nnz, 256), 1184));
-    pos_scatter_kernel<<<blocks, 256, 0, st>>>(g, ps, pl, nnz, h->tile_cnt, h->entries);
-    CUDA_TRY(cudaGetLastError());
-  }
+  pos_scan_kernel<<<1, 1024, T * 4, st>>>(h->tile_cnt, h->tile_ptr, T);
+  CUDA_TRY(cudaGetLastError());
+  pos_scatter_kernel<<<blocks, 256, 0, st>>>(nnz, h->tmp_tile, h->tmp_entry, h->tile_cnt, h->entries);
+  CUDA_TRY(cudaGetLastError());
   return XMC_OK;
 }
 
@@ -699,12 +903,15 @@ extern "C" xmc_status xmc_head_step(xmc_head_t h, void* W, const float* X, int32
   const int Bp = padded_batch(h->eb, B);
   XMC_TRY(launch_x_prep(h, X, B, Bp, st));
   XMC_TRY(prepare_positives(h, pos_sample, pos_label, nnz, B, st));
-  XMC_TRY(zero_gx_ws(h, Bp, st));
+  // the first chunk overwrites every partial slot unless it has fewer tiles
+  // than slots; later chunks accumulate
+  const bool first_covers = !h->chunks.empty() && cdiv(h->chunks[0].second - h->chunks[0].first, 128) >= h->R;
+  if (!first_covers) XMC_TRY(zero_gx_ws(h, Bp, st));
   if (stats) CUDA_TRY(cudaMemsetAsync(stats, 0, 8, st));
   for (size_t c = 0; c < h->chunks.size(); ++c) {
     const int64_t r0 = h->chunks[c].first, rows = h->chunks[c].second - h->chunks[c].first;
     XMC_TRY(launch_fwd(h, W, r0, rows, B, Bp, 0, h->tile_ptr + h->tile_base[c], h->gbuf, Bp, stats, st));
-    XMC_TRY(run_backward(h, W, r0, rows, Bp, true, true, args, st));
+    XMC_TRY(run_backward(h, W, r0, rows, Bp, true, true, first_covers && c == 0, args, st));
   }
   return reduce_gx(h, B, Bp, grad_x, false, st);
 }
@@ -739,7 +946,7 @@ extern "C" xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, i
   else g_quant_kernel<2><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, 1.0f, h->gbuf, h->status);
   CUDA_TRY(cudaGetLastError());
   if (accumulate_gx) XMC_TRY(zero_gx_ws(h, Bp, st));
-  XMC_TRY(run_backward(h, W, row0, rows, Bp, accumulate_gx != 0, update != 0, args, st));
+  XMC_TRY(run_backward(h, W, row0, rows, Bp, accumulate_gx != 0, update != 0, false, args, st));
   if (accumulate_gx) XMC_TRY(reduce_gx(h, B, Bp, acc, true, st));
   return XMC_OK;
 }

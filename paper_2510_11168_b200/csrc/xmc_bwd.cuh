@@ -57,6 +57,7 @@ struct BwdParams {
   float* gx_ws;          // [R][d][gx_ld] fp32 partials (gx_ld = padded batch)
   int32_t gx_ld;
   int32_t gx_accumulate; // 1: add into the partial slot, 0: overwrite it
+  int32_t debug;         // measurement only (XMC_DEBUG_BWD): 1 skip dW MMAs, 2 skip update epilogue
   int32_t* status;
 };
 
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (elect_one()) {
           const uint32_t g_addr = smem_u32(k_s + ks * C::kKSlot);
           const uint32_t x_addr = XT_RES ? smem_u32(xt_s + kc * C::kBox) : g_addr + C::kBox;
-          if (p.do_update) {
+          if (p.do_update && !(p.debug & 1)) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t ad = umma_desc_sw128(g_addr + k * 32, 16, 1024);
@@ -357,12 +358,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // the 4 warps of sub-partition q own rows [32q, 32q+32) of every tile;
     // they sync among themselves and one lane TMA-stores their 32-row slab
     const bool storer = (quarter == 0) && lane_id() == 0;
+    const uint64_t pol_w_out = policy_evict_first();   // W_new streams out; keep L2 for G
     int ws = 0, ds = 0, prev_ws = -1;
     uint32_t wph = 0, dph = 0;
     for (int tile = r0; tile < p.num_tiles; tile += R) {
       uint8_t* wt = w_s + ws * C::kWBytes;
       mbar_wait(&w_full[ws], wph);
-      if (p.do_update) {
+      if (p.do_update && !(p.debug & 2)) {
         const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
         const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + c0;
         // --- independent of dW: W_old and random bits, overlapping the MMAs
@@ -394,7 +396,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (storer) {
 #pragma unroll
           for (int b = 0; b < C::kWBoxes; ++b)
-            tma_store_2d(&tm_ws, wt + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK, tile * 128 + q * 32);
+            tma_store_2d_hint(&tm_ws, wt + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK, tile * 128 + q * 32,
+                              pol_w_out);
           bulk_commit();
           // release the previous tile's slot once its store has read smem
           bulk_wait_read<1>();

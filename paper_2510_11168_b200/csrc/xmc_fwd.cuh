@@ -22,8 +22,6 @@
 
 namespace xmc {
 
-constexpr int kFwdEpiWarps = 8;
-constexpr int kFwdThreads = 64 + kFwdEpiWarps * 32;
 
 struct FwdParams {
   int32_t rows;        // labels in this chunk
@@ -55,10 +53,15 @@ struct FwdCfg {
   static constexpr int kBitmapBytes = 128 * kWordsPerRow * 4;
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kBitmapBytes + 256;
   static constexpr int kMmaN = BN > 256 ? 256 : BN;
+  // epilogue: 4 warps per TMEM sub-partition for wide tiles, 2 otherwise
+  static constexpr int kEpiWarps = BN >= 256 ? 16 : 8;
+  static constexpr int kThreads = 64 + kEpiWarps * 32;
+  static constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
+  static constexpr int kChunks = kColsPerWarp / 32;
 };
 
 template <int EB, int BN>
-__global__ void __launch_bounds__(kFwdThreads, 1)
+__global__ void __launch_bounds__(FwdCfg<EB, BN>::kThreads, 1)
     xmc_fwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                    FwdParams p) {
   using C = FwdCfg<EB, BN>;
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     for (int a = 0; a < C::kAccStages; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kFwdEpiWarps);
+      mbar_init(&tempty[a], C::kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -158,43 +161,56 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 2;                 // 0..7
+    constexpr int NT = C::kEpiWarps * 32;
+    const int ew = warp - 2;                 // 0 .. kEpiWarps-1
     const int q = warp & 3;                  // TMEM sub-partition of this warp
-    const int half = ew >> 2;                // column half
+    const int grp = ew >> 2;                 // which column group of the tile
     const int row = q * 32 + lane_id();      // row within the 128-label tile
-    const int etid = ew * 32 + lane_id();    // 0..255
-    constexpr int kHalfCols = BN / 2;
-    constexpr int kChunks = kHalfCols / 32;
+    const int etid = ew * 32 + lane_id();
     const bool want_stats = p.stats != nullptr && p.mode == 0;
     const bool pad_cols = p.B < BN;
+    const bool use_pos = p.mode == 0 && p.tile_ptr != nullptr;
+    const uint64_t pol_g = policy_evict_last();   // G is re-read by the backward kernel
     float abs_sum = 0.f;
     bool nan_seen = false;
     int acc = 0;
     uint32_t acc_phase = 0;
+    // tile_ptr of the first tile; the next tile's bounds are prefetched below
+    int e0 = 0, e1 = 0;
+    if (use_pos && blockIdx.x < p.num_tiles) {
+      e0 = p.tile_ptr[blockIdx.x];
+      e1 = p.tile_ptr[blockIdx.x + 1];
+    }
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      int n0 = 0, n1 = 0;
+      const int nxt = tile + gridDim.x;
+      if (use_pos && nxt < p.num_tiles) {
+        n0 = p.tile_ptr[nxt];
+        n1 = p.tile_ptr[nxt + 1];
+      }
       // positives of this tile -> bitmap, only when the tile has any (uniform)
-      const int e0 = (p.mode == 0 && p.tile_ptr) ? p.tile_ptr[tile] : 0;
-      const int e1 = (p.mode == 0 && p.tile_ptr) ? p.tile_ptr[tile + 1] : 0;
       const bool has_pos = e1 > e0;
       if (has_pos) {
-        named_bar_sync(1, kFwdEpiWarps * 32);   // previous users of the bitmap are done
-        for (int w = etid; w < 128 * C::kWordsPerRow; w += kFwdEpiWarps * 32) bitmap[w] = 0u;
-        named_bar_sync(1, kFwdEpiWarps * 32);
-        for (int e = e0 + etid; e < e1; e += kFwdEpiWarps * 32) {
+        named_bar_sync(1, NT);   // previous users of the bitmap are done
+        for (int w = etid; w < 128 * C::kWordsPerRow; w += NT) bitmap[w] = 0u;
+        named_bar_sync(1, NT);
+        for (int e = e0 + etid; e < e1; e += NT) {
           const uint32_t v = p.entries[e];
           const uint32_t r = v >> 16, s = v & 0xFFFFu;
           atomicOr(&bitmap[r * C::kWordsPerRow + (s >> 5)], 1u << (s & 31));
         }
-        named_bar_sync(1, kFwdEpiWarps * 32);
+        named_bar_sync(1, NT);
       }
+      e0 = n0;
+      e1 = n1;
 
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
       const bool row_ok = grow < p.rows;
 #pragma unroll 1
-      for (int cc = 0; cc < kChunks; ++cc) {
-        const int col0 = half * kHalfCols + cc * 32;
+      for (int cc = 0; cc < C::kChunks; ++cc) {
+        const int col0 = grp * C::kColsPerWarp + cc * 32;
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, r);
         tmem_ld_wait();
@@ -253,15 +269,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               pk[j] = lo | (hi << 16);
             }
             uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out) + grow * p.ld + col0);
-            o[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            o[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            st_global_v4_hint(o, make_uint4(pk[0], pk[1], pk[2], pk[3]), pol_g);
+            st_global_v4_hint(o + 1, make_uint4(pk[4], pk[5], pk[6], pk[7]), pol_g);
           } else {
             uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) pk[j] = cvt_bf16x2_rn(g[2 * j + 1], g[2 * j]);
             uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + grow * p.ld + col0);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) o[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            for (int j = 0; j < 4; ++j)
+              st_global_v4_hint(o + j, make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]), pol_g);
           }
         }
       }

@@ -102,6 +102,19 @@ XMC_DEV void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0, int
                "r"(smem_u32(src)), "r"(c0), "r"(c1)
                : "memory");
 }
+XMC_DEV void tma_store_2d_hint(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
+// 16-B global store with an L2 eviction-priority policy
+XMC_DEV void st_global_v4_hint(void* p, uint4 v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(policy)
+               : "memory");
+}
 XMC_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 XMC_DEV void bulk_wait_read() {
