@@ -44,7 +44,9 @@ def parse():
     ap.add_argument("--dim", type=int, default=768)
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--fmt", default="e4m3")
-    ap.add_argument("--chunks", type=int, default=8)
+    # label chunks per rank (the reference's memory knob, head.num_chunks):
+    # k=2 measured fastest on B200 (fewer launch tails), peak HBM ~2.5 GiB
+    ap.add_argument("--chunks", type=int, default=2)
     ap.add_argument("--rounding", default="stochastic")
     ap.add_argument("--sr-impl", default="philox")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -346,8 +348,17 @@ def main():
         achieved = bytes_ / (ms_launch * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"]}
+    # DRAM traffic of the same kernel from the committed ncu capture (per launch,
+    # scaled to this launch's rows): profiles/ncu_traffic.json
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            tr = json.load(f).get(dom)
+        if tr and tr.get("fmt") == a.fmt and tr.get("batch") == B:
+            traffic = tr["dram_bytes"] * rows_launch / tr["rows"]
     roof.update({"kernel": "xmc_bwd_kernel (grad_X + dW + SGD/SR update)" if dom == "bwd"
-                 else "xmc_fwd_kernel (logits + sigmoid - Y)", "traffic": None,
+                 else "xmc_fwd_kernel (logits + sigmoid - Y)", "traffic": traffic,
                  "ms_per_launch": ms_launch, "launches_per_step": n_launch,
                  "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": bytes_,
                  "peak_source": tc_src if bound == "tensor" else f"hbm {peaks['source']}",

@@ -190,6 +190,8 @@ struct xmc_head {
   int64_t* chunk_dev;  // [k+1] chunk starts (local rows) + [k+1] tile bases
   int32_t* status;     // [4]
   int R;               // bwd CTAs per d-tile
+  size_t l2_persist;   // persisting-L2 bytes granted for the G window (0 = off)
+  size_t l2_window_max;
 };
 
 struct Layout {
@@ -297,6 +299,26 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->tile_cnt = reinterpret_cast<int32_t*>(w + L.cnt);
   h->tile_ptr = reinterpret_cast<int32_t*>(w + L.ptr);
   h->entries = reinterpret_cast<uint32_t*>(w + L.ent);
+  // Optional L2 persistence for the G chunk buffer (XMC_L2_PERSIST=1).  Off by
+  // default: measured on B200 it thrashes once G exceeds the persisting carve-
+  // out and gains nothing below it (profiles/r1_notes.md).
+  h->l2_persist = 0;
+  h->l2_window_max = 0;
+  {
+    const char* env = getenv("XMC_L2_PERSIST");
+    int dev = 0, pmax = 0, wmax = 0;
+    if ((env && atoi(env) != 0) && cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&pmax, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&wmax, cudaDevAttrMaxAccessPolicyWindowSize, dev) == cudaSuccess && pmax > 0 &&
+        wmax > 0) {
+      const size_t want = std::min<size_t>(pmax, (size_t)(maxrows + 128) * bp * eb);
+      if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+        h->l2_persist = want;
+        h->l2_window_max = wmax;
+      }
+      cudaGetLastError();
+    }
+  }
   h->tmp_tile = reinterpret_cast<uint32_t*>(w + L.tmp);
   h->tmp_entry = h->tmp_tile + std::max<int64_t>(desc->max_positives, 1);
   h->chunk_dev = reinterpret_cast<int64_t*>(w + L.chunk);
@@ -697,6 +719,33 @@ static xmc_status launch_x_prep(xmc_head* h, const float* X, int B, int Bp, cuda
   return XMC_OK;
 }
 
+// Launch with an optional L2 access-policy window: the chunk's G buffer is
+// marked persisting so it survives in L2 between the forward that writes it
+// and the backward that re-reads it once per d-tile, while W streams past.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_ex(void (*kernel)(KArgs...), int grid, int block, int smem, cudaStream_t st,
+                             const xmc_head* h, size_t win_bytes, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  cfg.attrs = at;
+  cfg.numAttrs = 0;
+  if (h->l2_persist > 0 && win_bytes > 0) {
+    const size_t nb = std::min(win_bytes, h->l2_window_max);
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = h->gbuf;
+    at[0].val.accessPolicyWindow.num_bytes = nb;
+    at[0].val.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(h->l2_persist) / static_cast<float>(nb));
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int EB, int BN>
 static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtensorMap& tx, const FwdParams& p,
                                cudaStream_t st) {
@@ -704,8 +753,9 @@ static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtenso
   if (grid <= 0) return XMC_OK;
   ProfRec pr;
   prof_begin(0, st, &pr);
-  xmc_fwd_kernel<EB, BN><<<grid, FwdCfg<EB, BN>::kThreads, FwdCfg<EB, BN>::kSmemBytes, st>>>(tw, tx, p);
-  CUDA_TRY(cudaGetLastError());
+  const size_t win = p.mode == 0 ? static_cast<size_t>(p.rows) * p.ld * EB : 0;
+  CUDA_TRY(launch_ex(xmc_fwd_kernel<EB, BN>, grid, FwdCfg<EB, BN>::kThreads, FwdCfg<EB, BN>::kSmemBytes, st, h, win,
+                     tw, tx, p));
   prof_end(st, &pr);
   return XMC_OK;
 }
@@ -743,12 +793,13 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t r
 }
 
 template <int EB, bool XR, int KC>
-static xmc_status launch_bwd_t(int grid, const CUtensorMap& tw, const CUtensorMap& tg, const CUtensorMap& tx,
-                               const CUtensorMap& tws, const BwdParams& p, cudaStream_t st) {
+static xmc_status launch_bwd_t(xmc_head* h, int grid, const CUtensorMap& tw, const CUtensorMap& tg,
+                               const CUtensorMap& tx, const CUtensorMap& tws, const BwdParams& p, size_t g_bytes,
+                               cudaStream_t st) {
   ProfRec pr;
   prof_begin(1, st, &pr);
-  xmc_bwd_kernel<EB, XR, KC><<<grid, kBwdThreads, BwdCfg<EB, XR, KC>::kSmemBytes, st>>>(tw, tg, tx, tws, p);
-  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC>, grid, kBwdThreads, BwdCfg<EB, XR, KC>::kSmemBytes, st, h, g_bytes,
+                     tw, tg, tx, tws, p));
   prof_end(st, &pr);
   return XMC_OK;
 }
@@ -789,14 +840,15 @@ static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, i
   p.debug = dbg;
   p.status = h->status;
   const int grid = R * h->dtiles;
+  const size_t gb = static_cast<size_t>(rows) * Bp * eb;
   if (eb == 1) {
-    if (Bp == 128) return launch_bwd_t<1, true, 1>(grid, tw, tg, tx, tws, p, st);
-    if (Bp == 256) return launch_bwd_t<1, true, 2>(grid, tw, tg, tx, tws, p, st);
+    if (Bp == 128) return launch_bwd_t<1, true, 1>(h, grid, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 256) return launch_bwd_t<1, true, 2>(h, grid, tw, tg, tx, tws, p, gb, st);
   } else {
-    if (Bp == 64) return launch_bwd_t<2, true, 1>(grid, tw, tg, tx, tws, p, st);
-    if (Bp == 128) return launch_bwd_t<2, true, 2>(grid, tw, tg, tx, tws, p, st);
-    if (Bp == 256) return launch_bwd_t<2, true, 4>(grid, tw, tg, tx, tws, p, st);
-    if (Bp == 512) return launch_bwd_t<2, false, 8>(grid, tw, tg, tx, tws, p, st);
+    if (Bp == 64) return launch_bwd_t<2, true, 1>(h, grid, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 128) return launch_bwd_t<2, true, 2>(h, grid, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 256) return launch_bwd_t<2, true, 4>(h, grid, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 512) return launch_bwd_t<2, false, 8>(h, grid, tw, tg, tx, tws, p, gb, st);
   }
   return fail(XMC_ERR_UNSUPPORTED, "no backward kernel for padded batch %d", Bp);
 }
