@@ -1,0 +1,101 @@
+"""Label-sharded head across GPUs.
+
+One process per GPU.  Rank r owns the contiguous label rows
+``partition(L, world)[r]`` (head.py:51-57) of W; a batch (X, positives with
+GLOBAL label ids) is given to every rank, each rank runs the fused head step
+on its shard (labels outside the shard are ignored there, exactly as the
+reference ignores labels outside a chunk) and the partial input gradients are
+summed with one all-reduce.  RNG keys use the global row index, so the
+weights each rank ends with are the rows the single-GPU run would produce.
+
+Evaluation (F1): per-rank scores -> per-rank top-k (score, global label) ->
+all-gather -> merge with ties broken toward the lower label index, the
+reference's ``top_k_indices`` order (metrics.py:38-47).
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import torch
+import torch.distributed as dist
+
+from .head import ChunkedHead, partition
+
+
+def shard_bounds(num_labels: int, world: int, rank: int) -> tuple[int, int]:
+    """Rows owned by `rank` (head.py:51-57 partition)."""
+    parts = partition(num_labels, world)
+    if len(parts) != world:
+        raise ValueError(f"cannot shard {num_labels} labels over {world} ranks")
+    return parts[rank]
+
+
+def topk_stable(scores: torch.Tensor, k: int, offset: int = 0) -> tuple[torch.Tensor, torch.Tensor]:
+    """Per-row top-k of a (B, L) score matrix with ties toward the lower index
+    (metrics.py:38-47); returns (values, global indices)."""
+    if not (1 <= k <= scores.shape[1]):
+        raise ValueError(f"k must lie in [1, {scores.shape[1]}]")
+    vals, idx = torch.topk(scores, k, dim=1, largest=True, sorted=True)
+    kth = vals[:, -1:]
+    n_ge = (scores >= kth).sum(dim=1)
+    tied = (n_ge > k).nonzero().flatten()
+    for r in tied.tolist():   # exact stable order only where the k-th score is tied
+        order = torch.sort(-scores[r], stable=True).indices[:k]
+        idx[r] = order
+        vals[r] = scores[r, order]
+    return vals, idx + offset
+
+
+def merge_topk(vals: torch.Tensor, idx: torch.Tensor, k: int) -> torch.Tensor:
+    """Merge per-rank candidates (B, world*k): order by (-score, label)."""
+    # lexicographic key: sort by label first, then stable by -score
+    o1 = torch.argsort(idx, dim=1, stable=True)
+    v1, i1 = torch.gather(vals, 1, o1), torch.gather(idx, 1, o1)
+    o2 = torch.argsort(-v1, dim=1, stable=True)
+    return torch.gather(i1, 1, o2)[:, :k]
+
+
+class ShardedHead:
+    """A rank's shard of a label-sharded head.
+
+    ``local_step(batch, cfg, rng, step) -> grad_X partial`` defaults to the
+    fused GPU step on this rank's ChunkedHead; tests may inject another
+    per-rank implementation to exercise the sharding logic on CPU (gloo).
+    """
+
+    def __init__(self, num_labels: int, rank: int, world: int, local: ChunkedHead | None = None,
+                 group=None, local_step: Callable | None = None, local_scores: Callable | None = None):
+        self.num_labels = num_labels
+        self.rank, self.world = rank, world
+        self.lo, self.hi = shard_bounds(num_labels, world, rank)
+        self.local = local
+        self.group = group
+        if local is not None:
+            if local.num_labels != self.hi - self.lo or local.label_offset != self.lo:
+                raise ValueError("local head does not match this rank's shard")
+        self._step = local_step or self._gpu_step
+        self._scores = local_scores or (lambda X: self.local.scores(X))
+
+    def _gpu_step(self, batch, cfg, rng, step):
+        from .head import head_update
+        return head_update(self.local, batch, cfg, rng, step)
+
+    def head_update(self, batch, cfg, rng, step: int) -> torch.Tensor:
+        """head_update over all shards; returns the full grad_X on every rank."""
+        gx = self._step(batch, cfg, rng, step)
+        if self.world > 1:
+            dist.all_reduce(gx, op=dist.ReduceOp.SUM, group=self.group)
+        return gx
+
+    def topk(self, X, k: int) -> torch.Tensor:
+        """Global top-k label ids per sample (B, k)."""
+        sc = self._scores(X)
+        vals, idx = topk_stable(sc, min(k, sc.shape[1]), offset=self.lo)
+        if self.world > 1:
+            vs = [torch.empty_like(vals) for _ in range(self.world)]
+            ix = [torch.empty_like(idx) for _ in range(self.world)]
+            dist.all_gather(vs, vals.contiguous(), group=self.group)
+            dist.all_gather(ix, idx.contiguous(), group=self.group)
+            vals, idx = torch.cat(vs, dim=1), torch.cat(ix, dim=1)
+        return merge_topk(vals, idx, k)
