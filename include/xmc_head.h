@@ -59,7 +59,7 @@ typedef struct {
   int32_t max_batch;         /* B capacity of the workspace               */
   int64_t max_positives;     /* nnz capacity of the workspace             */
   int32_t num_sms;           /* persistent-grid size (0 = device SM count)*/
-  int32_t reserved;
+  int32_t comp_bytes;        /* Kahan compensation storage: 0 none, 2 bf16, 4 fp32 */
 } xmc_head_desc;
 
 typedef struct xmc_head* xmc_head_t;
@@ -100,6 +100,16 @@ xmc_status xmc_head_destroy(xmc_head_t h);
 xmc_status xmc_head_step(xmc_head_t h, void* W, const float* X, int32_t B, const int32_t* pos_sample,
                          const int32_t* pos_label, int64_t nnz, const xmc_step_args* args,
                          float* grad_x, float* stats, void* stream);
+
+/* head_update with the head-Kahan extension: kahan_add
+ * (formats.py:246-263) composed with the SGD update (optimizers.py:51-74),
+ *   v = -lr (g + wd s); y = v - c; s' = ROUND(s + y); c' = (s' - s) - y,
+ * with the compensation c stored per weight in `comp` (desc.comp_bytes: bf16
+ * as in PAPER.md:795, or fp32 as in the reference's KahanState).  comp NULL
+ * == xmc_head_step. */
+xmc_status xmc_head_step_kahan(xmc_head_t h, void* W, void* comp, const float* X, int32_t B,
+                               const int32_t* pos_sample, const int32_t* pos_label, int64_t nnz,
+                               const xmc_step_args* args, float* grad_x, float* stats, void* stream);
 
 /* Synchronise `stream` and report a latched device error (and clear it). */
 xmc_status xmc_head_check(xmc_head_t h, void* stream);

@@ -284,7 +284,7 @@ def sgd_sr_values(w, grad, cfg: SgdSrConfig, rng, step, tensor_id, global_index)
 
 
 def kahan_sgd_values(w, comp, grad, cfg: SgdSrConfig, rng, step, tensor_id,
-                     global_index):
+                     global_index, comp_fmt=None):
     """Head-Kahan extension composed from
     kahan_add (formats.py:246-263) and the SGD update (optimizers.py:51-74):
         v = -lr*(g + wd*s); y = v - c; t = ROUND(s + y); c = (t - s) - y.
@@ -306,7 +306,10 @@ def kahan_sgd_values(w, comp, grad, cfg: SgdSrConfig, rng, step, tensor_id,
         t = round_stochastic(cfg.fmt, x, rng, step, tensor_id, global_index)
     else:
         t = round_nearest(cfg.fmt, x)
-    return t, (t - s) - y
+    c_new = (t - s) - y
+    if comp_fmt is not None:   # compensation stored on a grid (bf16 in the paper)
+        c_new = round_nearest(comp_fmt, c_new)
+    return t, c_new
 
 
 # ---------------------------------------------------------------------------
@@ -423,7 +426,7 @@ def input_gradient_accumulate(acc, G, head, chunk, rng, step):
     return acc
 
 
-def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None):
+def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None, comp_fmt=None):
     """Per 64-row block: scratch = G_rows @ Xq, then the SGD+rounding step
     keyed by the global flat index.  head.py:212-251 (rounding vectorised
     across the row block; see module docstring).  With ``comp`` (float32
@@ -448,7 +451,7 @@ def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None):
             else:
                 head.values[r0:r1], comp[r0:r1] = kahan_sgd_values(
                     head.values[r0:r1], comp[r0:r1], scratch, cfg, rng, step,
-                    head.tensor_id, idx)
+                    head.tensor_id, idx, comp_fmt)
 
 
 def quantize_g_operand(G, fmt):
@@ -463,7 +466,7 @@ def quantize_g_operand(G, fmt):
 
 
 def head_update(head, X, sample_idx, label_idx, cfg, rng, step, comp=None,
-                probe=None, g_quant=False):
+                probe=None, g_quant=False, comp_fmt=None):
     """One head step over all chunks; returns grad_X (b, d).  head.py:254-298.
     ``g_quant=True`` applies quantize_g_operand to each chunk's G before the
     backward (the GPU's operand precision)."""
@@ -485,7 +488,7 @@ def head_update(head, X, sample_idx, label_idx, cfg, rng, step, comp=None,
         if g_quant:
             G = quantize_g_operand(G, head.fmt)
         input_gradient_accumulate(acc, G, head, chunk, rng, step)
-        fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp)
+        fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp, comp_fmt)
     return acc
 
 

@@ -32,7 +32,7 @@ class HeadDesc(ctypes.Structure):
                 ("num_labels_local", ctypes.c_int64), ("dim", ctypes.c_int32),
                 ("fmt", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
                 ("max_batch", ctypes.c_int32), ("max_positives", ctypes.c_int64),
-                ("num_sms", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("num_sms", ctypes.c_int32), ("comp_bytes", ctypes.c_int32)]
 
 
 class StepArgs(ctypes.Structure):
@@ -57,6 +57,7 @@ _SIGNATURES = {
     "xmc_head_create": ([ctypes.POINTER(HeadDesc), _P, ctypes.c_size_t, ctypes.POINTER(_P)], _I32),
     "xmc_head_destroy": ([_P], _I32),
     "xmc_head_step": ([_P, _P, _P, _I32, _P, _P, _I64, ctypes.POINTER(StepArgs), _P, _P, _P], _I32),
+    "xmc_head_step_kahan": ([_P, _P, _P, _P, _I32, _P, _P, _I64, ctypes.POINTER(StepArgs), _P, _P, _P], _I32),
     "xmc_head_check": ([_P, _P], _I32),
     "xmc_head_logits": ([_P, _P, _P, _I32, _I64, _I64, _P, _I64, _P], _I32),
     "xmc_logit_gradient": ([_P, _I64, _I32, _I64, _P, _P, _I64, _I64, _P, _P], _I32),

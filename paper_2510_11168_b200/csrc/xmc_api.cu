@@ -207,6 +207,8 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   if (d->dim <= 0 || d->dim % 128 != 0)
     return fail(XMC_ERR_SHAPE, "dim must be a positive multiple of 128 (got %d)", d->dim);
   if (d->num_chunks < 1) return fail(XMC_ERR_ARG, "num_chunks must be >= 1");
+  if (d->comp_bytes != 0 && d->comp_bytes != 2 && d->comp_bytes != 4)
+    return fail(XMC_ERR_ARG, "comp_bytes must be 0 (none), 2 (bf16) or 4 (fp32)");
   if (d->num_labels_local < 1 || d->label_offset < 0 ||
       d->label_offset + d->num_labels_local > d->num_labels_global)
     return fail(XMC_ERR_ARG, "bad label shard [%lld, +%lld) of %lld", (long long)d->label_offset,
@@ -265,7 +267,11 @@ static void set_fwd_attr() {
 }
 template <int EB, bool XR, int KC>
 static void set_bwd_attr() {
-  cudaFuncSetAttribute(xmc_bwd_kernel<EB, XR, KC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(xmc_bwd_kernel<EB, XR, KC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       BwdCfg<EB, XR, KC>::kSmemBytes);
+  cudaFuncSetAttribute(xmc_bwd_kernel<EB, XR, KC, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       BwdCfg<EB, XR, KC>::kSmemBytes);
+  cudaFuncSetAttribute(xmc_bwd_kernel<EB, XR, KC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        BwdCfg<EB, XR, KC>::kSmemBytes);
 }
 
@@ -798,16 +804,23 @@ static xmc_status launch_bwd_t(xmc_head* h, int grid, const CUtensorMap& tw, con
                                cudaStream_t st) {
   ProfRec pr;
   prof_begin(1, st, &pr);
-  CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC>, grid, kBwdThreads, BwdCfg<EB, XR, KC>::kSmemBytes, st, h, g_bytes,
-                     tw, tg, tx, tws, p));
+  constexpr int sm = BwdCfg<EB, XR, KC>::kSmemBytes;
+  const int ce = p.comp ? h->desc.comp_bytes : 0;
+  if (ce == 2)
+    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 2>, grid, kBwdThreads, sm, st, h, g_bytes, tw, tg, tx, tws, p));
+  else if (ce == 4)
+    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 4>, grid, kBwdThreads, sm, st, h, g_bytes, tw, tg, tx, tws, p));
+  else
+    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 0>, grid, kBwdThreads, sm, st, h, g_bytes, tw, tg, tx, tws, p));
   prof_end(st, &pr);
   return XMC_OK;
 }
 
 // one bwd pass over local rows [row0, row0+rows), G from gbuf; grad_X partials
 // accumulate into the [R][d][Bp] workspace (zeroed by the caller per step)
-static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, int Bp, bool update, int gx_kc0,
-                             int gx_kc_count, bool gx_overwrite, const xmc_step_args* a, cudaStream_t st) {
+static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int64_t rows, int Bp, bool update,
+                             int gx_kc0, int gx_kc_count, bool gx_overwrite, const xmc_step_args* a,
+                             cudaStream_t st) {
   const int eb = h->eb, D = h->desc.dim;
   const int box_k = 128 / eb;
   CUtensorMap tw, tg, tx, tws;
@@ -827,6 +840,7 @@ static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, i
   p.gx_kc0 = gx_kc0;
   p.gx_kc_count = gx_kc_count;
   p.W = static_cast<uint8_t*>(W) + row0 * D * eb;
+  p.comp = comp ? static_cast<uint8_t*>(comp) + row0 * D * h->desc.comp_bytes : nullptr;
   p.row0_global = h->desc.label_offset + row0;
   p.lr = a ? a->lr : 0.f;
   p.wd = a ? a->weight_decay : 0.f;
@@ -854,18 +868,18 @@ static xmc_status launch_bwd(xmc_head* h, void* W, int64_t row0, int64_t rows, i
 }
 
 // grad_X partials + update for one chunk whose G is in gbuf (Bp = 512 takes two passes)
-static xmc_status run_backward(xmc_head* h, void* W, int64_t row0, int64_t rows, int Bp, bool gx, bool update,
-                               bool gx_overwrite, const xmc_step_args* a, cudaStream_t st) {
+static xmc_status run_backward(xmc_head* h, void* W, void* comp, int64_t row0, int64_t rows, int Bp, bool gx,
+                               bool update, bool gx_overwrite, const xmc_step_args* a, cudaStream_t st) {
   const int kcs = Bp * h->eb / 128;
   const int per = 256 * h->eb / 128;   // k-chunks whose grad_X columns fit 256 TMEM columns
-  if (!gx) return launch_bwd(h, W, row0, rows, Bp, update, 0, 0, false, a, st);
+  if (!gx) return launch_bwd(h, W, comp, row0, rows, Bp, update, 0, 0, false, a, st);
   // passes over grad_X column groups; the update rides on the LAST pass so
   // every grad_X pass reads the pre-update weights (head.py:290-291)
   const int groups = (kcs + per - 1) / per;
   for (int gi = groups - 1; gi >= 0; --gi) {
     const int kc0 = gi * per;
     const int cnt = std::min(per, kcs - kc0);
-    XMC_TRY(launch_bwd(h, W, row0, rows, Bp, update && gi == 0, kc0, cnt, gx_overwrite, a, st));
+    XMC_TRY(launch_bwd(h, W, comp, row0, rows, Bp, update && gi == 0, kc0, cnt, gx_overwrite, a, st));
   }
   return XMC_OK;
 }
@@ -947,7 +961,15 @@ extern "C" xmc_status xmc_head_check(xmc_head_t h, void* stream) {
 extern "C" xmc_status xmc_head_step(xmc_head_t h, void* W, const float* X, int32_t B, const int32_t* pos_sample,
                                     const int32_t* pos_label, int64_t nnz, const xmc_step_args* args,
                                     float* grad_x, float* stats, void* stream) {
+  return xmc_head_step_kahan(h, W, nullptr, X, B, pos_sample, pos_label, nnz, args, grad_x, stats, stream);
+}
+
+extern "C" xmc_status xmc_head_step_kahan(xmc_head_t h, void* W, void* comp, const float* X, int32_t B,
+                                          const int32_t* pos_sample, const int32_t* pos_label, int64_t nnz,
+                                          const xmc_step_args* args, float* grad_x, float* stats, void* stream) {
   if (!h || !W || !X || !grad_x) return fail(XMC_ERR_ARG, "null argument");
+  if (comp && h->desc.comp_bytes != 2 && h->desc.comp_bytes != 4)
+    return fail(XMC_ERR_ARG, "head created without a Kahan compensation format (comp_bytes 2 or 4)");
   XMC_TRY(check_args(args));
   if (B < 1 || B > h->desc.max_batch) return fail(XMC_ERR_SHAPE, "batch %d outside [1, %d]", B, h->desc.max_batch);
   if (nnz < 0 || (nnz > 0 && (!pos_sample || !pos_label))) return fail(XMC_ERR_ARG, "bad positives");
@@ -963,7 +985,7 @@ extern "C" xmc_status xmc_head_step(xmc_head_t h, void* W, const float* X, int32
   for (size_t c = 0; c < h->chunks.size(); ++c) {
     const int64_t r0 = h->chunks[c].first, rows = h->chunks[c].second - h->chunks[c].first;
     XMC_TRY(launch_fwd(h, W, r0, rows, B, Bp, 0, h->tile_ptr + h->tile_base[c], h->gbuf, Bp, stats, st));
-    XMC_TRY(run_backward(h, W, r0, rows, Bp, true, true, first_covers && c == 0, args, st));
+    XMC_TRY(run_backward(h, W, comp, r0, rows, Bp, true, true, first_covers && c == 0, args, st));
   }
   return reduce_gx(h, B, Bp, grad_x, false, st);
 }
@@ -998,7 +1020,7 @@ extern "C" xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, i
   else g_quant_kernel<2><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, 1.0f, h->gbuf, h->status);
   CUDA_TRY(cudaGetLastError());
   if (accumulate_gx) XMC_TRY(zero_gx_ws(h, Bp, st));
-  XMC_TRY(run_backward(h, W, row0, rows, Bp, accumulate_gx != 0, update != 0, false, args, st));
+  XMC_TRY(run_backward(h, W, nullptr, row0, rows, Bp, accumulate_gx != 0, update != 0, false, args, st));
   if (accumulate_gx) XMC_TRY(reduce_gx(h, B, Bp, acc, true, st));
   return XMC_OK;
 }

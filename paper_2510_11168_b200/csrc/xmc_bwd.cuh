@@ -50,6 +50,7 @@ struct BwdParams {
   int32_t gx_kc0;        // first sample k-chunk accumulated into grad_X
   int32_t gx_kc_count;   // 0 = no grad_X
   uint8_t* W;            // chunk base (row-major rows x d, EB bytes/elem), written in place
+  uint8_t* comp;         // Kahan compensation, chunk base (rows x d, CE bytes/elem) or null
   int64_t row0_global;   // global label of chunk row 0 (RNG key)
   float lr, wd, dw_scale;
   int32_t rounding;      // ROUND_NEAREST / ROUND_SR_EXACT / ROUND_SR_FAST
@@ -193,7 +194,89 @@ XMC_DEV void w_update_pack(const BwdParams& p, const uint32_t (&acc)[32], const 
   for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
 }
 
-template <int EB, bool XT_RES, int KCMAX>
+// Head-Kahan variant (kahan_add formats.py:246-263 composed
+// with the SGD update optimizers.py:51-74; PAPER.md:795 keeps the
+// compensation in BF16):
+//   v = -lr (g + wd s);  y = v - c;  t = ROUND(s + y);  c' = (t - s) - y;  s' = t
+// comp (CE = 2: bf16, CE = 4: fp32) is read/written straight from/to HBM by
+// the owning thread; `craw` was loaded before dW was ready.
+template <int EB, int CE>
+XMC_DEV void w_update_pack_kahan(const BwdParams& p, const uint32_t (&acc)[32], const float (&w)[32],
+                                 const uint32_t (&rw)[8 * EB], int64_t flat0, const uint4 (&craw)[CE * 2],
+                                 uint4 (&out)[2 * EB], uint4 (&cout)[CE * 2]) {
+  float c[32];
+#pragma unroll
+  for (int h = 0; h < CE * 2; ++h) {
+    const uint32_t v4[4] = {craw[h].x, craw[h].y, craw[h].z, craw[h].w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if constexpr (CE == 2) {
+        c[h * 8 + 2 * k] = __uint_as_float(v4[k] << 16);
+        c[h * 8 + 2 * k + 1] = __uint_as_float(v4[k] & 0xFFFF0000u);
+      } else {
+        c[h * 4 + k] = __uint_as_float(v4[k]);
+      }
+    }
+  }
+  const float a_lr = -p.lr * p.dw_scale;
+  const float b_wd = -p.lr * p.wd;
+  float y[32], x[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const float v = fmaf(a_lr, __uint_as_float(acc[k]), b_wd * w[k]);
+    y[k] = v - c[k];
+    x[k] = w[k] + y[k];
+  }
+  if (p.rounding == ROUND_SR_EXACT) {
+    const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      x[k] = grid_round_stochastic(gf, x[k], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + k)));
+  }
+  uint32_t pk[8 * EB];
+  float t[32];
+  if constexpr (EB == 1) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      pk[k] = p.rounding == ROUND_SR_FAST
+                  ? cvt_e4m3x4_rs(x[4 * k + 3], x[4 * k + 2], x[4 * k + 1], x[4 * k], rw[k])
+                  : (cvt_e4m3x2_rn(x[4 * k + 1], x[4 * k]) |
+                     (static_cast<uint32_t>(cvt_e4m3x2_rn(x[4 * k + 3], x[4 * k + 2])) << 16));
+      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(pk[k] & 0xFFFF));
+      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(pk[k] >> 16));
+      t[4 * k] = lo.x;
+      t[4 * k + 1] = lo.y;
+      t[4 * k + 2] = hi.x;
+      t[4 * k + 3] = hi.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      pk[k] = p.rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[2 * k + 1], x[2 * k], rw[k])
+                                           : cvt_bf16x2_rn(x[2 * k + 1], x[2 * k]);
+      t[2 * k] = __uint_as_float(pk[k] << 16);
+      t[2 * k + 1] = __uint_as_float(pk[k] & 0xFFFF0000u);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
+  float cn[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) cn[k] = (t[k] - w[k]) - y[k];
+  if constexpr (CE == 2) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h)
+      cout[h] = make_uint4(cvt_bf16x2_rn(cn[8 * h + 1], cn[8 * h]), cvt_bf16x2_rn(cn[8 * h + 3], cn[8 * h + 2]),
+                           cvt_bf16x2_rn(cn[8 * h + 5], cn[8 * h + 4]), cvt_bf16x2_rn(cn[8 * h + 7], cn[8 * h + 6]));
+  } else {
+#pragma unroll
+    for (int h = 0; h < 8; ++h)
+      cout[h] = make_uint4(__float_as_uint(cn[4 * h]), __float_as_uint(cn[4 * h + 1]), __float_as_uint(cn[4 * h + 2]),
+                           __float_as_uint(cn[4 * h + 3]));
+  }
+}
+
+template <int EB, bool XT_RES, int KCMAX, int CE>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
                    const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
@@ -372,6 +455,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int h = 0; h < C::kChunks16; ++h)
           raw[h] = *reinterpret_cast<const uint4*>(wt + w_chunk_off<EB>(row, c0, h));
+        uint4 craw[CE > 0 ? CE * 2 : 1];
+        if constexpr (CE > 0) {   // Kahan compensation of this thread's 32 elements (HBM)
+          const uint4* csrc = reinterpret_cast<const uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE);
+#pragma unroll
+          for (int h = 0; h < CE * 2; ++h)
+            craw[h] = grow < p.rows ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
+        }
         uint32_t rw[C::kRandWords];
         if (p.rounding == ROUND_SR_FAST) sr_words<EB>(p.rng_base, flat0, rw);
         float w[32];
@@ -386,7 +476,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&t_empty[ds]);
         uint4 out[C::kChunks16];
-        w_update_pack<EB>(p, acc, w, rw, flat0, out);
+        if constexpr (CE > 0) {
+          uint4 cout[CE * 2];
+          w_update_pack_kahan<EB, CE>(p, acc, w, rw, flat0, craw, out, cout);
+          if (grow < p.rows) {
+            uint4* cdst = reinterpret_cast<uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE);
+#pragma unroll
+            for (int h = 0; h < CE * 2; ++h) st_global_v4_hint(cdst + h, cout[h], pol_w_out);
+          }
+        } else {
+          w_update_pack<EB>(p, acc, w, rw, flat0, out);
+        }
         // W_new back into the same swizzled smem tile, then one TMA store per
         // 32-row slab (full 128-B lines to HBM, no LSU traffic)
 #pragma unroll

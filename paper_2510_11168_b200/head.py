@@ -78,9 +78,10 @@ class _Handle:
     def __init__(self, head: "ChunkedHead", max_batch: int, max_positives: int):
         lib = _lib.load()
         self.key = (max_batch, max_positives, head.num_chunks, head.weights.values.device)
+        comp_bytes = 0 if head.comp is None else head.comp.element_size()
         self.desc = _lib.HeadDesc(head.num_labels_global, head.label_offset, head.num_labels,
                                   head.dim, head.fmt.code, head.num_chunks, max_batch,
-                                  max_positives, 0, 0)
+                                  max_positives, 0, comp_bytes)
         size = ctypes.c_size_t()
         _lib.check(lib.xmc_head_workspace_size(ctypes.byref(self.desc), ctypes.byref(size)))
         self.workspace = torch.empty(size.value + 1024, dtype=torch.uint8,
@@ -107,7 +108,8 @@ class ChunkedHead:
 
     def __init__(self, weights: QuantizedMatrix, num_chunks: int = 1, dropout_p: float = 0.0,
                  block_m: int = 64, block_n: int = 64, tensor_id: int = HEAD_WEIGHTS_TAG,
-                 num_labels_global: int | None = None, label_offset: int = 0):
+                 num_labels_global: int | None = None, label_offset: int = 0,
+                 kahan: str | None = None):
         if num_chunks < 1:
             raise ValueError("num_chunks must be >= 1")
         if not (0.0 <= dropout_p < 1.0):
@@ -124,6 +126,12 @@ class ChunkedHead:
         self.tensor_id = tensor_id
         self.num_labels_global = num_labels_global or weights.values.shape[0]
         self.label_offset = label_offset
+        # head-Kahan compensation buffer (PAPER.md:795 uses bf16)
+        if kahan not in (None, "bf16", "fp32"):
+            raise ValueError("kahan must be None, 'bf16' or 'fp32'")
+        self.comp = None if kahan is None else torch.zeros(
+            weights.values.shape, dtype=torch.bfloat16 if kahan == "bf16" else torch.float32,
+            device=weights.values.device)
         self._handle = None
         self.last_stats = None
         self.collect_stats = False   # True: head_update also returns sum|G| in last_stats[0]
@@ -176,8 +184,9 @@ class ChunkedHead:
     def handle(self, batch: int, nnz: int) -> _Handle:
         h = self._handle
         dev = self.weights.values.device
+        comp_bytes = 0 if self.comp is None else self.comp.element_size()
         if (h is None or batch > h.max_batch or nnz > h.max_positives
-                or h.key[2] != self.num_chunks or h.key[3] != dev):
+                or h.key[2] != self.num_chunks or h.key[3] != dev or h.desc.comp_bytes != comp_bytes):
             mb = max(batch, h.max_batch if h else 0)
             mp = max(nnz, h.max_positives if h else 0, 1024)
             self._handle = _Handle(self, mb, mp)
@@ -268,6 +277,8 @@ def head_update(head: ChunkedHead, batch: BatchInput, cfg: SgdSrConfig, rng: Rou
         acc_h = tracker.alloc("input_grad_accumulator", "accumulator", b * head.dim * 4)
     try:
         if probe is not None:
+            if head.comp is not None:
+                raise NotImplementedError("probe + head-Kahan: use the fused step (probe=None)")
             return _head_update_unfused(head, X, si, li, cfg, rng, step, tracker, probe)
         h = head.handle(b, si.numel())
         gx = grad_out if grad_out is not None else torch.empty((b, head.dim), dtype=torch.float32, device=dev)
@@ -281,9 +292,9 @@ def head_update(head: ChunkedHead, batch: BatchInput, cfg: SgdSrConfig, rng: Rou
         if tracker is not None:
             for s, e in head.chunks():
                 lhs.append(tracker.alloc("chunk_logits", "logits", (e - s) * b * 2))
-        _lib.check(_lib.load().xmc_head_step(
-            h.h, head.weights.values.data_ptr(), X.data_ptr(), b, si.data_ptr(), li.data_ptr(),
-            si.numel(), ctypes.byref(args), gx.data_ptr(), stats_ptr, _lib.stream_ptr()))
+        _lib.check(_lib.load().xmc_head_step_kahan(
+            h.h, head.weights.values.data_ptr(), _lib.ptr(head.comp), X.data_ptr(), b, si.data_ptr(),
+            li.data_ptr(), si.numel(), ctypes.byref(args), gx.data_ptr(), stats_ptr, _lib.stream_ptr()))
         for lh in lhs:
             tracker.free(lh)
         if check:

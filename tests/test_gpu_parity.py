@@ -37,17 +37,28 @@ def ulp_dist(a, b, fmt):
     return np.abs(a - b) / O._ulp_of(fmt, np.maximum(np.abs(a), np.abs(b)))
 
 
-def assert_update_within_bound(got, ref, fmt, lr, Xq, G_gpu, G_ref=None, wd=0.0):
+def assert_update_within_bound(got, ref, fmt, lr, Xq, G_gpu, G_ref=None, wd=0.0, g_flips=0):
     """Per-element bound for W_new = ROUND(w - lr (G.Xq + wd w)) computed from
     two gradients: one grid ulp (RTN / SR with the same draw) plus lr times
     the dW difference, i.e. |G_gpu - G_ref| . |Xq| (operand quantisation) and
     an fp32 accumulation-order term 2^-17 |G| . |Xq| (tensor-core vs BLAS
-    summation order; it dominates only where dW cancels to ~0)."""
+    summation order; it dominates only where dW cancels to ~0).  When G is
+    formed on the GPU from its own logits (head-level tests), `g_flips`
+    allows that many operand-grid flips of G per weight row (logits differ
+    from numpy in summation order, so entries next to a rounding boundary can
+    round the other way): + g_flips * max_s ulp_G(G[l,s]) |Xq[s,c]|."""
     Xa = np.abs(np.asarray(Xq, np.float64))
     Ga = np.abs(np.asarray(G_gpu, np.float64))
     err = 2.0 ** -17 * (Ga @ Xa)
     if G_ref is not None:
         err += np.abs(np.asarray(G_gpu, np.float64) - np.asarray(G_ref, np.float64)) @ Xa
+    if g_flips:
+        gfmt, scale = (O.E4M3, 256.0) if fmt.name == "e4m3" else (fmt, 1.0)
+        uG = O._ulp_of(gfmt, Ga * scale) / scale                       # (L, B)
+        mx = np.zeros_like(err)
+        for r0 in range(0, uG.shape[0], 64):
+            mx[r0:r0 + 64] = (uG[r0:r0 + 64, :, None] * Xa[None, :, :]).max(axis=1)
+        err += g_flips * mx
     ulp = O._ulp_of(fmt, np.maximum(np.abs(got), np.abs(ref)).astype(np.float64))
     bound = ulp + lr * err * 1.01 + 1e-30
     diff = np.abs(np.asarray(got, np.float64) - np.asarray(ref, np.float64))
@@ -249,7 +260,7 @@ def test_head_update_matches_reference_golden(xmc, ci):
     W0 = GOLD[p + "W0"]
     G = O.logit_gradient(W0 @ Xq.T, GOLD[p + "sample_idx"], GOLD[p + "label_idx"], (0, W0.shape[0]))
     Gq = O.quantize_g_operand(G, ofmt)
-    assert_update_within_bound(got, oh.values, ofmt, c["lr"], Xq, Gq)
+    assert_update_within_bound(got, oh.values, ofmt, c["lr"], Xq, Gq, g_flips=2)
     # (b) against the reference's own fp32-G result: the bound adds the
     # G operand-quantisation term |Gq - G| . |Xq|
     assert_update_within_bound(got, GOLD[p + "W1"], ofmt, c["lr"], Xq, Gq, G_ref=G)
@@ -360,3 +371,57 @@ def test_checkpoint_roundtrip_bytes_equal_reference_format(xmc, tmp_path):
     assert f.read_bytes() == ref
     h2 = xmc.load_head(str(f))
     assert torch.equal(h2.weights.values.view(torch.uint8), head.weights.values.view(torch.uint8))
+
+
+@pytest.mark.parametrize("fmt_name,kahan,rmode", [("e4m3", "bf16", "stochastic"), ("bf16", "fp32", "nearest"),
+                                                  ("e4m3", "fp32", "nearest")])
+def test_head_kahan_matches_oracle(xmc, fmt_name, kahan, rmode):
+    """Fused head-Kahan (row A8k) against the composed oracle on the same
+    operand-precision G; the compensation is stored in `kahan` format."""
+    L, d, B = 700, 256, 128
+    fmt, W, X, si, li = _rand_problem(L, d, B, fmt_name, 61)
+    head = xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.parse_format(fmt_name), num_chunks=2, kahan=kahan)
+    cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=xmc.parse_format(fmt_name), rounding=rmode,
+                          sr_impl="splitmix64")
+    oh = O.OracleHead(W.copy(), fmt, 2)
+    comp = np.zeros_like(W)
+    cfg_o = O.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt, rounding=rmode)
+    cfmt = O.BF16 if kahan == "bf16" else None
+    for step in range(3):
+        gx = xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(4), step)
+        Wb = oh.values.copy()
+        gx_o = O.head_update(oh, X, si, li, cfg_o, O.RoundingRng(4), step, comp=comp, g_quant=True, comp_fmt=cfmt)
+        # logits differ from numpy in fp32 summation order, so a few G entries
+        # land on the other side of an operand-grid rounding boundary (one
+        # grid ulp of G, 2^-8 relative for bf16); each such flip moves grad_X
+        # by ~ulp(G)|W|: loose pointwise, tight on average
+        d = np.abs(gx.cpu().numpy() - gx_o)
+        assert d.max() < 2e-3 and d.mean() < 2e-5, (d.max(), d.mean())
+        got = head.weights.values.float().cpu().numpy()
+        assert np.mean(bits(got) == bits(oh.values)) > 0.98
+        Xq = O.round_nearest(fmt, X)
+        Gq = O.quantize_g_operand(O.logit_gradient(Wb @ Xq.T, si, li, (0, L)), fmt)
+        assert_update_within_bound(got, oh.values, fmt, 0.05, Xq, Gq, g_flips=2)
+        # resync so later steps compare like for like
+        head.weights.values.copy_(xmc.cast_native(torch.from_numpy(oh.values).cuda(), xmc.parse_format(fmt_name)))
+        head.comp.copy_(torch.from_numpy(comp).to(head.comp.dtype).cuda())
+    c_gpu = head.comp.float().cpu().numpy()
+    assert np.isfinite(c_gpu).all()
+
+
+def test_kahan_rescues_small_updates(xmc):
+    """test_formats.py:216-229 at head level: with a bf16 head and updates far
+    below half an ulp, plain RTN never moves W, Kahan accumulates them."""
+    L, d, B = 256, 128, 64
+    W = O.round_nearest(O.BF16, np.full((L, d), 1.0, np.float32))
+    X = np.zeros((B, d), np.float32)
+    X[0, :] = 1.0
+    plain = xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.BF16)
+    kah = xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.BF16, kahan="fp32")
+    cfg = xmc.SgdSrConfig(lr=1e-4, fmt=xmc.BF16, rounding="nearest")
+    batch = xmc.BatchInput(X, np.zeros(0), np.zeros(0))
+    for step in range(64):
+        xmc.head_update(plain, batch, cfg, xmc.RoundingRng(0), step)
+        xmc.head_update(kah, batch, cfg, xmc.RoundingRng(0), step)
+    assert torch.all(plain.weights.values.float() == 1.0)        # sub-ulp updates lost
+    assert torch.all(kah.weights.values.float() < 1.0)           # accumulated by Kahan
