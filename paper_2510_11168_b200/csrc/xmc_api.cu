@@ -262,8 +262,11 @@ extern "C" xmc_status xmc_head_workspace_size(const xmc_head_desc* desc, size_t*
 
 template <int EB, int BN>
 static void set_fwd_attr() {
-  cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       FwdCfg<EB, BN>::kSmemBytes);
+  cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       FwdCfg<EB, BN, false>::kSmemBytes);
+  if constexpr (BN <= 256 && BN >= 128)
+    cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FwdCfg<EB, BN, true>::kSmemBytes);
 }
 template <int EB, bool XR, int KC>
 static void set_bwd_attr() {
@@ -730,38 +733,54 @@ static xmc_status launch_x_prep(xmc_head* h, const float* X, int B, int Bp, cuda
 // and the backward that re-reads it once per d-tile, while W streams past.
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_ex(void (*kernel)(KArgs...), int grid, int block, int smem, cudaStream_t st,
-                             const xmc_head* h, size_t win_bytes, Args&&... args) {
+                             const xmc_head* h, size_t win_bytes, int cluster, Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   cfg.attrs = at;
   cfg.numAttrs = 0;
   if (h->l2_persist > 0 && win_bytes > 0) {
     const size_t nb = std::min(win_bytes, h->l2_window_max);
-    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[0].val.accessPolicyWindow.base_ptr = h->gbuf;
-    at[0].val.accessPolicyWindow.num_bytes = nb;
-    at[0].val.accessPolicyWindow.hitRatio = std::min(1.0f, static_cast<float>(h->l2_persist) / static_cast<float>(nb));
-    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    cfg.numAttrs = 1;
+    at[cfg.numAttrs].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[cfg.numAttrs].val.accessPolicyWindow.base_ptr = h->gbuf;
+    at[cfg.numAttrs].val.accessPolicyWindow.num_bytes = nb;
+    at[cfg.numAttrs].val.accessPolicyWindow.hitRatio =
+        std::min(1.0f, static_cast<float>(h->l2_persist) / static_cast<float>(nb));
+    at[cfg.numAttrs].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[cfg.numAttrs].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++cfg.numAttrs;
+  }
+  if (cluster > 1) {
+    at[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    at[cfg.numAttrs].val.clusterDim.x = cluster;
+    at[cfg.numAttrs].val.clusterDim.y = 1;
+    at[cfg.numAttrs].val.clusterDim.z = 1;
+    ++cfg.numAttrs;
   }
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-template <int EB, int BN>
+// forward on CTA pairs (tcgen05 cta_group::2) unless XMC_FWD_PAIR=0
+static bool fwd_pairs_enabled() {
+  static const int v = getenv("XMC_FWD_PAIR") ? atoi(getenv("XMC_FWD_PAIR")) : 1;
+  return v != 0;
+}
+
+template <int EB, int BN, bool PAIR>
 static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtensorMap& tx, const FwdParams& p,
                                cudaStream_t st) {
-  const int grid = static_cast<int>(std::min<int64_t>(h->num_sms, p.num_tiles));
+  using C = FwdCfg<EB, BN, PAIR>;
+  int grid = static_cast<int>(std::min<int64_t>(h->num_sms, PAIR ? 2 * ((p.num_tiles + 1) / 2) : p.num_tiles));
+  if (PAIR) grid &= ~1;
   if (grid <= 0) return XMC_OK;
   ProfRec pr;
   prof_begin(0, st, &pr);
   const size_t win = p.mode == 0 ? static_cast<size_t>(p.rows) * p.ld * EB : 0;
-  CUDA_TRY(launch_ex(xmc_fwd_kernel<EB, BN>, grid, FwdCfg<EB, BN>::kThreads, FwdCfg<EB, BN>::kSmemBytes, st, h, win,
-                     tw, tx, p));
+  CUDA_TRY(launch_ex(xmc_fwd_kernel<EB, BN, PAIR>, grid, C::kThreads, C::kSmemBytes, st, h, win, PAIR ? 2 : 1, tw,
+                     tx, p));
   prof_end(st, &pr);
   return XMC_OK;
 }
@@ -770,9 +789,10 @@ static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtenso
 static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t rows, int B, int Bp, int mode,
                              const int32_t* tile_ptr, void* out, int64_t ld, float* stats, cudaStream_t st) {
   const int eb = h->eb, D = h->desc.dim;
+  const bool pair = fwd_pairs_enabled() && (Bp == 128 || Bp == 256);
   CUtensorMap tw, tx;
   XMC_TRY(make_map(&tw, static_cast<const uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 128));
-  XMC_TRY(make_map(&tx, h->xq, eb, D, Bp, D, std::min(Bp, 256)));
+  XMC_TRY(make_map(&tx, h->xq, eb, D, Bp, D, std::min(pair ? Bp / 2 : Bp, 256)));
   FwdParams p{};
   p.rows = static_cast<int32_t>(rows);
   p.B = B;
@@ -787,31 +807,36 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t r
   p.stats = stats;
   p.status = h->status;
   if (eb == 1) {
-    if (Bp == 128) return launch_fwd_t<1, 128>(h, tw, tx, p, st);
-    if (Bp == 256) return launch_fwd_t<1, 256>(h, tw, tx, p, st);
+    if (Bp == 128) return pair ? launch_fwd_t<1, 128, true>(h, tw, tx, p, st) : launch_fwd_t<1, 128, false>(h, tw, tx, p, st);
+    if (Bp == 256) return pair ? launch_fwd_t<1, 256, true>(h, tw, tx, p, st) : launch_fwd_t<1, 256, false>(h, tw, tx, p, st);
   } else {
-    if (Bp == 64) return launch_fwd_t<2, 64>(h, tw, tx, p, st);
-    if (Bp == 128) return launch_fwd_t<2, 128>(h, tw, tx, p, st);
-    if (Bp == 256) return launch_fwd_t<2, 256>(h, tw, tx, p, st);
-    if (Bp == 512) return launch_fwd_t<2, 512>(h, tw, tx, p, st);
+    if (Bp == 64) return launch_fwd_t<2, 64, false>(h, tw, tx, p, st);
+    if (Bp == 128) return pair ? launch_fwd_t<2, 128, true>(h, tw, tx, p, st) : launch_fwd_t<2, 128, false>(h, tw, tx, p, st);
+    if (Bp == 256) return pair ? launch_fwd_t<2, 256, true>(h, tw, tx, p, st) : launch_fwd_t<2, 256, false>(h, tw, tx, p, st);
+    if (Bp == 512) return launch_fwd_t<2, 512, false>(h, tw, tx, p, st);
   }
   return fail(XMC_ERR_UNSUPPORTED, "no forward kernel for padded batch %d", Bp);
 }
 
 template <int EB, bool XR, int KC>
-static xmc_status launch_bwd_t(xmc_head* h, int grid, const CUtensorMap& tw, const CUtensorMap& tg,
+static xmc_status launch_bwd_t(xmc_head* h, int R, const CUtensorMap& tw, const CUtensorMap& tg,
                                const CUtensorMap& tx, const CUtensorMap& tws, const BwdParams& p, size_t g_bytes,
                                cudaStream_t st) {
+  constexpr int sm = BwdCfg<EB, XR, KC>::kSmemBytes;
+  const int cluster = 1;
+  const int grid = R * h->dtiles;
   ProfRec pr;
   prof_begin(1, st, &pr);
-  constexpr int sm = BwdCfg<EB, XR, KC>::kSmemBytes;
   const int ce = p.comp ? h->desc.comp_bytes : 0;
   if (ce == 2)
-    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 2>, grid, kBwdThreads, sm, st, h, g_bytes, tw, tg, tx, tws, p));
+    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 2>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx, tws,
+                       p));
   else if (ce == 4)
-    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 4>, grid, kBwdThreads, sm, st, h, g_bytes, tw, tg, tx, tws, p));
+    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 4>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx, tws,
+                       p));
   else
-    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 0>, grid, kBwdThreads, sm, st, h, g_bytes, tw, tg, tx, tws, p));
+    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 0>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx, tws,
+                       p));
   prof_end(st, &pr);
   return XMC_OK;
 }
@@ -853,16 +878,15 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   static const int dbg = getenv("XMC_DEBUG_BWD") ? atoi(getenv("XMC_DEBUG_BWD")) : 0;
   p.debug = dbg;
   p.status = h->status;
-  const int grid = R * h->dtiles;
   const size_t gb = static_cast<size_t>(rows) * Bp * eb;
   if (eb == 1) {
-    if (Bp == 128) return launch_bwd_t<1, true, 1>(h, grid, tw, tg, tx, tws, p, gb, st);
-    if (Bp == 256) return launch_bwd_t<1, true, 2>(h, grid, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 128) return launch_bwd_t<1, true, 1>(h, R, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 256) return launch_bwd_t<1, true, 2>(h, R, tw, tg, tx, tws, p, gb, st);
   } else {
-    if (Bp == 64) return launch_bwd_t<2, true, 1>(h, grid, tw, tg, tx, tws, p, gb, st);
-    if (Bp == 128) return launch_bwd_t<2, true, 2>(h, grid, tw, tg, tx, tws, p, gb, st);
-    if (Bp == 256) return launch_bwd_t<2, true, 4>(h, grid, tw, tg, tx, tws, p, gb, st);
-    if (Bp == 512) return launch_bwd_t<2, false, 8>(h, grid, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 64) return launch_bwd_t<2, true, 1>(h, R, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 128) return launch_bwd_t<2, true, 2>(h, R, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 256) return launch_bwd_t<2, true, 4>(h, R, tw, tg, tx, tws, p, gb, st);
+    if (Bp == 512) return launch_bwd_t<2, false, 8>(h, R, tw, tg, tx, tws, p, gb, st);
   }
   return fail(XMC_ERR_UNSUPPORTED, "no backward kernel for padded batch %d", Bp);
 }
@@ -977,6 +1001,8 @@ extern "C" xmc_status xmc_head_step_kahan(xmc_head_t h, void* W, void* comp, con
   const int Bp = padded_batch(h->eb, B);
   XMC_TRY(launch_x_prep(h, X, B, Bp, st));
   XMC_TRY(prepare_positives(h, pos_sample, pos_label, nnz, B, st));
+  // the first chunk overwrites every partial slot unless it has fewer tiles
+  // than slots; later chunks accumulate
   // the first chunk overwrites every partial slot unless it has fewer tiles
   // than slots; later chunks accumulate
   const bool first_covers = !h->chunks.empty() && cdiv(h->chunks[0].second - h->chunks[0].first, 128) >= h->R;

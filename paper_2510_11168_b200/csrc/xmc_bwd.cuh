@@ -398,6 +398,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               else mma_f16(d_dw, ad, bd, idesc_dw, (kc | k) != 0);
             }
           }
+          // dW complete -> hand it to the update epilogue before the grad_X
+          // MMAs are queued (commit tracks only the MMAs issued so far)
+          if (kc == p.kc_count - 1) mma_commit(&t_full[ds]);
           // grad_X^T: one MMA group with N = all samples of the pass, issued
           // once its G boxes (contiguous ring slots, LBO = slot pitch) landed;
           // W (A operand) is then read from smem once per tile.
@@ -420,10 +423,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
         if (++ks == KS) { ks = 0; kph ^= 1; }
       }
-      if (elect_one()) {
-        mma_commit(&t_full[ds]);
-        mma_commit(&w_empty[ws]);
-      }
+      if (elect_one()) mma_commit(&w_empty[ws]);
       __syncwarp();
       if (++ws == WS) { ws = 0; wph ^= 1; }
       if (++ds == 2) { ds = 0; dph ^= 1; }
@@ -455,6 +455,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int h = 0; h < C::kChunks16; ++h)
           raw[h] = *reinterpret_cast<const uint4*>(wt + w_chunk_off<EB>(row, c0, h));
+        // lazily release the previous tile's W slot: its TMA store has had a
+        // tile's worth of time to read the smem, so this rarely waits
+        if (storer && prev_ws >= 0) {
+          bulk_wait_read<0>();
+          mbar_arrive(&w_empty[prev_ws]);
+          prev_ws = -1;
+        }
         uint4 craw[CE > 0 ? CE * 2 : 1];
         if constexpr (CE > 0) {   // Kahan compensation of this thread's 32 elements (HBM)
           const uint4* csrc = reinterpret_cast<const uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE);
@@ -499,9 +506,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tma_store_2d_hint(&tm_ws, wt + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK, tile * 128 + q * 32,
                               pol_w_out);
           bulk_commit();
-          // release the previous tile's slot once its store has read smem
-          bulk_wait_read<1>();
-          if (prev_ws >= 0) mbar_arrive(&w_empty[prev_ws]);
         }
         prev_ws = ws;
       } else {

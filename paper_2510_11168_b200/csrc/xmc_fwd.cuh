@@ -8,20 +8,27 @@
 // Warp roles (persistent, one CTA per SM):
 //   warp 0      TMA producer  (W k-chunk + Xq k-chunk per stage)
 //   warp 1      MMA issuer    (one elected lane), owns the TMEM allocation
-//   warps 2..9  epilogue      (2 warps per TMEM sub-partition, each half the columns)
+//   warps 2..   epilogue      (2 or 4 warps per TMEM sub-partition)
 //
-// Epilogue numerics.  sigmoid = rcp(1 + ex2(-z log2 e)) (MUFU, rel. err ~2^-21).
-// e4m3 G is stored as e4m3(256 g): the 2^8 scale is folded into the reciprocal
-// (256 / (1 + e) = rcp(2^-8 + 2^-8 e)) and the [2^-24, 1-2^-24] clip is dropped
-// because it is below e4m3 resolution at that scale (both clip edges round to
-// the same code, 0 / 256, as the unclipped value).  bf16 G keeps the clip.
+// PAIR = true: CTA pairs (cluster of 2, tcgen05 cta_group::2).  The pair
+// computes M = 256 labels (128 per CTA) x N = B with ONE MMA stream issued by
+// the leader; each CTA stages only its half of Xq (N/2 samples) and its own
+// 128 W rows, so Xq traffic from L2 and shared-memory traffic per label halve.
+// TMA completions of both CTAs land on the leader's full barrier; the
+// leader's commits multicast to both CTAs' empty / tmem-full barriers; the
+// peer's epilogue releases the accumulator on the leader's barrier.
+//
+// Epilogue numerics.  sigmoid = 1 / (1 + 2^(-z log2 e)): ex2 on MUFU.  e4m3 G
+// is stored as e4m3(256 g): the 2^8 scale is folded into the reciprocal, which
+// runs on the FMA pipe (magic seed + 3 Newton steps, rel. err < 2^-20), and the
+// [2^-24, 1-2^-24] clip is dropped because both clip edges round to the same
+// e4m3 code (0 / 256) as the unclipped value.  bf16 G keeps MUFU rcp + clip.
 #pragma once
 
 #include "xmc_ptx.cuh"
 #include "xmc_round.cuh"
 
 namespace xmc {
-
 
 struct FwdParams {
   int32_t rows;        // labels in this chunk
@@ -38,13 +45,14 @@ struct FwdParams {
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
 };
 
-template <int EB, int BN>
+template <int EB, int BN, bool PAIR>
 struct FwdCfg {
   static constexpr int kBoxK = 128 / EB;                  // K elements per 128-B swizzle atom
   static constexpr int kWBytes = 128 * 128;               // W box: 128 rows x 128 B
-  static constexpr int kXBoxRows = BN > 256 ? 256 : BN;
-  static constexpr int kXBoxes = BN / kXBoxRows;
-  static constexpr int kXBytes = BN * 128;
+  static constexpr int kXRows = PAIR ? BN / 2 : BN;       // Xq rows staged by this CTA
+  static constexpr int kXBoxRows = kXRows > 256 ? 256 : kXRows;
+  static constexpr int kXBoxes = kXRows / kXBoxRows;
+  static constexpr int kXBytes = kXRows * 128;
   static constexpr int kStageBytes = kWBytes + kXBytes;
   static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
   static constexpr int kAccStages = (2 * BN <= 512) ? 2 : 1;
@@ -60,11 +68,12 @@ struct FwdCfg {
   static constexpr int kChunks = kColsPerWarp / 32;
 };
 
-template <int EB, int BN>
-__global__ void __launch_bounds__(FwdCfg<EB, BN>::kThreads, 1)
+template <int EB, int BN, bool PAIR>
+__global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     xmc_fwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                    FwdParams p) {
-  using C = FwdCfg<EB, BN>;
+  using C = FwdCfg<EB, BN, PAIR>;
+  static_assert(!PAIR || BN <= 256, "paired tiles use one N <= 256 accumulator");
   if (*p.status != 0) return;
 
   extern __shared__ uint8_t smem_raw[];
@@ -72,31 +81,41 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN>::kThreads, 1)
   uint8_t* stage_base = smem;
   uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + C::kStages * C::kStageBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kBitmapBytes);
-  uint64_t* full = bars;                          // [kStages]
+  uint64_t* full = bars;                          // [kStages]   (leader's counts both CTAs)
   uint64_t* empty = bars + C::kStages;            // [kStages]
   uint64_t* tfull = bars + 2 * C::kStages;        // [kAccStages]
-  uint64_t* tempty = tfull + C::kAccStages;       // [kAccStages]
+  uint64_t* tempty = tfull + C::kAccStages;       // [kAccStages] (leader's counts both CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kAccStages);
 
   const uint32_t warp = warp_id_sync();
   const int kc_count = p.d / C::kBoxK;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  // work units: single tiles, or tile pairs (2u, 2u+1) for a CTA pair
+  const int num_units = PAIR ? (p.num_tiles + 1) / 2 : p.num_tiles;
+  const int unit0 = PAIR ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
+  const int ustride = PAIR ? static_cast<int>(num_clusters_x()) : static_cast<int>(gridDim.x);
 
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tm_w);
     prefetch_tmap(&tm_x);
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], PAIR ? 2 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < C::kAccStages; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], C::kEpiWarps);
+      mbar_init(&tempty[a], (PAIR ? 2 : 1) * C::kEpiWarps);
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_2sm<C::kTmemCols>(tmem_slot);
+    else tmem_alloc<C::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -107,16 +126,28 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN>::kThreads, 1)
       const uint64_t pol_x = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      for (int u = unit0; u < num_units; u += ustride) {
+        const int tile = PAIR ? 2 * u + static_cast<int>(rank) : u;
         for (int kc = 0; kc < kc_count; ++kc) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sb = stage_base + stage * C::kStageBytes;
-          mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-          tma_load_2d_hint(sb, &tm_w, &full[stage], kc * C::kBoxK, tile * 128, pol_w);
+          if constexpr (PAIR) {
+            const uint32_t lbar = mapa_shared(&full[stage], 0);
+            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
+            else mbar_arrive_cluster(lbar);
+            tma_load_2d_2sm(sb, &tm_w, lbar, kc * C::kBoxK, tile * 128, pol_w);
 #pragma unroll
-          for (int xb = 0; xb < C::kXBoxes; ++xb)
-            tma_load_2d_hint(sb + C::kWBytes + xb * C::kXBoxRows * 128, &tm_x, &full[stage],
-                             kc * C::kBoxK, xb * C::kXBoxRows, pol_x);
+            for (int xb = 0; xb < C::kXBoxes; ++xb)
+              tma_load_2d_2sm(sb + C::kWBytes + xb * C::kXBoxRows * 128, &tm_x, lbar, kc * C::kBoxK,
+                              static_cast<int>(rank) * C::kXRows + xb * C::kXBoxRows, pol_x);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
+            tma_load_2d_hint(sb, &tm_w, &full[stage], kc * C::kBoxK, tile * 128, pol_w);
+#pragma unroll
+            for (int xb = 0; xb < C::kXBoxes; ++xb)
+              tma_load_2d_hint(sb + C::kWBytes + xb * C::kXBoxRows * 128, &tm_x, &full[stage],
+                               kc * C::kBoxK, xb * C::kXBoxRows, pol_x);
+          }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
       }
@@ -124,41 +155,54 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN>::kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    constexpr uint32_t idesc = (EB == 1) ? umma_idesc(0, 0, false, false, 128, C::kMmaN)
-                                         : umma_idesc(1, 1, false, false, 128, C::kMmaN);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kc = 0; kc < kc_count; ++kc) {
-        mbar_wait(&full[stage], phase);
+    if (leader) {
+      constexpr uint32_t kM = PAIR ? 256 : 128;
+      constexpr uint32_t idesc = (EB == 1) ? umma_idesc(0, 0, false, false, kM, C::kMmaN)
+                                           : umma_idesc(1, 1, false, false, kM, C::kMmaN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = unit0; u < num_units; u += ustride) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t sa = smem_u32(stage_base + stage * C::kStageBytes);
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kc = 0; kc < kc_count; ++kc) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(stage_base + stage * C::kStageBytes);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = umma_desc_sw128(sa + k * 32, 16, 1024);
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t ad = umma_desc_sw128(sa + k * 32, 16, 1024);
 #pragma unroll
-            for (int xb = 0; xb < C::kXBoxes; ++xb) {
-              const uint64_t bd = umma_desc_sw128(sa + C::kWBytes + xb * C::kXBoxRows * 128 + k * 32, 16, 1024);
-              if constexpr (EB == 1)
-                mma_f8(d_tmem + xb * 256, ad, bd, idesc, (kc | k) != 0);
-              else
-                mma_f16(d_tmem + xb * 256, ad, bd, idesc, (kc | k) != 0);
+              for (int xb = 0; xb < (PAIR ? 1 : C::kXBoxes); ++xb) {
+                const uint64_t bd =
+                    umma_desc_sw128(sa + C::kWBytes + xb * C::kXBoxRows * 128 + k * 32, 16, 1024);
+                if constexpr (PAIR) {
+                  if constexpr (EB == 1) mma_f8_2sm(d_tmem, ad, bd, idesc, (kc | k) != 0);
+                  else mma_f16_2sm(d_tmem, ad, bd, idesc, (kc | k) != 0);
+                } else {
+                  if constexpr (EB == 1) mma_f8(d_tmem + xb * 256, ad, bd, idesc, (kc | k) != 0);
+                  else mma_f16(d_tmem + xb * 256, ad, bd, idesc, (kc | k) != 0);
+                }
+              }
+            }
+            if constexpr (PAIR) {
+              mma_commit_2sm_mc(&empty[stage], 0x3);
+              if (kc == kc_count - 1) mma_commit_2sm_mc(&tfull[acc], 0x3);
+            } else {
+              mma_commit(&empty[stage]);
+              if (kc == kc_count - 1) mma_commit(&tfull[acc]);
             }
           }
-          mma_commit(&empty[stage]);
-          if (kc == kc_count - 1) mma_commit(&tfull[acc]);
+          __syncwarp();
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
-        __syncwarp();
-        if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
       }
-      if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
     }
+    __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
     constexpr int NT = C::kEpiWarps * 32;
@@ -175,18 +219,20 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN>::kThreads, 1)
     bool nan_seen = false;
     int acc = 0;
     uint32_t acc_phase = 0;
-    // tile_ptr of the first tile; the next tile's bounds are prefetched below
+    auto tile_of = [&](int u) { return PAIR ? 2 * u + static_cast<int>(rank) : u; };
+    // tile_ptr bounds of the first tile; the next tile's are prefetched below
     int e0 = 0, e1 = 0;
-    if (use_pos && blockIdx.x < p.num_tiles) {
-      e0 = p.tile_ptr[blockIdx.x];
-      e1 = p.tile_ptr[blockIdx.x + 1];
+    if (use_pos && unit0 < num_units && tile_of(unit0) < p.num_tiles) {
+      e0 = p.tile_ptr[tile_of(unit0)];
+      e1 = p.tile_ptr[tile_of(unit0) + 1];
     }
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int u = unit0; u < num_units; u += ustride) {
+      const int tile = tile_of(u);
       int n0 = 0, n1 = 0;
-      const int nxt = tile + gridDim.x;
-      if (use_pos && nxt < p.num_tiles) {
-        n0 = p.tile_ptr[nxt];
-        n1 = p.tile_ptr[nxt + 1];
+      const int nt = tile_of(u + ustride);
+      if (use_pos && u + ustride < num_units && nt < p.num_tiles) {
+        n0 = p.tile_ptr[nt];
+        n1 = p.tile_ptr[nt + 1];
       }
       // positives of this tile -> bitmap, only when the tile has any (uniform)
       const bool has_pos = e1 > e0;
@@ -226,11 +272,23 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN>::kThreads, 1)
         const uint32_t pos = has_pos ? bitmap[row * C::kWordsPerRow + (col0 >> 5)] : 0u;
         float g[32];
         if constexpr (EB == 1) {
-          // g256 = 256 sigmoid(z) - 256 y
+          // g256 = 256 sigmoid(z) = 1 / y, y = 2^-8 (1 + 2^(-z log2 e))
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float e = fast_ex2(__uint_as_float(r[j]) * -1.4426950408889634f);
-            g[j] = fast_rcp(fmaf(e, 0.00390625f, 0.00390625f));
+          for (int j = 0; j < 32; j += 2) {
+            // e clamped to 2^100 keeps y finite (g then rounds to 0 in e4m3)
+            const float ea = fminf(fast_ex2(__uint_as_float(r[j]) * -1.4426950408889634f), 1.2676506e30f);
+            const float eb = fminf(fast_ex2(__uint_as_float(r[j + 1]) * -1.4426950408889634f), 1.2676506e30f);
+            const uint64_t y = ffma2(f2pack(ea, eb), f2pack(0.00390625f, 0.00390625f),
+                                     f2pack(0.00390625f, 0.00390625f));
+            float y0, y1;
+            f2unpack(y, y0, y1);
+            uint64_t x = f2pack(__uint_as_float(0x7EF311C3u - __float_as_uint(y0)),
+                                __uint_as_float(0x7EF311C3u - __float_as_uint(y1)));
+            const uint64_t two = f2pack(2.0f, 2.0f);
+            const uint64_t ny = f2pack(-y0, -y1);
+#pragma unroll
+            for (int it = 0; it < 3; ++it) x = fmul2(x, ffma2(ny, x, two));   // x (2 - y x)
+            f2unpack(x, g[j], g[j + 1]);
           }
         } else {
           const float SIG_LO = 5.9604644775390625e-08f;   // 2^-24  (head.py:47-48)
@@ -284,7 +342,10 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN>::kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&tempty[acc]);
+      if (lane_id() == 0) {
+        if (PAIR && !leader) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
     }
     if (want_stats) {
@@ -297,10 +358,12 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN>::kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem_base);
+    if constexpr (PAIR) tmem_dealloc_2sm<C::kTmemCols>(tmem_base);
+    else tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
