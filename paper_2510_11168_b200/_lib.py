@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libxmc_b200.so")
+# XMC_LIB_PATH selects another in-tree build (A/B measurements in tools/ab.sh)
+LIB_PATH = os.environ.get("XMC_LIB_PATH") or os.path.join(_HERE, "libxmc_b200.so")
 
 XMC_OK = 0
 XMC_ERR_ARG = 1

@@ -451,10 +451,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
         const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + c0;
         // --- independent of dW: W_old and random bits, overlapping the MMAs
+        const uint32_t wt_s = smem_u32(wt);
         uint4 raw[C::kChunks16];
 #pragma unroll
-        for (int h = 0; h < C::kChunks16; ++h)
-          raw[h] = *reinterpret_cast<const uint4*>(wt + w_chunk_off<EB>(row, c0, h));
+        for (int h = 0; h < C::kChunks16; ++h) raw[h] = lds128(wt_s + w_chunk_off<EB>(row, c0, h));
         // lazily release the previous tile's W slot: its TMA store has had a
         // tile's worth of time to read the smem, so this rarely waits
         if (storer && prev_ws >= 0) {
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // W_new back into the same swizzled smem tile, then one TMA store per
         // 32-row slab (full 128-B lines to HBM, no LSU traffic)
 #pragma unroll
-        for (int h = 0; h < C::kChunks16; ++h) *reinterpret_cast<uint4*>(wt + w_chunk_off<EB>(row, c0, h)) = out[h];
+        for (int h = 0; h < C::kChunks16; ++h) sts128(wt_s + w_chunk_off<EB>(row, c0, h), out[h]);
         fence_proxy_async_smem();
         named_bar_sync(1 + q, 128);
         if (storer) {
