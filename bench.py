@@ -81,8 +81,12 @@ def synthetic_positives(num_labels, batch, mean_labels, seed=0):
 # ------------------------------------------------------------- clocks
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / clock-event (throttle) reasons sampled DURING the timed
+    region: NVML polled every ~2 ms from a thread (the timed region is tens of
+    ms), nvidia-smi -lms 100 as the fallback when NVML is unavailable."""
 
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -90,9 +94,23 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []
+        self.stop_evt = threading.Event()
 
     def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -102,11 +120,32 @@ class ClockSampler:
         except FileNotFoundError:
             self.proc = None
 
+    def _poll(self):
+        nv = self.nvml
+        while not self.stop_evt.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                self.samples.append((sm, rs, pw))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml is not None:
+            self.stop_evt.set()
+            self.t.join(timeout=5)
+            sm = [s[0] for s in self.samples]
+            reasons = sorted({n for _, rs, _ in self.samples for n, bit in self.REASONS.items() if rs & bit})
+            pw = [s[2] for s in self.samples]
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
+                    "sm_max_mhz": self.smax, "reasons": reasons, "samples": len(sm),
+                    "power_w_median": statistics.median(pw) if pw else None, "source": "nvml 2 ms poll"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -130,7 +169,7 @@ class ClockSampler:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 # ------------------------------------------------------------- peaks
@@ -264,7 +303,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
-    time.sleep(0.3)
+    if clocks.nvml is None:
+        time.sleep(0.3)   # nvidia-smi needs to be running before the timed region
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for s in range(a.steps):
@@ -329,13 +369,19 @@ def main():
     else:              # logits GEMM, W read, G write
         flops = 2.0 * B * rows_launch * D
         bytes_ = rows_launch * D * eb + rows_launch * Bp * eb
-    # kernels are timed inside a long step loop -> the SUSTAINED peaks apply
+    # Burst vs sustained peak by the clocks seen in the timed region: a short
+    # region runs at boost clocks (burst peak); a long one hits the ~1 kW power
+    # cap, the SM clock drops to ~1.3-1.4 GHz and the sustained peak applies.
     fp8 = peaks.get("fp8", {})
-    tc_peak = (fp8.get("tflops_sustained") if eb == 1 and fp8 else None)
-    tc_src = ("measured fp8 sustained: " + fp8.get("how", "")) if tc_peak else ""
-    if tc_peak is None:
-        tc_peak = peaks["bf16_tflops_sustained"] * (2.0 if eb == 1 else 1.0)
-        tc_src = ("2x measured bf16 sustained (no measured fp8)" if eb == 1 else "measured bf16 sustained") \
+    smax = clk.get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
+    burst = bool(clk.get("sm_mhz")) and clk["sm_mhz"] >= 0.95 * smax and "sw_power_cap" not in clk.get("reasons", [])
+    regime = "burst" if burst else "sustained"
+    if eb == 1 and fp8:
+        tc_peak = fp8["tflops"] if burst else fp8["tflops_sustained"]
+        tc_src = f"measured fp8 {regime}: " + fp8.get("how", "")
+    else:
+        tc_peak = (peaks["bf16_tflops"] if burst else peaks["bf16_tflops_sustained"]) * (2.0 if eb == 1 else 1.0)
+        tc_src = (f"2x measured bf16 {regime} (no measured fp8)" if eb == 1 else f"measured bf16 {regime}") \
             + f" [{peaks['source']}]"
     t_tc = flops / (tc_peak * 1e12)
     t_hbm = bytes_ / (peaks["hbm_gbs"] * 1e9)
@@ -362,6 +408,7 @@ def main():
                  "ms_per_launch": ms_launch, "launches_per_step": n_launch,
                  "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": bytes_,
                  "peak_source": tc_src if bound == "tensor" else f"hbm {peaks['source']}",
+                 "peak_regime": regime,
                  "step_kernel_ms": {"fwd": per_step["fwd"][0], "bwd": per_step["bwd"][0]}})
     step_flops = 6.0 * B * a.labels * D
     ms_step = t_ms / a.steps

@@ -4,8 +4,8 @@ import csv
 import sys
 from collections import defaultdict
 
-TIME = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
-BYTES = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
+TIME = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+BYTES = {"byte": 1e-6, "B": 1e-6, "Kbyte": 1e-3, "KB": 1e-3, "Mbyte": 1.0, "MB": 1.0, "Gbyte": 1e3, "GB": 1e3}
 rows = list(csv.reader(open(sys.argv[1])))
 hdr, agg, cnt = None, defaultdict(lambda: defaultdict(float)), defaultdict(int)
 for r in rows:
