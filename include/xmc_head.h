@@ -60,6 +60,9 @@ typedef struct {
   int64_t max_positives;     /* nnz capacity of the workspace             */
   int32_t num_sms;           /* persistent-grid size (0 = device SM count)*/
   int32_t comp_bytes;        /* Kahan compensation storage: 0 none, 2 bf16, 4 fp32 */
+  int32_t dropout;           /* 1: reserve the keyed-dropout scratch (masked W chunk + keep bits),
+                                needed for steps with dropout_p > 0 (head.py:138-161) */
+  int32_t reserved;
 } xmc_head_desc;
 
 typedef struct xmc_head* xmc_head_t;
@@ -73,6 +76,8 @@ typedef struct {
   uint64_t seed;       /* RoundingRng(seed)                     */
   uint64_t step;       /* step index keying the draws           */
   uint64_t tensor_id;  /* ChunkedHead.tensor_id (HEAD_WEIGHTS_TAG) */
+  double dropout_p;    /* ChunkedHead.dropout_p in [0, 1): keyed weight dropout,
+                          keep = u(seed, step, DROPOUT_TAG, r*d + c) >= p (head.py:138-161) */
 } xmc_step_args;
 
 const char* xmc_last_error(void);
@@ -116,11 +121,21 @@ xmc_status xmc_head_check(xmc_head_t h, void* stream);
 
 /* ---- unfused pieces, for parity isolation (same kernels as the step) ---- */
 
-/* head_forward_logits (head.py:164-178): logits[r][s] = sum_c W[row0+r][c] Xq[s][c],
+/* head_forward_logits (head.py:164-178): logits[r][s] = sum_c W_eff[row0+r][c] Xq[s][c],
  * for local rows [row0, row1), fp32 out with leading dimension ld (>= B).
- * Also ChunkedHead.scores (head.py:109-112) transposed. */
+ * W_eff = W * keep / (1 - p) when args && args->dropout_p > 0 (seed/step from
+ * args; head.py:155-161), else W -- which is also ChunkedHead.scores
+ * (head.py:109-112, dropout disabled) transposed.  args may be NULL. */
 xmc_status xmc_head_logits(xmc_head_t h, const void* W, const float* X, int32_t B, int64_t row0,
-                           int64_t row1, float* logits, int64_t ld, void* stream);
+                           int64_t row1, float* logits, int64_t ld, const xmc_step_args* args,
+                           void* stream);
+
+/* dropout_mask (head.py:138-152) for global rows [row0, row1) of a matrix with
+ * num_cols columns: bit k of keep[(r - row0) * ceil(num_cols / 32) + c / 32]
+ * (k = c % 32) = (u >= p), u = RoundingRng(seed).uniform(step, DROPOUT_TAG,
+ * r * num_cols + c).  keep is caller device memory. */
+xmc_status xmc_dropout_mask(int64_t row0, int64_t row1, int32_t num_cols, uint64_t seed, uint64_t step,
+                            double p, uint32_t* keep, void* stream);
 
 /* logit_gradient (head.py:181-196): G = clip(sigmoid(logits)) - Y, elementwise fp32.
  * Labels are chunk-relative GLOBAL ids in [chunk_start, chunk_start + rows). */

@@ -9,7 +9,7 @@ from .formats import (BF16, E4M3, E5M2, FP16, FP32, FloatFormat, RoundingRng, pa
                       round_nearest, round_stochastic, tensor_tag)
 from .optimizers import SgdSrConfig, kahan_sgd_step, sgd_sr_step
 from .head import (DROPOUT_TAG, HEAD_WEIGHTS_TAG, N_CELLS, BatchInput, ChunkedHead, QuantizedMatrix,
-                   canonical_pieces, cast_native, fused_weight_update, head_forward_logits,
+                   canonical_pieces, cast_native, dropout_mask, fused_weight_update, head_forward_logits,
                    head_update, input_gradient_accumulate, load_head, logit_gradient, partition,
                    save_head)
 

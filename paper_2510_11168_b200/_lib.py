@@ -33,14 +33,15 @@ class HeadDesc(ctypes.Structure):
                 ("num_labels_local", ctypes.c_int64), ("dim", ctypes.c_int32),
                 ("fmt", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
                 ("max_batch", ctypes.c_int32), ("max_positives", ctypes.c_int64),
-                ("num_sms", ctypes.c_int32), ("comp_bytes", ctypes.c_int32)]
+                ("num_sms", ctypes.c_int32), ("comp_bytes", ctypes.c_int32),
+                ("dropout", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class StepArgs(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_float), ("weight_decay", ctypes.c_float),
                 ("rounding", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("seed", ctypes.c_uint64), ("step", ctypes.c_uint64),
-                ("tensor_id", ctypes.c_uint64)]
+                ("tensor_id", ctypes.c_uint64), ("dropout_p", ctypes.c_double)]
 
 
 class Grid(ctypes.Structure):
@@ -60,7 +61,8 @@ _SIGNATURES = {
     "xmc_head_step": ([_P, _P, _P, _I32, _P, _P, _I64, ctypes.POINTER(StepArgs), _P, _P, _P], _I32),
     "xmc_head_step_kahan": ([_P, _P, _P, _P, _I32, _P, _P, _I64, ctypes.POINTER(StepArgs), _P, _P, _P], _I32),
     "xmc_head_check": ([_P, _P], _I32),
-    "xmc_head_logits": ([_P, _P, _P, _I32, _I64, _I64, _P, _I64, _P], _I32),
+    "xmc_head_logits": ([_P, _P, _P, _I32, _I64, _I64, _P, _I64, ctypes.POINTER(StepArgs), _P], _I32),
+    "xmc_dropout_mask": ([_I64, _I64, _I32, _U64, _U64, ctypes.c_double, _P, _P], _I32),
     "xmc_logit_gradient": ([_P, _I64, _I32, _I64, _P, _P, _I64, _I64, _P, _P], _I32),
     "xmc_head_backward": ([_P, _P, _P, _I64, _P, _I32, _I64, _I64, _P, _I32, _I32,
                            ctypes.POINTER(StepArgs), _P], _I32),

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -189,13 +190,15 @@ struct xmc_head {
   uint32_t* tmp_entry; // [max_positives] packed entry per positive
   int64_t* chunk_dev;  // [k+1] chunk starts (local rows) + [k+1] tile bases
   int32_t* status;     // [4]
+  uint8_t* wm;         // [max_chunk_rows + 128][d] masked W chunk (dropout only)
+  uint32_t* keep;      // [max_chunk_rows + 128][d / 32] dropout keep bits (dropout only)
   int R;               // bwd CTAs per d-tile
   size_t l2_persist;   // persisting-L2 bytes granted for the G window (0 = off)
   size_t l2_window_max;
 };
 
 struct Layout {
-  size_t xq, xqt, gbuf, gx, cnt, ptr, ent, tmp, chunk, status, total;
+  size_t xq, xqt, gbuf, gx, cnt, ptr, ent, tmp, chunk, status, wm, keep, total;
 };
 
 static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out, int* bp_out, int* R_out,
@@ -235,7 +238,9 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   L->tmp = align_up(L->ent + (size_t)std::max<int64_t>(d->max_positives, 1) * 4, 256);
   L->chunk = align_up(L->tmp + (size_t)std::max<int64_t>(d->max_positives, 1) * 8, 256);
   L->status = align_up(L->chunk + (size_t)(2 * (ch.size() + 1)) * 8, 256);
-  L->total = align_up(L->status + 64, 1024);
+  L->wm = align_up(L->status + 64, 1024);
+  L->keep = align_up(L->wm + (d->dropout ? (size_t)(maxrows + 128) * D * eb : 0), 1024);
+  L->total = align_up(L->keep + (d->dropout ? (size_t)(maxrows + 128) * (D / 32) * 4 : 0), 1024);
   *eb_out = eb;
   *bp_out = bp;
   *R_out = R;
@@ -332,6 +337,8 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->tmp_entry = h->tmp_tile + std::max<int64_t>(desc->max_positives, 1);
   h->chunk_dev = reinterpret_cast<int64_t*>(w + L.chunk);
   h->status = reinterpret_cast<int32_t*>(w + L.status);
+  h->wm = desc->dropout ? w + L.wm : nullptr;
+  h->keep = desc->dropout ? reinterpret_cast<uint32_t*>(w + L.keep) : nullptr;
   std::vector<int64_t> host(2 * (h->chunks.size() + 1));
   int64_t tb = 0;
   for (size_t c = 0; c < h->chunks.size(); ++c) {
@@ -719,6 +726,89 @@ __global__ void g_quant_kernel(const float* __restrict__ G, int64_t ld, int64_t 
   if (bad) atomicOr(status, ST_NONFINITE_GRAD);
 }
 
+// ---- keyed weight dropout (head.py:138-161) ---------------------------------
+// keep = u >= p with u = (mix(base + flat * gamma) >> 11) * 2^-53, i.e.
+// (mix(...) >> 11) >= ceil(p * 2^53) exactly.  One thread per 32 consecutive
+// elements of a row: one keep word, and (wm != null) the masked copy W * keep
+// in storage format (dropped elements -> +0; the 1/(1-p) factor is applied to
+// the fp32 accumulators by the consumers).
+constexpr uint64_t kDropoutTag = 0xbfe79d70c7098ab2ull;   // tensor_tag("head.dropout"), head.py:43
+
+template <int EB>
+__global__ void __launch_bounds__(256) dropout_prep_kernel(const uint8_t* __restrict__ W, int64_t rows, int d,
+                                                           int64_t row0_global, uint64_t base, uint64_t thr,
+                                                           uint8_t* __restrict__ wm, uint32_t* __restrict__ keep) {
+  const int wpr = d / 32;
+  const int64_t n = rows * wpr;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / wpr;
+    const int cw = static_cast<int>(i - r * wpr);
+    const uint64_t flat0 = static_cast<uint64_t>(row0_global + r) * static_cast<uint64_t>(d) + cw * 32;
+    uint32_t m = 0;
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k)
+      if ((sm64_mix(base + (flat0 + k) * kGamma) >> 11) >= thr) m |= 1u << k;
+    keep[i] = m;
+    if (wm) {
+      const uint4* src = reinterpret_cast<const uint4*>(W + (r * d + cw * 32) * EB);
+      uint4* dst = reinterpret_cast<uint4*>(wm + (r * d + cw * 32) * EB);
+#pragma unroll
+      for (int h = 0; h < 2 * EB; ++h) {
+        uint4 v = src[h];
+        uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t mask = 0;
+          if constexpr (EB == 1) {
+            const int e0 = h * 16 + q * 4;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) mask |= ((m >> (e0 + b)) & 1u) ? (0xFFu << (8 * b)) : 0u;
+          } else {
+            const int e0 = h * 8 + q * 2;
+#pragma unroll
+            for (int b = 0; b < 2; ++b) mask |= ((m >> (e0 + b)) & 1u) ? (0xFFFFu << (16 * b)) : 0u;
+          }
+          wv[q] &= mask;
+        }
+        dst[h] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      }
+    }
+  }
+}
+
+struct DropoutPlan {
+  bool on = false;
+  uint64_t base = 0, thr = 0;
+  float scale = 1.0f;   // f32(1) / f32(1 - p): head.py:161 / :236, :243
+};
+
+static xmc_status dropout_plan(const xmc_head* h, const xmc_step_args* a, DropoutPlan* dp) {
+  *dp = DropoutPlan{};
+  if (!a || a->dropout_p == 0.0) return XMC_OK;
+  if (!(a->dropout_p > 0.0 && a->dropout_p < 1.0))
+    return fail(XMC_ERR_ARG, "dropout probability must lie in [0, 1)");
+  if (!h->keep) return fail(XMC_ERR_ARG, "head created without dropout scratch (desc.dropout = 0)");
+  dp->on = true;
+  dp->base = sm64_base(a->seed, a->step, kDropoutTag);
+  dp->thr = static_cast<uint64_t>(std::ceil(a->dropout_p * 9007199254740992.0));
+  dp->scale = 1.0f / static_cast<float>(1.0 - a->dropout_p);
+  return XMC_OK;
+}
+
+// keep bits (+ masked W copy when wm) for local rows [row0, row0 + rows)
+static xmc_status launch_dropout_prep(const xmc_head* h, const void* W, int64_t row0, int64_t rows,
+                                      const DropoutPlan& dp, uint8_t* wm, uint32_t* keep, cudaStream_t st) {
+  const int D = h->desc.dim, eb = h->eb;
+  const int64_t n = rows * (D / 32);
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16)));
+  const uint8_t* src = W ? static_cast<const uint8_t*>(W) + row0 * D * eb : nullptr;
+  const int64_t g0 = h->desc.label_offset + row0;
+  if (eb == 1) dropout_prep_kernel<1><<<blocks, 256, 0, st>>>(src, rows, D, g0, dp.base, dp.thr, wm, keep);
+  else dropout_prep_kernel<2><<<blocks, 256, 0, st>>>(src, rows, D, g0, dp.base, dp.thr, wm, keep);
+  CUDA_TRY(cudaGetLastError());
+  return XMC_OK;
+}
+
 // ============================================================== launches
 static xmc_status launch_x_prep(xmc_head* h, const float* X, int B, int Bp, cudaStream_t st) {
   dim3 grid(h->desc.dim / 32, Bp / 32), block(32, 8);
@@ -787,7 +877,8 @@ static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtenso
 
 // rows [row0, row0+rows) of W (local), mode 0 -> G into gbuf, mode 1 -> fp32 logits
 static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t rows, int B, int Bp, int mode,
-                             const int32_t* tile_ptr, void* out, int64_t ld, float* stats, cudaStream_t st) {
+                             const int32_t* tile_ptr, void* out, int64_t ld, float* stats, cudaStream_t st,
+                             float logit_scale = 1.0f) {
   const int eb = h->eb, D = h->desc.dim;
   const bool pair = fwd_pairs_enabled() && (Bp == 128 || Bp == 256);
   CUtensorMap tw, tx;
@@ -805,6 +896,7 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t r
   p.out = out;
   p.ld = ld;
   p.stats = stats;
+  p.logit_scale = logit_scale;
   p.status = h->status;
   if (eb == 1) {
     if (Bp == 128) return pair ? launch_fwd_t<1, 128, true>(h, tw, tx, p, st) : launch_fwd_t<1, 128, false>(h, tw, tx, p, st);
@@ -845,7 +937,7 @@ static xmc_status launch_bwd_t(xmc_head* h, int R, const CUtensorMap& tw, const 
 // accumulate into the [R][d][Bp] workspace (zeroed by the caller per step)
 static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int64_t rows, int Bp, bool update,
                              int gx_kc0, int gx_kc_count, bool gx_overwrite, const xmc_step_args* a,
-                             cudaStream_t st) {
+                             cudaStream_t st, const uint32_t* keep = nullptr, float drop_scale = 1.0f) {
   const int eb = h->eb, D = h->desc.dim;
   const int box_k = 128 / eb;
   CUtensorMap tw, tg, tx, tws;
@@ -877,6 +969,8 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   p.gx_accumulate = gx_overwrite ? 0 : 1;
   static const int dbg = getenv("XMC_DEBUG_BWD") ? atoi(getenv("XMC_DEBUG_BWD")) : 0;
   p.debug = dbg;
+  p.keep = keep;
+  p.drop_scale = drop_scale;
   p.status = h->status;
   const size_t gb = static_cast<size_t>(rows) * Bp * eb;
   if (eb == 1) {
@@ -909,10 +1003,11 @@ static xmc_status run_backward(xmc_head* h, void* W, void* comp, int64_t row0, i
 }
 
 // acc[s][c] (+)= scale * sum_r ws[r][c][s]  -- one deterministic reduction per step
-static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumulate, cudaStream_t st) {
+static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumulate, cudaStream_t st,
+                            float scale = 1.0f) {
   const int D = h->desc.dim;
   dim3 g(D / 32, (Bp + 31) / 32), b(32, 32);
-  gx_reduce_kernel<<<g, b, 0, st>>>(h->gx_ws, h->R, D, Bp, B, h->eb == 1 ? (1.0f / 256.0f) : 1.0f,
+  gx_reduce_kernel<<<g, b, 0, st>>>(h->gx_ws, h->R, D, Bp, B, (h->eb == 1 ? (1.0f / 256.0f) : 1.0f) * scale,
                                      accumulate ? 1 : 0, acc);
   CUDA_TRY(cudaGetLastError());
   return XMC_OK;
@@ -1006,26 +1101,75 @@ extern "C" xmc_status xmc_head_step_kahan(xmc_head_t h, void* W, void* comp, con
   // the first chunk overwrites every partial slot unless it has fewer tiles
   // than slots; later chunks accumulate
   const bool first_covers = !h->chunks.empty() && cdiv(h->chunks[0].second - h->chunks[0].first, 128) >= h->R;
+  DropoutPlan dp;
+  XMC_TRY(dropout_plan(h, args, &dp));
   if (!first_covers) XMC_TRY(zero_gx_ws(h, Bp, st));
   if (stats) CUDA_TRY(cudaMemsetAsync(stats, 0, 8, st));
   for (size_t c = 0; c < h->chunks.size(); ++c) {
     const int64_t r0 = h->chunks[c].first, rows = h->chunks[c].second - h->chunks[c].first;
-    XMC_TRY(launch_fwd(h, W, r0, rows, B, Bp, 0, h->tile_ptr + h->tile_base[c], h->gbuf, Bp, stats, st));
-    XMC_TRY(run_backward(h, W, comp, r0, rows, Bp, true, true, first_covers && c == 0, args, st));
+    const int32_t* tp = h->tile_ptr + h->tile_base[c];
+    if (!dp.on) {
+      XMC_TRY(launch_fwd(h, W, r0, rows, B, Bp, 0, tp, h->gbuf, Bp, stats, st));
+      XMC_TRY(run_backward(h, W, comp, r0, rows, Bp, true, true, first_covers && c == 0, args, st));
+      continue;
+    }
+    // keyed dropout (head.py:155-161, 239-242): logits and grad_X read the
+    // masked chunk copy W*keep (1/(1-p) applied to the fp32 accumulators);
+    // the update pass reads W and scales kept dW by 1/(1-p)
+    XMC_TRY(launch_dropout_prep(h, W, r0, rows, dp, h->wm, h->keep, st));
+    XMC_TRY(launch_fwd(h, h->wm, 0, rows, B, Bp, 0, tp, h->gbuf, Bp, stats, st, dp.scale));
+    XMC_TRY(run_backward(h, h->wm, nullptr, 0, rows, Bp, true, false, first_covers && c == 0, args, st));
+    XMC_TRY(launch_bwd(h, W, comp, r0, rows, Bp, true, 0, 0, false, args, st, h->keep, dp.scale));
   }
-  return reduce_gx(h, B, Bp, grad_x, false, st);
+  return reduce_gx(h, B, Bp, grad_x, false, st, dp.scale);
 }
 
 extern "C" xmc_status xmc_head_logits(xmc_head_t h, const void* W, const float* X, int32_t B, int64_t row0,
-                                      int64_t row1, float* logits, int64_t ld, void* stream) {
+                                      int64_t row1, float* logits, int64_t ld, const xmc_step_args* args,
+                                      void* stream) {
   if (!h || !W || !X || !logits) return fail(XMC_ERR_ARG, "null argument");
   if (B < 1 || B > h->desc.max_batch) return fail(XMC_ERR_SHAPE, "batch %d outside [1, %d]", B, h->desc.max_batch);
   if (row0 < 0 || row1 > h->desc.num_labels_local || row1 <= row0) return fail(XMC_ERR_ARG, "bad row range");
   if (ld < B) return fail(XMC_ERR_ARG, "ld < B");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int Bp = padded_batch(h->eb, B);
+  DropoutPlan dp;
+  XMC_TRY(dropout_plan(h, args, &dp));
   XMC_TRY(launch_x_prep(h, X, B, Bp, st));
-  return launch_fwd(h, W, row0, row1 - row0, B, Bp, 1, nullptr, logits, ld, nullptr, st);
+  if (!dp.on) return launch_fwd(h, W, row0, row1 - row0, B, Bp, 1, nullptr, logits, ld, nullptr, st);
+  if (row1 - row0 > h->max_chunk_rows + 128) return fail(XMC_ERR_CAPACITY, "row range exceeds the dropout scratch");
+  XMC_TRY(launch_dropout_prep(h, W, row0, row1 - row0, dp, h->wm, h->keep, st));
+  return launch_fwd(h, h->wm, 0, row1 - row0, B, Bp, 1, nullptr, logits, ld, nullptr, st, dp.scale);
+}
+
+// standalone dropout_mask (head.py:138-152) for any column count
+__global__ void dropout_mask_kernel(int64_t row0, int64_t rows, int32_t cols, uint64_t base, uint64_t thr,
+                                    uint32_t* __restrict__ keep) {
+  const int wpr = (cols + 31) / 32;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * wpr; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / wpr;
+    const int c0 = static_cast<int>(i - r * wpr) * 32;
+    const uint64_t flat0 = static_cast<uint64_t>(row0 + r) * static_cast<uint64_t>(cols) + c0;
+    uint32_t m = 0;
+    for (int k = 0; k < 32 && c0 + k < cols; ++k)
+      if ((sm64_mix(base + (flat0 + k) * kGamma) >> 11) >= thr) m |= 1u << k;
+    keep[i] = m;
+  }
+}
+
+extern "C" xmc_status xmc_dropout_mask(int64_t row0, int64_t row1, int32_t num_cols, uint64_t seed, uint64_t step,
+                                       double p, uint32_t* keep, void* stream) {
+  if (!keep) return fail(XMC_ERR_ARG, "null argument");
+  if (row0 < 0 || row1 < row0 || num_cols < 0) return fail(XMC_ERR_ARG, "bad row range");
+  if (!(p >= 0.0 && p < 1.0)) return fail(XMC_ERR_ARG, "dropout probability must lie in [0, 1)");
+  const int64_t n = (row1 - row0) * ((num_cols + 31) / 32);
+  if (n == 0) return XMC_OK;
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16)));
+  dropout_mask_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      row0, row1 - row0, num_cols, sm64_base(seed, step, kDropoutTag),
+      static_cast<uint64_t>(std::ceil(p * 9007199254740992.0)), keep);
+  CUDA_TRY(cudaGetLastError());
+  return XMC_OK;
 }
 
 extern "C" xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, int64_t ld, const float* X,
@@ -1045,9 +1189,17 @@ extern "C" xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, i
   if (h->eb == 1) g_quant_kernel<1><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, 256.0f, h->gbuf, h->status);
   else g_quant_kernel<2><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, 1.0f, h->gbuf, h->status);
   CUDA_TRY(cudaGetLastError());
+  DropoutPlan dp;
+  XMC_TRY(dropout_plan(h, args, &dp));
   if (accumulate_gx) XMC_TRY(zero_gx_ws(h, Bp, st));
-  XMC_TRY(run_backward(h, W, nullptr, row0, rows, Bp, accumulate_gx != 0, update != 0, false, args, st));
-  if (accumulate_gx) XMC_TRY(reduce_gx(h, B, Bp, acc, true, st));
+  if (!dp.on) {
+    XMC_TRY(run_backward(h, W, nullptr, row0, rows, Bp, accumulate_gx != 0, update != 0, false, args, st));
+  } else {
+    XMC_TRY(launch_dropout_prep(h, W, row0, rows, dp, accumulate_gx ? h->wm : nullptr, h->keep, st));
+    if (accumulate_gx) XMC_TRY(run_backward(h, h->wm, nullptr, 0, rows, Bp, true, false, false, args, st));
+    if (update) XMC_TRY(launch_bwd(h, W, nullptr, row0, rows, Bp, true, 0, 0, false, args, st, h->keep, dp.scale));
+  }
+  if (accumulate_gx) XMC_TRY(reduce_gx(h, B, Bp, acc, true, st, dp.scale));
   return XMC_OK;
 }
 

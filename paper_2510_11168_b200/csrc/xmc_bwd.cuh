@@ -58,6 +58,8 @@ struct BwdParams {
   float* gx_ws;          // [R][d][gx_ld] fp32 partials (gx_ld = padded batch)
   int32_t gx_ld;
   int32_t gx_accumulate; // 1: add into the partial slot, 0: overwrite it
+  const uint32_t* keep;  // keyed dropout keep bits [rows][d / 32] (chunk-local) or null
+  float drop_scale;      // f32(1) / f32(1 - p) applied to kept dW (head.py:239-242)
   int32_t debug;         // measurement only (XMC_DEBUG_BWD): 1 skip dW MMAs, 2 skip update epilogue
   int32_t* status;
 };
@@ -469,6 +471,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int h = 0; h < CE * 2; ++h)
             craw[h] = grow < p.rows ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
         }
+        uint32_t km = 0u;   // dropout keep bits of this thread's 32 columns
+        if (p.keep != nullptr && grow < p.rows) km = __ldg(p.keep + grow * (p.d >> 5) + ((j * 128 + c0) >> 5));
         uint32_t rw[C::kRandWords];
         if (p.rounding == ROUND_SR_FAST) sr_words<EB>(p.rng_base, flat0, rw);
         float w[32];
@@ -482,6 +486,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&t_empty[ds]);
+        if (p.keep != nullptr) {   // scratch *= mask / (1 - p)  (head.py:239-242)
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            acc[k] = __float_as_uint(__uint_as_float(acc[k]) * (((km >> k) & 1u) ? p.drop_scale : 0.0f));
+        }
         uint4 out[C::kChunks16];
         if constexpr (CE > 0) {
           uint4 cout[CE * 2];

@@ -42,6 +42,7 @@ struct FwdParams {
   void* out;                 // G [rows][ld] or logits fp32 [rows][ld]
   int64_t ld;                // leading dimension (elements) of out
   float* stats;              // [0] += sum |G| over valid entries (optional)
+  float logit_scale;         // z = logit_scale * acc (1, or 1/(1-p) under keyed dropout)
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
 };
 
@@ -217,6 +218,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     const uint64_t pol_g = policy_evict_last();   // G is re-read by the backward kernel
     float abs_sum = 0.f;
     bool nan_seen = false;
+    const float zk = -1.4426950408889634f * p.logit_scale;   // -log2(e) * scale
     int acc = 0;
     uint32_t acc_phase = 0;
     auto tile_of = [&](int u) { return PAIR ? 2 * u + static_cast<int>(rank) : u; };
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
             float* o = reinterpret_cast<float*>(p.out) + grow * p.ld;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (col0 + j < p.B) o[col0 + j] = __uint_as_float(r[j]);
+              if (col0 + j < p.B) o[col0 + j] = __uint_as_float(r[j]) * p.logit_scale;
           }
           continue;
         }
@@ -276,8 +278,8 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             // e clamped to 2^100 keeps y finite (g then rounds to 0 in e4m3)
-            const float ea = fminf(fast_ex2(__uint_as_float(r[j]) * -1.4426950408889634f), 1.2676506e30f);
-            const float eb = fminf(fast_ex2(__uint_as_float(r[j + 1]) * -1.4426950408889634f), 1.2676506e30f);
+            const float ea = fminf(fast_ex2(__uint_as_float(r[j]) * zk), 1.2676506e30f);
+            const float eb = fminf(fast_ex2(__uint_as_float(r[j + 1]) * zk), 1.2676506e30f);
             const uint64_t y = ffma2(f2pack(ea, eb), f2pack(0.00390625f, 0.00390625f),
                                      f2pack(0.00390625f, 0.00390625f));
             float y0, y1;
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
           for (int j = 0; j < 32; ++j) {
             const float z = __uint_as_float(r[j]);
             nan_seen |= (z != z);
-            float sg = fast_rcp(1.0f + fast_ex2(z * -1.4426950408889634f));
+            float sg = fast_rcp(1.0f + fast_ex2(z * zk));
             sg = sg < SIG_LO ? SIG_LO : sg;   // NaN propagates like np.clip
             g[j] = sg > SIG_HI ? SIG_HI : sg;
           }

@@ -81,7 +81,7 @@ class _Handle:
         comp_bytes = 0 if head.comp is None else head.comp.element_size()
         self.desc = _lib.HeadDesc(head.num_labels_global, head.label_offset, head.num_labels,
                                   head.dim, head.fmt.code, head.num_chunks, max_batch,
-                                  max_positives, 0, comp_bytes)
+                                  max_positives, 0, comp_bytes, 1 if head.dropout_p > 0.0 else 0, 0)
         size = ctypes.c_size_t()
         _lib.check(lib.xmc_head_workspace_size(ctypes.byref(self.desc), ctypes.byref(size)))
         self.workspace = torch.empty(size.value + 1024, dtype=torch.uint8,
@@ -177,7 +177,7 @@ class ChunkedHead:
         h = self.handle(X.shape[0], 0)
         _lib.check(_lib.load().xmc_head_logits(h.h, self.weights.values.data_ptr(), X.data_ptr(),
                                                X.shape[0], 0, self.num_labels, out.data_ptr(),
-                                               X.shape[0], _lib.stream_ptr()))
+                                               X.shape[0], None, _lib.stream_ptr()))
         return out.t()
 
     # -- plumbing -----------------------------------------------------------
@@ -186,7 +186,8 @@ class ChunkedHead:
         dev = self.weights.values.device
         comp_bytes = 0 if self.comp is None else self.comp.element_size()
         if (h is None or batch > h.max_batch or nnz > h.max_positives
-                or h.key[2] != self.num_chunks or h.key[3] != dev or h.desc.comp_bytes != comp_bytes):
+                or h.key[2] != self.num_chunks or h.key[3] != dev or h.desc.comp_bytes != comp_bytes
+                or h.desc.dropout != (1 if self.dropout_p > 0.0 else 0)):
             mb = max(batch, h.max_batch if h else 0)
             mp = max(nnz, h.max_positives if h else 0, 1024)
             self._handle = _Handle(self, mb, mp)
@@ -220,6 +221,23 @@ def cast_native(x: torch.Tensor, fmt: FloatFormat) -> torch.Tensor:
     return out
 
 
+def dropout_mask(rng: RoundingRng, step: int, p: float, row_range: tuple[int, int],
+                 num_cols: int, device="cuda") -> torch.Tensor:
+    """Keep/drop mask (rows x num_cols) float32 of a global row slice
+    (head.py:138-152), generated on the GPU bit-exactly (integer threshold on
+    the splitmix64 draw)."""
+    if not (0.0 <= p < 1.0):
+        raise ValueError("dropout probability must lie in [0, 1)")
+    start, stop = row_range
+    wpr = (num_cols + 31) // 32
+    words = torch.empty((max(stop - start, 0), wpr), dtype=torch.int32, device=device)
+    _lib.check(_lib.load().xmc_dropout_mask(start, stop, num_cols, rng.seed, step & (2**64 - 1), float(p),
+                                            words.data_ptr(), _lib.stream_ptr()))
+    bits = torch.arange(32, dtype=torch.int32, device=device)
+    m = (words.unsqueeze(-1) >> bits) & 1
+    return m.reshape(words.shape[0], wpr * 32)[:, :num_cols].to(torch.float32)
+
+
 def _as_x(X, dim) -> torch.Tensor:
     t = torch.as_tensor(X, dtype=torch.float32) if not isinstance(X, torch.Tensor) else X.to(torch.float32)
     if not t.is_cuda:
@@ -238,20 +256,24 @@ def _as_idx(a, device) -> torch.Tensor:
     return t.to(device, non_blocking=True).contiguous().reshape(-1)
 
 
-def _step_args(cfg: SgdSrConfig, rng: RoundingRng, step: int, tensor_id: int) -> _lib.StepArgs:
-    return _lib.StepArgs(cfg.lr, cfg.weight_decay, cfg.rounding_code, 0, rng.seed,
-                         step & (2**64 - 1), tensor_id & (2**64 - 1))
+def _step_args(cfg: SgdSrConfig | None, rng: RoundingRng, step: int, tensor_id: int,
+               dropout_p: float = 0.0) -> _lib.StepArgs:
+    lr, wd, rc = (cfg.lr, cfg.weight_decay, cfg.rounding_code) if cfg is not None else (0.0, 0.0, 0)
+    return _lib.StepArgs(lr, wd, rc, 0, rng.seed, step & (2**64 - 1), tensor_id & (2**64 - 1),
+                         float(dropout_p))
+
+
+def _dropout_args(head: "ChunkedHead", rng: RoundingRng, step: int):
+    """Step args carrying only the dropout key (seed, step, p), or None at p = 0."""
+    if head.dropout_p == 0.0:
+        return None
+    return ctypes.byref(_step_args(None, rng, step, head.tensor_id, head.dropout_p))
 
 
 def _check_cfg(head: ChunkedHead, cfg: SgdSrConfig):
     if cfg.fmt != head.fmt:
         raise ValueError(f"SgdSrConfig.fmt {cfg.fmt.name} != head format {head.fmt.name}; "
                          "the head stores weights natively in its own grid")
-
-
-def _no_dropout(head: ChunkedHead):
-    if head.dropout_p > 0.0:
-        raise NotImplementedError("keyed weight dropout (head.py:138-161) is not in the GPU path yet")
 
 
 # --------------------------------------------------------------- hot path
@@ -264,7 +286,6 @@ def head_update(head: ChunkedHead, batch: BatchInput, cfg: SgdSrConfig, rng: Rou
     and raises device-detected errors like the reference (non-finite X or
     gradient -> ValueError, bad sample index -> IndexError)."""
     _check_cfg(head, cfg)
-    _no_dropout(head)
     dev = head.weights.values.device
     X = _as_x(batch.X, head.dim)
     si = _as_idx(batch.sample_idx, dev)
@@ -287,7 +308,7 @@ def head_update(head: ChunkedHead, batch: BatchInput, cfg: SgdSrConfig, rng: Rou
             if head.last_stats is None or head.last_stats.device != dev:
                 head.last_stats = torch.zeros(2, dtype=torch.float32, device=dev)
             stats_ptr = head.last_stats.data_ptr()
-        args = _step_args(cfg, rng, step, head.tensor_id)
+        args = _step_args(cfg, rng, step, head.tensor_id, head.dropout_p)
         lhs = []
         if tracker is not None:
             for s, e in head.chunks():
@@ -320,15 +341,15 @@ def _head_update_unfused(head, X, si, li, cfg, rng, step, tracker, probe):
 
 
 def head_forward_logits(head: ChunkedHead, chunk, Xq, rng, step) -> torch.Tensor:
-    """Logits of one chunk, (chunk labels, batch) fp32 (head.py:164-178)."""
-    _no_dropout(head)
+    """Logits of one chunk, (chunk labels, batch) fp32 (head.py:164-178);
+    W_eff = W * keep / (1 - p) under keyed dropout (head.py:155-161)."""
     start, stop = chunk
     X = _as_x(Xq, head.dim)
     out = torch.empty((stop - start, X.shape[0]), dtype=torch.float32, device=X.device)
     h = head.handle(X.shape[0], 0)
     _lib.check(_lib.load().xmc_head_logits(h.h, head.weights.values.data_ptr(), X.data_ptr(),
                                            X.shape[0], start, stop, out.data_ptr(), X.shape[0],
-                                           _lib.stream_ptr()))
+                                           _dropout_args(head, rng, step), _lib.stream_ptr()))
     return out
 
 
@@ -351,7 +372,6 @@ def input_gradient_accumulate(acc: torch.Tensor, G: torch.Tensor, head: ChunkedH
                               rng, step) -> torch.Tensor:
     """acc += G^T @ W_chunk (head.py:199-209).  G is consumed in the backward
     operand format (e4m3 x 2^8 for an e4m3 head, bf16 for a bf16 head)."""
-    _no_dropout(head)
     start, stop = chunk
     if tuple(acc.shape) != (G.shape[1], head.dim):
         raise ValueError("accumulator shape mismatch")
@@ -359,7 +379,7 @@ def input_gradient_accumulate(acc: torch.Tensor, G: torch.Tensor, head: ChunkedH
     h = head.handle(G.shape[1], 0)
     _lib.check(_lib.load().xmc_head_backward(
         h.h, head.weights.values.data_ptr(), Gc.data_ptr(), Gc.shape[1], None, Gc.shape[1],
-        start, stop, acc.data_ptr(), 1, 0, None, _lib.stream_ptr()))
+        start, stop, acc.data_ptr(), 1, 0, _dropout_args(head, rng, step), _lib.stream_ptr()))
     _lib.check(_lib.load().xmc_head_check(h.h, _lib.stream_ptr()))
     return acc
 
@@ -369,7 +389,6 @@ def fused_weight_update(head: ChunkedHead, G: torch.Tensor, Xq, cfg: SgdSrConfig
     """Gradient + SGD + rounding per tile, in place, no resident gradient
     (head.py:212-251)."""
     _check_cfg(head, cfg)
-    _no_dropout(head)
     start, stop = chunk
     X = _as_x(Xq, head.dim)
     Gc = G.to(torch.float32).contiguous()
@@ -378,7 +397,7 @@ def fused_weight_update(head: ChunkedHead, G: torch.Tensor, Xq, cfg: SgdSrConfig
     if tracker is not None:
         handle = tracker.alloc("fused_block_scratch", "scratch", head.block_m * head.block_n * 4)
     try:
-        args = _step_args(cfg, rng, step, head.tensor_id)
+        args = _step_args(cfg, rng, step, head.tensor_id, head.dropout_p)
         _lib.check(_lib.load().xmc_head_backward(
             h.h, head.weights.values.data_ptr(), Gc.data_ptr(), Gc.shape[1], X.data_ptr(),
             X.shape[0], start, stop, None, 0, 1, ctypes.byref(args), _lib.stream_ptr()))

@@ -115,7 +115,8 @@ def main():
     # -- head.py:254-298: full head steps at small shapes ------------------
     cases = [("bf16", "nearest", 1, 0.0, 0.0), ("bf16", "stochastic", 3, 1e-4, 0.0),
              ("e4m3", "nearest", 2, 1e-4, 0.0), ("e4m3", "stochastic", 1, 0.0, 0.0),
-             ("e4m3", "stochastic", 4, 1e-4, 0.0), ("bf16", "stochastic", 1, 0.0, 0.1)]
+             ("e4m3", "stochastic", 4, 1e-4, 0.0), ("bf16", "stochastic", 1, 0.0, 0.1),
+             ("e4m3", "stochastic", 2, 1e-4, 0.2), ("bf16", "nearest", 3, 1e-4, 0.35)]
     L, d, b = 300, 128, 16
     for ci, (name, rmode, k, wd, p) in enumerate(cases):
         fmt = F.parse_format(name)

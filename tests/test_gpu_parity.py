@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLD = np.load(os.path.join(ROOT, "tests", "golden", "lpxmc_golden.npz"))
+NCASES = int(GOLD["head_ncases"])
 
 
 @pytest.fixture(scope="module")
@@ -149,24 +150,32 @@ def _golden_case(ci):
                 fmt=str(GOLD[p + "fmt"]), rounding=str(GOLD[p + "rounding"]), p=p)
 
 
-def _make(xmc, W, fmt_name, k, device="cuda"):
+def _make(xmc, W, fmt_name, k, device="cuda", dropout_p=0.0):
     fmt = xmc.parse_format(fmt_name)
-    return xmc.ChunkedHead.from_float(torch.from_numpy(np.ascontiguousarray(W)), fmt, num_chunks=k)
+    return xmc.ChunkedHead.from_float(torch.from_numpy(np.ascontiguousarray(W)), fmt, num_chunks=k,
+                                      dropout_p=dropout_p)
+
+
+def _w_eff(W, p, seed, step):
+    """head.py:155-161 on the oracle: W * mask / f32(1 - p)."""
+    if p == 0.0:
+        return W
+    m = O.dropout_mask(O.RoundingRng(seed), step, p, (0, W.shape[0]), W.shape[1])
+    return W * (m / np.float32(1.0 - p))
 
 
 def test_forward_logits_match_golden(xmc):
-    for ci in range(6):
+    for ci in range(NCASES):
         c = _golden_case(ci)
-        if c["drop"] > 0:
-            continue
-        head = _make(xmc, GOLD[c["p"] + "W0"], c["fmt"], c["k"])
+        head = _make(xmc, GOLD[c["p"] + "W0"], c["fmt"], c["k"], dropout_p=c["drop"])
         ch = head.chunks()[0]
-        got = xmc.head_forward_logits(head, ch, torch.from_numpy(GOLD[c["p"] + "X"]), None, 0)
+        got = xmc.head_forward_logits(head, ch, torch.from_numpy(GOLD[c["p"] + "X"]),
+                                      xmc.RoundingRng(c["seed"]), 0)
         np.testing.assert_allclose(got.cpu().numpy(), GOLD[c["p"] + "logits0"], rtol=1e-5, atol=1e-5)
 
 
 def test_logit_gradient_match_golden(xmc):
-    for ci in range(6):
+    for ci in range(NCASES):
         c = _golden_case(ci)
         p = c["p"]
         head = O.OracleHead(GOLD[p + "W0"], O.parse_format(c["fmt"]), c["k"])
@@ -235,21 +244,19 @@ def test_fused_update_matches_oracle_on_operand_G(xmc, fmt_name, B, rmode, impl)
     assert_update_within_bound(got, ref, fmt, 0.05, Xq, Gq)
 
 
-@pytest.mark.parametrize("ci", range(6))
+@pytest.mark.parametrize("ci", range(NCASES))
 def test_head_update_matches_reference_golden(xmc, ci):
     c = _golden_case(ci)
-    if c["drop"] > 0:
-        pytest.skip("weight dropout not on the GPU path (SURVEY F4)")
-    p = c["p"]
+    p, drop = c["p"], c["drop"]
     fmt = xmc.parse_format(c["fmt"])
-    head = _make(xmc, GOLD[p + "W0"], c["fmt"], c["k"])
+    head = _make(xmc, GOLD[p + "W0"], c["fmt"], c["k"], dropout_p=drop)
     cfg = xmc.SgdSrConfig(lr=c["lr"], weight_decay=c["wd"], fmt=fmt, rounding=c["rounding"],
                           sr_impl="splitmix64")
     batch = xmc.BatchInput(GOLD[p + "X"], GOLD[p + "sample_idx"], GOLD[p + "label_idx"])
     gx = xmc.head_update(head, batch, cfg, xmc.RoundingRng(c["seed"]), 0)
     ofmt = O.parse_format(c["fmt"])
     # (a) against the GPU's operand-precision oracle: tight
-    oh = O.OracleHead(GOLD[p + "W0"].copy(), ofmt, c["k"])
+    oh = O.OracleHead(GOLD[p + "W0"].copy(), ofmt, c["k"], dropout_p=drop)
     cfg_o = O.SgdSrConfig(lr=c["lr"], weight_decay=c["wd"], fmt=ofmt, rounding=c["rounding"])
     gx_o = O.head_update(oh, GOLD[p + "X"], GOLD[p + "sample_idx"], GOLD[p + "label_idx"], cfg_o,
                          O.RoundingRng(c["seed"]), 0, g_quant=True)
@@ -258,14 +265,82 @@ def test_head_update_matches_reference_golden(xmc, ci):
     assert np.mean(bits(got) == bits(oh.values)) > 0.99
     Xq = O.round_nearest(ofmt, GOLD[p + "X"])
     W0 = GOLD[p + "W0"]
-    G = O.logit_gradient(W0 @ Xq.T, GOLD[p + "sample_idx"], GOLD[p + "label_idx"], (0, W0.shape[0]))
+    We = _w_eff(W0, drop, c["seed"], 0)
+    G = O.logit_gradient(We @ Xq.T, GOLD[p + "sample_idx"], GOLD[p + "label_idx"], (0, W0.shape[0]))
     Gq = O.quantize_g_operand(G, ofmt)
-    assert_update_within_bound(got, oh.values, ofmt, c["lr"], Xq, Gq, g_flips=2)
+    Xs = Xq / np.float32(1.0 - drop)   # kept dW carries the 1/(1-p) factor
+    assert_update_within_bound(got, oh.values, ofmt, c["lr"], Xs, Gq, g_flips=2)
     # (b) against the reference's own fp32-G result: the bound adds the
     # G operand-quantisation term |Gq - G| . |Xq|
-    assert_update_within_bound(got, GOLD[p + "W1"], ofmt, c["lr"], Xq, Gq, G_ref=G)
-    gx_bound = np.abs(Gq - G).T @ np.abs(W0) + 1e-4
+    assert_update_within_bound(got, GOLD[p + "W1"], ofmt, c["lr"], Xs, Gq, G_ref=G)
+    gx_bound = np.abs(Gq - G).T @ np.abs(We) + 1e-4
     assert np.all(np.abs(gx.cpu().numpy() - GOLD[p + "gradX1"]) <= gx_bound * 1.01)
+
+
+@pytest.mark.parametrize("p,cols,rows,step", [(0.1, 768, (0, 300), 0), (0.5, 100, (17, 90), 3),
+                                              (0.0, 64, (0, 8), 1), (0.999, 33, (5, 40), 2),
+                                              (0.2, 768, (2_812_000, 2_812_281), 7)])
+def test_dropout_mask_bit_exact(xmc, p, cols, rows, step):
+    """head.py:138-152: the keep mask from the integer-threshold GPU draw equals
+    the fp64 u >= p of the reference bit for bit."""
+    got = xmc.dropout_mask(xmc.RoundingRng(9), step, p, rows, cols).cpu().numpy()
+    ref = O.dropout_mask(O.RoundingRng(9), step, p, rows, cols)
+    assert np.array_equal(got, ref)
+    if p > 0 and got.size > 10000:
+        assert abs(1.0 - got.mean() - p) < 5 * np.sqrt(p * (1 - p) / got.size)
+
+
+@pytest.mark.parametrize("fmt_name,B,p", [("e4m3", 256, 0.25), ("bf16", 128, 0.1), ("bf16", 512, 0.3)])
+def test_dropout_subops_match_oracle(xmc, fmt_name, B, p):
+    """Unfused pieces under keyed dropout: logits and grad_X on W*keep/(1-p),
+    update scales kept dW by 1/(1-p) (head.py:155-161, 199-209, 239-242)."""
+    L, d = 600, 256
+    fmt, W, X, si, li = _rand_problem(L, d, B, fmt_name, 41)
+    oh = O.OracleHead(W.copy(), fmt, 1, dropout_p=p)
+    rng_o, rng = O.RoundingRng(13), xmc.RoundingRng(13)
+    Xq = O.round_nearest(fmt, X)
+    z_ref = O.head_forward_logits(oh, (0, L), Xq, rng_o, 4)
+    head = _make(xmc, W, fmt_name, 1, dropout_p=p)
+    z = xmc.head_forward_logits(head, (0, L), torch.from_numpy(X), rng, 4).cpu().numpy()
+    np.testing.assert_allclose(z, z_ref, rtol=1e-5, atol=1e-5)
+    G = O.logit_gradient(z_ref, si, li, (0, L))
+    Gq = O.quantize_g_operand(G, fmt)
+    acc_ref = O.input_gradient_accumulate(np.zeros((B, d), np.float32), Gq, oh, (0, L), rng_o, 4)
+    acc = torch.zeros((B, d), device="cuda")
+    xmc.input_gradient_accumulate(acc, torch.from_numpy(G).cuda(), head, (0, L), rng, 4)
+    np.testing.assert_allclose(acc.cpu().numpy(), acc_ref, rtol=1e-4, atol=1e-4)
+    cfg_o = O.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt, rounding="stochastic")
+    O.fused_weight_update(oh, Gq, Xq, cfg_o, rng_o, 4, (0, L))
+    cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=xmc.parse_format(fmt_name), rounding="stochastic",
+                          sr_impl="splitmix64")
+    xmc.fused_weight_update(head, torch.from_numpy(G).cuda(), torch.from_numpy(X), cfg, rng, 4, (0, L))
+    got = head.weights.values.float().cpu().numpy()
+    assert np.mean(bits(got) == bits(oh.values)) > 0.99
+    assert_update_within_bound(got, oh.values, fmt, 0.05, Xq / np.float32(1 - p), Gq)
+    # dropped elements only see weight decay: equal to the oracle up to the
+    # fp32 association of w (1 - lr wd) vs w - lr (wd w) at an SR threshold
+    m = O.dropout_mask(rng_o, 4, p, (0, L), d) == 0
+    assert np.mean(bits(got)[m] == bits(oh.values)[m]) > 0.999
+
+
+@pytest.mark.parametrize("fmt_name,B,k", [("e4m3", 256, 3), ("bf16", 64, 2)])
+def test_dropout_step_chunk_invariant_and_matches_oracle(xmc, fmt_name, B, k):
+    L, d, p = 900, 256, 0.15
+    fmt, W, X, si, li = _rand_problem(L, d, B, fmt_name, 51)
+    outs = []
+    for kk in (1, k):
+        head = _make(xmc, W, fmt_name, kk, dropout_p=p)
+        cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=xmc.parse_format(fmt_name), rounding="stochastic",
+                              sr_impl="splitmix64")
+        gx = xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(4), 2)
+        outs.append((head.weights.values.float().cpu().numpy(), gx.cpu().numpy()))
+    assert np.array_equal(bits(outs[0][0]), bits(outs[1][0]))
+    np.testing.assert_allclose(outs[0][1], outs[1][1], rtol=1e-5, atol=1e-5)
+    oh = O.OracleHead(W.copy(), fmt, k, dropout_p=p)
+    cfg_o = O.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt, rounding="stochastic")
+    gx_o = O.head_update(oh, X, si, li, cfg_o, O.RoundingRng(4), 2, g_quant=True)
+    np.testing.assert_allclose(outs[1][1], gx_o, rtol=1e-4, atol=1e-4)
+    assert np.mean(bits(outs[1][0]) == bits(oh.values)) > 0.99
 
 
 @pytest.mark.parametrize("fmt_name,B", [("e4m3", 256), ("bf16", 128)])

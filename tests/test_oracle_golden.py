@@ -13,6 +13,7 @@ sys.path.insert(0, ROOT)
 from oracle import lpxmc_oracle as O  # noqa: E402
 
 GOLD = np.load(os.path.join(ROOT, "tests", "golden", "lpxmc_golden.npz"))
+NCASES = int(GOLD["head_ncases"])
 
 
 def _bits(a):
@@ -94,7 +95,7 @@ def test_partition_and_pieces():
         assert (s, e) in O.canonical_pieces(int(a), int(b), int(total))
 
 
-@pytest.mark.parametrize("ci", range(6))
+@pytest.mark.parametrize("ci", range(NCASES))
 def test_head_update_matches_reference(ci):
     p = f"head{ci}_"
     L, d, b, k = (int(v) for v in GOLD[p + "meta"])
