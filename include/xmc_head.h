@@ -137,6 +137,14 @@ xmc_status xmc_head_logits(xmc_head_t h, const void* W, const float* X, int32_t 
 xmc_status xmc_dropout_mask(int64_t row0, int64_t row1, int32_t num_cols, uint64_t seed, uint64_t step,
                             double p, uint32_t* keep, void* stream);
 
+/* Streaming top-k scoring: ChunkedHead.scores (head.py:109-112, dropout off)
+ * followed by metrics.top_k_indices (metrics.py:38-47) per sample, without
+ * materialising the B x L score matrix.  top_scores / top_labels are B x k
+ * (row-major), labels GLOBAL (desc.label_offset added), ordered by score
+ * descending with ties toward the lower label.  1 <= k <= 8. */
+xmc_status xmc_head_topk(xmc_head_t h, const void* W, const float* X, int32_t B, int32_t k,
+                         float* top_scores, int64_t* top_labels, void* stream);
+
 /* logit_gradient (head.py:181-196): G = clip(sigmoid(logits)) - Y, elementwise fp32.
  * Labels are chunk-relative GLOBAL ids in [chunk_start, chunk_start + rows). */
 xmc_status xmc_logit_gradient(const float* logits, int64_t rows, int32_t B, int64_t ld,

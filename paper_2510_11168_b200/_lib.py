@@ -62,6 +62,7 @@ _SIGNATURES = {
     "xmc_head_step_kahan": ([_P, _P, _P, _P, _I32, _P, _P, _I64, ctypes.POINTER(StepArgs), _P, _P, _P], _I32),
     "xmc_head_check": ([_P, _P], _I32),
     "xmc_head_logits": ([_P, _P, _P, _I32, _I64, _I64, _P, _I64, ctypes.POINTER(StepArgs), _P], _I32),
+    "xmc_head_topk": ([_P, _P, _P, _I32, _I32, _P, _P, _P], _I32),
     "xmc_dropout_mask": ([_I64, _I64, _I32, _U64, _U64, ctypes.c_double, _P, _P], _I32),
     "xmc_logit_gradient": ([_P, _I64, _I32, _I64, _P, _P, _I64, _I64, _P, _P], _I32),
     "xmc_head_backward": ([_P, _P, _P, _I64, _P, _I32, _I64, _I64, _P, _I32, _I32,

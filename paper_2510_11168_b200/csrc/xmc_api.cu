@@ -192,13 +192,15 @@ struct xmc_head {
   int32_t* status;     // [4]
   uint8_t* wm;         // [max_chunk_rows + 128][d] masked W chunk (dropout only)
   uint32_t* keep;      // [max_chunk_rows + 128][d / 32] dropout keep bits (dropout only)
+  float* cand_s;       // [max_bp][4 num_sms][kTopK] streaming top-k candidates (scores)
+  int32_t* cand_l;     // [max_bp][4 num_sms][kTopK] (global labels)
   int R;               // bwd CTAs per d-tile
   size_t l2_persist;   // persisting-L2 bytes granted for the G window (0 = off)
   size_t l2_window_max;
 };
 
 struct Layout {
-  size_t xq, xqt, gbuf, gx, cnt, ptr, ent, tmp, chunk, status, wm, keep, total;
+  size_t xq, xqt, gbuf, gx, cnt, ptr, ent, tmp, chunk, status, wm, keep, cand, total;
 };
 
 static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out, int* bp_out, int* R_out,
@@ -240,7 +242,8 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   L->status = align_up(L->chunk + (size_t)(2 * (ch.size() + 1)) * 8, 256);
   L->wm = align_up(L->status + 64, 1024);
   L->keep = align_up(L->wm + (d->dropout ? (size_t)(maxrows + 128) * D * eb : 0), 1024);
-  L->total = align_up(L->keep + (d->dropout ? (size_t)(maxrows + 128) * (D / 32) * 4 : 0), 1024);
+  L->cand = align_up(L->keep + (d->dropout ? (size_t)(maxrows + 128) * (D / 32) * 4 : 0), 1024);
+  L->total = align_up(L->cand + (size_t)bp * 4 * num_sms * kTopK * 8, 1024);
   *eb_out = eb;
   *bp_out = bp;
   *R_out = R;
@@ -269,6 +272,9 @@ template <int EB, int BN>
 static void set_fwd_attr() {
   cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        FwdCfg<EB, BN, false>::kSmemBytes);
+  if constexpr (BN <= 256)
+    cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FwdCfg<EB, BN, false>::kSmemBytes);
   if constexpr (BN <= 256 && BN >= 128)
     cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FwdCfg<EB, BN, true>::kSmemBytes);
@@ -339,6 +345,8 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->status = reinterpret_cast<int32_t*>(w + L.status);
   h->wm = desc->dropout ? w + L.wm : nullptr;
   h->keep = desc->dropout ? reinterpret_cast<uint32_t*>(w + L.keep) : nullptr;
+  h->cand_s = reinterpret_cast<float*>(w + L.cand);
+  h->cand_l = reinterpret_cast<int32_t*>(w + L.cand + (size_t)bp * 4 * sms * kTopK * 4);
   std::vector<int64_t> host(2 * (h->chunks.size() + 1));
   int64_t tb = 0;
   for (size_t c = 0; c < h->chunks.size(); ++c) {
@@ -1122,6 +1130,122 @@ extern "C" xmc_status xmc_head_step_kahan(xmc_head_t h, void* W, void* comp, con
     XMC_TRY(launch_bwd(h, W, comp, r0, rows, Bp, true, 0, 0, false, args, st, h->keep, dp.scale));
   }
   return reduce_gx(h, B, Bp, grad_x, false, st, dp.scale);
+}
+
+// ---- streaming top-k scoring ------------------------------------
+// Merge the per-(CTA, sub-partition) candidate lists of one sample into its
+// top-k, ordered by (score desc, label asc) (metrics.py:38-47).  One CTA per sample.
+__global__ void __launch_bounds__(256) topk_merge_kernel(const float* __restrict__ cs, const int32_t* __restrict__ cl,
+                                                         int nslots, int k, float* __restrict__ out_s,
+                                                         int64_t* __restrict__ out_l) {
+  __shared__ float ss[256 * kTopK];
+  __shared__ int32_t sl[256 * kTopK];
+  const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  float ls[kTopK];
+  int32_t ll[kTopK];
+#pragma unroll
+  for (int i = 0; i < kTopK; ++i) {
+    ls[i] = -INFINITY;
+    ll[i] = 0x7fffffff;
+  }
+  const int n = nslots * kTopK;
+  const float* a = cs + static_cast<size_t>(s) * n;
+  const int32_t* b = cl + static_cast<size_t>(s) * n;
+  for (int i = tid; i < n; i += blockDim.x) topk_insert(ls, ll, a[i], b[i]);
+#pragma unroll
+  for (int i = 0; i < kTopK; ++i) {
+    ss[tid * kTopK + i] = ls[i];
+    sl[tid * kTopK + i] = ll[i];
+  }
+  __syncthreads();
+  if (tid >= 32) return;
+  // warp 0: lane l folds the lists of threads l, l+32, ... into its own
+  for (int t = tid + 32; t < blockDim.x; t += 32)
+    for (int i = 0; i < kTopK; ++i) topk_insert(ls, ll, ss[t * kTopK + i], sl[t * kTopK + i]);
+  // k rounds of a warp-wide best-of-heads selection
+  int head = 0;
+  for (int r = 0; r < k; ++r) {
+    float v = -INFINITY;
+    int32_t lv = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < kTopK; ++i)
+      if (i == head) {
+        v = ls[i];
+        lv = ll[i];
+      }
+    float bv = v;
+    int32_t bl = lv;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int32_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (topk_better(ov, ol, bv, bl)) {
+        bv = ov;
+        bl = ol;
+      }
+    }
+    if (v == bv && lv == bl) ++head;   // labels are unique: exactly one lane owns the winner
+    if (lane == 0) {
+      out_s[static_cast<size_t>(s) * k + r] = bv;
+      out_l[static_cast<size_t>(s) * k + r] = bl;
+    }
+  }
+}
+
+template <int EB, int BN>
+static xmc_status launch_topk_t(xmc_head* h, const CUtensorMap& tw, const CUtensorMap& tx, const FwdParams& p,
+                                cudaStream_t st) {
+  using C = FwdCfg<EB, BN, false>;
+  const int grid = static_cast<int>(std::min<int64_t>(h->num_sms, p.num_tiles));
+  CUDA_TRY(launch_ex(xmc_fwd_kernel<EB, BN, false, true>, grid, C::kThreads, C::kSmemBytes, st, h, 0, 1, tw, tx, p));
+  return XMC_OK;
+}
+
+extern "C" xmc_status xmc_head_topk(xmc_head_t h, const void* W, const float* X, int32_t B, int32_t k,
+                                    float* top_scores, int64_t* top_labels, void* stream) {
+  if (!h || !W || !X || !top_scores || !top_labels) return fail(XMC_ERR_ARG, "null argument");
+  if (B < 1 || B > h->desc.max_batch) return fail(XMC_ERR_SHAPE, "batch %d outside [1, %d]", B, h->desc.max_batch);
+  if (k < 1 || k > h->desc.num_labels_local) return fail(XMC_ERR_ARG, "k must lie in [1, %lld]",
+                                                         (long long)h->desc.num_labels_local);
+  if (k > kTopK) return fail(XMC_ERR_UNSUPPORTED, "fused top-k supports k <= %d (got %d)", kTopK, k);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int eb = h->eb, D = h->desc.dim, Bp = padded_batch(eb, B);
+  const int64_t rows = h->desc.num_labels_local;
+  XMC_TRY(launch_x_prep(h, X, B, Bp, st));
+  CUtensorMap tw;
+  XMC_TRY(make_map(&tw, static_cast<const uint8_t*>(W), eb, D, rows, D, 128));
+  const int nslots = 4 * static_cast<int>(std::min<int64_t>(h->num_sms, cdiv(rows, 128)));
+  // Bp = 512 runs as two N = 256 launches over the sample halves (the 512-wide
+  // epilogue would need twice the candidate registers)
+  const int bn = std::min(Bp, 256);
+  for (int s0 = 0; s0 < B; s0 += bn) {
+    CUtensorMap tx;
+    XMC_TRY(make_map(&tx, h->xq + static_cast<size_t>(s0) * D * eb, eb, D, bn, D, bn));
+    FwdParams p{};
+    p.rows = static_cast<int32_t>(rows);
+    p.B = std::min(bn, B - s0);
+    p.d = D;
+    p.num_tiles = static_cast<int32_t>(cdiv(rows, 128));
+    p.mode = 2;
+    p.logit_scale = 1.0f;
+    p.cand_s = h->cand_s + static_cast<size_t>(s0) * nslots * kTopK;
+    p.cand_l = h->cand_l + static_cast<size_t>(s0) * nslots * kTopK;
+    p.label0 = h->desc.label_offset;
+    p.status = h->status;
+    xmc_status r = XMC_ERR_UNSUPPORTED;
+    if (eb == 1) {
+      if (bn == 128) r = launch_topk_t<1, 128>(h, tw, tx, p, st);
+      else if (bn == 256) r = launch_topk_t<1, 256>(h, tw, tx, p, st);
+    } else {
+      if (bn == 64) r = launch_topk_t<2, 64>(h, tw, tx, p, st);
+      else if (bn == 128) r = launch_topk_t<2, 128>(h, tw, tx, p, st);
+      else if (bn == 256) r = launch_topk_t<2, 256>(h, tw, tx, p, st);
+    }
+    if (r != XMC_OK) return r == XMC_ERR_UNSUPPORTED ? fail(r, "no top-k kernel for padded batch %d", Bp) : r;
+  }
+  topk_merge_kernel<<<B, 256, 0, st>>>(h->cand_s, h->cand_l, nslots, k, top_scores, top_labels);
+  CUDA_TRY(cudaGetLastError());
+  return XMC_OK;
 }
 
 extern "C" xmc_status xmc_head_logits(xmc_head_t h, const void* W, const float* X, int32_t B, int64_t row0,

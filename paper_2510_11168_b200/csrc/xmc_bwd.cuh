@@ -70,12 +70,31 @@ struct BwdCfg {
   static constexpr int kBox = 128 * 128;             // one [128 rows x 128 B] box
   static constexpr int kWBoxes = EB;                 // d-tile of 128 elements
   static constexpr int kWBytes = kWBoxes * kBox;
-  static constexpr int kWStages = EB == 1 ? 5 : 3;
+  // e4m3: W_new is staged in its own smem tile (kOutBytes), so the W_old slot
+  // is released right after the epilogue has read it and the update never
+  // waits for the grad_X MMAs still reading W_old; bf16 (no smem left for a
+  // second tile) writes W_new in place after the grad_X MMAs completed.
+// (measured equal within box noise: in place / 1 / 2 staging tiles with 5 / 4 / 3
+// W stages; two staging tiles need one named barrier per tile, one needs two)
+#ifndef XMC_BWD_OUT
+#define XMC_BWD_OUT 2
+#endif
+#ifndef XMC_BWD_WST
+#define XMC_BWD_WST 3
+#endif
+#ifndef XMC_BWD_KST
+#define XMC_BWD_KST 6
+#endif
+  static constexpr int kOutTiles = EB == 1 ? XMC_BWD_OUT : 0;   // W_new staging tiles (0 = in place)
+  static constexpr bool kOutBuf = kOutTiles > 0;
+  static constexpr int kWStages = EB == 1 ? XMC_BWD_WST : 3;
+  static constexpr int kOutBytes = kOutTiles * kWBytes;
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
-  static constexpr int kKStages = EB == 1 ? 6 : 4;
+  static constexpr int kKStages = EB == 1 ? XMC_BWD_KST : 4;
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
   static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2) + 16;
-  static constexpr int kSmemBytes = 1024 + kXtBytes + kWStages * kWBytes + kKStages * kKSlot + kBarBytes;
+  static constexpr int kSmemBytes =
+      1024 + kXtBytes + kWStages * kWBytes + kOutBytes + kKStages * kKSlot + kBarBytes;
   static constexpr int kKmma = 32 / EB;              // K per MMA instruction (elements)
   static constexpr int kChunks16 = 2 * EB;           // 16-B smem chunks per thread (32 elements)
   static constexpr int kRandWords = 8 * EB;          // cvt.rs words per 32 elements
@@ -292,7 +311,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* xt_s = smem;
   uint8_t* w_s = smem + C::kXtBytes;
-  uint8_t* k_s = w_s + WS * C::kWBytes;
+  uint8_t* out_s = w_s + WS * C::kWBytes;      // W_new staging tile (kOutBuf)
+  uint8_t* k_s = out_s + C::kOutBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(k_s + KS * C::kKSlot);
   uint64_t* w_full = bars;                 // [WS]
   uint64_t* w_empty = w_full + WS;         // [WS]
@@ -316,7 +336,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     prefetch_tmap(&tm_xt);
     for (int s = 0; s < WS; ++s) {
       mbar_init(&w_full[s], 1);
-      mbar_init(&w_empty[s], 5);   // MMA commit + one store thread per TMEM sub-partition
+      // MMA commit + (kOutBuf) every epilogue warp once it has read W_old, or
+      // (in place) one store thread per TMEM sub-partition once W_new is stored
+      mbar_init(&w_empty[s], C::kOutBuf ? 1 + kBwdEpiWarps : 5);
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -402,7 +424,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           // dW complete -> hand it to the update epilogue before the grad_X
           // MMAs are queued (commit tracks only the MMAs issued so far)
-          if (kc == p.kc_count - 1) mma_commit(&t_full[ds]);
+          if (C::kOutBuf && kc == p.kc_count - 1) mma_commit(&t_full[ds]);
           // grad_X^T: one MMA group with N = all samples of the pass, issued
           // once its G boxes (contiguous ring slots, LBO = slot pitch) landed;
           // W (A operand) is then read from smem once per tile.
@@ -421,6 +443,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           } else if (!in_gx) {
             mma_commit(&k_empty[ks]);
           }
+          // in place: dW is handed over only after the grad_X MMAs, which read
+          // the W_old tile the epilogue overwrites with W_new
+          if (!C::kOutBuf && kc == p.kc_count - 1) mma_commit(&t_full[ds]);
         }
         __syncwarp();
         if (++ks == KS) { ks = 0; kph ^= 1; }
@@ -445,6 +470,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const bool storer = (quarter == 0) && lane_id() == 0;
     const uint64_t pol_w_out = policy_evict_first();   // W_new streams out; keep L2 for G
     int ws = 0, ds = 0, prev_ws = -1;
+    int ot_flip = 0;
     uint32_t wph = 0, dph = 0;
     for (int tile = r0; tile < p.num_tiles; tile += R) {
       uint8_t* wt = w_s + ws * C::kWBytes;
@@ -457,9 +483,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint4 raw[C::kChunks16];
 #pragma unroll
         for (int h = 0; h < C::kChunks16; ++h) raw[h] = lds128(wt_s + w_chunk_off<EB>(row, c0, h));
-        // lazily release the previous tile's W slot: its TMA store has had a
-        // tile's worth of time to read the smem, so this rarely waits
-        if (storer && prev_ws >= 0) {
+        if constexpr (C::kOutBuf) {
+          // W_old is in registers: the slot can be refilled once the MMAs are done too
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&w_empty[ws]);
+        } else if (storer && prev_ws >= 0) {
+          // lazily release the previous tile's W slot: its TMA store has had a
+          // tile's worth of time to read the smem, so this rarely waits
           bulk_wait_read<0>();
           mbar_arrive(&w_empty[prev_ws]);
           prev_ws = -1;
@@ -503,16 +533,32 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         } else {
           w_update_pack<EB>(p, acc, w, rw, flat0, out);
         }
-        // W_new back into the same swizzled smem tile, then one TMA store per
-        // 32-row slab (full 128-B lines to HBM, no LSU traffic)
+        // W_new into a swizzled smem tile (the staging tile, or in place once
+        // the grad_X MMAs have read W_old), then one TMA store per 32-row slab
+        // (full 128-B lines to HBM, no LSU traffic)
+        uint8_t* ot = wt;
+        if constexpr (C::kOutTiles == 1) {
+          ot = out_s;
+          // the previous tile's store of this slab must have read the staging smem
+          if (storer && prev_ws >= 0) bulk_wait_read<0>();
+          named_bar_sync(1 + q, 128);
+        } else if constexpr (C::kOutTiles == 2) {
+          ot = out_s + (ot_flip & 1) * C::kWBytes;
+          ++ot_flip;
+        }
+        const uint32_t ot_s = smem_u32(ot);
 #pragma unroll
-        for (int h = 0; h < C::kChunks16; ++h) sts128(wt_s + w_chunk_off<EB>(row, c0, h), out[h]);
+        for (int h = 0; h < C::kChunks16; ++h) sts128(ot_s + w_chunk_off<EB>(row, c0, h), out[h]);
         fence_proxy_async_smem();
+        // two staging tiles: before this barrier the storer waits until the
+        // previous tile's store (the only one outstanding) has read its smem,
+        // so after it every warp may overwrite that tile on the next tile
+        if (C::kOutTiles == 2 && storer && prev_ws >= 0) bulk_wait_read<0>();
         named_bar_sync(1 + q, 128);
         if (storer) {
 #pragma unroll
           for (int b = 0; b < C::kWBoxes; ++b)
-            tma_store_2d_hint(&tm_ws, wt + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK, tile * 128 + q * 32,
+            tma_store_2d_hint(&tm_ws, ot + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK, tile * 128 + q * 32,
                               pol_w_out);
           bulk_commit();
         }
@@ -523,14 +569,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&t_empty[ds]);
-        if (storer) mbar_arrive(&w_empty[ws]);
+        if (C::kOutBuf ? lane_id() == 0 : storer) mbar_arrive(&w_empty[ws]);
       }
       if (++ws == WS) { ws = 0; wph ^= 1; }
       if (++ds == 2) { ds = 0; dph ^= 1; }
     }
     if (storer && p.do_update) {
       bulk_wait<0>();
-      if (prev_ws >= 0) mbar_arrive(&w_empty[prev_ws]);
+      if (!C::kOutBuf && prev_ws >= 0) mbar_arrive(&w_empty[prev_ws]);
     }
     if (do_gx) {
       mbar_wait(gx_full, 0);

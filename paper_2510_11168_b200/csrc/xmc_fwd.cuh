@@ -43,6 +43,11 @@ struct FwdParams {
   int64_t ld;                // leading dimension (elements) of out
   float* stats;              // [0] += sum |G| over valid entries (optional)
   float logit_scale;         // z = logit_scale * acc (1, or 1/(1-p) under keyed dropout)
+  // top-k scoring (TOPK instantiation): per (sample, CTA, sub-partition) the
+  // kTopK best (score, global label) of that warp's rows, [Bp][nslots][kTopK]
+  float* cand_s;
+  int32_t* cand_l;
+  int64_t label0;            // global label of local row 0 of this launch
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
 };
 
@@ -69,7 +74,29 @@ struct FwdCfg {
   static constexpr int kChunks = kColsPerWarp / 32;
 };
 
-template <int EB, int BN, bool PAIR>
+constexpr int kTopK = 8;   // candidates kept per (sample, warp list); user k <= kTopK
+
+// (v, lv) ranks before (s, ls): higher score, ties toward the lower label
+// (metrics.py:38-47 stable descending order)
+XMC_DEV bool topk_better(float v, int32_t lv, float s, int32_t ls) { return v > s || (v == s && lv < ls); }
+
+// insert into a descending list (registers, fully unrolled)
+XMC_DEV void topk_insert(float (&s)[kTopK], int32_t (&l)[kTopK], float v, int32_t lv) {
+  if (!topk_better(v, lv, s[kTopK - 1], l[kTopK - 1])) return;
+#pragma unroll
+  for (int i = 0; i < kTopK; ++i) {
+    if (topk_better(v, lv, s[i], l[i])) {
+      const float ts = s[i];
+      const int32_t tl = l[i];
+      s[i] = v;
+      l[i] = lv;
+      v = ts;
+      lv = tl;
+    }
+  }
+}
+
+template <int EB, int BN, bool PAIR, bool TOPK = false>
 __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     xmc_fwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                    FwdParams p) {
@@ -204,6 +231,86 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       }
     }
     __syncwarp();
+  } else if constexpr (TOPK) {
+    // --------------------------------------------- streaming top-k epilogue
+    // ChunkedHead.scores (head.py:109-112) + top_k_indices (metrics.py:38-47)
+    // without materialising scores: lane j of a warp keeps the kTopK best
+    // (score, label) of column (sample) col0 + j over this warp's rows of all
+    // tiles; per-column thresholds in smem let a whole warp reject a column
+    // with one compare + ballot.  Labels arrive in increasing order per warp,
+    // so a later equal score never displaces an earlier one (stable order).
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int grp = ew >> 2;
+    const int lane = lane_id();
+    const int row = q * 32 + lane;
+    float* th = reinterpret_cast<float*>(bitmap) + ew * C::kColsPerWarp;   // kEpiWarps * kColsPerWarp = 4 BN floats
+    for (int j = lane; j < C::kColsPerWarp; j += 32) th[j] = -INFINITY;
+    __syncwarp();
+    float ls[C::kChunks][kTopK];
+    int32_t ll[C::kChunks][kTopK];
+#pragma unroll
+    for (int cc = 0; cc < C::kChunks; ++cc)
+#pragma unroll
+      for (int i = 0; i < kTopK; ++i) {
+        ls[cc][i] = -INFINITY;
+        ll[cc][i] = 0x7fffffff;
+      }
+    auto tile_of = [&](int u) { return PAIR ? 2 * u + static_cast<int>(rank) : u; };
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = unit0; u < num_units; u += ustride) {
+      const int tile = tile_of(u);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const bool row_ok = static_cast<int64_t>(tile) * 128 + row < p.rows;
+      const int32_t lab0 = static_cast<int32_t>(p.label0 + static_cast<int64_t>(tile) * 128 + q * 32);
+#pragma unroll
+      for (int cc = 0; cc < C::kChunks; ++cc) {
+        const int col0 = grp * C::kColsPerWarp + cc * 32;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, r);
+        tmem_ld_wait();
+        float4 t4;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if ((j & 3) == 0) t4 = *reinterpret_cast<const float4*>(th + cc * 32 + j);
+          const float tj = (j & 3) == 0 ? t4.x : ((j & 3) == 1 ? t4.y : ((j & 3) == 2 ? t4.z : t4.w));
+          const bool pass = row_ok && col0 + j < p.B && __uint_as_float(r[j]) > tj;
+          uint32_t m = __ballot_sync(0xffffffffu, pass);
+          while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const float v = __shfl_sync(0xffffffffu, __uint_as_float(r[j]), src);
+            if (lane == j) topk_insert(ls[cc], ll[cc], v, lab0 + src);
+          }
+        }
+        __syncwarp();
+        th[cc * 32 + lane] = ls[cc][kTopK - 1];
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR && !leader) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
+        else mbar_arrive(&tempty[acc]);
+      }
+      if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
+    }
+    const int nslots = gridDim.x * 4;
+    const int slot = blockIdx.x * 4 + q;
+#pragma unroll
+    for (int cc = 0; cc < C::kChunks; ++cc) {
+      const int s = grp * C::kColsPerWarp + cc * 32 + lane;
+      if (s < p.B) {
+        const size_t o = (static_cast<size_t>(s) * nslots + slot) * kTopK;
+#pragma unroll
+        for (int i = 0; i < kTopK; ++i) {
+          p.cand_s[o + i] = ls[cc][i];
+          p.cand_l[o + i] = ll[cc][i];
+        }
+      }
+    }
   } else {
     // ------------------------------------------------------------ epilogue
     constexpr int NT = C::kEpiWarps * 32;

@@ -180,6 +180,20 @@ class ChunkedHead:
                                                X.shape[0], None, _lib.stream_ptr()))
         return out.t()
 
+    def topk(self, X, k: int) -> tuple[torch.Tensor, torch.Tensor]:
+        """Per-sample top-k of ``scores(X)`` without materialising it: (scores
+        (B, k) fp32, GLOBAL labels (B, k) int64), ordered like
+        metrics.top_k_indices (metrics.py:38-47: descending, ties toward the
+        lower label).  One fused tcgen05 launch + a per-sample merge; k <= 8."""
+        X = _as_x(X, self.dim)
+        b = X.shape[0]
+        vals = torch.empty((b, k), dtype=torch.float32, device=X.device)
+        labs = torch.empty((b, k), dtype=torch.int64, device=X.device)
+        h = self.handle(b, 0)
+        _lib.check(_lib.load().xmc_head_topk(h.h, self.weights.values.data_ptr(), X.data_ptr(), b, k,
+                                             vals.data_ptr(), labs.data_ptr(), _lib.stream_ptr()))
+        return vals, labs
+
     # -- plumbing -----------------------------------------------------------
     def handle(self, batch: int, nnz: int) -> _Handle:
         h = self._handle

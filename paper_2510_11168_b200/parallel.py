@@ -75,6 +75,7 @@ class ShardedHead:
             if local.num_labels != self.hi - self.lo or local.label_offset != self.lo:
                 raise ValueError("local head does not match this rank's shard")
         self._step = local_step or self._gpu_step
+        self._fused_scores = local_scores is None
         self._scores = local_scores or (lambda X: self.local.scores(X))
 
     def _gpu_step(self, batch, cfg, rng, step):
@@ -89,9 +90,14 @@ class ShardedHead:
         return gx
 
     def topk(self, X, k: int) -> torch.Tensor:
-        """Global top-k label ids per sample (B, k)."""
-        sc = self._scores(X)
-        vals, idx = topk_stable(sc, min(k, sc.shape[1]), offset=self.lo)
+        """Global top-k label ids per sample (B, k).  A GPU shard ranks with the
+        fused streaming top-k (no B x L_r score matrix); injected CPU scorers
+        (gloo tests) go through topk_stable on their score matrix."""
+        if self.local is not None and k <= 8 and self._scores is not None and self._fused_scores:
+            vals, idx = self.local.topk(X, min(k, self.hi - self.lo))
+        else:
+            sc = self._scores(X)
+            vals, idx = topk_stable(sc, min(k, sc.shape[1]), offset=self.lo)
         if self.world > 1:
             vs = [torch.empty_like(vals) for _ in range(self.world)]
             ix = [torch.empty_like(idx) for _ in range(self.world)]

@@ -98,3 +98,22 @@ def test_chunk_invariance_and_shard_linearity(setup):
     # global-row RNG keys: shard weights equal the single-GPU rows bit for bit
     assert torch.equal(ha.weights.values.view(torch.uint8), h1.weights.values[:half].view(torch.uint8))
     assert torch.equal(hb.weights.values.view(torch.uint8), h1.weights.values[half:].view(torch.uint8))
+
+
+def test_fused_topk_full_size(setup):
+    """Streaming top-k over all 2.8M labels equals the ranking of the same
+    logits materialised slab by slab (merge with ties toward the lower label)."""
+    xmc, W0, X, si, li = setup
+    head = xmc.ChunkedHead(xmc.QuantizedMatrix(W0, xmc.E4M3))
+    Xt = torch.from_numpy(X).cuda()
+    vals, labs = head.topk(Xt, 5)
+    cand_v, cand_l = [], []
+    for r0 in range(0, L, 400_000):
+        r1 = min(L, r0 + 400_000)
+        sc = xmc.ChunkedHead(xmc.QuantizedMatrix(W0[r0:r1], xmc.E4M3)).scores(Xt)
+        order = torch.sort(-sc, dim=1, stable=True).indices[:, :5]
+        cand_v.append(torch.gather(sc, 1, order))
+        cand_l.append(order + r0)
+    from paper_2510_11168_b200.parallel import merge_topk
+    ref = merge_topk(torch.cat(cand_v, 1), torch.cat(cand_l, 1), 5)
+    assert torch.equal(labs, ref)

@@ -500,3 +500,58 @@ def test_kahan_rescues_small_updates(xmc):
         xmc.head_update(kah, batch, cfg, xmc.RoundingRng(0), step)
     assert torch.all(plain.weights.values.float() == 1.0)        # sub-ulp updates lost
     assert torch.all(kah.weights.values.float() < 1.0)           # accumulated by Kahan
+
+
+# ------------------------------------------------------- streaming top-k (F1)
+
+@pytest.mark.parametrize("fmt_name,B,L,k,offset", [("e4m3", 256, 5000, 5, 0), ("e4m3", 100, 3001, 8, 0),
+                                                  ("bf16", 64, 2000, 1, 0), ("bf16", 200, 4100, 3, 0),
+                                                  ("bf16", 512, 1500, 5, 0), ("e4m3", 256, 2900, 5, 12345)])
+def test_fused_topk_equals_ranking_of_gpu_scores(xmc, fmt_name, B, L, k, offset):
+    """The fused top-k ranks exactly the logits the scoring GEMM produces:
+    equal to metrics.top_k_indices (metrics.py:38-47) applied to head.scores."""
+    d = 256
+    fmt, W, X, si, li = _rand_problem(L, d, B, fmt_name, 61, scale=0.05)
+    # duplicated rows -> exactly tied scores: ties must go to the lower label
+    W[777 % L] = W[5]
+    W[(L - 3)] = W[5]
+    head = xmc.ChunkedHead(xmc.QuantizedMatrix(xmc.cast_native(torch.from_numpy(W).cuda(), xmc.parse_format(fmt_name)),
+                                               xmc.parse_format(fmt_name)),
+                           num_labels_global=offset + L, label_offset=offset)
+    sc = head.scores(torch.from_numpy(X)).cpu().numpy()
+    vals, labs = head.topk(torch.from_numpy(X), k)
+    vals, labs = vals.cpu().numpy(), labs.cpu().numpy()
+    for s in range(B):
+        ref = O.top_k_indices(sc[s], k)
+        assert np.array_equal(labs[s], ref + offset), (s, labs[s], ref + offset)
+        assert np.array_equal(vals[s], sc[s][ref])
+
+
+def test_fused_topk_ties_toward_lower_label(xmc):
+    L, d, B = 1000, 128, 16
+    W = np.zeros((L, d), np.float32)
+    W[[3, 400, 999, 512, 7]] = 0.5          # five identical best rows
+    W[100] = 0.25
+    X = np.ones((B, d), np.float32)
+    head = _make(xmc, W, "bf16", 1)
+    vals, labs = head.topk(torch.from_numpy(X), 6)
+    assert labs.cpu().numpy().tolist() == [[3, 7, 400, 512, 999, 100]] * B
+
+
+def test_fused_topk_p_at_k_equals_oracle(xmc):
+    L, d, B = 6000, 256, 128
+    fmt, W, X, si, li = _rand_problem(L, d, B, "e4m3", 71, scale=0.05)
+    head = _make(xmc, W, "e4m3", 1)
+    truths = [li[si == i] for i in range(B)]
+    got = xmc.metrics.head_precision_at_k(head, torch.from_numpy(X), truths, (1, 3, 5))
+    ref = O.OracleHead(W, fmt, 1).scores(X)
+    for k in (1, 3, 5):
+        assert got[f"p_at_{k}"] == O.dataset_precision_at_k(ref, truths, k)
+
+
+def test_fused_topk_rejects_large_k(xmc):
+    head = _make(xmc, np.zeros((300, 128), np.float32), "bf16", 1)
+    with pytest.raises(NotImplementedError):
+        head.topk(torch.zeros((4, 128)), 9)
+    with pytest.raises(ValueError):
+        head.topk(torch.zeros((4, 128)), 0)

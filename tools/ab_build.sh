@@ -6,10 +6,16 @@
 set -euo pipefail
 rev=${1:?revision}
 tag=${2:?tag}
+shift 2
+extra="$*"   # extra nvcc flags, e.g. -DXMC_BWD_LATE_TFULL
 root=$(cd "$(dirname "$0")/.." && pwd)
 tmp=$(mktemp -d)
-git -C "$root" archive "$rev" paper_2510_11168_b200/csrc include | tar -x -C "$tmp"
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared \
+if [ "$rev" = "WORKTREE" ]; then
+  cp -r "$root/paper_2510_11168_b200" "$root/include" "$tmp/"
+else
+  git -C "$root" archive "$rev" paper_2510_11168_b200/csrc include | tar -x -C "$tmp"
+fi
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared $extra \
   -o "$root/paper_2510_11168_b200/libxmc_b200_$tag.so" "$tmp/paper_2510_11168_b200/csrc/xmc_api.cu"
 rm -rf "$tmp"
 echo "built paper_2510_11168_b200/libxmc_b200_$tag.so from $rev"
