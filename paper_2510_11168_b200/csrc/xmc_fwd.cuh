@@ -234,19 +234,16 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
   } else if constexpr (TOPK) {
     // --------------------------------------------- streaming top-k epilogue
     // ChunkedHead.scores (head.py:109-112) + top_k_indices (metrics.py:38-47)
-    // without materialising scores: lane j of a warp keeps the kTopK best
-    // (score, label) of column (sample) col0 + j over this warp's rows of all
-    // tiles; per-column thresholds in smem let a whole warp reject a column
-    // with one compare + ballot.  Labels arrive in increasing order per warp,
-    // so a later equal score never displaces an earlier one (stable order).
+    // without materialising scores.  Per 32x32 block (32 rows of this warp's
+    // sub-partition x 32 samples) a register transpose across the warp gives
+    // lane c the 32 scores of sample col0 + c; each lane keeps a sorted
+    // register list of the kTopK best (score, label) of its sample over every
+    // row this warp sees.  Rows arrive in increasing label order, so strict
+    // ">" keeps the reference's stable tie order (lower label first).
     const int ew = warp - 2;
     const int q = warp & 3;
     const int grp = ew >> 2;
     const int lane = lane_id();
-    const int row = q * 32 + lane;
-    float* th = reinterpret_cast<float*>(bitmap) + ew * C::kColsPerWarp;   // kEpiWarps * kColsPerWarp = 4 BN floats
-    for (int j = lane; j < C::kColsPerWarp; j += 32) th[j] = -INFINITY;
-    __syncwarp();
     float ls[C::kChunks][kTopK];
     int32_t ll[C::kChunks][kTopK];
 #pragma unroll
@@ -263,31 +260,47 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       const int tile = tile_of(u);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const bool row_ok = static_cast<int64_t>(tile) * 128 + row < p.rows;
-      const int32_t lab0 = static_cast<int32_t>(p.label0 + static_cast<int64_t>(tile) * 128 + q * 32);
+      const int64_t r0w = static_cast<int64_t>(tile) * 128 + q * 32;   // first row of this warp
+      const int64_t left = static_cast<int64_t>(p.rows) - r0w;
+      const int vrows = left >= 32 ? 32 : (left <= 0 ? 0 : static_cast<int>(left));
+      const uint32_t rowmask = vrows >= 32 ? 0xffffffffu : ((1u << vrows) - 1u);
+      const int32_t lab0 = static_cast<int32_t>(p.label0 + r0w);
 #pragma unroll
       for (int cc = 0; cc < C::kChunks; ++cc) {
         const int col0 = grp * C::kColsPerWarp + cc * 32;
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, r);
         tmem_ld_wait();
-        float4 t4;
+        // butterfly transpose: afterwards r[i] of lane c = score(row i, sample col0 + c)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if ((j & 3) == 0) t4 = *reinterpret_cast<const float4*>(th + cc * 32 + j);
-          const float tj = (j & 3) == 0 ? t4.x : ((j & 3) == 1 ? t4.y : ((j & 3) == 2 ? t4.z : t4.w));
-          const bool pass = row_ok && col0 + j < p.B && __uint_as_float(r[j]) > tj;
-          uint32_t m = __ballot_sync(0xffffffffu, pass);
-          while (m) {
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            const float v = __shfl_sync(0xffffffffu, __uint_as_float(r[j]), src);
-            if (lane == j) topk_insert(ls[cc], ll[cc], v, lab0 + src);
+        for (int o = 16; o > 0; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (i & o) continue;
+            const uint32_t a = r[i], b = r[i | o];
+            const uint32_t recv = __shfl_xor_sync(0xffffffffu, up ? a : b, o);
+            r[i] = up ? recv : a;
+            r[i | o] = up ? b : recv;
           }
         }
-        __syncwarp();
-        th[cc * 32 + lane] = ls[cc][kTopK - 1];
-        __syncwarp();
+        const float th = ls[cc][kTopK - 1];
+        uint32_t pm = 0u;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) pm |= (__uint_as_float(r[i]) > th ? 1u : 0u) << i;
+        pm &= rowmask;
+        if (col0 + lane >= p.B) pm = 0u;
+        if (__any_sync(0xffffffffu, pm != 0u)) {   // rare once the lists are warm
+          float rv[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) rv[i] = __uint_as_float(r[i]);
+#pragma unroll 1
+          while (pm) {
+            const int i = __ffs(pm) - 1;
+            pm &= pm - 1;
+            topk_insert(ls[cc], ll[cc], rv[i], lab0 + i);
+          }
+        }
       }
       tc_fence_before();
       __syncwarp();
