@@ -63,6 +63,10 @@ typedef struct {
   int32_t dropout;           /* 1: reserve the keyed-dropout scratch (masked W chunk + keep bits),
                                 needed for steps with dropout_p > 0 (head.py:138-161) */
   int32_t reserved;
+  int64_t comp_labels;       /* with comp_bytes > 0: only GLOBAL labels < comp_labels carry a
+                                compensation (top-p% head-Kahan over frequency-sorted labels,
+                                PAPER.md:795); <= 0 = every label.  The comp buffer then holds the
+                                shard's rows [0, clamp(comp_labels - label_offset, 0, local)). */
 } xmc_head_desc;
 
 typedef struct xmc_head* xmc_head_t;

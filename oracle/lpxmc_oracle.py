@@ -430,7 +430,9 @@ def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None, comp_fmt=
     """Per 64-row block: scratch = G_rows @ Xq, then the SGD+rounding step
     keyed by the global flat index.  head.py:212-251 (rounding vectorised
     across the row block; see module docstring).  With ``comp`` (float32
-    (L, d) array) the head-Kahan extension kahan_sgd_values is used."""
+    (n, d) array) the head-Kahan extension kahan_sgd_values is used for rows
+    < n (n = L: every row; n < L: top-p% head-Kahan, on
+    frequency-sorted labels) and the plain SR step for the others."""
     start, stop = chunk
     m = head.dim
     keep = np.float32(1.0 - head.dropout_p)
@@ -445,13 +447,14 @@ def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None, comp_fmt=
                                                   (r0, r1), m) / keep)
             idx = (np.arange(r0, r1, dtype=np.uint64)[:, None] * np.uint64(m)
                    + np.arange(m, dtype=np.uint64)[None, :])
-            if comp is None:
-                head.values[r0:r1] = sgd_sr_values(head.values[r0:r1], scratch, cfg,
-                                                   rng, step, head.tensor_id, idx)
-            else:
-                head.values[r0:r1], comp[r0:r1] = kahan_sgd_values(
-                    head.values[r0:r1], comp[r0:r1], scratch, cfg, rng, step,
-                    head.tensor_id, idx, comp_fmt)
+            n_c = 0 if comp is None else min(max(comp.shape[0] - r0, 0), r1 - r0)
+            if n_c > 0:
+                head.values[r0:r0 + n_c], comp[r0:r0 + n_c] = kahan_sgd_values(
+                    head.values[r0:r0 + n_c], comp[r0:r0 + n_c], scratch[:n_c], cfg, rng, step,
+                    head.tensor_id, idx[:n_c], comp_fmt)
+            if n_c < r1 - r0:
+                head.values[r0 + n_c:r1] = sgd_sr_values(head.values[r0 + n_c:r1], scratch[n_c:], cfg,
+                                                         rng, step, head.tensor_id, idx[n_c:])
 
 
 def quantize_g_operand(G, fmt):

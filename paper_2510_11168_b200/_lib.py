@@ -34,7 +34,8 @@ class HeadDesc(ctypes.Structure):
                 ("fmt", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
                 ("max_batch", ctypes.c_int32), ("max_positives", ctypes.c_int64),
                 ("num_sms", ctypes.c_int32), ("comp_bytes", ctypes.c_int32),
-                ("dropout", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("dropout", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("comp_labels", ctypes.c_int64)]
 
 
 class StepArgs(ctypes.Structure):

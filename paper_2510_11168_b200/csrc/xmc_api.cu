@@ -192,6 +192,7 @@ struct xmc_head {
   int32_t* status;     // [4]
   uint8_t* wm;         // [max_chunk_rows + 128][d] masked W chunk (dropout only)
   uint32_t* keep;      // [max_chunk_rows + 128][d / 32] dropout keep bits (dropout only)
+  int64_t comp_rows;   // local rows [0, comp_rows) carry a Kahan compensation
   float* cand_s;       // [max_bp][4 num_sms][kTopK] streaming top-k candidates (scores)
   int32_t* cand_l;     // [max_bp][4 num_sms][kTopK] (global labels)
   int R;               // bwd CTAs per d-tile
@@ -345,6 +346,11 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->status = reinterpret_cast<int32_t*>(w + L.status);
   h->wm = desc->dropout ? w + L.wm : nullptr;
   h->keep = desc->dropout ? reinterpret_cast<uint32_t*>(w + L.keep) : nullptr;
+  h->comp_rows = desc->comp_bytes == 0 ? 0
+                 : desc->comp_labels <= 0
+                     ? desc->num_labels_local
+                     : std::min<int64_t>(desc->num_labels_local,
+                                         std::max<int64_t>(0, desc->comp_labels - desc->label_offset));
   h->cand_s = reinterpret_cast<float*>(w + L.cand);
   h->cand_l = reinterpret_cast<int32_t*>(w + L.cand + (size_t)bp * 4 * sms * kTopK * 4);
   std::vector<int64_t> host(2 * (h->chunks.size() + 1));
@@ -965,7 +971,9 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   p.gx_kc0 = gx_kc0;
   p.gx_kc_count = gx_kc_count;
   p.W = static_cast<uint8_t*>(W) + row0 * D * eb;
-  p.comp = comp ? static_cast<uint8_t*>(comp) + row0 * D * h->desc.comp_bytes : nullptr;
+  const int64_t crows = comp ? std::min<int64_t>(rows, std::max<int64_t>(0, h->comp_rows - row0)) : 0;
+  p.comp = crows > 0 ? static_cast<uint8_t*>(comp) + row0 * D * h->desc.comp_bytes : nullptr;
+  p.comp_rows = static_cast<int32_t>(crows);
   p.row0_global = h->desc.label_offset + row0;
   p.lr = a ? a->lr : 0.f;
   p.wd = a ? a->weight_decay : 0.f;

@@ -50,7 +50,8 @@ struct BwdParams {
   int32_t gx_kc0;        // first sample k-chunk accumulated into grad_X
   int32_t gx_kc_count;   // 0 = no grad_X
   uint8_t* W;            // chunk base (row-major rows x d, EB bytes/elem), written in place
-  uint8_t* comp;         // Kahan compensation, chunk base (rows x d, CE bytes/elem) or null
+  uint8_t* comp;         // Kahan compensation, chunk base (comp_rows x d, CE bytes/elem) or null
+  int32_t comp_rows;     // leading chunk rows that carry a compensation (top-p% head-Kahan)
   int64_t row0_global;   // global label of chunk row 0 (RNG key)
   float lr, wd, dw_scale;
   int32_t rounding;      // ROUND_NEAREST / ROUND_SR_EXACT / ROUND_SR_FAST
@@ -215,86 +216,96 @@ XMC_DEV void w_update_pack(const BwdParams& p, const uint32_t (&acc)[32], const 
   for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
 }
 
+// 32-bit word `i` of a packed 16-B-chunk array (compile-time index)
+template <int N>
+XMC_DEV uint32_t word_of(const uint4 (&v)[N], int i) {
+  const uint4 q = v[i >> 2];
+  return (i & 3) == 0 ? q.x : ((i & 3) == 1 ? q.y : ((i & 3) == 2 ? q.z : q.w));
+}
+
 // Head-Kahan variant (kahan_add formats.py:246-263 composed
 // with the SGD update optimizers.py:51-74; PAPER.md:795 keeps the
 // compensation in BF16):
 //   v = -lr (g + wd s);  y = v - c;  t = ROUND(s + y);  c' = (t - s) - y;  s' = t
-// comp (CE = 2: bf16, CE = 4: fp32) is read/written straight from/to HBM by
-// the owning thread; `craw` was loaded before dW was ready.
+// Works 4 elements at a time straight from the packed W (`raw`) and comp
+// (`craw`) registers so only acc[32] is live at full width (no spills at
+// 576 threads).  comp (CE = 2: bf16, CE = 4: fp32) is read/written from/to
+// HBM by the owning thread; rows without compensation (top-p% head-Kahan,
+// PAPER.md:795) pass craw = 0 and drop cout.
 template <int EB, int CE>
-XMC_DEV void w_update_pack_kahan(const BwdParams& p, const uint32_t (&acc)[32], const float (&w)[32],
+XMC_DEV void w_update_pack_kahan(const BwdParams& p, const uint32_t (&acc)[32], const uint4 (&raw)[2 * EB],
                                  const uint32_t (&rw)[8 * EB], int64_t flat0, const uint4 (&craw)[CE * 2],
-                                 uint4 (&out)[2 * EB], uint4 (&cout)[CE * 2]) {
-  float c[32];
-#pragma unroll
-  for (int h = 0; h < CE * 2; ++h) {
-    const uint32_t v4[4] = {craw[h].x, craw[h].y, craw[h].z, craw[h].w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if constexpr (CE == 2) {
-        c[h * 8 + 2 * k] = __uint_as_float(v4[k] << 16);
-        c[h * 8 + 2 * k + 1] = __uint_as_float(v4[k] & 0xFFFF0000u);
-      } else {
-        c[h * 4 + k] = __uint_as_float(v4[k]);
-      }
-    }
-  }
+                                 uint4 (&out)[2 * EB], uint4* cdst, uint64_t pol) {
   const float a_lr = -p.lr * p.dw_scale;
   const float b_wd = -p.lr * p.wd;
-  float y[32], x[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const float v = fmaf(a_lr, __uint_as_float(acc[k]), b_wd * w[k]);
-    y[k] = v - c[k];
-    x[k] = w[k] + y[k];
-  }
-  if (p.rounding == ROUND_SR_EXACT) {
-    const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-      x[k] = grid_round_stochastic(gf, x[k], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + k)));
-  }
   uint32_t pk[8 * EB];
-  float t[32];
-  if constexpr (EB == 1) {
+  uint32_t cw[4];   // one 16-B chunk of new compensation, stored as soon as it is complete
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      pk[k] = p.rounding == ROUND_SR_FAST
-                  ? cvt_e4m3x4_rs(x[4 * k + 3], x[4 * k + 2], x[4 * k + 1], x[4 * k], rw[k])
-                  : (cvt_e4m3x2_rn(x[4 * k + 1], x[4 * k]) |
-                     (static_cast<uint32_t>(cvt_e4m3x2_rn(x[4 * k + 3], x[4 * k + 2])) << 16));
-      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(pk[k] & 0xFFFF));
-      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(pk[k] >> 16));
-      t[4 * k] = lo.x;
-      t[4 * k + 1] = lo.y;
-      t[4 * k + 2] = hi.x;
-      t[4 * k + 3] = hi.y;
+  for (int g = 0; g < 8; ++g) {   // elements 4g .. 4g+3
+    float w[4], c[4];
+    if constexpr (EB == 1) {
+      const uint32_t wv = word_of(raw, g);
+      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(wv & 0xFFFF));
+      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(wv >> 16));
+      w[0] = lo.x; w[1] = lo.y; w[2] = hi.x; w[3] = hi.y;
+    } else {
+      const uint32_t w0 = word_of(raw, 2 * g), w1 = word_of(raw, 2 * g + 1);
+      w[0] = __uint_as_float(w0 << 16); w[1] = __uint_as_float(w0 & 0xFFFF0000u);
+      w[2] = __uint_as_float(w1 << 16); w[3] = __uint_as_float(w1 & 0xFFFF0000u);
     }
-  } else {
+    if constexpr (CE == 2) {
+      const uint32_t c0 = word_of(craw, 2 * g), c1 = word_of(craw, 2 * g + 1);
+      c[0] = __uint_as_float(c0 << 16); c[1] = __uint_as_float(c0 & 0xFFFF0000u);
+      c[2] = __uint_as_float(c1 << 16); c[3] = __uint_as_float(c1 & 0xFFFF0000u);
+    } else {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      pk[k] = p.rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[2 * k + 1], x[2 * k], rw[k])
-                                           : cvt_bf16x2_rn(x[2 * k + 1], x[2 * k]);
-      t[2 * k] = __uint_as_float(pk[k] << 16);
-      t[2 * k + 1] = __uint_as_float(pk[k] & 0xFFFF0000u);
+      for (int e = 0; e < 4; ++e) c[e] = __uint_as_float(word_of(craw, 4 * g + e));
+    }
+    float y[4], x[4], t[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float v = fmaf(a_lr, __uint_as_float(acc[4 * g + e]), b_wd * w[e]);
+      y[e] = v - c[e];
+      x[e] = w[e] + y[e];
+    }
+    if (p.rounding == ROUND_SR_EXACT) {
+      const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        x[e] = grid_round_stochastic(gf, x[e], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + 4 * g + e)));
+    }
+    if constexpr (EB == 1) {
+      const uint32_t w4 = p.rounding == ROUND_SR_FAST
+                              ? cvt_e4m3x4_rs(x[3], x[2], x[1], x[0], rw[g])
+                              : (cvt_e4m3x2_rn(x[1], x[0]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(x[3], x[2])) << 16));
+      pk[g] = w4;
+      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(w4 & 0xFFFF));
+      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(w4 >> 16));
+      t[0] = lo.x; t[1] = lo.y; t[2] = hi.x; t[3] = hi.y;
+    } else {
+      const uint32_t w0 = p.rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[1], x[0], rw[2 * g]) : cvt_bf16x2_rn(x[1], x[0]);
+      const uint32_t w1 =
+          p.rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[3], x[2], rw[2 * g + 1]) : cvt_bf16x2_rn(x[3], x[2]);
+      pk[2 * g] = w0;
+      pk[2 * g + 1] = w1;
+      t[0] = __uint_as_float(w0 << 16); t[1] = __uint_as_float(w0 & 0xFFFF0000u);
+      t[2] = __uint_as_float(w1 << 16); t[3] = __uint_as_float(w1 & 0xFFFF0000u);
+    }
+    float cn[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) cn[e] = (t[e] - w[e]) - y[e];
+    if constexpr (CE == 2) {
+      cw[2 * (g & 1)] = cvt_bf16x2_rn(cn[1], cn[0]);
+      cw[2 * (g & 1) + 1] = cvt_bf16x2_rn(cn[3], cn[2]);
+      if ((g & 1) && cdst) st_global_v4_hint(cdst + (g >> 1), make_uint4(cw[0], cw[1], cw[2], cw[3]), pol);
+    } else {
+      if (cdst)
+        st_global_v4_hint(cdst + g, make_uint4(__float_as_uint(cn[0]), __float_as_uint(cn[1]), __float_as_uint(cn[2]),
+                                               __float_as_uint(cn[3])), pol);
     }
   }
 #pragma unroll
   for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
-  float cn[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) cn[k] = (t[k] - w[k]) - y[k];
-  if constexpr (CE == 2) {
-#pragma unroll
-    for (int h = 0; h < 4; ++h)
-      cout[h] = make_uint4(cvt_bf16x2_rn(cn[8 * h + 1], cn[8 * h]), cvt_bf16x2_rn(cn[8 * h + 3], cn[8 * h + 2]),
-                           cvt_bf16x2_rn(cn[8 * h + 5], cn[8 * h + 4]), cvt_bf16x2_rn(cn[8 * h + 7], cn[8 * h + 6]));
-  } else {
-#pragma unroll
-    for (int h = 0; h < 8; ++h)
-      cout[h] = make_uint4(__float_as_uint(cn[4 * h]), __float_as_uint(cn[4 * h + 1]), __float_as_uint(cn[4 * h + 2]),
-                           __float_as_uint(cn[4 * h + 3]));
-  }
 }
 
 template <int EB, bool XT_RES, int KCMAX, int CE>
@@ -495,18 +506,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           prev_ws = -1;
         }
         uint4 craw[CE > 0 ? CE * 2 : 1];
+        const bool krow = CE > 0 && grow < p.comp_rows;   // this row carries a compensation
         if constexpr (CE > 0) {   // Kahan compensation of this thread's 32 elements (HBM)
           const uint4* csrc = reinterpret_cast<const uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE);
 #pragma unroll
-          for (int h = 0; h < CE * 2; ++h)
-            craw[h] = grow < p.rows ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
+          for (int h = 0; h < CE * 2; ++h) craw[h] = krow ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
         }
         uint32_t km = 0u;   // dropout keep bits of this thread's 32 columns
         if (p.keep != nullptr && grow < p.rows) km = __ldg(p.keep + grow * (p.d >> 5) + ((j * 128 + c0) >> 5));
         uint32_t rw[C::kRandWords];
         if (p.rounding == ROUND_SR_FAST) sr_words<EB>(p.rng_base, flat0, rw);
-        float w[32];
-        w_decode<EB>(raw, w);
+        float w[CE > 0 ? 1 : 32];
+        if constexpr (CE == 0) w_decode<EB>(raw, w);
         // --- dW from TMEM, then release the accumulator buffer at once
         mbar_wait(&t_full[ds], dph);
         tc_fence_after();
@@ -523,13 +534,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         uint4 out[C::kChunks16];
         if constexpr (CE > 0) {
-          uint4 cout[CE * 2];
-          w_update_pack_kahan<EB, CE>(p, acc, w, rw, flat0, craw, out, cout);
-          if (grow < p.rows) {
-            uint4* cdst = reinterpret_cast<uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE);
-#pragma unroll
-            for (int h = 0; h < CE * 2; ++h) st_global_v4_hint(cdst + h, cout[h], pol_w_out);
-          }
+          uint4* cdst = krow ? reinterpret_cast<uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE) : nullptr;
+          w_update_pack_kahan<EB, CE>(p, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
         } else {
           w_update_pack<EB>(p, acc, w, rw, flat0, out);
         }

@@ -81,7 +81,8 @@ class _Handle:
         comp_bytes = 0 if head.comp is None else head.comp.element_size()
         self.desc = _lib.HeadDesc(head.num_labels_global, head.label_offset, head.num_labels,
                                   head.dim, head.fmt.code, head.num_chunks, max_batch,
-                                  max_positives, 0, comp_bytes, 1 if head.dropout_p > 0.0 else 0, 0)
+                                  max_positives, 0, comp_bytes, 1 if head.dropout_p > 0.0 else 0, 0,
+                                  head.kahan_labels or 0)
         size = ctypes.c_size_t()
         _lib.check(lib.xmc_head_workspace_size(ctypes.byref(self.desc), ctypes.byref(size)))
         self.workspace = torch.empty(size.value + 1024, dtype=torch.uint8,
@@ -109,7 +110,7 @@ class ChunkedHead:
     def __init__(self, weights: QuantizedMatrix, num_chunks: int = 1, dropout_p: float = 0.0,
                  block_m: int = 64, block_n: int = 64, tensor_id: int = HEAD_WEIGHTS_TAG,
                  num_labels_global: int | None = None, label_offset: int = 0,
-                 kahan: str | None = None):
+                 kahan: str | None = None, kahan_labels: int | None = None):
         if num_chunks < 1:
             raise ValueError("num_chunks must be >= 1")
         if not (0.0 <= dropout_p < 1.0):
@@ -129,8 +130,14 @@ class ChunkedHead:
         # head-Kahan compensation buffer (PAPER.md:795 uses bf16)
         if kahan not in (None, "bf16", "fp32"):
             raise ValueError("kahan must be None, 'bf16' or 'fp32'")
+        # top-p% head-Kahan: only GLOBAL labels < kahan_labels
+        # (the most frequent ones, labels sorted by frequency) keep a
+        # compensation; this shard's comp buffer holds its rows of that prefix
+        self.kahan_labels = kahan_labels
+        n_comp = weights.values.shape[0] if kahan_labels is None else max(
+            0, min(weights.values.shape[0], kahan_labels - label_offset))
         self.comp = None if kahan is None else torch.zeros(
-            weights.values.shape, dtype=torch.bfloat16 if kahan == "bf16" else torch.float32,
+            (n_comp, weights.values.shape[1]), dtype=torch.bfloat16 if kahan == "bf16" else torch.float32,
             device=weights.values.device)
         self._handle = None
         self.last_stats = None

@@ -448,18 +448,26 @@ def test_checkpoint_roundtrip_bytes_equal_reference_format(xmc, tmp_path):
     assert torch.equal(h2.weights.values.view(torch.uint8), head.weights.values.view(torch.uint8))
 
 
-@pytest.mark.parametrize("fmt_name,kahan,rmode", [("e4m3", "bf16", "stochastic"), ("bf16", "fp32", "nearest"),
-                                                  ("e4m3", "fp32", "nearest")])
-def test_head_kahan_matches_oracle(xmc, fmt_name, kahan, rmode):
+@pytest.mark.parametrize("fmt_name,kahan,rmode,n_comp", [("e4m3", "bf16", "stochastic", None),
+                                                         ("bf16", "fp32", "nearest", None),
+                                                         ("e4m3", "fp32", "nearest", None),
+                                                         ("e4m3", "bf16", "stochastic", 333),
+                                                         ("bf16", "bf16", "nearest", 420),
+                                                         ("e4m3", "fp32", "stochastic", 0)])
+def test_head_kahan_matches_oracle(xmc, fmt_name, kahan, rmode, n_comp):
     """Fused head-Kahan (row A8k) against the composed oracle on the same
-    operand-precision G; the compensation is stored in `kahan` format."""
+    operand-precision G; the compensation is stored in `kahan` format.
+    n_comp: top-p% head-Kahan, compensation only for the
+    first n_comp labels (333: inside chunk 0 and a tile; 420: into chunk 1)."""
     L, d, B = 700, 256, 128
     fmt, W, X, si, li = _rand_problem(L, d, B, fmt_name, 61)
-    head = xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.parse_format(fmt_name), num_chunks=2, kahan=kahan)
+    head = xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.parse_format(fmt_name), num_chunks=2, kahan=kahan,
+                                      kahan_labels=n_comp)
     cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=xmc.parse_format(fmt_name), rounding=rmode,
                           sr_impl="splitmix64")
     oh = O.OracleHead(W.copy(), fmt, 2)
-    comp = np.zeros_like(W)
+    comp = np.zeros((L if n_comp is None else n_comp, d), np.float32)
+    assert tuple(head.comp.shape) == comp.shape
     cfg_o = O.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt, rounding=rmode)
     cfmt = O.BF16 if kahan == "bf16" else None
     for step in range(3):
