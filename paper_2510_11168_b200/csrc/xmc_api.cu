@@ -70,8 +70,37 @@ static PFN_encodeTiled get_encode() {
 }
 
 // 2-D row-major tensor [rows][cols] of `eb`-byte elements, box [box_rows][128 B], 128-B swizzle.
+// Tensor maps are pure functions of (base, shape, box): a small per-thread
+// cache saves the ~1-2 us host encode per map on every step (6 maps per chunk).
+struct MapEntry {
+  CUtensorMap map;
+  const void* base;
+  uint64_t cols, rows, ld;
+  int eb;
+  uint32_t box;
+};
+static xmc_status encode_map(CUtensorMap* m, const void* base, int eb, uint64_t cols, uint64_t rows,
+                             uint64_t ld_elems, uint32_t box_rows);
+
 static xmc_status make_map(CUtensorMap* m, const void* base, int eb, uint64_t cols, uint64_t rows,
                            uint64_t ld_elems, uint32_t box_rows) {
+  constexpr int kCache = 64;
+  static thread_local std::vector<MapEntry> cache;
+  static thread_local int next = 0;
+  for (const MapEntry& e : cache)
+    if (e.base == base && e.cols == cols && e.rows == rows && e.ld == ld_elems && e.eb == eb && e.box == box_rows) {
+      *m = e.map;
+      return XMC_OK;
+    }
+  XMC_TRY(encode_map(m, base, eb, cols, rows, ld_elems, box_rows));
+  MapEntry e{*m, base, cols, rows, ld_elems, eb, box_rows};
+  if (static_cast<int>(cache.size()) < kCache) cache.push_back(e);
+  else cache[next++ % kCache] = e;
+  return XMC_OK;
+}
+
+static xmc_status encode_map(CUtensorMap* m, const void* base, int eb, uint64_t cols, uint64_t rows,
+                             uint64_t ld_elems, uint32_t box_rows) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return fail(XMC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const CUtensorMapDataType dt = eb == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;

@@ -16,3 +16,7 @@ for k in fwd bwd; do
 done
 tail -1 $out/bench_$tag.json
 tail -1 $out/bench_ref_$tag.json
+timeout 300 python bench.py --steps 1000 --no-cpu --e2e-steps 2 > $out/bench_sustained_$tag.json 2>/dev/null
+timeout 300 python tools/bench_topk.py > $out/topk_$tag.json 2>/dev/null
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:xmc_fwd_kernel -c 1 -f \
+  -o $out/prof_topk_$tag python tools/bench_topk.py --iters 1 > /dev/null 2>&1
