@@ -225,6 +225,7 @@ struct xmc_head {
   float* cand_s;       // [max_bp][4 num_sms][kTopK] streaming top-k candidates (scores)
   int32_t* cand_l;     // [max_bp][4 num_sms][kTopK] (global labels)
   int R;               // bwd CTAs per d-tile
+  int gcl;             // bwd G-sharing cluster size (TMA multicast across consecutive d-tiles)
   size_t l2_persist;   // persisting-L2 bytes granted for the G window (0 = off)
   size_t l2_window_max;
 };
@@ -317,6 +318,64 @@ static void set_bwd_attr() {
                        BwdCfg<EB, XR, KC>::kSmemBytes);
   cudaFuncSetAttribute(xmc_bwd_kernel<EB, XR, KC, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        BwdCfg<EB, XR, KC>::kSmemBytes);
+  cudaFuncSetAttribute(xmc_bwd_kernel<EB, XR, KC, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       BwdCfg<EB, XR, KC>::kSmemBytes);
+}
+
+// Measurement only: XMC_TRACE=1 records clock64 per tile and pipeline event
+// of the first backward CTA (xmc_trace_read, tools/trace_bwd.py).
+static uint64_t* trace_buf() {
+  static uint64_t* buf = nullptr;
+  static const bool on = getenv("XMC_TRACE") && atoi(getenv("XMC_TRACE")) != 0;
+  if (on && !buf && cudaMalloc(&buf, kTraceTiles * 8 * 8) != cudaSuccess) {
+    cudaGetLastError();
+    buf = nullptr;
+  }
+  return on ? buf : nullptr;
+}
+
+extern "C" xmc_status xmc_trace_read(uint64_t* out, int64_t n) {
+  uint64_t* b = trace_buf();
+  if (!b) return fail(XMC_ERR_ARG, "tracing is off (set XMC_TRACE=1)");
+  CUDA_TRY(cudaMemcpy(out, b, std::min<int64_t>(n, kTraceTiles * 8) * 8, cudaMemcpyDeviceToHost));
+  return XMC_OK;
+}
+
+// Backward G sharing: the d-tiles of one label tile run as a cluster and each G
+// tile is read from L2 once per cluster (TMA multicast) instead of once per
+// d-tile.  The cluster size c divides d/128; R (CTAs per d-tile) shrinks if
+// fewer than R*dtiles/c clusters can be co-resident (a second wave would cost
+// more than the shared reads save).  XMC_BWD_GCL overrides (1 = off).
+static void choose_bwd_cluster(xmc_head* h) {
+  const char* env = getenv("XMC_BWD_GCL");
+  const int want = env ? atoi(env) : 1;
+  h->gcl = 1;
+  for (int c : {want, 6, 3, 2}) {
+    if (c <= 1 || c > 8 || c > want || h->dtiles % c != 0) continue;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(h->R * h->dtiles);
+    cfg.blockDim = dim3(kBwdThreads);
+    cfg.dynamicSmemBytes = BwdCfg<1, true, 2>::kSmemBytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, xmc_bwd_kernel<1, true, 2, 0>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    const int r = std::min(h->R, n * c / h->dtiles);
+    if (getenv("XMC_VERBOSE")) fprintf(stderr, "xmc: bwd cluster %d: %d co-resident clusters\n", c, n);
+    if (r >= 1 && r * 10 >= h->R * 9) {   // keep >= 90 % of the CTAs
+      h->R = r;
+      h->gcl = c;
+      return;
+    }
+  }
 }
 
 extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace, size_t workspace_bytes,
@@ -411,6 +470,7 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   set_bwd_attr<2, true, 2>();
   set_bwd_attr<2, true, 4>();
   set_bwd_attr<2, false, 8>();
+  choose_bwd_cluster(h);
   *out = h;
   return XMC_OK;
 }
@@ -958,7 +1018,7 @@ static xmc_status launch_bwd_t(xmc_head* h, int R, const CUtensorMap& tw, const 
                                const CUtensorMap& tx, const CUtensorMap& tws, const BwdParams& p, size_t g_bytes,
                                cudaStream_t st) {
   constexpr int sm = BwdCfg<EB, XR, KC>::kSmemBytes;
-  const int cluster = 1;
+  const int cluster = p.gcl;
   const int grid = R * h->dtiles;
   ProfRec pr;
   prof_begin(1, st, &pr);
@@ -969,6 +1029,10 @@ static xmc_status launch_bwd_t(xmc_head* h, int R, const CUtensorMap& tw, const 
   else if (ce == 4)
     CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 4>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx, tws,
                        p));
+  else if (p.rounding == ROUND_SR_FAST && p.keep == nullptr && p.trace == nullptr && p.debug == 0 && p.gcl == 1 &&
+           p.pf_dist == 0)
+    CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 0, true>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx,
+                       tws, p));
   else
     CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 0>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx, tws,
                        p));
@@ -986,10 +1050,12 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   CUtensorMap tw, tg, tx, tws;
   XMC_TRY(make_map(&tw, static_cast<uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 128));
   XMC_TRY(make_map(&tws, static_cast<uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 32));
-  XMC_TRY(make_map(&tg, h->gbuf, eb, Bp, rows, Bp, 128));
-  XMC_TRY(make_map(&tx, h->xqt, eb, Bp, D, Bp, 128));
   const int64_t tiles = cdiv(rows, 128);
   const int R = static_cast<int>(std::min<int64_t>(h->R, tiles));
+  // clusters span d-tiles of one row group, so every R keeps them on the same label tiles
+  const int gcl = h->gcl;
+  XMC_TRY(make_map(&tg, h->gbuf, eb, Bp, rows, Bp, gcl > 1 ? 32 : 128));
+  XMC_TRY(make_map(&tx, h->xqt, eb, Bp, D, Bp, 128));
   BwdParams p{};
   p.rows = static_cast<int32_t>(rows);
   p.d = D;
@@ -1014,6 +1080,10 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   p.gx_accumulate = gx_overwrite ? 0 : 1;
   static const int dbg = getenv("XMC_DEBUG_BWD") ? atoi(getenv("XMC_DEBUG_BWD")) : 0;
   p.debug = dbg;
+  p.gcl = gcl;
+  static const int pf = getenv("XMC_BWD_PF") ? atoi(getenv("XMC_BWD_PF")) : 0;
+  p.pf_dist = pf;
+  p.trace = trace_buf();
   p.keep = keep;
   p.drop_scale = drop_scale;
   p.status = h->status;

@@ -62,8 +62,18 @@ struct BwdParams {
   const uint32_t* keep;  // keyed dropout keep bits [rows][d / 32] (chunk-local) or null
   float drop_scale;      // f32(1) / f32(1 - p) applied to kept dW (head.py:239-242)
   int32_t debug;         // measurement only (XMC_DEBUG_BWD): 1 skip dW MMAs, 2 skip update epilogue
+  int32_t pf_dist;       // L2 prefetch distance in this CTA's tiles (0 = off)
+  int32_t gcl;           // CTAs (consecutive d-tiles of one label-tile row group) sharing each G tile
+                         // through TMA multicast: 1 = every CTA loads G itself
   int32_t* status;
+  uint64_t* trace;       // measurement only (XMC_TRACE): clock64 per tile and event of CTA 0, [kTraceTiles][8]
 };
+
+constexpr int kTraceTiles = 512;
+// trace event e of local tile iteration i (CTA 0 only)
+XMC_DEV void trace_ev(uint64_t* tr, int i, int e) {
+  if (tr != nullptr && blockIdx.x == 0 && i < kTraceTiles) tr[i * 8 + e] = clock64();
+}
 
 template <int EB, bool XT_RES, int KCMAX>
 struct BwdCfg {
@@ -147,13 +157,11 @@ XMC_DEV void w_decode(const uint4 (&raw)[2 * EB], float (&w)[32]) {
 // of 32).  e4m3: one word per cvt.rs.e4m3x4 (4 elements, 16 random bits per
 // lane, see profiles/r1_probe_cvt_rs.txt); bf16: one word per bf16x2.
 template <int EB>
-XMC_DEV void sr_words(uint64_t key, int64_t flat0, uint32_t (&rw)[8 * EB]) {
-  const uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
+XMC_DEV void sr_words(const PhiloxKeys& ks, int64_t flat0, uint32_t (&rw)[8 * EB]) {
 #pragma unroll
   for (int h = 0; h < 2 * EB; ++h) {
     const uint64_t ctr = static_cast<uint64_t>(flat0) / (16 / EB) + h;
-    const U4 r = philox4x32<kPhiloxRounds>(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), EB - 1u, 0u},
-                                           k0, k1);
+    const U4 r = philox4x32_keys(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), EB - 1u, 0u}, ks);
     rw[4 * h + 0] = r.x;
     rw[4 * h + 1] = r.y;
     rw[4 * h + 2] = r.z;
@@ -166,7 +174,7 @@ XMC_DEV void sr_words(uint64_t key, int64_t flat0, uint32_t (&rw)[8 * EB]) {
 // storage bytes.  FMA contraction moves the fp32 update by <= 1 fp32 ulp,
 // far below the tensor-core accumulation noise of acc.
 template <int EB>
-XMC_DEV void w_update_pack(const BwdParams& p, const uint32_t (&acc)[32], const float (&w)[32],
+XMC_DEV void w_update_pack(const BwdParams& p, int rounding, const uint32_t (&acc)[32], const float (&w)[32],
                            const uint32_t (&rw)[8 * EB], int64_t flat0, uint4 (&out)[2 * EB]) {
   const float a_lr = -p.lr * p.dw_scale;
   const float c_wd = 1.0f - p.lr * p.wd;
@@ -187,7 +195,7 @@ XMC_DEV void w_update_pack(const BwdParams& p, const uint32_t (&acc)[32], const 
       f2unpack(r, u[2 * k], u[2 * k + 1]);
     }
   }
-  if (p.rounding == ROUND_SR_EXACT) {
+  if (rounding == ROUND_SR_EXACT) {
     const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
 #pragma unroll
     for (int k = 0; k < 32; ++k)
@@ -195,7 +203,7 @@ XMC_DEV void w_update_pack(const BwdParams& p, const uint32_t (&acc)[32], const 
   }
   uint32_t pk[8 * EB];
   if constexpr (EB == 1) {
-    if (p.rounding == ROUND_SR_FAST) {
+    if (rounding == ROUND_SR_FAST) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) pk[k] = cvt_e4m3x4_rs(u[4 * k + 3], u[4 * k + 2], u[4 * k + 1], u[4 * k], rw[k]);
     } else {
@@ -204,7 +212,7 @@ XMC_DEV void w_update_pack(const BwdParams& p, const uint32_t (&acc)[32], const 
         pk[k] = cvt_e4m3x2_rn(u[4 * k + 1], u[4 * k]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(u[4 * k + 3], u[4 * k + 2])) << 16);
     }
   } else {
-    if (p.rounding == ROUND_SR_FAST) {
+    if (rounding == ROUND_SR_FAST) {
 #pragma unroll
       for (int k = 0; k < 16; ++k) pk[k] = cvt_bf16x2_rs(u[2 * k + 1], u[2 * k], rw[k]);
     } else {
@@ -233,7 +241,7 @@ XMC_DEV uint32_t word_of(const uint4 (&v)[N], int i) {
 // HBM by the owning thread; rows without compensation (top-p% head-Kahan,
 // PAPER.md:795) pass craw = 0 and drop cout.
 template <int EB, int CE>
-XMC_DEV void w_update_pack_kahan(const BwdParams& p, const uint32_t (&acc)[32], const uint4 (&raw)[2 * EB],
+XMC_DEV void w_update_pack_kahan(const BwdParams& p, int rounding, const uint32_t (&acc)[32], const uint4 (&raw)[2 * EB],
                                  const uint32_t (&rw)[8 * EB], int64_t flat0, const uint4 (&craw)[CE * 2],
                                  uint4 (&out)[2 * EB], uint4* cdst, uint64_t pol) {
   const float a_lr = -p.lr * p.dw_scale;
@@ -268,14 +276,14 @@ XMC_DEV void w_update_pack_kahan(const BwdParams& p, const uint32_t (&acc)[32], 
       y[e] = v - c[e];
       x[e] = w[e] + y[e];
     }
-    if (p.rounding == ROUND_SR_EXACT) {
+    if (rounding == ROUND_SR_EXACT) {
       const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         x[e] = grid_round_stochastic(gf, x[e], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + 4 * g + e)));
     }
     if constexpr (EB == 1) {
-      const uint32_t w4 = p.rounding == ROUND_SR_FAST
+      const uint32_t w4 = rounding == ROUND_SR_FAST
                               ? cvt_e4m3x4_rs(x[3], x[2], x[1], x[0], rw[g])
                               : (cvt_e4m3x2_rn(x[1], x[0]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(x[3], x[2])) << 16));
       pk[g] = w4;
@@ -283,9 +291,9 @@ XMC_DEV void w_update_pack_kahan(const BwdParams& p, const uint32_t (&acc)[32], 
       const float2 hi = dec_e4m3x2(static_cast<uint16_t>(w4 >> 16));
       t[0] = lo.x; t[1] = lo.y; t[2] = hi.x; t[3] = hi.y;
     } else {
-      const uint32_t w0 = p.rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[1], x[0], rw[2 * g]) : cvt_bf16x2_rn(x[1], x[0]);
+      const uint32_t w0 = rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[1], x[0], rw[2 * g]) : cvt_bf16x2_rn(x[1], x[0]);
       const uint32_t w1 =
-          p.rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[3], x[2], rw[2 * g + 1]) : cvt_bf16x2_rn(x[3], x[2]);
+          rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[3], x[2], rw[2 * g + 1]) : cvt_bf16x2_rn(x[3], x[2]);
       pk[2 * g] = w0;
       pk[2 * g + 1] = w1;
       t[0] = __uint_as_float(w0 << 16); t[1] = __uint_as_float(w0 & 0xFFFF0000u);
@@ -308,12 +316,22 @@ XMC_DEV void w_update_pack_kahan(const BwdParams& p, const uint32_t (&acc)[32], 
   for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
 }
 
-template <int EB, bool XT_RES, int KCMAX, int CE>
+// FAST: the production specialisation (Philox SR, no dropout mask, no
+// measurement hooks, no G sharing) with every runtime mode switch folded away
+template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
                    const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
                    BwdParams p) {
   using C = BwdCfg<EB, XT_RES, KCMAX>;
+  if constexpr (FAST) {
+    p.debug = 0;
+    p.trace = nullptr;
+    p.keep = nullptr;
+    p.rounding = ROUND_SR_FAST;
+    p.gcl = 1;
+    p.pf_dist = 0;
+  }
   constexpr int WS = C::kWStages;
   constexpr int KS = C::kKStages;
   if (*p.status != 0) return;
@@ -353,7 +371,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
+      mbar_init(&k_empty[s], p.gcl);   // one MMA commit from every CTA the slot is multicast to
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&t_full[s], 1);
@@ -365,7 +383,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  // G sharing: peers multicast into this CTA's slots and arrive on its
+  // barriers, so every barrier of the cluster is initialised first
+  if (p.gcl > 1) cluster_sync();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t tmem_gx = tmem_base + 256;   // cols [256, 512): grad_X^T partial
@@ -373,34 +394,110 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (elect_one()) {
-      const uint64_t pol_stream = policy_evict_first();
-      const uint64_t pol_keep = policy_evict_last();
-      if constexpr (XT_RES) {
-        mbar_arrive_expect_tx(xt_full, p.kc_count * C::kBox);
-        for (int kc = 0; kc < p.kc_count; ++kc)
-          tma_load_2d_hint(xt_s + kc * C::kBox, &tm_xt, xt_full, kc * C::kBoxK, j * 128, pol_keep);
-      }
-      int ws = 0, ks = 0;
-      uint32_t wph = 0, kph = 0;
-      for (int tile = r0; tile < p.num_tiles; tile += R) {
-        mbar_wait(&w_empty[ws], wph ^ 1);
-        mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
+    // Boxes are dealt round-robin over the 32 lanes: one thread's bulk-tensor
+    // copies are served one after another (~550 cycles per 16-KB box,
+    // tools/probe_tma.cu), which used to bound the whole pipeline.
+    const uint32_t lane = lane_id();
+    uint32_t nbox = 0;   // warp-uniform; box i belongs to lane i mod 32
+    auto mine = [&]() { return (nbox++ & 31u) == lane; };
+    // debug & 4 (measurement): evict_normal everywhere, so a chunk that fits
+    // in L2 stays there across repeated launches
+    const uint64_t pol_stream = (p.debug & 4) ? policy_evict_normal() : policy_evict_first();
+    const uint64_t pol_keep = (p.debug & 4) ? policy_evict_normal() : policy_evict_last();
+    if constexpr (XT_RES) {
+      if (lane == 0) mbar_arrive_expect_tx(xt_full, p.kc_count * C::kBox);
+      __syncwarp();
+      if (static_cast<int>(lane) < p.kc_count)
+        tma_load_2d_hint(xt_s + lane * C::kBox, &tm_xt, xt_full, static_cast<int>(lane) * C::kBoxK, j * 128, pol_keep);
+      __syncwarp();
+    }
+    int ws = 0, ks = 0;
+    uint32_t wph = 0, kph = 0;
+    const int crank = p.gcl > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+    const uint16_t gmask = static_cast<uint16_t>((1u << p.gcl) - 1u);
+    // L2 prefetch of the tile pf_dist steps ahead: W[t, j] by its own CTA,
+    // G[t] split over the d-tile CTAs (box kc by CTA j == kc mod dtiles)
+    const int grows = p.gcl > 1 ? 32 : 128;
+    auto prefetch = [&](int t) {
+      if (t >= p.num_tiles) return;
 #pragma unroll
-        for (int b = 0; b < C::kWBoxes; ++b)
-          tma_load_2d_hint(w_s + ws * C::kWBytes + b * C::kBox, &tm_w, &w_full[ws],
-                           j * 128 + b * C::kBoxK, tile * 128, pol_stream);
-        if (++ws == WS) { ws = 0; wph ^= 1; }
+      for (int b = 0; b < C::kWBoxes; ++b)
+        if (mine()) tma_prefetch_2d(&tm_w, j * 128 + b * C::kBoxK, t * 128);
+      for (int kc = j; kc < p.kc_count; kc += p.dtiles)
+        for (int rr = 0; rr < 128; rr += grows)
+          if (mine()) tma_prefetch_2d(&tm_g, kc * C::kBoxK, t * 128 + rr);
+    };
+    for (int i = 1; i < p.pf_dist; ++i) prefetch(r0 + i * R);
+    int it = 0;
+    for (int tile = r0; tile < p.num_tiles; tile += R, ++it) {
+      if (p.pf_dist > 0) prefetch(tile + p.pf_dist * R);
+      mbar_wait(&w_empty[ws], wph ^ 1);
+      if (lane == 0) trace_ev(p.trace, it, 0);
+      if (p.gcl == 1 && p.kc_count <= KS) {
+        // the tile's W boxes and all its G (+Xq^T) boxes as ONE warp-wide TMA
+        // instruction (lane l = box l): a copy instruction costs its warp
+        // ~max(585, 1.8 x lines) cycles however few lanes it carries
         for (int kc = 0; kc < p.kc_count; ++kc) {
-          mbar_wait(&k_empty[ks], kph ^ 1);
-          uint8_t* slot = k_s + ks * C::kKSlot;
-          mbar_arrive_expect_tx(&k_full[ks], C::kKSlot);
-          tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
-          if constexpr (!XT_RES)
-            tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], kc * C::kBoxK, j * 128, pol_keep);
-          if (++ks == KS) { ks = 0; kph ^= 1; }
+          const int kk = (ks + kc) % KS;
+          mbar_wait(&k_empty[kk], kph ^ (ks + kc >= KS ? 0u : 1u));
         }
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&w_full[ws], (p.debug & 32) ? 0 : C::kWBytes);
+          for (int kc = 0; kc < p.kc_count; ++kc)
+            mbar_arrive_expect_tx(&k_full[(ks + kc) % KS], (p.debug & 16) ? 0 : C::kKSlot);
+        }
+        __syncwarp();
+        constexpr int kGB = XT_RES ? 1 : 2;   // boxes per G slot
+        const int gl = static_cast<int>(lane) - C::kWBoxes;
+        const int kc = gl / kGB, sub = gl % kGB;
+        const int kk = (ks + kc) % KS;
+        const bool is_w = static_cast<int>(lane) < C::kWBoxes;
+        const bool active = is_w || (gl >= 0 && kc < p.kc_count);
+        const CUtensorMap* m = is_w ? &tm_w : (sub == 0 ? &tm_g : &tm_xt);
+        uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + kk * C::kKSlot + sub * C::kBox;
+        uint64_t* bar = is_w ? &w_full[ws] : &k_full[kk];
+        const int32_t c0 = is_w ? j * 128 + static_cast<int>(lane) * C::kBoxK : kc * C::kBoxK;
+        const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? tile * 128 : j * 128);
+        const uint64_t pol = is_w ? pol_stream : pol_keep;
+        // measurement: debug & 16 skips the G loads, debug & 32 the W loads
+        // (the barrier then completes through a plain arrive + tx of 0)
+        const bool skip = (p.debug & 16) ? !is_w : ((p.debug & 32) ? is_w : false);
+        if (active && !skip) tma_load_2d_hint(dst, m, bar, c0, c1, pol);
+        __syncwarp();
+        if (++ws == WS) { ws = 0; wph ^= 1; }
+        for (int q = 0; q < p.kc_count; ++q)
+          if (++ks == KS) { ks = 0; kph ^= 1; }
+        if (lane == 0) trace_ev(p.trace, it, 1);
+        continue;
       }
+      if (lane == 0) mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
+#pragma unroll
+      for (int b = 0; b < C::kWBoxes; ++b)
+        if (mine())
+          tma_load_2d_hint(w_s + ws * C::kWBytes + b * C::kBox, &tm_w, &w_full[ws], j * 128 + b * C::kBoxK,
+                           tile * 128, pol_stream);
+      if (++ws == WS) { ws = 0; wph ^= 1; }
+      for (int kc = 0; kc < p.kc_count; ++kc) {
+        mbar_wait(&k_empty[ks], kph ^ 1);
+        uint8_t* slot = k_s + ks * C::kKSlot;
+        if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], C::kKSlot);
+        // G sharing: the slot's 128 G rows as four 32-row boxes, spread over
+        // the cluster's CTAs; each lands in every CTA of the cluster (the
+        // slot is free everywhere: k_empty counts every CTA's commit)
+        if (p.gcl == 1) {
+          if (mine()) tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
+        } else {
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq)
+            if ((kc * 4 + qq) % p.gcl == crank && mine())
+              tma_load_2d_mc(slot + qq * 32 * 128, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128 + qq * 32, gmask,
+                             pol_keep);
+        }
+        if constexpr (!XT_RES)
+          if (mine()) tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], kc * C::kBoxK, j * 128, pol_keep);
+        if (++ks == KS) { ks = 0; kph ^= 1; }
+      }
+      if (lane == 0) trace_ev(p.trace, it, 1);
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -408,12 +505,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     constexpr uint32_t fa = EB == 1 ? 0u : 1u;   // e4m3 : bf16
     constexpr uint32_t idesc_dw = umma_idesc(fa, fa, false, false, 128, 128);
     const uint32_t idesc_gx = umma_idesc(fa, fa, true, true, 128, p.gx_kc_count * C::kBoxK);
+    const uint16_t gmask = static_cast<uint16_t>((1u << p.gcl) - 1u);
     if constexpr (XT_RES) mbar_wait(xt_full, 0);
     int ws = 0, ks = 0, ds = 0;
     uint32_t wph = 0, kph = 0, dph = 0;
     int it = 0;
     for (int tile = r0; tile < p.num_tiles; tile += R, ++it) {
       mbar_wait(&w_full[ws], wph);
+      if (lane_id() == 0) trace_ev(p.trace, it, 2);
       mbar_wait(&t_empty[ds], dph ^ 1);
       tc_fence_after();
       const uint32_t w_addr = smem_u32(w_s + ws * C::kWBytes);
@@ -421,6 +520,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int kc = 0; kc < p.kc_count; ++kc) {
         mbar_wait(&k_full[ks], kph);
         tc_fence_after();
+        if (kc == p.kc_count - 1 && lane_id() == 0) trace_ev(p.trace, it, 3);
         if (elect_one()) {
           const uint32_t g_addr = smem_u32(k_s + ks * C::kKSlot);
           const uint32_t x_addr = XT_RES ? smem_u32(xt_s + kc * C::kBox) : g_addr + C::kBox;
@@ -450,9 +550,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               if constexpr (EB == 1) mma_f8(tmem_gx, ad, bd, idesc_gx, (it | k) != 0);
               else mma_f16(tmem_gx, ad, bd, idesc_gx, (it | k) != 0);
             }
-            for (int s = ks - gk; s <= ks; ++s) mma_commit(&k_empty[s]);
+            for (int s = ks - gk; s <= ks; ++s) {
+              if (p.gcl > 1) mma_commit_mc(&k_empty[s], gmask);
+              else mma_commit(&k_empty[s]);
+            }
           } else if (!in_gx) {
-            mma_commit(&k_empty[ks]);
+            if (p.gcl > 1) mma_commit_mc(&k_empty[ks], gmask);
+            else mma_commit(&k_empty[ks]);
           }
           // in place: dW is handed over only after the grad_X MMAs, which read
           // the W_old tile the epilogue overwrites with W_new
@@ -462,6 +566,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (++ks == KS) { ks = 0; kph ^= 1; }
       }
       if (elect_one()) mma_commit(&w_empty[ws]);
+      if (lane_id() == 0) trace_ev(p.trace, it, 4);
       __syncwarp();
       if (++ws == WS) { ws = 0; wph ^= 1; }
       if (++ds == 2) { ds = 0; dph ^= 1; }
@@ -479,13 +584,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // the 4 warps of sub-partition q own rows [32q, 32q+32) of every tile;
     // they sync among themselves and one lane TMA-stores their 32-row slab
     const bool storer = (quarter == 0) && lane_id() == 0;
-    const uint64_t pol_w_out = policy_evict_first();   // W_new streams out; keep L2 for G
+    const uint64_t pol_w_out = (p.debug & 4) ? policy_evict_normal() : policy_evict_first();   // W_new streams out; keep L2 for G
     int ws = 0, ds = 0, prev_ws = -1;
     int ot_flip = 0;
     uint32_t wph = 0, dph = 0;
-    for (int tile = r0; tile < p.num_tiles; tile += R) {
+    const bool tracer = warp == 2 && lane_id() == 0;
+    const PhiloxKeys pk = philox_keys(p.rng_base);   // round keys, once per launch
+    int it = 0;
+    for (int tile = r0; tile < p.num_tiles; tile += R, ++it) {
       uint8_t* wt = w_s + ws * C::kWBytes;
       mbar_wait(&w_full[ws], wph);
+      if (tracer) trace_ev(p.trace, it, 5);
       if (p.do_update && !(p.debug & 2)) {
         const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
         const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + c0;
@@ -512,15 +621,84 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int h = 0; h < CE * 2; ++h) craw[h] = krow ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
         }
+        if constexpr (FAST && EB == 1 && CE == 0 && C::kOutTiles == 2) {
+          // production path: everything independent of dW (Philox words,
+          // W_old decoded and scaled by 1 - lr wd) is computed and pinned in
+          // registers BEFORE the dW wait, so it overlaps the MMAs
+          uint32_t rw[8];
+          sr_words<1>(pk, flat0, rw);
+          const float c_wd = 1.0f - p.lr * p.wd;
+          const float a_lr = -p.lr * p.dw_scale;
+          float wc[32];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t wv[4] = {raw[h].x, raw[h].y, raw[h].z, raw[h].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 lo = dec_e4m3x2(static_cast<uint16_t>(wv[k] & 0xFFFF));
+              const float2 hi = dec_e4m3x2(static_cast<uint16_t>(wv[k] >> 16));
+              wc[h * 16 + 4 * k + 0] = lo.x;
+              wc[h * 16 + 4 * k + 1] = lo.y;
+              wc[h * 16 + 4 * k + 2] = hi.x;
+              wc[h * 16 + 4 * k + 3] = hi.y;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {   // w (1 - lr wd)  (optimizers.py:71-73, wd folded)
+            const uint64_t r = fmul2(f2pack(wc[2 * k], wc[2 * k + 1]), f2pack(c_wd, c_wd));
+            f2unpack(r, wc[2 * k], wc[2 * k + 1]);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pin(rw[k]);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) pin(wc[k]);
+          mbar_wait(&t_full[ds], dph);
+          tc_fence_after();
+          uint32_t acc[32];
+          tmem_ld32(tmem_base + lane_off + ds * 128 + c0, acc);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&t_empty[ds]);
+          uint32_t pk8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            float u[4];
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              const uint64_t r = ffma2(f2pack(__uint_as_float(acc[4 * k + e]), __uint_as_float(acc[4 * k + e + 1])),
+                                       f2pack(a_lr, a_lr), f2pack(wc[4 * k + e], wc[4 * k + e + 1]));
+              f2unpack(r, u[e], u[e + 1]);
+            }
+            pk8[k] = cvt_e4m3x4_rs(u[3], u[2], u[1], u[0], rw[k]);
+          }
+          uint8_t* ot = out_s + (ot_flip & 1) * C::kWBytes;
+          ++ot_flip;
+          const uint32_t ot_s = smem_u32(ot);
+          sts128(ot_s + w_chunk_off<EB>(row, c0, 0), make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]));
+          sts128(ot_s + w_chunk_off<EB>(row, c0, 1), make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]));
+          fence_proxy_async_smem();
+          if (storer && prev_ws >= 0) bulk_wait_read<0>();
+          named_bar_sync(1 + q, 128);
+          if (storer) {
+            tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
+            bulk_commit();
+          }
+          prev_ws = ws;
+          if (++ws == WS) { ws = 0; wph ^= 1; }
+          if (++ds == 2) { ds = 0; dph ^= 1; }
+          continue;
+        }
         uint32_t km = 0u;   // dropout keep bits of this thread's 32 columns
         if (p.keep != nullptr && grow < p.rows) km = __ldg(p.keep + grow * (p.d >> 5) + ((j * 128 + c0) >> 5));
         uint32_t rw[C::kRandWords];
-        if (p.rounding == ROUND_SR_FAST) sr_words<EB>(p.rng_base, flat0, rw);
+        if (p.rounding == ROUND_SR_FAST) sr_words<EB>(pk, flat0, rw);
         float w[CE > 0 ? 1 : 32];
         if constexpr (CE == 0) w_decode<EB>(raw, w);
         // --- dW from TMEM, then release the accumulator buffer at once
         mbar_wait(&t_full[ds], dph);
         tc_fence_after();
+        if (tracer) trace_ev(p.trace, it, 6);
         uint32_t acc[32];
         tmem_ld32(tmem_base + lane_off + ds * 128 + c0, acc);
         tmem_ld_wait();
@@ -535,9 +713,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint4 out[C::kChunks16];
         if constexpr (CE > 0) {
           uint4* cdst = krow ? reinterpret_cast<uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE) : nullptr;
-          w_update_pack_kahan<EB, CE>(p, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
+          w_update_pack_kahan<EB, CE>(p, p.rounding, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
         } else {
-          w_update_pack<EB>(p, acc, w, rw, flat0, out);
+          w_update_pack<EB>(p, p.rounding, acc, w, rw, flat0, out);
         }
         // W_new into a swizzled smem tile (the staging tile, or in place once
         // the grad_X MMAs have read W_old), then one TMA store per 32-row slab
@@ -564,10 +742,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (storer) {
 #pragma unroll
           for (int b = 0; b < C::kWBoxes; ++b)
-            tma_store_2d_hint(&tm_ws, ot + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK, tile * 128 + q * 32,
-                              pol_w_out);
+            if (!(p.debug & 8))   // measurement: debug & 8 drops the W_new store
+              tma_store_2d_hint(&tm_ws, ot + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK,
+                                tile * 128 + q * 32, pol_w_out);
           bulk_commit();
         }
+        if (tracer) trace_ev(p.trace, it, 7);
         prev_ws = ws;
       } else {
         mbar_wait(&t_full[ds], dph);
@@ -615,7 +795,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  // no CTA leaves while a peer may still multicast into it or arrive on it
+  if (p.gcl > 1) cluster_sync();
+  else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);

@@ -149,38 +149,53 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (elect_one()) {
-      const uint64_t pol_w = policy_evict_first();
-      const uint64_t pol_x = policy_evict_last();
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int u = unit0; u < num_units; u += ustride) {
-        const int tile = PAIR ? 2 * u + static_cast<int>(rank) : u;
-        for (int kc = 0; kc < kc_count; ++kc) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sb = stage_base + stage * C::kStageBytes;
-          if constexpr (PAIR) {
-            const uint32_t lbar = mapa_shared(&full[stage], 0);
-            if (leader) mbar_arrive_expect_tx(&full[stage], 2 * C::kStageBytes);
-            else mbar_arrive_cluster(lbar);
-            tma_load_2d_2sm(sb, &tm_w, lbar, kc * C::kBoxK, tile * 128, pol_w);
-#pragma unroll
-            for (int xb = 0; xb < C::kXBoxes; ++xb)
-              tma_load_2d_2sm(sb + C::kWBytes + xb * C::kXBoxRows * 128, &tm_x, lbar, kc * C::kBoxK,
-                              static_cast<int>(rank) * C::kXRows + xb * C::kXBoxRows, pol_x);
-          } else {
-            mbar_arrive_expect_tx(&full[stage], C::kStageBytes);
-            tma_load_2d_hint(sb, &tm_w, &full[stage], kc * C::kBoxK, tile * 128, pol_w);
-#pragma unroll
-            for (int xb = 0; xb < C::kXBoxes; ++xb)
-              tma_load_2d_hint(sb + C::kWBytes + xb * C::kXBoxRows * 128, &tm_x, &full[stage],
-                               kc * C::kBoxK, xb * C::kXBoxRows, pol_x);
-          }
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+    // A bulk-tensor copy instruction occupies its warp for ~max(585, 1.8 x
+    // 128-B lines of ALL its lanes) cycles (tools/probe_tma.cu), so one box
+    // per instruction caps a CTA at ~28 B/clk.  The producer therefore issues
+    // the boxes of kIPB consecutive stages as ONE warp-wide instruction, lane
+    // l carrying box l (W or an Xq box of one stage).
+    constexpr int kBPI = 1 + (PAIR ? 1 : C::kXBoxes);   // boxes per stage
+    constexpr int kIPB = 2;                              // stages per instruction
+    static_assert(kBPI * kIPB <= 32, "one lane per box");
+    const int lane = static_cast<int>(lane_id());
+    const uint64_t pol_w = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    const int my_units = unit0 < num_units ? (num_units - unit0 + ustride - 1) / ustride : 0;
+    const int total = my_units * kc_count;   // stages this CTA fills
+    for (int n0 = 0; n0 < total; n0 += kIPB) {
+      const int cnt = min(kIPB, total - n0);
+      // stage / phase of item n: ring position n mod kStages, lap n / kStages
+      for (int i = 0; i < cnt; ++i) {
+        const int n = n0 + i;
+        mbar_wait(&empty[n % C::kStages], ((n / C::kStages) & 1) ^ 1);
+      }
+      const int it = lane / kBPI, b = lane % kBPI;
+      const int n = n0 + it;
+      const int st_i = n % C::kStages;
+      const int u = unit0 + (n / kc_count) * ustride;
+      const int kc = n % kc_count;
+      const int tile = PAIR ? 2 * u + static_cast<int>(rank) : u;
+      uint8_t* sb = stage_base + st_i * C::kStageBytes;
+      const bool active = it < cnt;
+      if (active && b == 0) {
+        if constexpr (PAIR) {
+          if (leader) mbar_arrive_expect_tx(&full[st_i], 2 * C::kStageBytes);
+          else mbar_arrive_cluster(mapa_shared(&full[st_i], 0));
+        } else {
+          mbar_arrive_expect_tx(&full[st_i], C::kStageBytes);
         }
       }
+      __syncwarp();
+      const CUtensorMap* m = b == 0 ? &tm_w : &tm_x;
+      uint8_t* dst = b == 0 ? sb : sb + C::kWBytes + (b - 1) * C::kXBoxRows * 128;
+      const int32_t c1 = b == 0 ? tile * 128 : static_cast<int>(rank) * C::kXRows + (b - 1) * C::kXBoxRows;
+      const uint64_t pol = b == 0 ? pol_w : pol_x;
+      if (active) {
+        if constexpr (PAIR) tma_load_2d_2sm(dst, m, mapa_shared(&full[st_i], 0), kc * C::kBoxK, c1, pol);
+        else tma_load_2d_hint(dst, m, &full[st_i], kc * C::kBoxK, c1, pol);
+      }
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
     if (leader) {

@@ -95,6 +95,14 @@ XMC_DEV void tma_load_2d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, in
       : "memory");
 }
 
+// TMA prefetch of one box into L2 (no smem, no completion): pulls a later
+// tile's DRAM latency off the smem pipeline
+XMC_DEV void tma_prefetch_2d(const CUtensorMap* m, int32_t c0, int32_t c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 // smem -> global tensor store (async proxy), bulk-group completion
 XMC_DEV void tma_store_2d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -130,6 +138,11 @@ XMC_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::
 XMC_DEV uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+XMC_DEV uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 XMC_DEV uint64_t policy_evict_last() {

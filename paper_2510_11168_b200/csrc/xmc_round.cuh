@@ -87,6 +87,35 @@ XMC_DEV U4 philox4x32(U4 c, uint32_t k0, uint32_t k1) {
 }
 constexpr int kPhiloxRounds = 7;
 
+// Philox4x32-7 with the round keys computed once (k_i = k + i * W): the key
+// schedule is the same for every counter of a launch
+struct PhiloxKeys {
+  uint32_t k0[kPhiloxRounds], k1[kPhiloxRounds];
+};
+XMC_DEV PhiloxKeys philox_keys(uint64_t key) {
+  PhiloxKeys ks;
+  uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
+#pragma unroll
+  for (int i = 0; i < kPhiloxRounds; ++i) {
+    ks.k0[i] = k0;
+    ks.k1[i] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return ks;
+}
+XMC_DEV U4 philox4x32_keys(U4 c, const PhiloxKeys& ks) {
+#pragma unroll
+  for (int i = 0; i < kPhiloxRounds; ++i) {
+    // one 32x32->64 multiply each (IMAD.WIDE.U32), not a lo/hi pair
+    const uint64_t m0 = static_cast<uint64_t>(0xD2511F53u) * c.x;
+    const uint64_t m1 = static_cast<uint64_t>(0xCD9E8D57u) * c.z;
+    c = U4{static_cast<uint32_t>(m1 >> 32) ^ c.y ^ ks.k0[i], static_cast<uint32_t>(m1),
+           static_cast<uint32_t>(m0 >> 32) ^ c.w ^ ks.k1[i], static_cast<uint32_t>(m0)};
+  }
+  return c;
+}
+
 XMC_DEV U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
@@ -191,6 +220,11 @@ XMC_DEV float dec_e5m2(uint8_t b) {
 XMC_DEV float dec_bf16(uint16_t b) { return __uint_as_float(static_cast<uint32_t>(b) << 16); }
 
 // two e4m3 bytes (lo, hi of a 16-bit word) -> two floats
+// keep a value in a register at this program point: volatile asms keep their
+// order, so work feeding `pin` cannot sink past a later barrier wait
+XMC_DEV void pin(uint32_t& v) { asm volatile("" : "+r"(v)); }
+XMC_DEV void pin(float& v) { asm volatile("" : "+f"(v)); }
+
 XMC_DEV float2 dec_e4m3x2(uint16_t v) {
   uint32_t h2;
   asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(v));
