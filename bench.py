@@ -372,17 +372,20 @@ def main():
     # Burst vs sustained peak by the clocks seen in the timed region: a short
     # region runs at boost clocks (burst peak); a long one hits the ~1 kW power
     # cap, the SM clock drops to ~1.3-1.4 GHz and the sustained peak applies.
-    fp8 = peaks.get("fp8", {})
     smax = clk.get("sm_max_mhz") or peaks.get("sm_max_mhz") or 1965.0
     burst = bool(clk.get("sm_mhz")) and clk["sm_mhz"] >= 0.95 * smax and "sw_power_cap" not in clk.get("reasons", [])
     regime = "burst" if burst else "sustained"
-    if eb == 1 and fp8:
-        tc_peak = fp8["tflops"] if burst else fp8["tflops_sustained"]
-        tc_src = f"measured fp8 {regime}: " + fp8.get("how", "")
-    else:
-        tc_peak = (peaks["bf16_tflops"] if burst else peaks["bf16_tflops_sustained"]) * (2.0 if eb == 1 else 1.0)
-        tc_src = (f"2x measured bf16 {regime} (no measured fp8)" if eb == 1 else f"measured bf16 {regime}") \
-            + f" [{peaks['source']}]"
+    # Tensor peak = the tensor pipe's measured issue rate (tools/probe_mma.cu,
+    # profiles/r1_probe_mma.txt: kind::f8f6f4 16384 flop/clk/SM, kind::f16 8192,
+    # for N >= 128 in either majorness) x SMs x the SM clock seen in the timed
+    # region.  This is the hardware ceiling (4.77 PF fp8 at 1965 MHz, 4.4-4.5 PF
+    # at the ~1.84 GHz a dense MMA loop holds); cuBLAS-class library GEMMs reach
+    # less (torch._scaled_mm 8192^3: 3.1 PF, profiles/fp8_peak.json).
+    sm_mhz = clk.get("sm_mhz") or smax
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    tc_peak = (16384.0 if eb == 1 else 8192.0) * n_sms * sm_mhz * 1e6 / 1e12
+    tc_src = (f"tensor pipe {'16384' if eb == 1 else '8192'} flop/clk/SM (probe_mma) x {n_sms} SMs x "
+              f"{sm_mhz:.0f} MHz observed ({regime})")
     t_tc = flops / (tc_peak * 1e12)
     t_hbm = bytes_ / (peaks["hbm_gbs"] * 1e9)
     bound = "tensor" if t_tc >= t_hbm else "hbm"

@@ -309,6 +309,9 @@ static void set_fwd_attr() {
   if constexpr (BN <= 256 && BN >= 128)
     cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FwdCfg<EB, BN, true>::kSmemBytes);
+  if constexpr (EB == 1 && BN <= 256 && BN >= 128)
+    cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FwdCfg<EB, BN, true, true>::kSmemBytes);
 }
 template <int EB, bool XR, int KC>
 static void set_bwd_attr() {
@@ -972,6 +975,17 @@ static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtenso
   ProfRec pr;
   prof_begin(0, st, &pr);
   const size_t win = p.mode == 0 ? static_cast<size_t>(p.rows) * p.ld * EB : 0;
+  // resident Xq (e4m3 pairs, d <= 768) unless XMC_FWD_XRES=0
+  static const bool xres_on = !getenv("XMC_FWD_XRES") || atoi(getenv("XMC_FWD_XRES")) != 0;
+  if constexpr (PAIR && EB == 1) {
+    using CX = FwdCfg<EB, BN, true, true>;
+    if (xres_on && p.d / CX::kBoxK <= CX::kXResChunks) {
+      CUDA_TRY(launch_ex(xmc_fwd_kernel<EB, BN, true, false, true>, grid, CX::kThreads, CX::kSmemBytes, st, h, win, 2,
+                         tw, tx, p));
+      prof_end(st, &pr);
+      return XMC_OK;
+    }
+  }
   CUDA_TRY(launch_ex(xmc_fwd_kernel<EB, BN, PAIR>, grid, C::kThreads, C::kSmemBytes, st, h, win, PAIR ? 2 : 1, tw,
                      tx, p));
   prof_end(st, &pr);
@@ -1029,8 +1043,11 @@ static xmc_status launch_bwd_t(xmc_head* h, int R, const CUtensorMap& tw, const 
   else if (ce == 4)
     CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 4>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx, tws,
                        p));
-  else if (p.rounding == ROUND_SR_FAST && p.keep == nullptr && p.trace == nullptr && p.debug == 0 && p.gcl == 1 &&
-           p.pf_dist == 0)
+#ifdef XMC_TRACE_FAST
+  else if (p.rounding == ROUND_SR_FAST && p.keep == nullptr && p.debug == 0 && p.pf_dist == 0)
+#else
+  else if (p.rounding == ROUND_SR_FAST && p.keep == nullptr && p.trace == nullptr && p.debug == 0 && p.pf_dist == 0)
+#endif
     CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 0, true>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx,
                        tws, p));
   else
@@ -1083,6 +1100,10 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   p.gcl = gcl;
   static const int pf = getenv("XMC_BWD_PF") ? atoi(getenv("XMC_BWD_PF")) : 0;
   p.pf_dist = pf;
+  static const int stg = getenv("XMC_BWD_STAGGER") ? atoi(getenv("XMC_BWD_STAGGER")) : 0;
+  p.stagger = stg;
+  static const int poln = getenv("XMC_POL_NORMAL") ? atoi(getenv("XMC_POL_NORMAL")) : 0;
+  p.pol_normal = poln;
   p.trace = trace_buf();
   p.keep = keep;
   p.drop_scale = drop_scale;

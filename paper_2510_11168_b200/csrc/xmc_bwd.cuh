@@ -63,6 +63,8 @@ struct BwdParams {
   float drop_scale;      // f32(1) / f32(1 - p) applied to kept dW (head.py:239-242)
   int32_t debug;         // measurement only (XMC_DEBUG_BWD): 1 skip dW MMAs, 2 skip update epilogue
   int32_t pf_dist;       // L2 prefetch distance in this CTA's tiles (0 = off)
+  int32_t stagger;
+  int32_t pol_normal;    // measurement: evict_normal for every load/store (L2-resident chunk experiments)       // d-tile j walks its tile list rotated by j*stagger (spreads G reads in time)
   int32_t gcl;           // CTAs (consecutive d-tiles of one label-tile row group) sharing each G tile
                          // through TMA multicast: 1 = every CTA loads G itself
   int32_t* status;
@@ -326,10 +328,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   using C = BwdCfg<EB, XT_RES, KCMAX>;
   if constexpr (FAST) {
     p.debug = 0;
+#ifndef XMC_TRACE_FAST   // measurement builds keep the pipeline trace in the fast path
     p.trace = nullptr;
+#endif
     p.keep = nullptr;
     p.rounding = ROUND_SR_FAST;
-    p.gcl = 1;
     p.pf_dist = 0;
   }
   constexpr int WS = C::kWStages;
@@ -358,6 +361,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int R = gridDim.x / p.dtiles;
   const int r0 = blockIdx.x / p.dtiles;
   const bool do_gx = p.gx_kc_count > 0;
+  // this CTA's label tiles r0, r0+R, ... walked from a j-dependent rotation, so
+  // the d-tile CTAs of one row group do not all request a G tile at once
+  const int ntl = r0 < p.num_tiles ? (p.num_tiles - r0 + R - 1) / R : 0;
+  const int rot = ntl > 0 ? (j * p.stagger) % ntl : 0;
+  auto tile_at = [&](int k) { const int kk = k + rot; return r0 + (kk >= ntl ? kk - ntl : kk) * R; };
 
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tm_w);
@@ -402,8 +410,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     auto mine = [&]() { return (nbox++ & 31u) == lane; };
     // debug & 4 (measurement): evict_normal everywhere, so a chunk that fits
     // in L2 stays there across repeated launches
-    const uint64_t pol_stream = (p.debug & 4) ? policy_evict_normal() : policy_evict_first();
-    const uint64_t pol_keep = (p.debug & 4) ? policy_evict_normal() : policy_evict_last();
+    const uint64_t pol_stream = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_first();
+    const uint64_t pol_keep = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_last();
     if constexpr (XT_RES) {
       if (lane == 0) mbar_arrive_expect_tx(xt_full, p.kc_count * C::kBox);
       __syncwarp();
@@ -429,10 +437,42 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     };
     for (int i = 1; i < p.pf_dist; ++i) prefetch(r0 + i * R);
     int it = 0;
-    for (int tile = r0; tile < p.num_tiles; tile += R, ++it) {
+    for (; it < ntl; ++it) {
+      const int tile = tile_at(it);
       if (p.pf_dist > 0) prefetch(tile + p.pf_dist * R);
       mbar_wait(&w_empty[ws], wph ^ 1);
       if (lane == 0) trace_ev(p.trace, it, 0);
+      if (XT_RES && p.gcl > 1 && p.kc_count <= KS) {
+        // G shared over the cluster: this CTA's 32-row G pieces (piece id
+        // kc*4+qq, owner id mod gcl) multicast to every CTA of the cluster in
+        // one warp-wide instruction, its own W box in another
+        for (int kc = 0; kc < p.kc_count; ++kc) {
+          const int kk = (ks + kc) % KS;
+          mbar_wait(&k_empty[kk], kph ^ (ks + kc >= KS ? 0u : 1u));
+        }
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
+          for (int kc = 0; kc < p.kc_count; ++kc) mbar_arrive_expect_tx(&k_full[(ks + kc) % KS], C::kKSlot);
+        }
+        __syncwarp();
+        if (static_cast<int>(lane) < C::kWBoxes)
+          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws],
+                           j * 128 + static_cast<int>(lane) * C::kBoxK, tile * 128, pol_stream);
+        // lane l issues this CTA's l-th piece
+        const int piece = crank + static_cast<int>(lane) * p.gcl;
+        if (piece < 4 * p.kc_count) {
+          const int kc = piece >> 2, qq = piece & 3;
+          const int kk = (ks + kc) % KS;
+          tma_load_2d_mc(k_s + kk * C::kKSlot + qq * 32 * 128, &tm_g, &k_full[kk], kc * C::kBoxK,
+                         tile * 128 + qq * 32, gmask, pol_keep);
+        }
+        __syncwarp();
+        if (++ws == WS) { ws = 0; wph ^= 1; }
+        for (int q = 0; q < p.kc_count; ++q)
+          if (++ks == KS) { ks = 0; kph ^= 1; }
+        if (lane == 0) trace_ev(p.trace, it, 1);
+        continue;
+      }
       if (p.gcl == 1 && p.kc_count <= KS) {
         // the tile's W boxes and all its G (+Xq^T) boxes as ONE warp-wide TMA
         // instruction (lane l = box l): a copy instruction costs its warp
@@ -510,7 +550,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     int ws = 0, ks = 0, ds = 0;
     uint32_t wph = 0, kph = 0, dph = 0;
     int it = 0;
-    for (int tile = r0; tile < p.num_tiles; tile += R, ++it) {
+    for (; it < ntl; ++it) {
+      const int tile = tile_at(it);
       mbar_wait(&w_full[ws], wph);
       if (lane_id() == 0) trace_ev(p.trace, it, 2);
       mbar_wait(&t_empty[ds], dph ^ 1);
@@ -584,14 +625,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // the 4 warps of sub-partition q own rows [32q, 32q+32) of every tile;
     // they sync among themselves and one lane TMA-stores their 32-row slab
     const bool storer = (quarter == 0) && lane_id() == 0;
-    const uint64_t pol_w_out = (p.debug & 4) ? policy_evict_normal() : policy_evict_first();   // W_new streams out; keep L2 for G
+    const uint64_t pol_w_out = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_first();   // W_new streams out; keep L2 for G
     int ws = 0, ds = 0, prev_ws = -1;
     int ot_flip = 0;
     uint32_t wph = 0, dph = 0;
     const bool tracer = warp == 2 && lane_id() == 0;
     const PhiloxKeys pk = philox_keys(p.rng_base);   // round keys, once per launch
     int it = 0;
-    for (int tile = r0; tile < p.num_tiles; tile += R, ++it) {
+    for (; it < ntl; ++it) {
+      const int tile = tile_at(it);
       uint8_t* wt = w_s + ws * C::kWBytes;
       mbar_wait(&w_full[ws], wph);
       if (tracer) trace_ev(p.trace, it, 5);
@@ -654,6 +696,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int k = 0; k < 32; ++k) pin(wc[k]);
           mbar_wait(&t_full[ds], dph);
           tc_fence_after();
+          if (tracer) trace_ev(p.trace, it, 6);
           uint32_t acc[32];
           tmem_ld32(tmem_base + lane_off + ds * 128 + c0, acc);
           tmem_ld_wait();
@@ -684,6 +727,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
             bulk_commit();
           }
+          if (tracer) trace_ev(p.trace, it, 7);
           prev_ws = ws;
           if (++ws == WS) { ws = 0; wph ^= 1; }
           if (++ds == 2) { ds = 0; dph ^= 1; }

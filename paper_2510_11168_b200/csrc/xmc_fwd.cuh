@@ -51,7 +51,10 @@ struct FwdParams {
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
 };
 
-template <int EB, int BN, bool PAIR>
+// XRES: this CTA's Xq rows stay resident in shared memory for the whole
+// launch (loaded once, kXResChunks K-chunks max, i.e. d <= 768 for e4m3), so a
+// stage carries only its W box: half the TMA work and L2->SM traffic per tile.
+template <int EB, int BN, bool PAIR, bool XRES = false>
 struct FwdCfg {
   static constexpr int kBoxK = 128 / EB;                  // K elements per 128-B swizzle atom
   static constexpr int kWBytes = 128 * 128;               // W box: 128 rows x 128 B
@@ -59,13 +62,15 @@ struct FwdCfg {
   static constexpr int kXBoxRows = kXRows > 256 ? 256 : kXRows;
   static constexpr int kXBoxes = kXRows / kXBoxRows;
   static constexpr int kXBytes = kXRows * 128;
-  static constexpr int kStageBytes = kWBytes + kXBytes;
-  static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
+  static constexpr int kXResChunks = 6;
+  static constexpr int kXResBytes = XRES ? kXResChunks * kXBytes : 0;
+  static constexpr int kStageBytes = kWBytes + (XRES ? 0 : kXBytes);
+  static constexpr int kStages = XRES ? 7 : ((200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes);
   static constexpr int kAccStages = (2 * BN <= 512) ? 2 : 1;
   static constexpr int kTmemCols = (BN * kAccStages) <= 128 ? 128 : ((BN * kAccStages) <= 256 ? 256 : 512);
   static constexpr int kWordsPerRow = BN / 32;
   static constexpr int kBitmapBytes = 128 * kWordsPerRow * 4;
-  static constexpr int kSmemBytes = 1024 /*align slack*/ + kStages * kStageBytes + kBitmapBytes + 256;
+  static constexpr int kSmemBytes = 1024 /*align slack*/ + kXResBytes + kStages * kStageBytes + kBitmapBytes + 256;
   static constexpr int kMmaN = BN > 256 ? 256 : BN;
   // epilogue: 4 warps per TMEM sub-partition for wide tiles, 2 otherwise
   static constexpr int kEpiWarps = BN >= 256 ? 16 : 8;
@@ -96,24 +101,27 @@ XMC_DEV void topk_insert(float (&s)[kTopK], int32_t (&l)[kTopK], float v, int32_
   }
 }
 
-template <int EB, int BN, bool PAIR, bool TOPK = false>
+template <int EB, int BN, bool PAIR, bool TOPK = false, bool XRES = false>
 __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     xmc_fwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                    FwdParams p) {
-  using C = FwdCfg<EB, BN, PAIR>;
+  using C = FwdCfg<EB, BN, PAIR, XRES>;
   static_assert(!PAIR || BN <= 256, "paired tiles use one N <= 256 accumulator");
+  static_assert(!XRES || PAIR, "resident Xq is a CTA-pair layout (one 128-B box per K-chunk)");
   if (*p.status != 0) return;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* stage_base = smem;
-  uint32_t* bitmap = reinterpret_cast<uint32_t*>(smem + C::kStages * C::kStageBytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + C::kBitmapBytes);
+  uint8_t* xres = smem;                           // [kXResChunks][kXRows x 128 B] (XRES)
+  uint8_t* stage_base = smem + C::kXResBytes;
+  uint32_t* bitmap = reinterpret_cast<uint32_t*>(stage_base + C::kStages * C::kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stage_base + C::kStages * C::kStageBytes + C::kBitmapBytes);
   uint64_t* full = bars;                          // [kStages]   (leader's counts both CTAs)
   uint64_t* empty = bars + C::kStages;            // [kStages]
   uint64_t* tfull = bars + 2 * C::kStages;        // [kAccStages]
   uint64_t* tempty = tfull + C::kAccStages;       // [kAccStages] (leader's counts both CTAs)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + C::kAccStages);
+  uint64_t* xfull = tempty + C::kAccStages;       // resident Xq landed (leader's counts both CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 1);
 
   const uint32_t warp = warp_id_sync();
   const int kc_count = p.d / C::kBoxK;
@@ -135,6 +143,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], (PAIR ? 2 : 1) * C::kEpiWarps);
     }
+    mbar_init(xfull, 2);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -154,12 +163,24 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     // per instruction caps a CTA at ~28 B/clk.  The producer therefore issues
     // the boxes of kIPB consecutive stages as ONE warp-wide instruction, lane
     // l carrying box l (W or an Xq box of one stage).
-    constexpr int kBPI = 1 + (PAIR ? 1 : C::kXBoxes);   // boxes per stage
-    constexpr int kIPB = 2;                              // stages per instruction
+    constexpr int kBPI = 1 + (XRES ? 0 : (PAIR ? 1 : C::kXBoxes));   // boxes per stage
+    constexpr int kIPB = XRES ? 3 : 2;                                 // stages per instruction
     static_assert(kBPI * kIPB <= 32, "one lane per box");
     const int lane = static_cast<int>(lane_id());
     const uint64_t pol_w = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
+    if constexpr (XRES) {
+      // this CTA's Xq rows, every K-chunk, once: one warp-wide instruction
+      if (lane == 0) {
+        if (leader) mbar_arrive_expect_tx(xfull, 2 * kc_count * C::kXBytes);
+        else mbar_arrive_cluster(mapa_shared(xfull, 0));
+      }
+      __syncwarp();
+      if (lane < kc_count)
+        tma_load_2d_2sm(xres + lane * C::kXBytes, &tm_x, mapa_shared(xfull, 0), lane * C::kBoxK,
+                        static_cast<int>(rank) * C::kXRows, pol_x);
+      __syncwarp();
+    }
     const int my_units = unit0 < num_units ? (num_units - unit0 + ustride - 1) / ustride : 0;
     const int total = my_units * kc_count;   // stages this CTA fills
     for (int n0 = 0; n0 < total; n0 += kIPB) {
@@ -206,6 +227,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      if constexpr (XRES) mbar_wait(xfull, 0);
       for (int u = unit0; u < num_units; u += ustride) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -220,8 +242,8 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
               const uint64_t ad = umma_desc_sw128(sa + k * 32, 16, 1024);
 #pragma unroll
               for (int xb = 0; xb < (PAIR ? 1 : C::kXBoxes); ++xb) {
-                const uint64_t bd =
-                    umma_desc_sw128(sa + C::kWBytes + xb * C::kXBoxRows * 128 + k * 32, 16, 1024);
+                const uint32_t xa = XRES ? smem_u32(xres + kc * C::kXBytes) : sa + C::kWBytes;
+                const uint64_t bd = umma_desc_sw128(xa + xb * C::kXBoxRows * 128 + k * 32, 16, 1024);
                 if constexpr (PAIR) {
                   if constexpr (EB == 1) mma_f8_2sm(d_tmem, ad, bd, idesc, (kc | k) != 0);
                   else mma_f16_2sm(d_tmem, ad, bd, idesc, (kc | k) != 0);
