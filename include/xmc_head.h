@@ -196,6 +196,17 @@ xmc_status xmc_kahan_sgd_step(xmc_grid g, float* w, float* comp, const float* gr
                               float wd, int32_t rounding, uint64_t seed, uint64_t step,
                               uint64_t tensor_id, const uint64_t* index, int32_t* status, void* stream);
 
+/* kahan_adamw_step (optimizers.py:112-137, kahan_add formats.py:246-263):
+ * AdamW with bias-corrected fp32 moments m, v and a Kahan-compensated
+ * parameter w (fp32 on-grid values) / comp (fp32), n elements, step t >= 1.
+ * beta1/beta2 are the config's Python floats (double): the bias corrections
+ * f32(1 - beta^t) are formed in double as the reference does.  Bit-exact with
+ * the reference; non-finite moments or updates return XMC_ERR_NONFINITE and
+ * leave every buffer unchanged. */
+xmc_status xmc_kahan_adamw_step(xmc_grid g, float* w, float* comp, float* m, float* v, const float* grad,
+                                int64_t n, float lr, double beta1, double beta2, float eps, float wd,
+                                int64_t t, void* stream);
+
 /* Native-storage RTN cast, e.g. X -> e4m3 bytes (head.py:265). */
 xmc_status xmc_cast_rn(const float* x, void* out, int64_t n, int32_t fmt, int32_t* status, void* stream);
 

@@ -312,6 +312,48 @@ def kahan_sgd_values(w, comp, grad, cfg: SgdSrConfig, rng, step, tensor_id,
     return t, c_new
 
 
+@dataclass
+class KahanAdamWConfig:
+    """optimizers.py:77-91."""
+
+    lr: float
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+    fmt: FloatFormat = field(default_factory=lambda: FP32)
+
+    def __post_init__(self):
+        if not (0.0 <= self.beta1 < 1.0 and 0.0 <= self.beta2 < 1.0):
+            raise ValueError("betas must lie in [0, 1)")
+        if self.eps <= 0:
+            raise ValueError("eps must be positive")
+
+
+def kahan_adamw_values(w, comp, m, v, grad, cfg: KahanAdamWConfig, t: int, lr=None):
+    """AdamW with Kahan-compensated parameter accumulation, optimizers.py:112-137
+    (moments in float32, bias-corrected; decoupled weight decay; kahan_add
+    formats.py:246-263 onto cfg.fmt).  Returns (w, comp, m, v) as new arrays;
+    the reference updates its KahanAdamWParam in place."""
+    if t < 1:
+        raise ValueError("step index t must be >= 1")
+    grad = np.asarray(grad, dtype=np.float32)
+    w = np.asarray(w, dtype=np.float32)
+    if grad.shape != w.shape:
+        raise ValueError("gradient shape mismatch")
+    lr = np.float32(cfg.lr if lr is None else lr)
+    b1, b2 = np.float32(cfg.beta1), np.float32(cfg.beta2)
+    m = b1 * np.asarray(m, np.float32) + (np.float32(1) - b1) * grad
+    v = b2 * np.asarray(v, np.float32) + (np.float32(1) - b2) * grad * grad
+    if not np.all(np.isfinite(m)) or not np.all(np.isfinite(v)):
+        raise ValueError("non-finite optimizer moments")
+    mhat = m / np.float32(1.0 - cfg.beta1 ** t)
+    vhat = v / np.float32(1.0 - cfg.beta2 ** t)
+    update = -lr * (mhat / (np.sqrt(vhat) + np.float32(cfg.eps)) + np.float32(cfg.weight_decay) * w)
+    s_new, c_new = kahan_add(w, comp, update, cfg.fmt)
+    return s_new, c_new, m, v
+
+
 # ---------------------------------------------------------------------------
 # head.py restatement
 

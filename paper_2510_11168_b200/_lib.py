@@ -74,6 +74,8 @@ _SIGNATURES = {
     "xmc_kahan_sgd_step": ([Grid, _P, _P, _P, _I64, _F32, _F32, _I32, _U64, _U64, _U64, _P, _P, _P],
                            _I32),
     "xmc_cast_rn": ([_P, _P, _I64, _I32, _P, _P], _I32),
+    "xmc_kahan_adamw_step": ([Grid, _P, _P, _P, _P, _P, _I64, _F32, ctypes.c_double, ctypes.c_double, _F32, _F32,
+                              _I64, _P], _I32),
     "xmc_profile_enable": ([_I32], _I32),
     "xmc_profile_read": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)], _I32),

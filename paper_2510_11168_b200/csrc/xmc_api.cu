@@ -1533,6 +1533,7 @@ static int32_t* scratch_status() {
 static xmc_status status_to_error(int32_t s) {
   if (s & ST_NONFINITE_X) return fail(XMC_ERR_NONFINITE, "non-finite input to rounding operation");
   if (s & ST_NONFINITE_GRAD) return fail(XMC_ERR_NONFINITE, "non-finite gradient entry");
+  if (s & ST_NONFINITE_MOMENTS) return fail(XMC_ERR_NONFINITE, "non-finite optimizer moments");
   return XMC_OK;
 }
 
@@ -1609,6 +1610,85 @@ extern "C" xmc_status xmc_kahan_sgd_step(xmc_grid g, float* w, float* comp, cons
                                          const uint64_t* index, int32_t* status, void* stream) {
   if (!comp) return fail(XMC_ERR_ARG, "null compensation buffer");
   return sgd_common(g, w, comp, grad, n, lr, wd, rounding, seed, step, tensor_id, index, status, stream);
+}
+
+// kahan_adamw_step (optimizers.py:112-137) elementwise, every operation an
+// explicitly rounded fp32 op in the reference's (numpy's) order; kahan_add
+// formats.py:246-263 with RTN onto the grid.  write = 0: only flag non-finite
+// moments / updates (the reference raises before the parameter changes).
+struct AdamWArgs {
+  float lr, b1, b2, omb1, omb2, eps, wd, bc1, bc2;
+};
+__device__ __forceinline__ void adamw_elem(const AdamWArgs& a, float g, float m, float v, float s, float& m1, float& v1,
+                                           float& upd) {
+  m1 = __fadd_rn(__fmul_rn(a.b1, m), __fmul_rn(a.omb1, g));
+  v1 = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(__fmul_rn(a.omb2, g), g));
+  const float mhat = __fdiv_rn(m1, a.bc1);
+  const float vhat = __fdiv_rn(v1, a.bc2);
+  const float den = __fadd_rn(__fsqrt_rn(vhat), a.eps);
+  upd = __fmul_rn(-a.lr, __fadd_rn(__fdiv_rn(mhat, den), __fmul_rn(a.wd, s)));
+}
+__global__ void adamw_kernel(GridFmt f, bool working_precision, AdamWArgs a, float* __restrict__ w,
+                             float* __restrict__ comp, float* __restrict__ m, float* __restrict__ v,
+                             const float* __restrict__ grad, int64_t n, int write, int32_t* status) {
+  if (write && *status != 0) return;
+  bool bad_mom = false, bad_upd = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float s = w[i];
+    float m1, v1, upd;
+    adamw_elem(a, grad[i], m[i], v[i], s, m1, v1, upd);
+    if (!write) {
+      bad_mom |= !isfinite(m1) || !isfinite(v1);
+      bad_upd |= !isfinite(upd);
+      continue;
+    }
+    m[i] = m1;
+    v[i] = v1;
+    if (working_precision) {
+      w[i] = __fadd_rn(s, upd);
+      continue;
+    }
+    const float c = comp[i];
+    const float y = __fsub_rn(upd, c);
+    const float t = grid_round_nearest(f, __fadd_rn(s, y));
+    comp[i] = __fsub_rn(__fsub_rn(t, s), y);
+    w[i] = t;
+  }
+  if (bad_mom) atomicOr(status, ST_NONFINITE_MOMENTS);
+  if (bad_upd) atomicOr(status, ST_NONFINITE_X);
+}
+
+extern "C" xmc_status xmc_kahan_adamw_step(xmc_grid g, float* w, float* comp, float* m, float* v, const float* grad,
+                                           int64_t n, float lr, double beta1, double beta2, float eps, float wd,
+                                           int64_t t, void* stream) {
+  xmc_status s;
+  const GridFmt f = grid_from(g, &s);
+  XMC_TRY(s);
+  if (!w || !comp || !m || !v || !grad) return fail(XMC_ERR_ARG, "null argument");
+  if (!(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0))
+    return fail(XMC_ERR_ARG, "betas must lie in [0, 1)");
+  if (!(eps > 0.0f)) return fail(XMC_ERR_ARG, "eps must be positive");
+  if (t < 1) return fail(XMC_ERR_ARG, "step index t must be >= 1");
+  if (n <= 0) return XMC_OK;
+  AdamWArgs a;
+  a.lr = lr;
+  a.b1 = static_cast<float>(beta1);   // np.float32(cfg.beta1)
+  a.b2 = static_cast<float>(beta2);
+  a.omb1 = 1.0f - a.b1;   // np.float32(1) - b1: fp32 subtraction
+  a.omb2 = 1.0f - a.b2;
+  a.eps = eps;
+  a.wd = wd;
+  // np.float32(1.0 - beta ** t): double, then one rounding to fp32
+  a.bc1 = static_cast<float>(1.0 - std::pow(beta1, static_cast<double>(t)));
+  a.bc2 = static_cast<float>(1.0 - std::pow(beta2, static_cast<double>(t)));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int32_t* status = scratch_status();
+  CUDA_TRY(cudaMemsetAsync(status, 0, 4, st));
+  const bool wp = g.exp_bits == 8 && g.man_bits == 23;
+  adamw_kernel<<<ew_blocks(n), 256, 0, st>>>(f, wp, a, w, comp, m, v, grad, n, 0, status);
+  adamw_kernel<<<ew_blocks(n), 256, 0, st>>>(f, wp, a, w, comp, m, v, grad, n, 1, status);
+  CUDA_TRY(cudaGetLastError());
+  return finish_elementwise(status, st);
 }
 
 __global__ void cast_kernel(const float* __restrict__ x, void* __restrict__ out, int64_t n, int fmt, int32_t* status) {

@@ -38,6 +38,7 @@ enum StatusBits : int32_t {
   ST_NONFINITE_GRAD = 4,
   ST_LABEL_OUTSIDE = 8,
   ST_CAPACITY = 16,
+  ST_NONFINITE_MOMENTS = 32,
 };
 
 struct BwdParams {
@@ -98,9 +99,16 @@ struct BwdCfg {
 #ifndef XMC_BWD_KST
 #define XMC_BWD_KST 6
 #endif
-  static constexpr int kOutTiles = EB == 1 ? XMC_BWD_OUT : 0;   // W_new staging tiles (0 = in place)
-  static constexpr bool kOutBuf = kOutTiles > 0;
-  static constexpr int kWStages = EB == 1 ? XMC_BWD_WST : 3;
+#ifndef XMC_BWD_STG
+#define XMC_BWD_STG 0
+#endif
+  // kDirect: W_new goes straight from registers to HBM (st.global, 32 B per
+  // thread and row) instead of smem staging + TMA store, saving 32 KB of smem
+  // traffic per tile; the W slot is then released as soon as W_old is read
+  static constexpr bool kDirect = EB == 1 && XMC_BWD_STG;
+  static constexpr int kOutTiles = kDirect ? 0 : (EB == 1 ? XMC_BWD_OUT : 0);   // W_new staging tiles (0 = in place)
+  static constexpr bool kOutBuf = kOutTiles > 0 || kDirect;
+  static constexpr int kWStages = EB == 1 ? (kDirect ? 5 : XMC_BWD_WST) : 3;
   static constexpr int kOutBytes = kOutTiles * kWBytes;
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
   static constexpr int kKStages = EB == 1 ? XMC_BWD_KST : 4;
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int h = 0; h < CE * 2; ++h) craw[h] = krow ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
         }
-        if constexpr (FAST && EB == 1 && CE == 0 && C::kOutTiles == 2) {
+        if constexpr (FAST && EB == 1 && CE == 0 && (C::kOutTiles == 2 || C::kDirect)) {
           // production path: everything independent of dW (Philox words,
           // W_old decoded and scaled by 1 - lr wd) is computed and pinned in
           // registers BEFORE the dW wait, so it overlaps the MMAs
@@ -715,17 +723,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
             pk8[k] = cvt_e4m3x4_rs(u[3], u[2], u[1], u[0], rw[k]);
           }
-          uint8_t* ot = out_s + (ot_flip & 1) * C::kWBytes;
-          ++ot_flip;
-          const uint32_t ot_s = smem_u32(ot);
-          sts128(ot_s + w_chunk_off<EB>(row, c0, 0), make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]));
-          sts128(ot_s + w_chunk_off<EB>(row, c0, 1), make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]));
-          fence_proxy_async_smem();
-          if (storer && prev_ws >= 0) bulk_wait_read<0>();
-          named_bar_sync(1 + q, 128);
-          if (storer) {
-            tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
-            bulk_commit();
+          if constexpr (C::kDirect) {
+            if (grow < p.rows) {
+              uint4* dst = reinterpret_cast<uint4*>(p.W + grow * p.d + j * 128 + c0);
+              st_global_v4_hint(dst, make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]), pol_w_out);
+              st_global_v4_hint(dst + 1, make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]), pol_w_out);
+            }
+          } else {
+            uint8_t* ot = out_s + (ot_flip & 1) * C::kWBytes;
+            ++ot_flip;
+            const uint32_t ot_s = smem_u32(ot);
+            sts128(ot_s + w_chunk_off<EB>(row, c0, 0), make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]));
+            sts128(ot_s + w_chunk_off<EB>(row, c0, 1), make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]));
+            fence_proxy_async_smem();
+            if (storer && prev_ws >= 0) bulk_wait_read<0>();
+            named_bar_sync(1 + q, 128);
+            if (storer) {
+              tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
+              bulk_commit();
+            }
           }
           if (tracer) trace_ev(p.trace, it, 7);
           prev_ws = ws;
@@ -760,6 +776,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           w_update_pack_kahan<EB, CE>(p, p.rounding, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
         } else {
           w_update_pack<EB>(p, p.rounding, acc, w, rw, flat0, out);
+        }
+        if constexpr (C::kDirect) {
+          if (grow < p.rows) {
+            uint4* dst = reinterpret_cast<uint4*>(p.W + (grow * p.d + j * 128 + c0) * EB);
+#pragma unroll
+            for (int h = 0; h < C::kChunks16; ++h) st_global_v4_hint(dst + h, out[h], pol_w_out);
+          }
+          prev_ws = ws;
+          if (++ws == WS) { ws = 0; wph ^= 1; }
+          if (++ds == 2) { ds = 0; dph ^= 1; }
+          continue;
         }
         // W_new into a swizzled smem tile (the staging tile, or in place once
         // the grad_X MMAs have read W_old), then one TMA store per 32-row slab

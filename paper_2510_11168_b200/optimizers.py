@@ -86,3 +86,60 @@ def kahan_sgd_step(w: torch.Tensor, comp: torch.Tensor, grad, cfg: SgdSrConfig, 
         cfg.weight_decay, rmode, rng.seed, step & (2**64 - 1), tensor_id & (2**64 - 1),
         _lib.ptr(idx), None, _lib.stream_ptr()))
     return w, comp
+
+
+@dataclass
+class KahanAdamWConfig:
+    """optimizers.py:77-91 (same fields and validation)."""
+    lr: float
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+    fmt: FloatFormat = field(default_factory=lambda: FP32)
+
+    def __post_init__(self):
+        if not (0.0 <= self.beta1 < 1.0 and 0.0 <= self.beta2 < 1.0):
+            raise ValueError("betas must lie in [0, 1)")
+        if self.eps <= 0:
+            raise ValueError("eps must be positive")
+
+
+class KahanAdamWParam:
+    """One parameter tensor with its compensation buffer and moments
+    (optimizers.py:93-109), as float32 CUDA tensors: ``sum`` holds on-grid
+    values, ``comp`` the Kahan compensation, ``m`` / ``v`` the moments."""
+
+    def __init__(self, sum_: torch.Tensor, comp: torch.Tensor, m: torch.Tensor, v: torch.Tensor):
+        for t in (sum_, comp, m, v):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+                raise ValueError("parameter state must be contiguous float32 CUDA tensors")
+            if t.shape != sum_.shape:
+                raise ValueError("parameter state shapes differ")
+        self.sum, self.comp, self.m, self.v = sum_, comp, m, v
+
+    @classmethod
+    def from_values(cls, values, fmt: FloatFormat) -> "KahanAdamWParam":
+        from .formats import round_nearest
+        vals = round_nearest(fmt, _f32_cuda(values).clone())
+        return cls(vals, torch.zeros_like(vals), torch.zeros_like(vals), torch.zeros_like(vals))
+
+    @property
+    def values(self) -> torch.Tensor:
+        return self.sum
+
+
+def kahan_adamw_step(param: KahanAdamWParam, grad, cfg: KahanAdamWConfig, t: int, lr: float | None = None) -> None:
+    """In-place AdamW step with Kahan-compensated parameter accumulation
+    (optimizers.py:112-137; kahan_add formats.py:246-263), bit-exact with the
+    reference.  ``lr`` overrides cfg.lr (warmup schedules).  Raises ValueError
+    on non-finite moments or updates, leaving the state unchanged."""
+    if t < 1:
+        raise ValueError("step index t must be >= 1")
+    g = _f32_cuda(grad)
+    if tuple(g.shape) != tuple(param.values.shape):
+        raise ValueError("gradient shape mismatch")
+    _lib.check(_lib.load().xmc_kahan_adamw_step(
+        cfg.fmt.grid(), param.sum.data_ptr(), param.comp.data_ptr(), param.m.data_ptr(), param.v.data_ptr(),
+        g.data_ptr(), param.sum.numel(), float(cfg.lr if lr is None else lr), float(cfg.beta1),
+        float(cfg.beta2), float(cfg.eps), float(cfg.weight_decay), int(t), _lib.stream_ptr()))

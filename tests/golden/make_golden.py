@@ -28,6 +28,26 @@ def main():
 
     out = {}
 
+    # -- optimizers.py:112-137 kahan_adamw_step (+ kahan_add formats.py:246-263):
+    # several steps on one parameter per format, with weight decay and an lr override
+    rs = np.random.default_rng(99)
+    for fname in ("bf16", "e4m3", "fp32"):
+        fmt = F.parse_format(fname) if hasattr(F, "parse_format") else getattr(F, fname.upper())
+        cfg = O.KahanAdamWConfig(lr=0.01, beta1=0.9, beta2=0.99, eps=1e-6, weight_decay=0.05, fmt=fmt)
+        w0 = (rs.standard_normal(4096) * 0.3).astype(np.float32)
+        param = O.KahanAdamWParam.from_values(w0, fmt)
+        out[f"adamw_{fname}_w0"] = param.values.copy()
+        grads = (rs.standard_normal((4, 4096)) * np.array([[1.0], [1e-3], [30.0], [1e-6]])).astype(np.float32)
+        out[f"adamw_{fname}_grads"] = grads
+        lrs = [None, 0.003, None, 0.02]
+        out[f"adamw_{fname}_lrs"] = np.array([np.nan if x is None else x for x in lrs])
+        for t, (g, lr) in enumerate(zip(grads, lrs), start=1):
+            O.kahan_adamw_step(param, g, cfg, t, lr=lr)
+            out[f"adamw_{fname}_w{t}"] = param.values.copy()
+            out[f"adamw_{fname}_c{t}"] = param.state.comp.copy()
+            out[f"adamw_{fname}_m{t}"] = param.m.copy()
+            out[f"adamw_{fname}_v{t}"] = param.v.copy()
+
     # -- rng.py:22-57: tags, base keys, bits, uniforms ----------------------
     tags = ["head.weights", "head.dropout", "", "encoder.w1"]
     out["rng_tag_names"] = np.array(tags)

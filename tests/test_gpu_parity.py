@@ -110,6 +110,33 @@ def test_sgd_rejects_nonfinite_grad_without_writing(xmc):
     assert torch.all(w == 1.0)
 
 
+@pytest.mark.parametrize("name", ["bf16", "e4m3", "fp32"])
+def test_kahan_adamw_bit_exact_vs_reference(xmc, name):
+    """kahan_adamw_step (optimizers.py:112-137) on the GPU reproduces the
+    reference's own four-step sequence (golden vectors) bit for bit: the
+    parameter, the Kahan compensation and both moments."""
+    fmt = xmc.parse_format(name)
+    cfg = xmc.KahanAdamWConfig(lr=0.01, beta1=0.9, beta2=0.99, eps=1e-6, weight_decay=0.05, fmt=fmt)
+    param = xmc.KahanAdamWParam.from_values(torch.from_numpy(GOLD[f"adamw_{name}_w0"]), fmt)
+    assert np.array_equal(bits(param.values), bits(GOLD[f"adamw_{name}_w0"]))
+    for t, (g, lr) in enumerate(zip(GOLD[f"adamw_{name}_grads"], GOLD[f"adamw_{name}_lrs"]), start=1):
+        xmc.kahan_adamw_step(param, torch.from_numpy(g), cfg, t, lr=None if np.isnan(lr) else float(lr))
+        for arr, key in ((param.sum, "w"), (param.comp, "c"), (param.m, "m"), (param.v, "v")):
+            assert np.array_equal(bits(arr), bits(GOLD[f"adamw_{name}_{key}{t}"])), (key, t)
+
+
+def test_kahan_adamw_rejects_nonfinite_without_writing(xmc):
+    cfg = xmc.KahanAdamWConfig(lr=0.01, fmt=xmc.BF16)
+    param = xmc.KahanAdamWParam.from_values(torch.ones(64), xmc.BF16)
+    g = torch.zeros(64)
+    g[5] = float("inf")
+    with pytest.raises(ValueError):
+        xmc.kahan_adamw_step(param, g, cfg, 1)
+    assert torch.all(param.sum == 1.0) and torch.all(param.m == 0) and torch.all(param.v == 0)
+    with pytest.raises(ValueError):
+        xmc.kahan_adamw_step(param, torch.zeros(64), cfg, 0)
+
+
 @pytest.mark.parametrize("rmode", ["nearest", "stochastic"])
 def test_kahan_sgd_matches_oracle(xmc, rmode):
     rs = np.random.default_rng(5)

@@ -144,3 +144,29 @@ def test_grid_bits_roundtrip():
         fmt = O.parse_format(name)
         v = O.round_nearest(fmt, np.random.default_rng(1).normal(size=1000).astype(np.float32))
         assert np.array_equal(_bits(O.decode_grid_bits(O.encode_grid_bits(v, fmt), fmt)), _bits(v))
+
+
+@pytest.mark.parametrize("name", ["bf16", "e4m3", "fp32"])
+def test_kahan_adamw_bit_exact(name):
+    """kahan_adamw_step (optimizers.py:112-137) over four steps, lr override on
+    steps 2 and 4: parameter, compensation and both moments bit-exact."""
+    fmt = O.parse_format(name)
+    cfg = O.KahanAdamWConfig(lr=0.01, beta1=0.9, beta2=0.99, eps=1e-6, weight_decay=0.05, fmt=fmt)
+    w = GOLD[f"adamw_{name}_w0"]
+    c = np.zeros_like(w)
+    m = np.zeros_like(w)
+    v = np.zeros_like(w)
+    for t, (g, lr) in enumerate(zip(GOLD[f"adamw_{name}_grads"], GOLD[f"adamw_{name}_lrs"]), start=1):
+        w, c, m, v = O.kahan_adamw_values(w, c, m, v, g, cfg, t, lr=None if np.isnan(lr) else float(lr))
+        for arr, key in ((w, "w"), (c, "c"), (m, "m"), (v, "v")):
+            assert np.array_equal(_bits(arr), _bits(GOLD[f"adamw_{name}_{key}{t}"])), (key, t)
+
+
+def test_kahan_adamw_config_validation():
+    with pytest.raises(ValueError):
+        O.KahanAdamWConfig(lr=0.1, beta1=1.0)
+    with pytest.raises(ValueError):
+        O.KahanAdamWConfig(lr=0.1, eps=0.0)
+    with pytest.raises(ValueError):
+        O.kahan_adamw_values(np.zeros(2, np.float32), np.zeros(2, np.float32), np.zeros(2, np.float32),
+                             np.zeros(2, np.float32), np.zeros(2, np.float32), O.KahanAdamWConfig(lr=0.1), 0)
