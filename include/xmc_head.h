@@ -120,6 +120,24 @@ xmc_status xmc_head_step_kahan(xmc_head_t h, void* W, void* comp, const float* X
                                const int32_t* pos_sample, const int32_t* pos_label, int64_t nnz,
                                const xmc_step_args* args, float* grad_x, float* stats, void* stream);
 
+/* Adam-style head (north_star: "the SGD or Adam-style update"): the chunk
+ * gradient dW of every weight goes through kahan_adamw_step
+ * (optimizers.py:112-137) -- fp32 moments m, v and an fp32 Kahan compensation
+ * comp, all [L_local][d] -- inside the fused backward epilogue instead of the
+ * SGD step.  beta1/beta2 are the config's Python floats (double) and t is the
+ * 1-based AdamW step; args supplies seed/step/tensor_id/dropout (lr, wd and
+ * rounding are taken from adam).  The handle needs comp_bytes 4 for every
+ * label.  Everything else is xmc_head_step. */
+typedef struct xmc_adamw_args {
+  float lr, weight_decay, eps, reserved;
+  double beta1, beta2;
+  int64_t t;
+} xmc_adamw_args;
+xmc_status xmc_head_step_adamw(xmc_head_t h, void* W, float* comp, float* m, float* v, const float* X,
+                               int32_t B, const int32_t* pos_sample, const int32_t* pos_label, int64_t nnz,
+                               const xmc_adamw_args* adam, const xmc_step_args* args, float* grad_x,
+                               float* stats, void* stream);
+
 /* Synchronise `stream` and report a latched device error (and clear it). */
 xmc_status xmc_head_check(xmc_head_t h, void* stream);
 

@@ -468,13 +468,19 @@ def input_gradient_accumulate(acc, G, head, chunk, rng, step):
     return acc
 
 
-def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None, comp_fmt=None):
+def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None, comp_fmt=None, adam=None):
     """Per 64-row block: scratch = G_rows @ Xq, then the SGD+rounding step
     keyed by the global flat index.  head.py:212-251 (rounding vectorised
     across the row block; see module docstring).  With ``comp`` (float32
     (n, d) array) the head-Kahan extension kahan_sgd_values is used for rows
     < n (n = L: every row; n < L: top-p% head-Kahan, on
-    frequency-sorted labels) and the plain SR step for the others."""
+    frequency-sorted labels) and the plain SR step for the others.
+
+    Adam-style head (north_star "SGD or Adam-style update"; no reference head
+    oracle exists, so this is the composition): with a KahanAdamWConfig and
+    ``adam = {"m": m, "v": v, "t": t, "lr": lr_or_None}`` (float32 (L, d)
+    moments, ``comp`` float32 (L, d)) every block's scratch goes through
+    kahan_adamw_values (optimizers.py:112-137) instead of the SGD step."""
     start, stop = chunk
     m = head.dim
     keep = np.float32(1.0 - head.dropout_p)
@@ -487,6 +493,11 @@ def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None, comp_fmt=
             if head.dropout_p > 0.0:
                 scratch = scratch * (dropout_mask(rng, step, head.dropout_p,
                                                   (r0, r1), m) / keep)
+            if isinstance(cfg, KahanAdamWConfig):
+                (head.values[r0:r1], comp[r0:r1], adam["m"][r0:r1], adam["v"][r0:r1]) = kahan_adamw_values(
+                    head.values[r0:r1], comp[r0:r1], adam["m"][r0:r1], adam["v"][r0:r1], scratch, cfg,
+                    adam["t"], adam.get("lr"))
+                continue
             idx = (np.arange(r0, r1, dtype=np.uint64)[:, None] * np.uint64(m)
                    + np.arange(m, dtype=np.uint64)[None, :])
             n_c = 0 if comp is None else min(max(comp.shape[0] - r0, 0), r1 - r0)
@@ -511,7 +522,7 @@ def quantize_g_operand(G, fmt):
 
 
 def head_update(head, X, sample_idx, label_idx, cfg, rng, step, comp=None,
-                probe=None, g_quant=False, comp_fmt=None):
+                probe=None, g_quant=False, comp_fmt=None, adam=None):
     """One head step over all chunks; returns grad_X (b, d).  head.py:254-298.
     ``g_quant=True`` applies quantize_g_operand to each chunk's G before the
     backward (the GPU's operand precision)."""
@@ -533,7 +544,7 @@ def head_update(head, X, sample_idx, label_idx, cfg, rng, step, comp=None,
         if g_quant:
             G = quantize_g_operand(G, head.fmt)
         input_gradient_accumulate(acc, G, head, chunk, rng, step)
-        fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp, comp_fmt)
+        fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp, comp_fmt, adam)
     return acc
 
 

@@ -45,6 +45,12 @@ class StepArgs(ctypes.Structure):
                 ("tensor_id", ctypes.c_uint64), ("dropout_p", ctypes.c_double)]
 
 
+class AdamWArgs(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_float), ("weight_decay", ctypes.c_float), ("eps", ctypes.c_float),
+                ("reserved", ctypes.c_float), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("t", ctypes.c_int64)]
+
+
 class Grid(ctypes.Structure):
     _fields_ = [("exp_bits", ctypes.c_int32), ("man_bits", ctypes.c_int32),
                 ("extended_range", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -74,6 +80,8 @@ _SIGNATURES = {
     "xmc_kahan_sgd_step": ([Grid, _P, _P, _P, _I64, _F32, _F32, _I32, _U64, _U64, _U64, _P, _P, _P],
                            _I32),
     "xmc_cast_rn": ([_P, _P, _I64, _I32, _P, _P], _I32),
+    "xmc_head_step_adamw": ([_P, _P, _P, _P, _P, _P, _I32, _P, _P, _I64, ctypes.POINTER(AdamWArgs),
+                             ctypes.POINTER(StepArgs), _P, _P, _P], _I32),
     "xmc_kahan_adamw_step": ([Grid, _P, _P, _P, _P, _P, _I64, _F32, ctypes.c_double, ctypes.c_double, _F32, _F32,
                               _I64, _P], _I32),
     "xmc_profile_enable": ([_I32], _I32),

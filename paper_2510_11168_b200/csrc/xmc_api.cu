@@ -226,6 +226,13 @@ struct xmc_head {
   int32_t* cand_l;     // [max_bp][4 num_sms][kTopK] (global labels)
   int R;               // bwd CTAs per d-tile
   int gcl;             // bwd G-sharing cluster size (TMA multicast across consecutive d-tiles)
+  // Adam-style head step in flight (xmc_head_step_adamw sets it for the call):
+  // moments at local row 0 and the kahan_adamw_step constants
+  struct {
+    float* m = nullptr;
+    float* v = nullptr;
+    float b1, b2, omb1, omb2, bc1, bc2, eps;
+  } adam;
   size_t l2_persist;   // persisting-L2 bytes granted for the G window (0 = off)
   size_t l2_window_max;
 };
@@ -1037,6 +1044,16 @@ static xmc_status launch_bwd_t(xmc_head* h, int R, const CUtensorMap& tw, const 
   ProfRec pr;
   prof_begin(1, st, &pr);
   const int ce = p.comp ? h->desc.comp_bytes : 0;
+  if (p.adam_m != nullptr) {
+    if constexpr (XR || EB == 2) {
+      cudaFuncSetAttribute(xmc_bwd_kernel<EB, XR, KC, 4, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           sm);
+      CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 4, false, true>, grid, kBwdThreads, sm, st, h, g_bytes, cluster,
+                         tw, tg, tx, tws, p));
+      prof_end(st, &pr);
+      return XMC_OK;
+    }
+  }
   if (ce == 2)
     CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 2>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx, tws,
                        p));
@@ -1098,6 +1115,17 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   static const int dbg = getenv("XMC_DEBUG_BWD") ? atoi(getenv("XMC_DEBUG_BWD")) : 0;
   p.debug = dbg;
   p.gcl = gcl;
+  if (h->adam.m && update) {
+    p.adam_m = h->adam.m + row0 * D;
+    p.adam_v = h->adam.v + row0 * D;
+    p.b1 = h->adam.b1;
+    p.b2 = h->adam.b2;
+    p.omb1 = h->adam.omb1;
+    p.omb2 = h->adam.omb2;
+    p.bc1 = h->adam.bc1;
+    p.bc2 = h->adam.bc2;
+    p.eps = h->adam.eps;
+  }
   static const int pf = getenv("XMC_BWD_PF") ? atoi(getenv("XMC_BWD_PF")) : 0;
   p.pf_dist = pf;
   static const int stg = getenv("XMC_BWD_STAGGER") ? atoi(getenv("XMC_BWD_STAGGER")) : 0;
@@ -1258,6 +1286,38 @@ extern "C" xmc_status xmc_head_step_kahan(xmc_head_t h, void* W, void* comp, con
     XMC_TRY(launch_bwd(h, W, comp, r0, rows, Bp, true, 0, 0, false, args, st, h->keep, dp.scale));
   }
   return reduce_gx(h, B, Bp, grad_x, false, st, dp.scale);
+}
+
+// Adam-style head step: head_update with the chunk gradient fed to
+// kahan_adamw_step (optimizers.py:112-137) in the fused backward epilogue.
+extern "C" xmc_status xmc_head_step_adamw(xmc_head_t h, void* W, float* comp, float* m, float* v, const float* X,
+                                          int32_t B, const int32_t* pos_sample, const int32_t* pos_label,
+                                          int64_t nnz, const xmc_adamw_args* adam, const xmc_step_args* args,
+                                          float* grad_x, float* stats, void* stream) {
+  if (!h || !comp || !m || !v || !adam || !args) return fail(XMC_ERR_ARG, "null argument");
+  if (h->desc.comp_bytes != 4 || h->comp_rows != h->desc.num_labels_local)
+    return fail(XMC_ERR_ARG, "the Adam-style head needs an fp32 compensation for every label (comp_bytes 4)");
+  if (!(adam->beta1 >= 0.0 && adam->beta1 < 1.0 && adam->beta2 >= 0.0 && adam->beta2 < 1.0))
+    return fail(XMC_ERR_ARG, "betas must lie in [0, 1)");
+  if (!(adam->eps > 0.0f)) return fail(XMC_ERR_ARG, "eps must be positive");
+  if (adam->t < 1) return fail(XMC_ERR_ARG, "step index t must be >= 1");
+  xmc_step_args a = *args;
+  a.lr = adam->lr;
+  a.weight_decay = adam->weight_decay;
+  a.rounding = 0;   // kahan_add rounds to nearest
+  h->adam.m = m;
+  h->adam.v = v;
+  h->adam.b1 = static_cast<float>(adam->beta1);
+  h->adam.b2 = static_cast<float>(adam->beta2);
+  h->adam.omb1 = 1.0f - h->adam.b1;
+  h->adam.omb2 = 1.0f - h->adam.b2;
+  h->adam.bc1 = static_cast<float>(1.0 - std::pow(adam->beta1, static_cast<double>(adam->t)));
+  h->adam.bc2 = static_cast<float>(1.0 - std::pow(adam->beta2, static_cast<double>(adam->t)));
+  h->adam.eps = adam->eps;
+  const xmc_status st = xmc_head_step_kahan(h, W, comp, X, B, pos_sample, pos_label, nnz, &a, grad_x, stats, stream);
+  h->adam.m = nullptr;
+  h->adam.v = nullptr;
+  return st;
 }
 
 // ---- streaming top-k scoring ------------------------------------

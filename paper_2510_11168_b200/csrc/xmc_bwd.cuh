@@ -69,6 +69,11 @@ struct BwdParams {
   int32_t gcl;           // CTAs (consecutive d-tiles of one label-tile row group) sharing each G tile
                          // through TMA multicast: 1 = every CTA loads G itself
   int32_t* status;
+  // Adam-style head (ADAMW instantiation): fp32 moments [rows][d] at the chunk
+  // base, comp (CE = 4) fp32, constants as kahan_adamw_step forms them
+  float* adam_m;
+  float* adam_v;
+  float b1, b2, omb1, omb2, bc1, bc2, eps;
   uint64_t* trace;       // measurement only (XMC_TRACE): clock64 per tile and event of CTA 0, [kTraceTiles][8]
 };
 
@@ -328,12 +333,84 @@ XMC_DEV void w_update_pack_kahan(const BwdParams& p, int rounding, const uint32_
 
 // FAST: the production specialisation (Philox SR, no dropout mask, no
 // measurement hooks, no G sharing) with every runtime mode switch folded away
-template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false>
+// Adam-style head update (kahan_adamw_step optimizers.py:112-137 with the
+// chunk gradient g = dW from TMEM, kahan_add formats.py:246-263 with RTN onto
+// the grid), 4 elements at a time: m, v, comp fp32 read and written from/to
+// HBM by the owning thread.  Every op explicitly rounded in the reference's
+// order, so given the same dW the result is the reference's bit for bit.
+template <int EB>
+XMC_DEV void w_update_pack_adamw(const BwdParams& p, const uint32_t (&acc)[32], const uint4 (&raw)[2 * EB],
+                                 int64_t eoff, bool row_ok, uint4 (&out)[2 * EB], uint64_t pol) {
+  uint32_t pk[8 * EB];
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    float w[4];
+    if constexpr (EB == 1) {
+      const uint32_t wv = word_of(raw, g);
+      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(wv & 0xFFFF));
+      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(wv >> 16));
+      w[0] = lo.x; w[1] = lo.y; w[2] = hi.x; w[3] = hi.y;
+    } else {
+      const uint32_t w0 = word_of(raw, 2 * g), w1 = word_of(raw, 2 * g + 1);
+      w[0] = __uint_as_float(w0 << 16); w[1] = __uint_as_float(w0 & 0xFFFF0000u);
+      w[2] = __uint_as_float(w1 << 16); w[3] = __uint_as_float(w1 & 0xFFFF0000u);
+    }
+    float4* mp = reinterpret_cast<float4*>(p.adam_m + eoff) + g;
+    float4* vp = reinterpret_cast<float4*>(p.adam_v + eoff) + g;
+    float4* cp = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.comp) + eoff) + g;
+    const float4 m4 = row_ok ? *mp : z4, v4 = row_ok ? *vp : z4, c4 = row_ok ? *cp : z4;
+    const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
+    const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+    float m1[4], v1[4], y[4], x[4], t[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float gg = __fmul_rn(__uint_as_float(acc[4 * g + e]), p.dw_scale);
+      m1[e] = __fadd_rn(__fmul_rn(p.b1, mm[e]), __fmul_rn(p.omb1, gg));
+      v1[e] = __fadd_rn(__fmul_rn(p.b2, vv[e]), __fmul_rn(__fmul_rn(p.omb2, gg), gg));
+      const float mhat = __fdiv_rn(m1[e], p.bc1);
+      const float vhat = __fdiv_rn(v1[e], p.bc2);
+      const float upd = __fmul_rn(-p.lr, __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), p.eps)),
+                                                  __fmul_rn(p.wd, w[e])));
+      y[e] = __fsub_rn(upd, cc[e]);
+      x[e] = __fadd_rn(w[e], y[e]);
+    }
+    if constexpr (EB == 1) {
+      const uint32_t w4 = cvt_e4m3x2_rn(x[1], x[0]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(x[3], x[2])) << 16);
+      pk[g] = w4;
+      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(w4 & 0xFFFF));
+      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(w4 >> 16));
+      t[0] = lo.x; t[1] = lo.y; t[2] = hi.x; t[3] = hi.y;
+    } else {
+      const uint32_t w0 = cvt_bf16x2_rn(x[1], x[0]), w1 = cvt_bf16x2_rn(x[3], x[2]);
+      pk[2 * g] = w0;
+      pk[2 * g + 1] = w1;
+      t[0] = __uint_as_float(w0 << 16); t[1] = __uint_as_float(w0 & 0xFFFF0000u);
+      t[2] = __uint_as_float(w1 << 16); t[3] = __uint_as_float(w1 & 0xFFFF0000u);
+    }
+    if (row_ok) {
+      st_global_v4_hint(mp, make_uint4(__float_as_uint(m1[0]), __float_as_uint(m1[1]), __float_as_uint(m1[2]),
+                                       __float_as_uint(m1[3])), pol);
+      st_global_v4_hint(vp, make_uint4(__float_as_uint(v1[0]), __float_as_uint(v1[1]), __float_as_uint(v1[2]),
+                                       __float_as_uint(v1[3])), pol);
+      float cn[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cn[e] = __fsub_rn(__fsub_rn(t[e], w[e]), y[e]);
+      st_global_v4_hint(cp, make_uint4(__float_as_uint(cn[0]), __float_as_uint(cn[1]), __float_as_uint(cn[2]),
+                                       __float_as_uint(cn[3])), pol);
+    }
+  }
+#pragma unroll
+  for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
+}
+
+template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false, bool ADAMW = false>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
                    const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
                    BwdParams p) {
   using C = BwdCfg<EB, XT_RES, KCMAX>;
+  static_assert(!ADAMW || (CE == 4 && !FAST), "the Adam-style head keeps an fp32 compensation");
   if constexpr (FAST) {
     p.debug = 0;
 #ifndef XMC_TRACE_FAST   // measurement builds keep the pipeline trace in the fast path
@@ -666,7 +743,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         uint4 craw[CE > 0 ? CE * 2 : 1];
         const bool krow = CE > 0 && grow < p.comp_rows;   // this row carries a compensation
-        if constexpr (CE > 0) {   // Kahan compensation of this thread's 32 elements (HBM)
+        if constexpr (CE > 0 && !ADAMW) {   // Kahan compensation of this thread's 32 elements (HBM)
           const uint4* csrc = reinterpret_cast<const uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE);
 #pragma unroll
           for (int h = 0; h < CE * 2; ++h) craw[h] = krow ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
@@ -771,7 +848,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             acc[k] = __float_as_uint(__uint_as_float(acc[k]) * (((km >> k) & 1u) ? p.drop_scale : 0.0f));
         }
         uint4 out[C::kChunks16];
-        if constexpr (CE > 0) {
+        if constexpr (ADAMW) {
+          w_update_pack_adamw<EB>(p, acc, raw, grow * p.d + j * 128 + c0, grow < p.rows, out, pol_w_out);
+        } else if constexpr (CE > 0) {
           uint4* cdst = krow ? reinterpret_cast<uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE) : nullptr;
           w_update_pack_kahan<EB, CE>(p, p.rounding, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
         } else {

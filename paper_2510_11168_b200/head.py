@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from .formats import FloatFormat, RoundingRng, parse_format, tensor_tag
-from .optimizers import SgdSrConfig
+from .optimizers import KahanAdamWConfig, SgdSrConfig
 
 __all__ = [
     "ChunkedHead", "BatchInput", "QuantizedMatrix", "partition", "canonical_pieces",
@@ -110,7 +110,7 @@ class ChunkedHead:
     def __init__(self, weights: QuantizedMatrix, num_chunks: int = 1, dropout_p: float = 0.0,
                  block_m: int = 64, block_n: int = 64, tensor_id: int = HEAD_WEIGHTS_TAG,
                  num_labels_global: int | None = None, label_offset: int = 0,
-                 kahan: str | None = None, kahan_labels: int | None = None):
+                 kahan: str | None = None, kahan_labels: int | None = None, adamw: bool = False):
         if num_chunks < 1:
             raise ValueError("num_chunks must be >= 1")
         if not (0.0 <= dropout_p < 1.0):
@@ -136,9 +136,17 @@ class ChunkedHead:
         self.kahan_labels = kahan_labels
         n_comp = weights.values.shape[0] if kahan_labels is None else max(
             0, min(weights.values.shape[0], kahan_labels - label_offset))
+        # Adam-style head (head_update with a KahanAdamWConfig): fp32 moments
+        # and an fp32 compensation for every label, as kahan_adamw_step keeps
+        if adamw:
+            if kahan not in (None, "fp32") or kahan_labels is not None:
+                raise ValueError("the Adam-style head keeps an fp32 compensation for every label")
+            kahan, n_comp = "fp32", weights.values.shape[0]
         self.comp = None if kahan is None else torch.zeros(
             (n_comp, weights.values.shape[1]), dtype=torch.bfloat16 if kahan == "bf16" else torch.float32,
             device=weights.values.device)
+        self.adam_m = torch.zeros_like(self.comp) if adamw else None
+        self.adam_v = torch.zeros_like(self.comp) if adamw else None
         self._handle = None
         self.last_stats = None
         self.collect_stats = False   # True: head_update also returns sum|G| in last_stats[0]
@@ -307,6 +315,8 @@ def head_update(head: ChunkedHead, batch: BatchInput, cfg: SgdSrConfig, rng: Rou
     and raises device-detected errors like the reference (non-finite X or
     gradient -> ValueError, bad sample index -> IndexError)."""
     _check_cfg(head, cfg)
+    if isinstance(cfg, KahanAdamWConfig) and head.adam_m is None:
+        raise ValueError("head_update with a KahanAdamWConfig needs ChunkedHead(..., adamw=True)")
     dev = head.weights.values.device
     X = _as_x(batch.X, head.dim)
     si = _as_idx(batch.sample_idx, dev)
@@ -329,14 +339,23 @@ def head_update(head: ChunkedHead, batch: BatchInput, cfg: SgdSrConfig, rng: Rou
             if head.last_stats is None or head.last_stats.device != dev:
                 head.last_stats = torch.zeros(2, dtype=torch.float32, device=dev)
             stats_ptr = head.last_stats.data_ptr()
-        args = _step_args(cfg, rng, step, head.tensor_id, head.dropout_p)
         lhs = []
         if tracker is not None:
             for s, e in head.chunks():
                 lhs.append(tracker.alloc("chunk_logits", "logits", (e - s) * b * 2))
-        _lib.check(_lib.load().xmc_head_step_kahan(
-            h.h, head.weights.values.data_ptr(), _lib.ptr(head.comp), X.data_ptr(), b, si.data_ptr(),
-            li.data_ptr(), si.numel(), ctypes.byref(args), gx.data_ptr(), stats_ptr, _lib.stream_ptr()))
+        if isinstance(cfg, KahanAdamWConfig):
+            # Adam-style head: t = step + 1 (head_update steps are 0-based)
+            args = _step_args(None, rng, step, head.tensor_id, head.dropout_p)
+            adam = _lib.AdamWArgs(cfg.lr, cfg.weight_decay, cfg.eps, 0.0, cfg.beta1, cfg.beta2, step + 1)
+            _lib.check(_lib.load().xmc_head_step_adamw(
+                h.h, head.weights.values.data_ptr(), head.comp.data_ptr(), head.adam_m.data_ptr(),
+                head.adam_v.data_ptr(), X.data_ptr(), b, si.data_ptr(), li.data_ptr(), si.numel(),
+                ctypes.byref(adam), ctypes.byref(args), gx.data_ptr(), stats_ptr, _lib.stream_ptr()))
+        else:
+            args = _step_args(cfg, rng, step, head.tensor_id, head.dropout_p)
+            _lib.check(_lib.load().xmc_head_step_kahan(
+                h.h, head.weights.values.data_ptr(), _lib.ptr(head.comp), X.data_ptr(), b, si.data_ptr(),
+                li.data_ptr(), si.numel(), ctypes.byref(args), gx.data_ptr(), stats_ptr, _lib.stream_ptr()))
         for lh in lhs:
             tracker.free(lh)
         if check:

@@ -519,6 +519,57 @@ def test_head_kahan_matches_oracle(xmc, fmt_name, kahan, rmode, n_comp):
     assert np.isfinite(c_gpu).all()
 
 
+@pytest.mark.parametrize("fmt_name,B,chunks", [("e4m3", 256, 2), ("bf16", 128, 3), ("bf16", 512, 1)])
+def test_head_adamw_matches_oracle(xmc, fmt_name, B, chunks):
+    """Adam-style head (north_star "SGD or Adam-style update"): every weight's
+    dW fed to kahan_adamw_step (optimizers.py:112-137) in the fused backward
+    epilogue, against the composed oracle on the same operand-precision G.
+    dW differs from numpy's in fp32 summation order only, so moments agree to
+    fp32 accumulation noise and >= 98 % of the weights bit for bit."""
+    L, d = 700, 256
+    fmt, W, X, si, li = _rand_problem(L, d, B, fmt_name, 71)
+    head = xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.parse_format(fmt_name), num_chunks=chunks,
+                                      adamw=True)
+    cfg = xmc.KahanAdamWConfig(lr=0.01, beta1=0.9, beta2=0.99, eps=1e-6, weight_decay=0.05,
+                               fmt=xmc.parse_format(fmt_name))
+    cfg_o = O.KahanAdamWConfig(lr=0.01, beta1=0.9, beta2=0.99, eps=1e-6, weight_decay=0.05, fmt=fmt)
+    oh = O.OracleHead(W.copy(), fmt, chunks)
+    comp = np.zeros((L, d), np.float32)
+    m = np.zeros((L, d), np.float32)
+    v = np.zeros((L, d), np.float32)
+    for step in range(3):
+        gx = xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(4), step)
+        gx_o = O.head_update(oh, X, si, li, cfg_o, O.RoundingRng(4), step, comp=comp, g_quant=True,
+                             adam={"m": m, "v": v, "t": step + 1})
+        dg = np.abs(gx.cpu().numpy() - gx_o)
+        assert dg.max() < 2e-3 and dg.mean() < 2e-5, (dg.max(), dg.mean())
+        got = head.weights.values.float().cpu().numpy()
+        assert np.mean(bits(got) == bits(oh.values)) > 0.98
+        # moments: fp32 accumulation noise everywhere; a G entry that rounds to
+        # the other operand-grid neighbour (2^-8 relative for bf16) moves one
+        # row of dW by ulp(G)|Xq|, so allow a 0.1 % tail
+        mg, vg = head.adam_m.cpu().numpy(), head.adam_v.cpu().numpy()
+        for got_, ref_ in ((mg, m), (vg, v)):
+            off = np.abs(got_ - ref_) > 1e-3 * np.abs(ref_) + 1e-4 * np.abs(ref_).max()
+            assert off.mean() < 1e-3, off.mean()
+        assert np.isfinite(head.comp.cpu().numpy()).all()
+        # resync so later steps compare like for like
+        head.weights.values.copy_(xmc.cast_native(torch.from_numpy(oh.values).cuda(), xmc.parse_format(fmt_name)))
+        for t_, a_ in ((head.comp, comp), (head.adam_m, m), (head.adam_v, v)):
+            t_.copy_(torch.from_numpy(a_).cuda())
+
+
+def test_head_adamw_requires_state(xmc):
+    W = np.zeros((300, 128), np.float32)
+    head = xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.BF16)
+    cfg = xmc.KahanAdamWConfig(lr=0.01, fmt=xmc.BF16)
+    with pytest.raises(ValueError):
+        xmc.head_update(head, xmc.BatchInput(np.zeros((4, 128), np.float32), np.zeros(0), np.zeros(0)), cfg,
+                        xmc.RoundingRng(0), 0)
+    with pytest.raises(ValueError):
+        xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.BF16, adamw=True, kahan="bf16")
+
+
 def test_kahan_rescues_small_updates(xmc):
     """test_formats.py:216-229 at head level: with a bf16 head and updates far
     below half an ulp, plain RTN never moves W, Kahan accumulates them."""
