@@ -44,7 +44,7 @@ typedef enum { XMC_FMT_FP32 = 0, XMC_FMT_BF16 = 1, XMC_FMT_FP16 = 2, XMC_FMT_E4M
 /* SgdSrConfig.rounding (optimizers.py:28-41).  SR_EXACT draws u from the
  * reference's splitmix64 keyed generator (rng.py:36-57) and compares in fp64
  * exactly like round_stochastic (formats.py:209-225): bit-identical decisions.
- * SR_FAST uses Philox4x32-10 bits with the hardware cvt.rs conversion. */
+ * SR_FAST uses Philox4x32-7 bits with the hardware cvt.rs conversion. */
 typedef enum { XMC_ROUND_NEAREST = 0, XMC_ROUND_SR_EXACT = 1, XMC_ROUND_SR_FAST = 2 } xmc_rounding;
 
 /* Head geometry: ChunkedHead (head.py:69-112) restricted to one rank's label

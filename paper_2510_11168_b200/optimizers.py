@@ -4,7 +4,7 @@
 (optimizers.py:28-41) and adds ``sr_impl``: the draw generator used when
 ``rounding == "stochastic"``.
 
-* ``"philox"`` (default, the fast product path): Philox4x32-10 random bits
+* ``"philox"`` (default, the fast product path): Philox4x32-7 random bits
   fed to the sm_100a hardware stochastic-rounding conversion (cvt.rs).  SR
   decisions match the reference in distribution (unbiased, same variance).
 * ``"splitmix64"``: the reference's own keyed generator (rng.py:36-57) and
