@@ -30,7 +30,14 @@
 namespace xmc {
 
 constexpr int kBwdEpiWarps = 16;
-constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32;
+// XMC_BWD_GPROD: a second producer warp (after the epilogue warps) owns the G
+// loads, so a G tile is requested as soon as its slots free up instead of
+// queueing behind the W-slot wait of the single producer
+#ifndef XMC_BWD_GPROD
+#define XMC_BWD_GPROD 0
+#endif
+constexpr int kBwdGWarp = 2 + kBwdEpiWarps;
+constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32 + (XMC_BWD_GPROD ? 32 : 0);
 
 enum StatusBits : int32_t {
   ST_NONFINITE_X = 1,
@@ -558,6 +565,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (lane == 0) trace_ev(p.trace, it, 1);
         continue;
       }
+      if (XMC_BWD_GPROD && XT_RES && p.gcl == 1 && p.kc_count <= KS) {
+        // split producers: this warp only streams W
+        if (lane == 0) mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
+        __syncwarp();
+        if (static_cast<int>(lane) < C::kWBoxes)
+          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws],
+                           j * 128 + static_cast<int>(lane) * C::kBoxK, tile * 128, pol_stream);
+        __syncwarp();
+        if (++ws == WS) { ws = 0; wph ^= 1; }
+        continue;
+      }
       if (p.gcl == 1 && p.kc_count <= KS) {
         // the tile's W boxes and all its G (+Xq^T) boxes as ONE warp-wide TMA
         // instruction (lane l = box l): a copy instruction costs its warp
@@ -698,6 +716,31 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (++ds == 2) { ds = 0; dph ^= 1; }
     }
     if (elect_one()) mma_commit(gx_full);
+    __syncwarp();
+  } else if (warp == kBwdGWarp) {
+    // ------------------------------------------------ G producer (GPROD)
+    if (XMC_BWD_GPROD && XT_RES && p.gcl == 1 && p.kc_count <= KS) {
+      const uint32_t lane = lane_id();
+      const uint64_t pol_keep = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_last();
+      int ks = 0;
+      uint32_t kph = 0;
+      for (int it = 0; it < ntl; ++it) {
+        const int tile = tile_at(it);
+        for (int kc = 0; kc < p.kc_count; ++kc) {
+          const int kk = (ks + kc) % KS;
+          mbar_wait(&k_empty[kk], kph ^ (ks + kc >= KS ? 0u : 1u));
+        }
+        if (lane == 0)
+          for (int kc = 0; kc < p.kc_count; ++kc) mbar_arrive_expect_tx(&k_full[(ks + kc) % KS], C::kKSlot);
+        __syncwarp();
+        if (static_cast<int>(lane) < p.kc_count)
+          tma_load_2d_hint(k_s + ((ks + lane) % KS) * C::kKSlot, &tm_g, &k_full[(ks + lane) % KS],
+                           static_cast<int>(lane) * C::kBoxK, tile * 128, pol_keep);
+        __syncwarp();
+        for (int q = 0; q < p.kc_count; ++q)
+          if (++ks == KS) { ks = 0; kph ^= 1; }
+      }
+    }
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
