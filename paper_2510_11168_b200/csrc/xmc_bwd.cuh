@@ -36,8 +36,15 @@ constexpr int kBwdEpiWarps = 16;
 #ifndef XMC_BWD_GPROD
 #define XMC_BWD_GPROD 0
 #endif
+// XMC_BWD_PFW: the extra warp is an L2 prefetcher instead: it runs pf_dist
+// tiles ahead of the producer (paced by a shared progress counter) and pulls
+// the tile's W box and G boxes into L2 with ONE warp-wide prefetch
+// instruction, so the producer's TMA loads hit L2
+#ifndef XMC_BWD_PFW
+#define XMC_BWD_PFW 0
+#endif
 constexpr int kBwdGWarp = 2 + kBwdEpiWarps;
-constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32 + (XMC_BWD_GPROD ? 32 : 0);
+constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32 + ((XMC_BWD_GPROD || XMC_BWD_PFW) ? 32 : 0);
 
 enum StatusBits : int32_t {
   ST_NONFINITE_X = 1,
@@ -447,6 +454,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* xt_full = t_empty + 2;
   uint64_t* gx_full = xt_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gx_full + 1);
+  volatile int32_t* prod_progress = reinterpret_cast<volatile int32_t*>(tmem_slot + 1);   // PFW pacing
 
   const uint32_t warp = warp_id_sync();
   const int j = blockIdx.x % p.dtiles;
@@ -479,6 +487,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_init(xt_full, 1);
     mbar_init(gx_full, 1);
+    *reinterpret_cast<volatile int32_t*>(reinterpret_cast<uint32_t*>(gx_full + 1) + 1) = -1;
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -534,6 +543,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (p.pf_dist > 0) prefetch(tile + p.pf_dist * R);
       mbar_wait(&w_empty[ws], wph ^ 1);
       if (lane == 0) trace_ev(p.trace, it, 0);
+      if (XMC_BWD_PFW && lane == 0) *prod_progress = it;
       if (XT_RES && p.gcl > 1 && p.kc_count <= KS) {
         // G shared over the cluster: this CTA's 32-row G pieces (piece id
         // kc*4+qq, owner id mod gcl) multicast to every CTA of the cluster in
@@ -717,6 +727,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     if (elect_one()) mma_commit(gx_full);
     __syncwarp();
+  } else if (XMC_BWD_PFW && warp == kBwdGWarp) {
+    // ------------------------------------------------ L2 prefetcher (PFW)
+    const int lane = static_cast<int>(lane_id());
+    const int D = p.pf_dist > 0 ? p.pf_dist : 4;
+    for (int it = 0; it < ntl; ++it) {
+      const int tgt = it + D;
+      if (tgt >= ntl) break;
+      // pace: tile `it` has been issued by the producer
+      while (*prod_progress < it) __nanosleep(64);
+      const int tile = tile_at(tgt);
+      // lanes [0, kWBoxes): this CTA's W boxes; then G box kc by the CTA whose
+      // d-tile j == kc mod dtiles (one prefetch per G box per row group)
+      const int gk = lane - C::kWBoxes;
+      const bool is_w = lane < C::kWBoxes;
+      const bool act = is_w || (gk >= 0 && gk < p.kc_count && (gk % p.dtiles) == j);
+      if (act) {
+        if (is_w) tma_prefetch_2d(&tm_w, j * 128 + lane * C::kBoxK, tile * 128);
+        else tma_prefetch_2d(&tm_g, gk * C::kBoxK, tile * 128);
+      }
+      __syncwarp();
+    }
   } else if (warp == kBwdGWarp) {
     // ------------------------------------------------ G producer (GPROD)
     if (XMC_BWD_GPROD && XT_RES && p.gcl == 1 && p.kc_count <= KS) {
