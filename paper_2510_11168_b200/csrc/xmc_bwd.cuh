@@ -43,8 +43,20 @@ constexpr int kBwdEpiWarps = 16;
 #ifndef XMC_BWD_PFW
 #define XMC_BWD_PFW 0
 #endif
+// XMC_BWD_NPROD: producer warps (warp 0 and warps 2 + kBwdEpiWarps ...).  A
+// bulk-tensor copy instruction holds its warp until the data is nearly in
+// (~700 cycles from L2, ~1,300+ from DRAM per instruction, tools/probe_ring.cu),
+// so one producer warp keeps only one tile in flight however deep the rings
+// are; NPROD warps take the tiles round-robin (issue order kept by a shared
+// sequence counter) and keep NPROD tiles in flight.
+#ifndef XMC_BWD_NPROD
+#define XMC_BWD_NPROD 1
+#endif
+constexpr int kBwdNProd = XMC_BWD_NPROD;
 constexpr int kBwdGWarp = 2 + kBwdEpiWarps;
-constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32 + ((XMC_BWD_GPROD || XMC_BWD_PFW) ? 32 : 0);
+constexpr int kBwdThreads =
+    64 + kBwdEpiWarps * 32 + ((XMC_BWD_GPROD || XMC_BWD_PFW) ? 32 : 0) + (kBwdNProd - 1) * 32;
+static_assert(!(kBwdNProd > 1 && (XMC_BWD_GPROD || XMC_BWD_PFW)), "one role for the extra warps");
 
 enum StatusBits : int32_t {
   ST_NONFINITE_X = 1,
@@ -501,7 +513,60 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t tmem_gx = tmem_base + 256;   // cols [256, 512): grad_X^T partial
   // cols [0,128) and [128,256): the two dW buffers
 
-  if (warp == 0) {
+  // multi-warp producers (batched path: resident Xq^T, no G sharing, whole
+  // G tiles in contiguous ring slots)
+  const bool mprod = kBwdNProd > 1 && XT_RES && p.gcl == 1 && p.kc_count <= KS && KS % p.kc_count == 0 &&
+                     p.pf_dist == 0;
+  const int pidx = warp == 0 ? 0 : static_cast<int>(warp) - (kBwdGWarp - 1);   // producer index
+  if (mprod && (warp == 0 || (warp >= kBwdGWarp && warp < kBwdGWarp + kBwdNProd - 1))) {
+    // ------------------------------------------------- producers (multi)
+    const int lane = static_cast<int>(lane_id());
+    const uint64_t pol_stream = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_first();
+    const uint64_t pol_keep = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_last();
+    if (pidx == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(xt_full, p.kc_count * C::kBox);
+      __syncwarp();
+      if (lane < p.kc_count)
+        tma_load_2d_hint(xt_s + lane * C::kBox, &tm_xt, xt_full, lane * C::kBoxK, j * 128, pol_keep);
+      __syncwarp();
+    }
+    for (int it = pidx; it < ntl; it += kBwdNProd) {
+      const int tile = tile_at(it);
+      // issue order: the previous tile's producer has claimed its slots
+      if (lane == 0)
+        while (*prod_progress != it - 1) __nanosleep(20);
+      __syncwarp();
+      const int ws = it % WS;
+      const uint32_t wlap = static_cast<uint32_t>(it / WS);
+      const int g0 = (it * p.kc_count) % KS;
+      const uint32_t glap = static_cast<uint32_t>((it * p.kc_count) / KS);
+      mbar_wait(&w_empty[ws], (wlap & 1u) ^ 1u);
+      for (int kc = 0; kc < p.kc_count; ++kc) mbar_wait(&k_empty[g0 + kc], (glap & 1u) ^ 1u);
+      if (lane == 0) {
+        trace_ev(p.trace, it, 0);
+        mbar_arrive_expect_tx(&w_full[ws], (p.debug & 32) ? 0 : C::kWBytes);
+        for (int kc = 0; kc < p.kc_count; ++kc)
+          mbar_arrive_expect_tx(&k_full[g0 + kc], (p.debug & 16) ? 0 : C::kKSlot);
+        __threadfence_block();
+        *prod_progress = it;
+      }
+      __syncwarp();
+      const int gl = lane - C::kWBoxes;
+      const bool is_w = lane < C::kWBoxes;
+      const bool active = is_w || (gl >= 0 && gl < p.kc_count);
+      const bool skip = (p.debug & 16) ? !is_w : ((p.debug & 32) ? is_w : false);
+      if (active && !skip) {
+        if (is_w)
+          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kBoxK,
+                           tile * 128, pol_stream);
+        else
+          tma_load_2d_hint(k_s + (g0 + gl) * C::kKSlot, &tm_g, &k_full[g0 + gl], gl * C::kBoxK, tile * 128,
+                           pol_keep);
+      }
+      __syncwarp();
+      if (lane == 0) trace_ev(p.trace, it, 1);
+    }
+  } else if (warp == 0) {
     // ------------------------------------------------------------ producer
     // Boxes are dealt round-robin over the 32 lanes: one thread's bulk-tensor
     // copies are served one after another (~550 cycles per 16-KB box,
@@ -748,6 +813,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       __syncwarp();
     }
+  } else if (warp >= kBwdGWarp && kBwdNProd > 1) {
+    // spare producer warp (multi-producer path not applicable): idle
   } else if (warp == kBwdGWarp) {
     // ------------------------------------------------ G producer (GPROD)
     if (XMC_BWD_GPROD && XT_RES && p.gcl == 1 && p.kc_count <= KS) {

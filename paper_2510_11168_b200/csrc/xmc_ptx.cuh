@@ -88,6 +88,10 @@ XMC_DEV void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t
 
 XMC_DEV void tma_load_2d_hint(void* dst, const CUtensorMap* m, uint64_t* bar, int32_t c0,
                               int32_t c1, uint64_t policy) {
+#ifdef XMC_NO_HINT   // measurement: plain loads without the L2 cache-policy operand
+  tma_load_2d(dst, m, bar, c0, c1);
+  return;
+#endif
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
