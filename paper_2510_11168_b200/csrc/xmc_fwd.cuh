@@ -74,7 +74,12 @@ struct FwdCfg {
   static constexpr int kMmaN = BN > 256 ? 256 : BN;
   // epilogue: 4 warps per TMEM sub-partition for wide tiles, 2 otherwise
   static constexpr int kEpiWarps = BN >= 256 ? 16 : 8;
-  static constexpr int kThreads = 64 + kEpiWarps * 32;
+#ifndef XMC_FWD_NPROD
+#define XMC_FWD_NPROD 1
+#endif
+  // producer warps: warp 0 and warps 2 + kEpiWarps ... (stage groups round-robin)
+  static constexpr int kNProd = XMC_FWD_NPROD;
+  static constexpr int kThreads = 64 + kEpiWarps * 32 + (kNProd - 1) * 32;
   static constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
   static constexpr int kChunks = kColsPerWarp / 32;
 };
@@ -122,6 +127,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
   uint64_t* tempty = tfull + C::kAccStages;       // [kAccStages] (leader's counts both CTAs)
   uint64_t* xfull = tempty + C::kAccStages;       // resident Xq landed (leader's counts both CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 1);
+  volatile int32_t* issue_seq = reinterpret_cast<volatile int32_t*>(tmem_slot + 1);   // multi-producer order
 
   const uint32_t warp = warp_id_sync();
   const int kc_count = p.d / C::kBoxK;
@@ -144,6 +150,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       mbar_init(&tempty[a], (PAIR ? 2 : 1) * C::kEpiWarps);
     }
     mbar_init(xfull, 2);
+    *reinterpret_cast<volatile int32_t*>(reinterpret_cast<uint32_t*>(xfull + 1) + 1) = -1;
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -156,7 +163,8 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  const int pidx = warp == 0 ? 0 : static_cast<int>(warp) - (1 + C::kEpiWarps);
+  if (warp == 0 || (C::kNProd > 1 && static_cast<int>(warp) >= 2 + C::kEpiWarps)) {
     // ------------------------------------------------------------ producer
     // A bulk-tensor copy instruction occupies its warp for ~max(585, 1.8 x
     // 128-B lines of ALL its lanes) cycles (tools/probe_tma.cu), so one box
@@ -169,7 +177,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     const int lane = static_cast<int>(lane_id());
     const uint64_t pol_w = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
-    if constexpr (XRES) {
+    if (XRES && pidx == 0) {
       // this CTA's Xq rows, every K-chunk, once: one warp-wide instruction
       if (lane == 0) {
         if (leader) mbar_arrive_expect_tx(xfull, 2 * kc_count * C::kXBytes);
@@ -183,8 +191,15 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     }
     const int my_units = unit0 < num_units ? (num_units - unit0 + ustride - 1) / ustride : 0;
     const int total = my_units * kc_count;   // stages this CTA fills
-    for (int n0 = 0; n0 < total; n0 += kIPB) {
+    for (int n0 = pidx * kIPB; n0 < total; n0 += kIPB * C::kNProd) {
       const int cnt = min(kIPB, total - n0);
+      const int grp = n0 / kIPB;
+      // several producers: keep the issue order (group grp after grp - 1)
+      if (C::kNProd > 1) {
+        if (lane == 0)
+          while (*issue_seq != grp - 1) __nanosleep(20);
+        __syncwarp();
+      }
       // stage / phase of item n: ring position n mod kStages, lap n / kStages
       for (int i = 0; i < cnt; ++i) {
         const int n = n0 + i;
@@ -207,6 +222,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
         }
       }
       __syncwarp();
+      if (C::kNProd > 1 && lane == 0) *issue_seq = grp;
       const CUtensorMap* m = b == 0 ? &tm_w : &tm_x;
       uint8_t* dst = b == 0 ? sb : sb + C::kWBytes + (b - 1) * C::kXBoxRows * 128;
       const int32_t c1 = b == 0 ? tile * 128 : static_cast<int>(rank) * C::kXRows + (b - 1) * C::kXBoxRows;
