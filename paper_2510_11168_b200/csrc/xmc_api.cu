@@ -226,6 +226,8 @@ struct xmc_head {
   int32_t* cand_l;     // [max_bp][4 num_sms][kTopK] (global labels)
   int R;               // bwd CTAs per d-tile
   int gcl;             // bwd G-sharing cluster size (TMA multicast across consecutive d-tiles)
+  int fwd_max_clusters;   // co-resident CTA pairs of the forward (grid cap, PDL safety)
+  bool pdl_ok;
   // Adam-style head step in flight (xmc_head_step_adamw sets it for the call):
   // moments at local row 0 and the kahan_adamw_step constants
   struct {
@@ -481,6 +483,27 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   set_bwd_attr<2, true, 4>();
   set_bwd_attr<2, false, 8>();
   choose_bwd_cluster(h);
+  // forward pairs: how many CTA pairs are co-resident.  The persistent grid is
+  // capped there, which keeps every primary of a PDL chain fully resident.
+  {
+    h->fwd_max_clusters = h->num_sms / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * (h->num_sms / 2));
+    cfg.blockDim = dim3(FwdCfg<1, 256, true, true>::kThreads);
+    cfg.dynamicSmemBytes = FwdCfg<1, 256, true, true>::kSmemBytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    h->pdl_ok = cudaOccupancyMaxActiveClusters(&n, xmc_fwd_kernel<1, 256, true, false, true>, &cfg) == cudaSuccess &&
+                n > 0;
+    cudaGetLastError();
+    if (h->pdl_ok) h->fwd_max_clusters = std::min(h->fwd_max_clusters, n);
+  }
   *out = h;
   return XMC_OK;
 }
@@ -551,6 +574,7 @@ __device__ __forceinline__ int64_t pos_tile(const PosGeom& g, int64_t local, int
 __global__ void __launch_bounds__(1024) gx_reduce_kernel(const float* __restrict__ ws, int R, int d, int ld, int B,
                                                          float scale, int accumulate, float* __restrict__ gx) {
   __shared__ float tile[32][33];
+  griddep_wait();   // launched as a PDL dependent of the last backward
   const int c = blockIdx.x * 32 + threadIdx.y, s = blockIdx.y * 32 + threadIdx.x;
   float acc = 0.f;
   if (s < B) {
@@ -931,6 +955,16 @@ static xmc_status launch_x_prep(xmc_head* h, const float* X, int B, int Bp, cuda
   return XMC_OK;
 }
 
+// Programmatic dependent launch for the fwd / bwd / reduce kernels: a kernel's
+// CTAs start (barriers, TMEM, tensor maps) on SMs the previous kernel's CTAs
+// vacate and then wait in griddepcontrol.wait.  Safe because every primary is
+// persistent and fully co-resident (forward clusters capped at the measured
+// co-resident count).  XMC_PDL=0 disables.
+static bool pdl_enabled(const xmc_head* h) {
+  static const bool env_on = !getenv("XMC_PDL") || atoi(getenv("XMC_PDL")) != 0;
+  return env_on && h->pdl_ok;
+}
+
 // Launch with an optional L2 access-policy window: the chunk's G buffer is
 // marked persisting so it survives in L2 between the forward that writes it
 // and the backward that re-reads it once per d-tile, while W streams past.
@@ -942,7 +976,7 @@ static cudaError_t launch_ex(void (*kernel)(KArgs...), int grid, int block, int 
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   cfg.attrs = at;
   cfg.numAttrs = 0;
   if (h->l2_persist > 0 && win_bytes > 0) {
@@ -963,6 +997,11 @@ static cudaError_t launch_ex(void (*kernel)(KArgs...), int grid, int block, int 
     at[cfg.numAttrs].val.clusterDim.z = 1;
     ++cfg.numAttrs;
   }
+  if (pdl_enabled(h)) {
+    at[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++cfg.numAttrs;
+  }
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -977,7 +1016,7 @@ static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtenso
                                cudaStream_t st) {
   using C = FwdCfg<EB, BN, PAIR>;
   int grid = static_cast<int>(std::min<int64_t>(h->num_sms, PAIR ? 2 * ((p.num_tiles + 1) / 2) : p.num_tiles));
-  if (PAIR) grid &= ~1;
+  if (PAIR) grid = std::min(grid & ~1, 2 * h->fwd_max_clusters);
   if (grid <= 0) return XMC_OK;
   ProfRec pr;
   prof_begin(0, st, &pr);
@@ -1022,6 +1061,8 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t r
   p.stats = stats;
   p.logit_scale = logit_scale;
   p.status = h->status;
+  static const int fdbg = getenv("XMC_DEBUG_FWD") ? atoi(getenv("XMC_DEBUG_FWD")) : 0;
+  p.debug = fdbg;
   if (eb == 1) {
     if (Bp == 128) return pair ? launch_fwd_t<1, 128, true>(h, tw, tx, p, st) : launch_fwd_t<1, 128, false>(h, tw, tx, p, st);
     if (Bp == 256) return pair ? launch_fwd_t<1, 256, true>(h, tw, tx, p, st) : launch_fwd_t<1, 256, false>(h, tw, tx, p, st);
@@ -1171,8 +1212,17 @@ static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumul
                             float scale = 1.0f) {
   const int D = h->desc.dim;
   dim3 g(D / 32, (Bp + 31) / 32), b(32, 32);
-  gx_reduce_kernel<<<g, b, 0, st>>>(h->gx_ws, h->R, D, Bp, B, (h->eb == 1 ? (1.0f / 256.0f) : 1.0f) * scale,
-                                     accumulate ? 1 : 0, acc);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled(h) ? 1 : 0;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, gx_reduce_kernel, static_cast<const float*>(h->gx_ws), h->R, D, Bp, B,
+                              (h->eb == 1 ? (1.0f / 256.0f) : 1.0f) * scale, accumulate ? 1 : 0, acc));
   CUDA_TRY(cudaGetLastError());
   return XMC_OK;
 }

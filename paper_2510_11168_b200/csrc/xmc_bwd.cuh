@@ -448,7 +448,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
   constexpr int WS = C::kWStages;
   constexpr int KS = C::kKStages;
-  if (*p.status != 0) return;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -518,7 +517,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const bool mprod = kBwdNProd > 1 && XT_RES && p.gcl == 1 && p.kc_count <= KS && KS % p.kc_count == 0 &&
                      p.pf_dist == 0;
   const int pidx = warp == 0 ? 0 : static_cast<int>(warp) - (kBwdGWarp - 1);   // producer index
-  if (mprod && (warp == 0 || (warp >= kBwdGWarp && warp < kBwdGWarp + kBwdNProd - 1))) {
+  // PDL: the prologue above (barriers, TMEM, tensor maps) overlapped the
+  // previous kernel's tail; from here on its outputs are read
+  griddep_wait();
+  griddep_launch_dependents();
+  // a latched error of an earlier kernel of the step turns this one into a no-op
+  const bool aborted = *p.status != 0;
+  if (aborted) {
+  } else if (mprod && (warp == 0 || (warp >= kBwdGWarp && warp < kBwdGWarp + kBwdNProd - 1))) {
     // ------------------------------------------------- producers (multi)
     const int lane = static_cast<int>(lane_id());
     const uint64_t pol_stream = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_first();

@@ -25,6 +25,10 @@
 // e4m3 code (0 / 256) as the unclipped value.  bf16 G keeps MUFU rcp + clip.
 #pragma once
 
+#ifndef XMC_FWD_MUFU_RCP
+#define XMC_FWD_MUFU_RCP 0
+#endif
+
 #include "xmc_ptx.cuh"
 #include "xmc_round.cuh"
 
@@ -49,6 +53,7 @@ struct FwdParams {
   int32_t* cand_l;
   int64_t label0;            // global label of local row 0 of this launch
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
+  int32_t debug;             // measurement only (XMC_DEBUG_FWD): 1 skip the G epilogue math and stores
 };
 
 // XRES: this CTA's Xq rows stay resident in shared memory for the whole
@@ -113,7 +118,6 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
   using C = FwdCfg<EB, BN, PAIR, XRES>;
   static_assert(!PAIR || BN <= 256, "paired tiles use one N <= 256 accumulator");
   static_assert(!XRES || PAIR, "resident Xq is a CTA-pair layout (one 128-B box per K-chunk)");
-  if (*p.status != 0) return;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -164,7 +168,14 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int pidx = warp == 0 ? 0 : static_cast<int>(warp) - (1 + C::kEpiWarps);
-  if (warp == 0 || (C::kNProd > 1 && static_cast<int>(warp) >= 2 + C::kEpiWarps)) {
+  // PDL: the prologue above (barriers, TMEM, tensor maps) overlapped the
+  // previous kernel's tail; from here on its outputs are read
+  griddep_wait();
+  griddep_launch_dependents();
+  // a latched error of an earlier kernel of the step turns this one into a no-op
+  const bool aborted = *p.status != 0;
+  if (aborted) {
+  } else if (warp == 0 || (C::kNProd > 1 && static_cast<int>(warp) >= 2 + C::kEpiWarps)) {
     // ------------------------------------------------------------ producer
     // A bulk-tensor copy instruction occupies its warp for ~max(585, 1.8 x
     // 128-B lines of ALL its lanes) cycles (tools/probe_tma.cu), so one box
@@ -430,7 +441,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
       const bool row_ok = grow < p.rows;
 #pragma unroll 1
-      for (int cc = 0; cc < C::kChunks; ++cc) {
+      for (int cc = 0; cc < ((p.debug & 1) ? 0 : C::kChunks); ++cc) {
         const int col0 = grp * C::kColsPerWarp + cc * 32;
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, r);
@@ -450,6 +461,15 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
           // g256 = 256 sigmoid(z) = 1 / y, y = 2^-8 (1 + 2^(-z log2 e))
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
+#if XMC_FWD_MUFU_RCP   // measurement: reciprocal on MUFU instead of the FMA-pipe Newton steps
+            {
+              const float ea = fminf(fast_ex2(__uint_as_float(r[j]) * zk), 1.2676506e30f);
+              const float eb = fminf(fast_ex2(__uint_as_float(r[j + 1]) * zk), 1.2676506e30f);
+              g[j] = fast_rcp(fmaf(ea, 0.00390625f, 0.00390625f));
+              g[j + 1] = fast_rcp(fmaf(eb, 0.00390625f, 0.00390625f));
+              continue;
+            }
+#endif
             // e clamped to 2^100 keeps y finite (g then rounds to 0 in e4m3)
             const float ea = fminf(fast_ex2(__uint_as_float(r[j]) * zk), 1.2676506e30f);
             const float eb = fminf(fast_ex2(__uint_as_float(r[j + 1]) * zk), 1.2676506e30f);

@@ -155,6 +155,13 @@ XMC_DEV uint64_t policy_evict_last() {
   return p;
 }
 
+// ------------------------------------------------- programmatic dependent launch
+// wait until the previous grid in the stream completed and its writes are
+// visible (no-op when the kernel was not launched as a dependent)
+XMC_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the next grid in the stream launch (its CTAs take SMs as ours exit)
+XMC_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ tcgen05
 template <uint32_t kCols>
 XMC_DEV void tmem_alloc(uint32_t* dst_smem) {
