@@ -339,7 +339,7 @@ static void set_bwd_attr() {
 static uint64_t* trace_buf() {
   static uint64_t* buf = nullptr;
   static const bool on = getenv("XMC_TRACE") && atoi(getenv("XMC_TRACE")) != 0;
-  if (on && !buf && cudaMalloc(&buf, kTraceTiles * 8 * 8) != cudaSuccess) {
+  if (on && !buf && cudaMalloc(&buf, kTraceTiles * 16 * 8) != cudaSuccess) {
     cudaGetLastError();
     buf = nullptr;
   }
@@ -349,7 +349,7 @@ static uint64_t* trace_buf() {
 extern "C" xmc_status xmc_trace_read(uint64_t* out, int64_t n) {
   uint64_t* b = trace_buf();
   if (!b) return fail(XMC_ERR_ARG, "tracing is off (set XMC_TRACE=1)");
-  CUDA_TRY(cudaMemcpy(out, b, std::min<int64_t>(n, kTraceTiles * 8) * 8, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(out, b, std::min<int64_t>(n, kTraceTiles * 16) * 8, cudaMemcpyDeviceToHost));
   return XMC_OK;
 }
 

@@ -100,13 +100,13 @@ struct BwdParams {
   float* adam_m;
   float* adam_v;
   float b1, b2, omb1, omb2, bc1, bc2, eps;
-  uint64_t* trace;       // measurement only (XMC_TRACE): clock64 per tile and event of CTA 0, [kTraceTiles][8]
+  uint64_t* trace;       // measurement only (XMC_TRACE): clock64 per tile and event of CTA 0, [kTraceTiles][16]
 };
 
 constexpr int kTraceTiles = 512;
 // trace event e of local tile iteration i (CTA 0 only)
 XMC_DEV void trace_ev(uint64_t* tr, int i, int e) {
-  if (tr != nullptr && blockIdx.x == 0 && i < kTraceTiles) tr[i * 8 + e] = clock64();
+  if (tr != nullptr && blockIdx.x == 0 && i < kTraceTiles) tr[i * 16 + e] = clock64();
 }
 
 template <int EB, bool XT_RES, int KCMAX>
@@ -739,12 +739,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(&w_full[ws], wph);
       if (lane_id() == 0) trace_ev(p.trace, it, 2);
       mbar_wait(&t_empty[ds], dph ^ 1);
+      if (lane_id() == 0) trace_ev(p.trace, it, 8);
       tc_fence_after();
       const uint32_t w_addr = smem_u32(w_s + ws * C::kWBytes);
       const uint32_t d_dw = tmem_base + ds * 128;
       for (int kc = 0; kc < p.kc_count; ++kc) {
+        if (kc == 1 && lane_id() == 0) trace_ev(p.trace, it, 10);
         mbar_wait(&k_full[ks], kph);
         tc_fence_after();
+        if (kc == 0 && lane_id() == 0) trace_ev(p.trace, it, 9);
         if (kc == p.kc_count - 1 && lane_id() == 0) trace_ev(p.trace, it, 3);
         if (elect_one()) {
           const uint32_t g_addr = smem_u32(k_s + ks * C::kKSlot);

@@ -31,14 +31,15 @@ __global__ void __launch_bounds__(256, 1) stream(const __grid_constant__ CUtenso
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bars[16];
   // lanes_mode: producers are lanes 0..nprod-1 of warp 0 instead of one lane per warp
-  const bool lanes_mode = gridDim.y == 2;
-  const int nprod = lanes_mode ? 4 : blockDim.x / 32, w = lanes_mode ? (threadIdx.x & 31) : threadIdx.x / 32;
+  const bool lanes_mode = gridDim.y >= 2;
+  const int nprod = lanes_mode ? static_cast<int>(gridDim.y) : blockDim.x / 32,
+            w = lanes_mode ? (threadIdx.x & 31) : threadIdx.x / 32;
   if (threadIdx.x == 0) {
     for (int s = 0; s < 16; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
   }
   __syncthreads();
-  if (lanes_mode ? (threadIdx.x >= 4) : ((threadIdx.x & 31) != 0)) return;
+  if (lanes_mode ? (static_cast<int>(threadIdx.x) >= nprod) : ((threadIdx.x & 31) != 0)) return;
   if (blockIdx.y != 0) return;
   // warp w of nprod issues every nprod-th box into its own share of the stages
   stages /= nprod;
@@ -81,7 +82,22 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-int main() {
+int sweep(PFN_encodeTiled enc, uint8_t* buf, long long* clk, int sms);
+int main(int argc, char** argv) {
+  if (argc > 1) {
+    void* p0 = nullptr;
+    cudaDriverEntryPointQueryResult q0;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p0, cudaEnableDefault, &q0);
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, 0);
+    uint8_t* b;
+    cudaMalloc(&b, 2000000ll * 768);
+    cudaMemset(b, 0x11, 2000000ll * 768);
+    long long* c;
+    cudaMalloc(&c, n * 8);
+    cudaFuncSetAttribute(stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    return sweep(reinterpret_cast<PFN_encodeTiled>(p0), b, c, n);
+  }
   void* p = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
@@ -159,6 +175,39 @@ int main() {
     const double bytes = (double)iters * box_bytes;
     printf("%-70s stages %2d: %6.1f B/clk/SM, %6.2f TB/s chip %s\n", c.what, c.stages, bytes / mc,
            bytes * sms / (ms * 1e-3) / 1e12, e == cudaSuccess ? "" : cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+// in-flight sweep: per-SM bytes/clk for 1..16 concurrently issuing lanes with a
+// 12-deep ring of 16 KB boxes, on 1 SM and on all SMs, L2-resident and DRAM
+int sweep(PFN_encodeTiled enc, uint8_t* buf, long long* clk, int sms) {
+  for (int src = 0; src < 2; ++src) {
+    const int64_t rows = src == 0 ? 2000000 : 32768;
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {768, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {768};
+    cuuint32_t box[2] = {128, 128};
+    cuuint32_t es[2] = {1, 1};
+    enc(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    for (int g : {1, 16, 74, sms})
+      for (int lanes : {2, 4, 8, 12}) {
+        const int stages = 12, box_bytes = 16384;
+        const int iters = 4096;
+        const dim3 grid(g, lanes);
+        stream<<<grid, 32, stages * box_bytes + 1024>>>(tm, 0, 128, 6, stages, box_bytes, rows, iters / 8, clk);
+        stream<<<grid, 32, stages * box_bytes + 1024>>>(tm, 0, 128, 6, stages, box_bytes, rows, iters, clk);
+        cudaError_t e = cudaDeviceSynchronize();
+        long long hc[256];
+        cudaMemcpy(hc, clk, g * 8, cudaMemcpyDeviceToHost);
+        long long mc = 0;
+        for (int i = 0; i < g; ++i) mc = hc[i] > mc ? hc[i] : mc;
+        const double bytes = (double)(iters / lanes) * lanes * box_bytes;
+        printf("%-4s grid %3d lanes %2d (<= %3d KB in flight): %6.1f B/clk/SM, %6.2f TB/s chip-equiv %s\n",
+               src == 0 ? "DRAM" : "L2", g, lanes, lanes * 16, bytes / mc, bytes / mc * g * 1.9e9 / 1e12,
+               e == cudaSuccess ? "" : cudaGetErrorString(e));
+      }
   }
   return 0;
 }

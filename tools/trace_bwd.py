@@ -46,7 +46,7 @@ def main():
                                          acc.data_ptr() if gx else None, gx, upd,
                                          ctypes.byref(args) if upd else None, st()))
     torch.cuda.synchronize()
-    buf = np.zeros((512, 8), dtype=np.uint64)
+    buf = np.zeros((512, 16), dtype=np.uint64)
     _lib.check(lib.xmc_trace_read(buf.ctypes.data, buf.size))
     n = int((buf[:, 7] > 0).sum()) if upd else int((buf[:, 4] > 0).sum())
     t = buf[:n].astype(np.int64)
@@ -59,6 +59,10 @@ def main():
     print(f"  G latency  (issue->MMA saw)   {d(1, 3):7.0f}")
     print(f"  MMA w->lastG wait             {d(2, 3):7.0f}")
     print(f"  MMA issue span                {d(3, 4):7.0f}")
+    print(f"    MMA: W seen -> t_empty      {d(2, 8):7.0f}")
+    print(f"    MMA: t_empty -> G kc0 seen  {d(8, 9):7.0f}")
+    print(f"    MMA: kc0 dW MMAs issued     {d(9, 10):7.0f}")
+    print(f"    MMA: -> G kc1 seen          {d(10, 3):7.0f}")
     if upd:
         print(f"  epi: W seen -> dW seen        {d(5, 6):7.0f}")
         print(f"  epi: dW seen -> stored        {d(6, 7):7.0f}")
@@ -67,7 +71,7 @@ def main():
     print(f"  producer W issue lead over MMA {d(0, 4):7.0f}")
     np.set_printoptions(linewidth=200)
     print("rows 8..16 (relative cycles):")
-    print(t[8:16] - t[8, 0])
+    print((t[8:16] - t[8, 0])[:, :11])
 
 
 if __name__ == "__main__":
