@@ -1102,9 +1102,9 @@ static xmc_status launch_bwd_t(xmc_head* h, int R, const CUtensorMap& tw, const 
     CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 4>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx, tws,
                        p));
 #ifdef XMC_TRACE_FAST
-  else if (p.rounding == ROUND_SR_FAST && p.keep == nullptr && p.debug == 0 && p.pf_dist == 0)
+  else if (p.rounding == ROUND_SR_FAST && p.keep == nullptr && p.debug == 0)
 #else
-  else if (p.rounding == ROUND_SR_FAST && p.keep == nullptr && p.trace == nullptr && p.debug == 0 && p.pf_dist == 0)
+  else if (p.rounding == ROUND_SR_FAST && p.keep == nullptr && p.trace == nullptr && p.debug == 0)
 #endif
     CUDA_TRY(launch_ex(xmc_bwd_kernel<EB, XR, KC, 0, true>, grid, kBwdThreads, sm, st, h, g_bytes, cluster, tw, tg, tx,
                        tws, p));
@@ -1127,8 +1127,9 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   XMC_TRY(make_map(&tws, static_cast<uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 32));
   const int64_t tiles = cdiv(rows, 128);
   const int R = static_cast<int>(std::min<int64_t>(h->R, tiles));
-  // clusters span d-tiles of one row group, so every R keeps them on the same label tiles
-  const int gcl = h->gcl;
+  // clusters span d-tiles of one row group, so every R keeps them on the same
+  // label tiles; G sharing needs the resident-Xq^T layout (not bf16 batch 512)
+  const int gcl = (eb == 2 && Bp == 512) ? 1 : h->gcl;
   XMC_TRY(make_map(&tg, h->gbuf, eb, Bp, rows, Bp, gcl > 1 ? 32 : 128));
   XMC_TRY(make_map(&tx, h->xqt, eb, Bp, D, Bp, 128));
   BwdParams p{};
@@ -1167,10 +1168,6 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
     p.bc2 = h->adam.bc2;
     p.eps = h->adam.eps;
   }
-  static const int pf = getenv("XMC_BWD_PF") ? atoi(getenv("XMC_BWD_PF")) : 0;
-  p.pf_dist = pf;
-  static const int stg = getenv("XMC_BWD_STAGGER") ? atoi(getenv("XMC_BWD_STAGGER")) : 0;
-  p.stagger = stg;
   static const int poln = getenv("XMC_POL_NORMAL") ? atoi(getenv("XMC_POL_NORMAL")) : 0;
   p.pol_normal = poln;
   p.trace = trace_buf();

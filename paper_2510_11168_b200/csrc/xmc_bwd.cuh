@@ -30,33 +30,7 @@
 namespace xmc {
 
 constexpr int kBwdEpiWarps = 16;
-// XMC_BWD_GPROD: a second producer warp (after the epilogue warps) owns the G
-// loads, so a G tile is requested as soon as its slots free up instead of
-// queueing behind the W-slot wait of the single producer
-#ifndef XMC_BWD_GPROD
-#define XMC_BWD_GPROD 0
-#endif
-// XMC_BWD_PFW: the extra warp is an L2 prefetcher instead: it runs pf_dist
-// tiles ahead of the producer (paced by a shared progress counter) and pulls
-// the tile's W box and G boxes into L2 with ONE warp-wide prefetch
-// instruction, so the producer's TMA loads hit L2
-#ifndef XMC_BWD_PFW
-#define XMC_BWD_PFW 0
-#endif
-// XMC_BWD_NPROD: producer warps (warp 0 and warps 2 + kBwdEpiWarps ...).  A
-// bulk-tensor copy instruction holds its warp until the data is nearly in
-// (~700 cycles from L2, ~1,300+ from DRAM per instruction, tools/probe_ring.cu),
-// so one producer warp keeps only one tile in flight however deep the rings
-// are; NPROD warps take the tiles round-robin (issue order kept by a shared
-// sequence counter) and keep NPROD tiles in flight.
-#ifndef XMC_BWD_NPROD
-#define XMC_BWD_NPROD 1
-#endif
-constexpr int kBwdNProd = XMC_BWD_NPROD;
-constexpr int kBwdGWarp = 2 + kBwdEpiWarps;
-constexpr int kBwdThreads =
-    64 + kBwdEpiWarps * 32 + ((XMC_BWD_GPROD || XMC_BWD_PFW) ? 32 : 0) + (kBwdNProd - 1) * 32;
-static_assert(!(kBwdNProd > 1 && (XMC_BWD_GPROD || XMC_BWD_PFW)), "one role for the extra warps");
+constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32;
 
 enum StatusBits : int32_t {
   ST_NONFINITE_X = 1,
@@ -89,9 +63,7 @@ struct BwdParams {
   const uint32_t* keep;  // keyed dropout keep bits [rows][d / 32] (chunk-local) or null
   float drop_scale;      // f32(1) / f32(1 - p) applied to kept dW (head.py:239-242)
   int32_t debug;         // measurement only (XMC_DEBUG_BWD): 1 skip dW MMAs, 2 skip update epilogue
-  int32_t pf_dist;       // L2 prefetch distance in this CTA's tiles (0 = off)
-  int32_t stagger;
-  int32_t pol_normal;    // measurement: evict_normal for every load/store (L2-resident chunk experiments)       // d-tile j walks its tile list rotated by j*stagger (spreads G reads in time)
+  int32_t pol_normal;    // measurement: evict_normal for every load/store (L2-resident chunk experiments)
   int32_t gcl;           // CTAs (consecutive d-tiles of one label-tile row group) sharing each G tile
                          // through TMA multicast: 1 = every CTA loads G itself
   int32_t* status;
@@ -130,16 +102,9 @@ struct BwdCfg {
 #ifndef XMC_BWD_KST
 #define XMC_BWD_KST 6
 #endif
-#ifndef XMC_BWD_STG
-#define XMC_BWD_STG 0
-#endif
-  // kDirect: W_new goes straight from registers to HBM (st.global, 32 B per
-  // thread and row) instead of smem staging + TMA store, saving 32 KB of smem
-  // traffic per tile; the W slot is then released as soon as W_old is read
-  static constexpr bool kDirect = EB == 1 && XMC_BWD_STG;
-  static constexpr int kOutTiles = kDirect ? 0 : (EB == 1 ? XMC_BWD_OUT : 0);   // W_new staging tiles (0 = in place)
-  static constexpr bool kOutBuf = kOutTiles > 0 || kDirect;
-  static constexpr int kWStages = EB == 1 ? (kDirect ? 5 : XMC_BWD_WST) : 3;
+  static constexpr int kOutTiles = EB == 1 ? XMC_BWD_OUT : 0;   // W_new staging tiles (0 = in place)
+  static constexpr bool kOutBuf = kOutTiles > 0;
+  static constexpr int kWStages = EB == 1 ? XMC_BWD_WST : 3;
   static constexpr int kOutBytes = kOutTiles * kWBytes;
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
   static constexpr int kKStages = EB == 1 ? XMC_BWD_KST : 4;
@@ -444,7 +409,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #endif
     p.keep = nullptr;
     p.rounding = ROUND_SR_FAST;
-    p.pf_dist = 0;
   }
   constexpr int WS = C::kWStages;
   constexpr int KS = C::kKStages;
@@ -465,18 +429,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* xt_full = t_empty + 2;
   uint64_t* gx_full = xt_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gx_full + 1);
-  volatile int32_t* prod_progress = reinterpret_cast<volatile int32_t*>(tmem_slot + 1);   // PFW pacing
 
   const uint32_t warp = warp_id_sync();
   const int j = blockIdx.x % p.dtiles;
   const int R = gridDim.x / p.dtiles;
   const int r0 = blockIdx.x / p.dtiles;
   const bool do_gx = p.gx_kc_count > 0;
-  // this CTA's label tiles r0, r0+R, ... walked from a j-dependent rotation, so
-  // the d-tile CTAs of one row group do not all request a G tile at once
+  // this CTA's label tiles: r0, r0 + R, ... (the d-tile CTAs of a row group
+  // walk them in step, so each G tile is requested by all six at once)
   const int ntl = r0 < p.num_tiles ? (p.num_tiles - r0 + R - 1) / R : 0;
-  const int rot = ntl > 0 ? (j * p.stagger) % ntl : 0;
-  auto tile_at = [&](int k) { const int kk = k + rot; return r0 + (kk >= ntl ? kk - ntl : kk) * R; };
+  auto tile_at = [&](int k) { return r0 + k * R; };
 
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tm_w);
@@ -498,7 +460,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_init(xt_full, 1);
     mbar_init(gx_full, 1);
-    *reinterpret_cast<volatile int32_t*>(reinterpret_cast<uint32_t*>(gx_full + 1) + 1) = -1;
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -512,11 +473,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t tmem_gx = tmem_base + 256;   // cols [256, 512): grad_X^T partial
   // cols [0,128) and [128,256): the two dW buffers
 
-  // multi-warp producers (batched path: resident Xq^T, no G sharing, whole
-  // G tiles in contiguous ring slots)
-  const bool mprod = kBwdNProd > 1 && XT_RES && p.gcl == 1 && p.kc_count <= KS && KS % p.kc_count == 0 &&
-                     p.pf_dist == 0;
-  const int pidx = warp == 0 ? 0 : static_cast<int>(warp) - (kBwdGWarp - 1);   // producer index
   // PDL: the prologue above (barriers, TMEM, tensor maps) overlapped the
   // previous kernel's tail; from here on its outputs are read
   griddep_wait();
@@ -524,203 +480,96 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // a latched error of an earlier kernel of the step turns this one into a no-op
   const bool aborted = *p.status != 0;
   if (aborted) {
-  } else if (mprod && (warp == 0 || (warp >= kBwdGWarp && warp < kBwdGWarp + kBwdNProd - 1))) {
-    // ------------------------------------------------- producers (multi)
+  } else if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    // A bulk-tensor copy instruction holds its thread for ~max(585, 1.8 x
+    // 128-B lines of all its lanes) cycles (tools/probe_tma.cu), so a tile's
+    // boxes go out together as ONE warp-wide instruction, lane l = box l.
     const int lane = static_cast<int>(lane_id());
-    const uint64_t pol_stream = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_first();
-    const uint64_t pol_keep = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_last();
-    if (pidx == 0) {
+    // debug & 4 / pol_normal (measurement): evict_normal everywhere, so a
+    // chunk that fits in L2 stays there across repeated launches
+    const bool pn = (p.debug & 4) || p.pol_normal;
+    const uint64_t pol_stream = pn ? policy_evict_normal() : policy_evict_first();
+    const uint64_t pol_keep = pn ? policy_evict_normal() : policy_evict_last();
+    if constexpr (XT_RES) {
       if (lane == 0) mbar_arrive_expect_tx(xt_full, p.kc_count * C::kBox);
       __syncwarp();
       if (lane < p.kc_count)
         tma_load_2d_hint(xt_s + lane * C::kBox, &tm_xt, xt_full, lane * C::kBoxK, j * 128, pol_keep);
       __syncwarp();
     }
-    for (int it = pidx; it < ntl; it += kBwdNProd) {
-      const int tile = tile_at(it);
-      // issue order: the previous tile's producer has claimed its slots
-      if (lane == 0)
-        while (*prod_progress != it - 1) __nanosleep(20);
-      __syncwarp();
-      const int ws = it % WS;
-      const uint32_t wlap = static_cast<uint32_t>(it / WS);
-      const int g0 = (it * p.kc_count) % KS;
-      const uint32_t glap = static_cast<uint32_t>((it * p.kc_count) / KS);
-      mbar_wait(&w_empty[ws], (wlap & 1u) ^ 1u);
-      for (int kc = 0; kc < p.kc_count; ++kc) mbar_wait(&k_empty[g0 + kc], (glap & 1u) ^ 1u);
-      if (lane == 0) {
-        trace_ev(p.trace, it, 0);
-        mbar_arrive_expect_tx(&w_full[ws], (p.debug & 32) ? 0 : C::kWBytes);
-        for (int kc = 0; kc < p.kc_count; ++kc)
-          mbar_arrive_expect_tx(&k_full[g0 + kc], (p.debug & 16) ? 0 : C::kKSlot);
-        __threadfence_block();
-        *prod_progress = it;
-      }
-      __syncwarp();
-      const int gl = lane - C::kWBoxes;
-      const bool is_w = lane < C::kWBoxes;
-      const bool active = is_w || (gl >= 0 && gl < p.kc_count);
-      const bool skip = (p.debug & 16) ? !is_w : ((p.debug & 32) ? is_w : false);
-      if (active && !skip) {
-        if (is_w)
-          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kBoxK,
-                           tile * 128, pol_stream);
-        else
-          tma_load_2d_hint(k_s + (g0 + gl) * C::kKSlot, &tm_g, &k_full[g0 + gl], gl * C::kBoxK, tile * 128,
-                           pol_keep);
-      }
-      __syncwarp();
-      if (lane == 0) trace_ev(p.trace, it, 1);
-    }
-  } else if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    // Boxes are dealt round-robin over the 32 lanes: one thread's bulk-tensor
-    // copies are served one after another (~550 cycles per 16-KB box,
-    // tools/probe_tma.cu), which used to bound the whole pipeline.
-    const uint32_t lane = lane_id();
-    uint32_t nbox = 0;   // warp-uniform; box i belongs to lane i mod 32
-    auto mine = [&]() { return (nbox++ & 31u) == lane; };
-    // debug & 4 (measurement): evict_normal everywhere, so a chunk that fits
-    // in L2 stays there across repeated launches
-    const uint64_t pol_stream = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_first();
-    const uint64_t pol_keep = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_last();
-    if constexpr (XT_RES) {
-      if (lane == 0) mbar_arrive_expect_tx(xt_full, p.kc_count * C::kBox);
-      __syncwarp();
-      if (static_cast<int>(lane) < p.kc_count)
-        tma_load_2d_hint(xt_s + lane * C::kBox, &tm_xt, xt_full, static_cast<int>(lane) * C::kBoxK, j * 128, pol_keep);
-      __syncwarp();
-    }
     int ws = 0, ks = 0;
     uint32_t wph = 0, kph = 0;
     const int crank = p.gcl > 1 ? static_cast<int>(cluster_ctarank()) : 0;
     const uint16_t gmask = static_cast<uint16_t>((1u << p.gcl) - 1u);
-    // L2 prefetch of the tile pf_dist steps ahead: W[t, j] by its own CTA,
-    // G[t] split over the d-tile CTAs (box kc by CTA j == kc mod dtiles)
-    const int grows = p.gcl > 1 ? 32 : 128;
-    auto prefetch = [&](int t) {
-      if (t >= p.num_tiles) return;
-#pragma unroll
-      for (int b = 0; b < C::kWBoxes; ++b)
-        if (mine()) tma_prefetch_2d(&tm_w, j * 128 + b * C::kBoxK, t * 128);
-      for (int kc = j; kc < p.kc_count; kc += p.dtiles)
-        for (int rr = 0; rr < 128; rr += grows)
-          if (mine()) tma_prefetch_2d(&tm_g, kc * C::kBoxK, t * 128 + rr);
-    };
-    for (int i = 1; i < p.pf_dist; ++i) prefetch(r0 + i * R);
-    int it = 0;
-    for (; it < ntl; ++it) {
+    // the tile's G slots are consecutive ring slots when the ring holds whole tiles
+    const bool whole = p.kc_count <= KS && KS % p.kc_count == 0;
+    for (int it = 0; it < ntl; ++it) {
       const int tile = tile_at(it);
-      if (p.pf_dist > 0) prefetch(tile + p.pf_dist * R);
       mbar_wait(&w_empty[ws], wph ^ 1);
       if (lane == 0) trace_ev(p.trace, it, 0);
-      if (XMC_BWD_PFW && lane == 0) *prod_progress = it;
-      if (XT_RES && p.gcl > 1 && p.kc_count <= KS) {
-        // G shared over the cluster: this CTA's 32-row G pieces (piece id
-        // kc*4+qq, owner id mod gcl) multicast to every CTA of the cluster in
-        // one warp-wide instruction, its own W box in another
-        for (int kc = 0; kc < p.kc_count; ++kc) {
-          const int kk = (ks + kc) % KS;
-          mbar_wait(&k_empty[kk], kph ^ (ks + kc >= KS ? 0u : 1u));
-        }
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
-          for (int kc = 0; kc < p.kc_count; ++kc) mbar_arrive_expect_tx(&k_full[(ks + kc) % KS], C::kKSlot);
-        }
-        __syncwarp();
-        if (static_cast<int>(lane) < C::kWBoxes)
-          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws],
-                           j * 128 + static_cast<int>(lane) * C::kBoxK, tile * 128, pol_stream);
-        // lane l issues this CTA's l-th piece
-        const int piece = crank + static_cast<int>(lane) * p.gcl;
-        if (piece < 4 * p.kc_count) {
-          const int kc = piece >> 2, qq = piece & 3;
-          const int kk = (ks + kc) % KS;
-          tma_load_2d_mc(k_s + kk * C::kKSlot + qq * 32 * 128, &tm_g, &k_full[kk], kc * C::kBoxK,
-                         tile * 128 + qq * 32, gmask, pol_keep);
-        }
-        __syncwarp();
-        if (++ws == WS) { ws = 0; wph ^= 1; }
-        for (int q = 0; q < p.kc_count; ++q)
-          if (++ks == KS) { ks = 0; kph ^= 1; }
-        if (lane == 0) trace_ev(p.trace, it, 1);
-        continue;
-      }
-      if (XMC_BWD_GPROD && XT_RES && p.gcl == 1 && p.kc_count <= KS) {
-        // split producers: this warp only streams W
-        if (lane == 0) mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
-        __syncwarp();
-        if (static_cast<int>(lane) < C::kWBoxes)
-          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws],
-                           j * 128 + static_cast<int>(lane) * C::kBoxK, tile * 128, pol_stream);
-        __syncwarp();
-        if (++ws == WS) { ws = 0; wph ^= 1; }
-        continue;
-      }
-      if (p.gcl == 1 && p.kc_count <= KS) {
-        // the tile's W boxes and all its G (+Xq^T) boxes as ONE warp-wide TMA
-        // instruction (lane l = box l): a copy instruction costs its warp
-        // ~max(585, 1.8 x lines) cycles however few lanes it carries
-        for (int kc = 0; kc < p.kc_count; ++kc) {
-          const int kk = (ks + kc) % KS;
-          mbar_wait(&k_empty[kk], kph ^ (ks + kc >= KS ? 0u : 1u));
-        }
+      if (whole) {
+        for (int kc = 0; kc < p.kc_count; ++kc) mbar_wait(&k_empty[ks + kc], kph ^ 1);
         if (lane == 0) {
           mbar_arrive_expect_tx(&w_full[ws], (p.debug & 32) ? 0 : C::kWBytes);
           for (int kc = 0; kc < p.kc_count; ++kc)
-            mbar_arrive_expect_tx(&k_full[(ks + kc) % KS], (p.debug & 16) ? 0 : C::kKSlot);
+            mbar_arrive_expect_tx(&k_full[ks + kc], (p.debug & 16) ? 0 : C::kKSlot);
         }
         __syncwarp();
-        constexpr int kGB = XT_RES ? 1 : 2;   // boxes per G slot
-        const int gl = static_cast<int>(lane) - C::kWBoxes;
-        const int kc = gl / kGB, sub = gl % kGB;
-        const int kk = (ks + kc) % KS;
-        const bool is_w = static_cast<int>(lane) < C::kWBoxes;
-        const bool active = is_w || (gl >= 0 && kc < p.kc_count);
-        const CUtensorMap* m = is_w ? &tm_w : (sub == 0 ? &tm_g : &tm_xt);
-        uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + kk * C::kKSlot + sub * C::kBox;
-        uint64_t* bar = is_w ? &w_full[ws] : &k_full[kk];
-        const int32_t c0 = is_w ? j * 128 + static_cast<int>(lane) * C::kBoxK : kc * C::kBoxK;
-        const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? tile * 128 : j * 128);
-        const uint64_t pol = is_w ? pol_stream : pol_keep;
-        // measurement: debug & 16 skips the G loads, debug & 32 the W loads
-        // (the barrier then completes through a plain arrive + tx of 0)
-        const bool skip = (p.debug & 16) ? !is_w : ((p.debug & 32) ? is_w : false);
-        if (active && !skip) tma_load_2d_hint(dst, m, bar, c0, c1, pol);
-        __syncwarp();
-        if (++ws == WS) { ws = 0; wph ^= 1; }
-        for (int q = 0; q < p.kc_count; ++q)
-          if (++ks == KS) { ks = 0; kph ^= 1; }
-        if (lane == 0) trace_ev(p.trace, it, 1);
-        continue;
-      }
-      if (lane == 0) mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
-#pragma unroll
-      for (int b = 0; b < C::kWBoxes; ++b)
-        if (mine())
-          tma_load_2d_hint(w_s + ws * C::kWBytes + b * C::kBox, &tm_w, &w_full[ws], j * 128 + b * C::kBoxK,
-                           tile * 128, pol_stream);
-      if (++ws == WS) { ws = 0; wph ^= 1; }
-      for (int kc = 0; kc < p.kc_count; ++kc) {
-        mbar_wait(&k_empty[ks], kph ^ 1);
-        uint8_t* slot = k_s + ks * C::kKSlot;
-        if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], C::kKSlot);
-        // G sharing: the slot's 128 G rows as four 32-row boxes, spread over
-        // the cluster's CTAs; each lands in every CTA of the cluster (the
-        // slot is free everywhere: k_empty counts every CTA's commit)
         if (p.gcl == 1) {
-          if (mine()) tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
+          // W boxes, then per k-chunk the G box (+ the Xq^T box when not resident)
+          constexpr int kGB = XT_RES ? 1 : 2;
+          const int gl = lane - C::kWBoxes;
+          const int kc = gl / kGB, sub = gl % kGB;
+          const bool is_w = lane < C::kWBoxes;
+          const bool active = is_w || (gl >= 0 && kc < p.kc_count);
+          const CUtensorMap* m = is_w ? &tm_w : (sub == 0 ? &tm_g : &tm_xt);
+          uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + (ks + kc) * C::kKSlot + sub * C::kBox;
+          uint64_t* bar = is_w ? &w_full[ws] : &k_full[ks + kc];
+          const int32_t c0 = is_w ? j * 128 + lane * C::kBoxK : kc * C::kBoxK;
+          const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? tile * 128 : j * 128);
+          // measurement: debug & 16 skips the G loads, debug & 32 the W loads
+          // (the barrier then completes through the arrive with a tx of 0)
+          const bool skip = (p.debug & 16) ? !is_w : ((p.debug & 32) ? is_w : false);
+          if (active && !skip) tma_load_2d_hint(dst, m, bar, c0, c1, is_w ? pol_stream : pol_keep);
         } else {
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq)
-            if ((kc * 4 + qq) % p.gcl == crank && mine())
-              tma_load_2d_mc(slot + qq * 32 * 128, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128 + qq * 32, gmask,
-                             pol_keep);
+          // G shared over the cluster (measured neutral, XMC_BWD_GCL): this
+          // CTA's 32-row G pieces (id kc*4+qq, owner id mod gcl) multicast to
+          // every CTA of the cluster; k_empty counts every CTA's commit
+          if (lane < C::kWBoxes)
+            tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kBoxK,
+                             tile * 128, pol_stream);
+          const int piece = crank + lane * p.gcl;
+          if (XT_RES && piece < 4 * p.kc_count) {
+            const int kc = piece >> 2, qq = piece & 3;
+            tma_load_2d_mc(k_s + (ks + kc) * C::kKSlot + qq * 32 * 128, &tm_g, &k_full[ks + kc], kc * C::kBoxK,
+                           tile * 128 + qq * 32, gmask, pol_keep);
+          }
         }
-        if constexpr (!XT_RES)
-          if (mine()) tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], kc * C::kBoxK, j * 128, pol_keep);
-        if (++ks == KS) { ks = 0; kph ^= 1; }
+        __syncwarp();
+        ks += p.kc_count;
+        if (ks == KS) { ks = 0; kph ^= 1; }
+      } else {
+        // more k-chunks than ring slots (bf16, batch 512): slot by slot
+        if (lane == 0) mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
+        __syncwarp();
+        if (lane < C::kWBoxes)
+          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kBoxK,
+                           tile * 128, pol_stream);
+        __syncwarp();
+        for (int kc = 0; kc < p.kc_count; ++kc) {
+          mbar_wait(&k_empty[ks], kph ^ 1);
+          uint8_t* slot = k_s + ks * C::kKSlot;
+          if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], C::kKSlot);
+          __syncwarp();
+          if (lane == 0) tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
+          if constexpr (!XT_RES)
+            if (lane == 1) tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], kc * C::kBoxK, j * 128, pol_keep);
+          __syncwarp();
+          if (++ks == KS) { ks = 0; kph ^= 1; }
+        }
       }
+      if (++ws == WS) { ws = 0; wph ^= 1; }
       if (lane == 0) trace_ev(p.trace, it, 1);
     }
     __syncwarp();
@@ -801,54 +650,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     if (elect_one()) mma_commit(gx_full);
     __syncwarp();
-  } else if (XMC_BWD_PFW && warp == kBwdGWarp) {
-    // ------------------------------------------------ L2 prefetcher (PFW)
-    const int lane = static_cast<int>(lane_id());
-    const int D = p.pf_dist > 0 ? p.pf_dist : 4;
-    for (int it = 0; it < ntl; ++it) {
-      const int tgt = it + D;
-      if (tgt >= ntl) break;
-      // pace: tile `it` has been issued by the producer
-      while (*prod_progress < it) __nanosleep(64);
-      const int tile = tile_at(tgt);
-      // lanes [0, kWBoxes): this CTA's W boxes; then G box kc by the CTA whose
-      // d-tile j == kc mod dtiles (one prefetch per G box per row group)
-      const int gk = lane - C::kWBoxes;
-      const bool is_w = lane < C::kWBoxes;
-      const bool act = is_w || (gk >= 0 && gk < p.kc_count && (gk % p.dtiles) == j);
-      if (act) {
-        if (is_w) tma_prefetch_2d(&tm_w, j * 128 + lane * C::kBoxK, tile * 128);
-        else tma_prefetch_2d(&tm_g, gk * C::kBoxK, tile * 128);
-      }
-      __syncwarp();
-    }
-  } else if (warp >= kBwdGWarp && kBwdNProd > 1) {
-    // spare producer warp (multi-producer path not applicable): idle
-  } else if (warp == kBwdGWarp) {
-    // ------------------------------------------------ G producer (GPROD)
-    if (XMC_BWD_GPROD && XT_RES && p.gcl == 1 && p.kc_count <= KS) {
-      const uint32_t lane = lane_id();
-      const uint64_t pol_keep = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_last();
-      int ks = 0;
-      uint32_t kph = 0;
-      for (int it = 0; it < ntl; ++it) {
-        const int tile = tile_at(it);
-        for (int kc = 0; kc < p.kc_count; ++kc) {
-          const int kk = (ks + kc) % KS;
-          mbar_wait(&k_empty[kk], kph ^ (ks + kc >= KS ? 0u : 1u));
-        }
-        if (lane == 0)
-          for (int kc = 0; kc < p.kc_count; ++kc) mbar_arrive_expect_tx(&k_full[(ks + kc) % KS], C::kKSlot);
-        __syncwarp();
-        if (static_cast<int>(lane) < p.kc_count)
-          tma_load_2d_hint(k_s + ((ks + lane) % KS) * C::kKSlot, &tm_g, &k_full[(ks + lane) % KS],
-                           static_cast<int>(lane) * C::kBoxK, tile * 128, pol_keep);
-        __syncwarp();
-        for (int q = 0; q < p.kc_count; ++q)
-          if (++ks == KS) { ks = 0; kph ^= 1; }
-      }
-    }
-    __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;                 // 0..15
@@ -898,7 +699,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int h = 0; h < CE * 2; ++h) craw[h] = krow ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
         }
-        if constexpr (FAST && EB == 1 && CE == 0 && (C::kOutTiles == 2 || C::kDirect)) {
+        if constexpr (FAST && EB == 1 && CE == 0 && C::kOutTiles == 2) {
           // production path: everything independent of dW (Philox words,
           // W_old decoded and scaled by 1 - lr wd) is computed and pinned in
           // registers BEFORE the dW wait, so it overlaps the MMAs
@@ -950,25 +751,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
             pk8[k] = cvt_e4m3x4_rs(u[3], u[2], u[1], u[0], rw[k]);
           }
-          if constexpr (C::kDirect) {
-            if (grow < p.rows) {
-              uint4* dst = reinterpret_cast<uint4*>(p.W + grow * p.d + j * 128 + c0);
-              st_global_v4_hint(dst, make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]), pol_w_out);
-              st_global_v4_hint(dst + 1, make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]), pol_w_out);
-            }
-          } else {
-            uint8_t* ot = out_s + (ot_flip & 1) * C::kWBytes;
-            ++ot_flip;
-            const uint32_t ot_s = smem_u32(ot);
-            sts128(ot_s + w_chunk_off<EB>(row, c0, 0), make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]));
-            sts128(ot_s + w_chunk_off<EB>(row, c0, 1), make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]));
-            fence_proxy_async_smem();
-            if (storer && prev_ws >= 0) bulk_wait_read<0>();
-            named_bar_sync(1 + q, 128);
-            if (storer) {
-              tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
-              bulk_commit();
-            }
+          uint8_t* ot = out_s + (ot_flip & 1) * C::kWBytes;
+          ++ot_flip;
+          const uint32_t ot_s = smem_u32(ot);
+          sts128(ot_s + w_chunk_off<EB>(row, c0, 0), make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]));
+          sts128(ot_s + w_chunk_off<EB>(row, c0, 1), make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]));
+          fence_proxy_async_smem();
+          if (storer && prev_ws >= 0) bulk_wait_read<0>();
+          named_bar_sync(1 + q, 128);
+          if (storer) {
+            tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
+            bulk_commit();
           }
           if (tracer) trace_ev(p.trace, it, 7);
           prev_ws = ws;
@@ -1005,17 +798,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           w_update_pack_kahan<EB, CE>(p, p.rounding, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
         } else {
           w_update_pack<EB>(p, p.rounding, acc, w, rw, flat0, out);
-        }
-        if constexpr (C::kDirect) {
-          if (grow < p.rows) {
-            uint4* dst = reinterpret_cast<uint4*>(p.W + (grow * p.d + j * 128 + c0) * EB);
-#pragma unroll
-            for (int h = 0; h < C::kChunks16; ++h) st_global_v4_hint(dst + h, out[h], pol_w_out);
-          }
-          prev_ws = ws;
-          if (++ws == WS) { ws = 0; wph ^= 1; }
-          if (++ds == 2) { ds = 0; dph ^= 1; }
-          continue;
         }
         // W_new into a swizzled smem tile (the staging tile, or in place once
         // the grad_X MMAs have read W_old), then one TMA store per 32-row slab

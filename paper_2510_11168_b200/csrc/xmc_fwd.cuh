@@ -25,10 +25,6 @@
 // e4m3 code (0 / 256) as the unclipped value.  bf16 G keeps MUFU rcp + clip.
 #pragma once
 
-#ifndef XMC_FWD_MUFU_RCP
-#define XMC_FWD_MUFU_RCP 0
-#endif
-
 #include "xmc_ptx.cuh"
 #include "xmc_round.cuh"
 
@@ -79,12 +75,7 @@ struct FwdCfg {
   static constexpr int kMmaN = BN > 256 ? 256 : BN;
   // epilogue: 4 warps per TMEM sub-partition for wide tiles, 2 otherwise
   static constexpr int kEpiWarps = BN >= 256 ? 16 : 8;
-#ifndef XMC_FWD_NPROD
-#define XMC_FWD_NPROD 1
-#endif
-  // producer warps: warp 0 and warps 2 + kEpiWarps ... (stage groups round-robin)
-  static constexpr int kNProd = XMC_FWD_NPROD;
-  static constexpr int kThreads = 64 + kEpiWarps * 32 + (kNProd - 1) * 32;
+  static constexpr int kThreads = 64 + kEpiWarps * 32;
   static constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
   static constexpr int kChunks = kColsPerWarp / 32;
 };
@@ -131,7 +122,6 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
   uint64_t* tempty = tfull + C::kAccStages;       // [kAccStages] (leader's counts both CTAs)
   uint64_t* xfull = tempty + C::kAccStages;       // resident Xq landed (leader's counts both CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 1);
-  volatile int32_t* issue_seq = reinterpret_cast<volatile int32_t*>(tmem_slot + 1);   // multi-producer order
 
   const uint32_t warp = warp_id_sync();
   const int kc_count = p.d / C::kBoxK;
@@ -154,7 +144,6 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       mbar_init(&tempty[a], (PAIR ? 2 : 1) * C::kEpiWarps);
     }
     mbar_init(xfull, 2);
-    *reinterpret_cast<volatile int32_t*>(reinterpret_cast<uint32_t*>(xfull + 1) + 1) = -1;
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -167,7 +156,6 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int pidx = warp == 0 ? 0 : static_cast<int>(warp) - (1 + C::kEpiWarps);
   // PDL: the prologue above (barriers, TMEM, tensor maps) overlapped the
   // previous kernel's tail; from here on its outputs are read
   griddep_wait();
@@ -175,7 +163,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
   // a latched error of an earlier kernel of the step turns this one into a no-op
   const bool aborted = *p.status != 0;
   if (aborted) {
-  } else if (warp == 0 || (C::kNProd > 1 && static_cast<int>(warp) >= 2 + C::kEpiWarps)) {
+  } else if (warp == 0) {
     // ------------------------------------------------------------ producer
     // A bulk-tensor copy instruction occupies its warp for ~max(585, 1.8 x
     // 128-B lines of ALL its lanes) cycles (tools/probe_tma.cu), so one box
@@ -188,7 +176,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     const int lane = static_cast<int>(lane_id());
     const uint64_t pol_w = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
-    if (XRES && pidx == 0) {
+    if constexpr (XRES) {
       // this CTA's Xq rows, every K-chunk, once: one warp-wide instruction
       if (lane == 0) {
         if (leader) mbar_arrive_expect_tx(xfull, 2 * kc_count * C::kXBytes);
@@ -202,15 +190,8 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     }
     const int my_units = unit0 < num_units ? (num_units - unit0 + ustride - 1) / ustride : 0;
     const int total = my_units * kc_count;   // stages this CTA fills
-    for (int n0 = pidx * kIPB; n0 < total; n0 += kIPB * C::kNProd) {
+    for (int n0 = 0; n0 < total; n0 += kIPB) {
       const int cnt = min(kIPB, total - n0);
-      const int grp = n0 / kIPB;
-      // several producers: keep the issue order (group grp after grp - 1)
-      if (C::kNProd > 1) {
-        if (lane == 0)
-          while (*issue_seq != grp - 1) __nanosleep(20);
-        __syncwarp();
-      }
       // stage / phase of item n: ring position n mod kStages, lap n / kStages
       for (int i = 0; i < cnt; ++i) {
         const int n = n0 + i;
@@ -233,7 +214,6 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
         }
       }
       __syncwarp();
-      if (C::kNProd > 1 && lane == 0) *issue_seq = grp;
       const CUtensorMap* m = b == 0 ? &tm_w : &tm_x;
       uint8_t* dst = b == 0 ? sb : sb + C::kWBytes + (b - 1) * C::kXBoxRows * 128;
       const int32_t c1 = b == 0 ? tile * 128 : static_cast<int>(rank) * C::kXRows + (b - 1) * C::kXBoxRows;
@@ -461,15 +441,6 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
           // g256 = 256 sigmoid(z) = 1 / y, y = 2^-8 (1 + 2^(-z log2 e))
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-#if XMC_FWD_MUFU_RCP   // measurement: reciprocal on MUFU instead of the FMA-pipe Newton steps
-            {
-              const float ea = fminf(fast_ex2(__uint_as_float(r[j]) * zk), 1.2676506e30f);
-              const float eb = fminf(fast_ex2(__uint_as_float(r[j + 1]) * zk), 1.2676506e30f);
-              g[j] = fast_rcp(fmaf(ea, 0.00390625f, 0.00390625f));
-              g[j + 1] = fast_rcp(fmaf(eb, 0.00390625f, 0.00390625f));
-              continue;
-            }
-#endif
             // e clamped to 2^100 keeps y finite (g then rounds to 0 in e4m3)
             const float ea = fminf(fast_ex2(__uint_as_float(r[j]) * zk), 1.2676506e30f);
             const float eb = fminf(fast_ex2(__uint_as_float(r[j + 1]) * zk), 1.2676506e30f);
