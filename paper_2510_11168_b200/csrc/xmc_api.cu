@@ -214,6 +214,7 @@ struct xmc_head {
   float* gx_ws;        // [R][d][256]
   int32_t* tile_cnt;   // [total_tiles + 1]
   int32_t* tile_ptr;   // [total_tiles + 1]
+  int32_t* tile_cur;   // [total_tiles + 1] scatter cursors (tile_cnt is re-zeroed by the scan)
   uint32_t* entries;   // [max_positives]
   uint32_t* tmp_tile;  // [max_positives] tile id per positive (bucketing scratch)
   uint32_t* tmp_entry; // [max_positives] packed entry per positive
@@ -240,7 +241,7 @@ struct xmc_head {
 };
 
 struct Layout {
-  size_t xq, xqt, gbuf, gx, cnt, ptr, ent, tmp, chunk, status, wm, keep, cand, total;
+  size_t xq, xqt, gbuf, gx, cnt, ptr, cur, ent, tmp, chunk, status, wm, keep, cand, total;
 };
 
 static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out, int* bp_out, int* R_out,
@@ -276,7 +277,8 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   L->gx = align_up(L->gbuf + (size_t)(maxrows + 128) * bp * eb, 1024);
   L->cnt = align_up(L->gx + (size_t)R * D * bp * 4, 256);
   L->ptr = align_up(L->cnt + (size_t)(tiles + 1) * 4, 256);
-  L->ent = align_up(L->ptr + (size_t)(tiles + 1) * 4, 256);
+  L->cur = align_up(L->ptr + (size_t)(tiles + 1) * 4, 256);
+  L->ent = align_up(L->cur + (size_t)(tiles + 1) * 4, 256);
   L->tmp = align_up(L->ent + (size_t)std::max<int64_t>(d->max_positives, 1) * 4, 256);
   L->chunk = align_up(L->tmp + (size_t)std::max<int64_t>(d->max_positives, 1) * 8, 256);
   L->status = align_up(L->chunk + (size_t)(2 * (ch.size() + 1)) * 8, 256);
@@ -419,6 +421,7 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->gx_ws = reinterpret_cast<float*>(w + L.gx);
   h->tile_cnt = reinterpret_cast<int32_t*>(w + L.cnt);
   h->tile_ptr = reinterpret_cast<int32_t*>(w + L.ptr);
+  h->tile_cur = reinterpret_cast<int32_t*>(w + L.cur);
   h->entries = reinterpret_cast<uint32_t*>(w + L.ent);
   // Optional L2 persistence for the G chunk buffer (XMC_L2_PERSIST=1).  Off by
   // default: measured on B200 it thrashes once G exceeds the persisting carve-
@@ -466,6 +469,7 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->tile_base.push_back(static_cast<int32_t>(tb));
   cudaError_t e1 = cudaMemcpy(h->chunk_dev, host.data(), host.size() * 8, cudaMemcpyHostToDevice);
   cudaError_t e2 = cudaMemset(h->status, 0, 64);
+  if (e2 == cudaSuccess) e2 = cudaMemset(h->tile_cnt, 0, (tiles + 1) * 4);   // re-zeroed by every scan
   if (e1 != cudaSuccess || e2 != cudaSuccess) {
     delete h;
     return fail(XMC_ERR_CUDA, "workspace init failed: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
@@ -517,13 +521,14 @@ extern "C" xmc_status xmc_head_destroy(xmc_head_t h) {
 // X fp32 [B][d] -> Xq [Bp][d] and Xq^T [d][Bp] on the head grid (RTN,
 // head.py:265 / formats.py:197-206); padding rows/cols are zero.
 template <int EB>
-__global__ void x_prep_kernel(const float* __restrict__ X, int B, int Bp, int d, uint8_t* __restrict__ xq,
-                              uint8_t* __restrict__ xqt, int32_t* status) {
+__device__ __forceinline__ void x_prep_body(const float* __restrict__ X, int B, int Bp, int d,
+                                            uint8_t* __restrict__ xq, uint8_t* __restrict__ xqt, int32_t* status,
+                                            int bx, int by, int tx, int ty, int ny) {
   __shared__ float tile[32][33];
-  const int c0 = blockIdx.x * 32, s0 = blockIdx.y * 32;
+  const int c0 = bx * 32, s0 = by * 32;
   bool bad = false;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int s = s0 + i, c = c0 + threadIdx.x;
+  for (int i = ty; i < 32; i += ny) {
+    const int s = s0 + i, c = c0 + tx;
     float v = 0.f;
     if (s < B) {
       v = X[(int64_t)s * d + c];
@@ -532,18 +537,24 @@ __global__ void x_prep_kernel(const float* __restrict__ X, int B, int Bp, int d,
     float q;
     if (EB == 1) q = dec_e4m3(enc_e4m3(v));
     else q = dec_bf16(enc_bf16(v));
-    tile[i][threadIdx.x] = q;
+    tile[i][tx] = q;
     if (EB == 1) xq[(int64_t)s * d + c] = enc_e4m3(v);
     else reinterpret_cast<uint16_t*>(xq)[(int64_t)s * d + c] = enc_bf16(v);
   }
   __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int c = c0 + i, s = s0 + threadIdx.x;
-    const float q = tile[threadIdx.x][i];
+  for (int i = ty; i < 32; i += ny) {
+    const int c = c0 + i, s = s0 + tx;
+    const float q = tile[tx][i];
     if (EB == 1) xqt[(int64_t)c * Bp + s] = enc_e4m3(q);
     else reinterpret_cast<uint16_t*>(xqt)[(int64_t)c * Bp + s] = enc_bf16(q);
   }
   if (bad) atomicOr(status, ST_NONFINITE_X);
+}
+
+template <int EB>
+__global__ void x_prep_kernel(const float* __restrict__ X, int B, int Bp, int d, uint8_t* __restrict__ xq,
+                              uint8_t* __restrict__ xqt, int32_t* status) {
+  x_prep_body<EB>(X, B, Bp, d, xq, xqt, status, blockIdx.x, blockIdx.y, threadIdx.x, threadIdx.y, blockDim.y);
 }
 
 struct PosGeom {
@@ -632,11 +643,11 @@ __device__ __forceinline__ void warp_runs(uint32_t key, int* start, int* len) {
 
 // ---- multi-CTA positive bucketing: count -> scan -> scatter -------------
 // K1: tile id per positive (kept for K3) + warp-aggregated global counts
-__global__ void __launch_bounds__(256) pos_count_kernel(PosGeom g, const int32_t* __restrict__ ps,
-                                                        const int32_t* __restrict__ pl, int64_t nnz,
-                                                        int32_t* __restrict__ cnt, uint32_t* __restrict__ tmp_tile,
-                                                        uint32_t* __restrict__ tmp_entry, int32_t* status) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+__device__ __forceinline__ void pos_count_body(PosGeom g, const int32_t* __restrict__ ps,
+                                               const int32_t* __restrict__ pl, int64_t nnz, int32_t* __restrict__ cnt,
+                                               uint32_t* __restrict__ tmp_tile, uint32_t* __restrict__ tmp_entry,
+                                               int32_t* status, int block) {
+  const int64_t i = block * 256ll + threadIdx.x;
   uint32_t key = 0xffffffffu, val = 0;
   bool bad = false;
   if (i < nnz) {
@@ -658,8 +669,34 @@ __global__ void __launch_bounds__(256) pos_count_kernel(PosGeom g, const int32_t
   if (key != 0xffffffffu && (threadIdx.x & 31) == st) atomicAdd(&cnt[key], len);
 }
 
+__global__ void __launch_bounds__(256) pos_count_kernel(PosGeom g, const int32_t* __restrict__ ps,
+                                                        const int32_t* __restrict__ pl, int64_t nnz,
+                                                        int32_t* __restrict__ cnt, uint32_t* __restrict__ tmp_tile,
+                                                        uint32_t* __restrict__ tmp_entry, int32_t* status) {
+  pos_count_body(g, ps, pl, nnz, cnt, tmp_tile, tmp_entry, status, blockIdx.x);
+}
+
+// x_prep (blocks [0, nx)) and K1 (blocks [nx, ...)) in one launch: they are
+// independent, and the counters they need zeroed were zeroed by the previous
+// step's scan (or at handle creation)
+template <int EB>
+__global__ void __launch_bounds__(256) prep_count_kernel(const float* __restrict__ X, int B, int Bp, int d,
+                                                         uint8_t* __restrict__ xq, uint8_t* __restrict__ xqt, int nx,
+                                                         PosGeom g, const int32_t* __restrict__ ps,
+                                                         const int32_t* __restrict__ pl, int64_t nnz,
+                                                         int32_t* __restrict__ cnt, uint32_t* __restrict__ tmp_tile,
+                                                         uint32_t* __restrict__ tmp_entry, int32_t* status) {
+  if (static_cast<int>(blockIdx.x) < nx) {
+    x_prep_body<EB>(X, B, Bp, d, xq, xqt, status, blockIdx.x % (d / 32), blockIdx.x / (d / 32), threadIdx.x & 31,
+                    threadIdx.x >> 5, 8);
+    return;
+  }
+  pos_count_body(g, ps, pl, nnz, cnt, tmp_tile, tmp_entry, status, blockIdx.x - nx);
+}
+
 // K2: exclusive scan of the T tile counters (one CTA; smem-staged segments)
-__global__ void __launch_bounds__(1024) pos_scan_kernel(int32_t* __restrict__ cnt, int32_t* __restrict__ ptr, int32_t T) {
+__global__ void __launch_bounds__(1024) pos_scan_kernel(int32_t* __restrict__ cnt, int32_t* __restrict__ ptr,
+                                                        int32_t* __restrict__ cur, int32_t T) {
   extern __shared__ int32_t sc[];   // [T]
   __shared__ int32_t wsum[32];
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, w = tid >> 5;
@@ -697,7 +734,8 @@ __global__ void __launch_bounds__(1024) pos_scan_kernel(int32_t* __restrict__ cn
   __syncthreads();
   for (int i = tid; i < T; i += nth) {
     ptr[i] = sc[i];
-    cnt[i] = sc[i];   // becomes the scatter cursor
+    cur[i] = sc[i];   // the scatter cursor
+    cnt[i] = 0;       // counters start the next step at zero (no memset launch)
   }
 }
 
@@ -1237,8 +1275,11 @@ static xmc_status check_args(const xmc_step_args* a) {
   return XMC_OK;
 }
 
-static xmc_status prepare_positives(xmc_head* h, const int32_t* ps, const int32_t* pl, int64_t nnz, int B,
-                                    cudaStream_t st) {
+// Xq / Xq^T and the positive buckets of one step.  Small batches: x_prep +
+// one single-CTA bucketing kernel; otherwise x_prep fused with the counting
+// pass, then scan and scatter (the scan re-zeroes the counters).
+static xmc_status prepare_step(xmc_head* h, const float* X, int Bp, const int32_t* ps, const int32_t* pl,
+                               int64_t nnz, int B, cudaStream_t st) {
   if (nnz > h->desc.max_positives)
     return fail(XMC_ERR_CAPACITY, "%lld positives exceed workspace capacity %lld", (long long)nnz,
                 (long long)h->desc.max_positives);
@@ -1256,17 +1297,23 @@ static xmc_status prepare_positives(xmc_head* h, const int32_t* ps, const int32_
                 kPosMaxTiles);
   if (nnz <= 2048) {
     // tiny batches: one launch, everything in one CTA's shared memory
+    XMC_TRY(launch_x_prep(h, X, B, Bp, st));
     pos_bucket_kernel<<<1, 1024, T * 4, st>>>(g, ps, pl, nnz, T, h->tile_ptr, h->entries, h->status);
     CUDA_TRY(cudaGetLastError());
     return XMC_OK;
   }
-  CUDA_TRY(cudaMemsetAsync(h->tile_cnt, 0, (h->total_tiles + 1) * 4, st));
   const int blocks = static_cast<int>(cdiv(nnz, 256));
-  pos_count_kernel<<<blocks, 256, 0, st>>>(g, ps, pl, nnz, h->tile_cnt, h->tmp_tile, h->tmp_entry, h->status);
+  const int nx = (h->desc.dim / 32) * (Bp / 32);
+  if (h->eb == 1)
+    prep_count_kernel<1><<<nx + blocks, 256, 0, st>>>(X, B, Bp, h->desc.dim, h->xq, h->xqt, nx, g, ps, pl, nnz,
+                                                      h->tile_cnt, h->tmp_tile, h->tmp_entry, h->status);
+  else
+    prep_count_kernel<2><<<nx + blocks, 256, 0, st>>>(X, B, Bp, h->desc.dim, h->xq, h->xqt, nx, g, ps, pl, nnz,
+                                                      h->tile_cnt, h->tmp_tile, h->tmp_entry, h->status);
   CUDA_TRY(cudaGetLastError());
-  pos_scan_kernel<<<1, 1024, T * 4, st>>>(h->tile_cnt, h->tile_ptr, T);
+  pos_scan_kernel<<<1, 1024, T * 4, st>>>(h->tile_cnt, h->tile_ptr, h->tile_cur, T);
   CUDA_TRY(cudaGetLastError());
-  pos_scatter_kernel<<<blocks, 256, 0, st>>>(nnz, h->tmp_tile, h->tmp_entry, h->tile_cnt, h->entries);
+  pos_scatter_kernel<<<blocks, 256, 0, st>>>(nnz, h->tmp_tile, h->tmp_entry, h->tile_cur, h->entries);
   CUDA_TRY(cudaGetLastError());
   return XMC_OK;
 }
@@ -1305,8 +1352,7 @@ extern "C" xmc_status xmc_head_step_kahan(xmc_head_t h, void* W, void* comp, con
   if (nnz < 0 || (nnz > 0 && (!pos_sample || !pos_label))) return fail(XMC_ERR_ARG, "bad positives");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int Bp = padded_batch(h->eb, B);
-  XMC_TRY(launch_x_prep(h, X, B, Bp, st));
-  XMC_TRY(prepare_positives(h, pos_sample, pos_label, nnz, B, st));
+  XMC_TRY(prepare_step(h, X, Bp, pos_sample, pos_label, nnz, B, st));
   // the first chunk overwrites every partial slot unless it has fewer tiles
   // than slots; later chunks accumulate
   // the first chunk overwrites every partial slot unless it has fewer tiles
