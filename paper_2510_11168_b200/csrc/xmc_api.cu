@@ -1101,6 +1101,21 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t r
   p.status = h->status;
   static const int fdbg = getenv("XMC_DEBUG_FWD") ? atoi(getenv("XMC_DEBUG_FWD")) : 0;
   p.debug = fdbg;
+  if (eb == 2 && Bp == 512 && fwd_pairs_enabled()) {
+    // batch 512 (bf16): two 256-sample passes of the CTA-pair kernel over the
+    // same rows (double-buffered accumulators) instead of one 512-column
+    // single-buffered pass; pass h writes G / logits columns [256h, 256h+256)
+    for (int pass = 0; pass < 2 && pass * 256 < B; ++pass) {
+      FwdParams q = p;
+      q.sample0 = pass * 256;
+      q.B = std::min(256, B - pass * 256);
+      q.out = static_cast<uint8_t*>(out) + static_cast<size_t>(pass) * 256 * (mode == 1 ? 4 : eb);
+      CUtensorMap txh;
+      XMC_TRY(make_map(&txh, h->xq + static_cast<size_t>(pass) * 256 * D * eb, eb, D, 256, D, 128));
+      XMC_TRY((launch_fwd_t<2, 256, true>(h, tw, txh, q, st)));
+    }
+    return XMC_OK;
+  }
   if (eb == 1) {
     if (Bp == 128) return pair ? launch_fwd_t<1, 128, true>(h, tw, tx, p, st) : launch_fwd_t<1, 128, false>(h, tw, tx, p, st);
     if (Bp == 256) return pair ? launch_fwd_t<1, 256, true>(h, tw, tx, p, st) : launch_fwd_t<1, 256, false>(h, tw, tx, p, st);

@@ -50,6 +50,8 @@ struct FwdParams {
   int64_t label0;            // global label of local row 0 of this launch
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
   int32_t debug;             // measurement only (XMC_DEBUG_FWD): 1 skip the G epilogue math and stores
+  int32_t sample0;           // first sample of this pass (batch split into BN-wide passes); entries of
+                             // other samples are skipped, this pass's are shifted by -sample0
 };
 
 // XRES: this CTA's Xq rows stay resident in shared memory for the whole
@@ -408,8 +410,8 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
         named_bar_sync(1, NT);
         for (int e = e0 + etid; e < e1; e += NT) {
           const uint32_t v = p.entries[e];
-          const uint32_t r = v >> 16, s = v & 0xFFFFu;
-          atomicOr(&bitmap[r * C::kWordsPerRow + (s >> 5)], 1u << (s & 31));
+          const uint32_t r = v >> 16, s = (v & 0xFFFFu) - static_cast<uint32_t>(p.sample0);
+          if (s < static_cast<uint32_t>(BN)) atomicOr(&bitmap[r * C::kWordsPerRow + (s >> 5)], 1u << (s & 31));
         }
         named_bar_sync(1, NT);
       }
