@@ -439,6 +439,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // walk them in step, so each G tile is requested by all six at once)
   const int ntl = r0 < p.num_tiles ? (p.num_tiles - r0 + R - 1) / R : 0;
   auto tile_at = [&](int k) { return r0 + k * R; };
+  // k-chunks (batch slices) a tile needs: all of them when the update runs
+  // (dW sums over the whole batch), else only the grad_X column group's
+  const int kb = p.do_update ? 0 : p.gx_kc0;
+  const int ke = p.do_update ? p.kc_count : p.gx_kc0 + p.gx_kc_count;
+  const int nk = ke - kb;
+  // bytes a k slot receives: the G box, plus the streamed Xq^T box (dW only)
+  const uint32_t kslot_bytes = (!XT_RES && p.do_update) ? C::kKSlot : C::kBox;
 
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tm_w);
@@ -503,30 +510,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int crank = p.gcl > 1 ? static_cast<int>(cluster_ctarank()) : 0;
     const uint16_t gmask = static_cast<uint16_t>((1u << p.gcl) - 1u);
     // the tile's G slots are consecutive ring slots when the ring holds whole tiles
-    const bool whole = p.kc_count <= KS && KS % p.kc_count == 0;
+    const bool whole = nk > 0 && nk <= KS && KS % nk == 0;
     for (int it = 0; it < ntl; ++it) {
       const int tile = tile_at(it);
       mbar_wait(&w_empty[ws], wph ^ 1);
       if (lane == 0) trace_ev(p.trace, it, 0);
       if (whole) {
-        for (int kc = 0; kc < p.kc_count; ++kc) mbar_wait(&k_empty[ks + kc], kph ^ 1);
+        for (int i = 0; i < nk; ++i) mbar_wait(&k_empty[ks + i], kph ^ 1);
         if (lane == 0) {
           mbar_arrive_expect_tx(&w_full[ws], (p.debug & 32) ? 0 : C::kWBytes);
-          for (int kc = 0; kc < p.kc_count; ++kc)
-            mbar_arrive_expect_tx(&k_full[ks + kc], (p.debug & 16) ? 0 : C::kKSlot);
+          for (int i = 0; i < nk; ++i) mbar_arrive_expect_tx(&k_full[ks + i], (p.debug & 16) ? 0 : kslot_bytes);
         }
         __syncwarp();
         if (p.gcl == 1) {
           // W boxes, then per k-chunk the G box (+ the Xq^T box when not resident)
-          constexpr int kGB = XT_RES ? 1 : 2;
+          const int kGB = (!XT_RES && p.do_update) ? 2 : 1;
           const int gl = lane - C::kWBoxes;
-          const int kc = gl / kGB, sub = gl % kGB;
+          const int i = gl / kGB, sub = gl % kGB;
           const bool is_w = lane < C::kWBoxes;
-          const bool active = is_w || (gl >= 0 && kc < p.kc_count);
+          const bool active = is_w || (gl >= 0 && i < nk);
           const CUtensorMap* m = is_w ? &tm_w : (sub == 0 ? &tm_g : &tm_xt);
-          uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + (ks + kc) * C::kKSlot + sub * C::kBox;
-          uint64_t* bar = is_w ? &w_full[ws] : &k_full[ks + kc];
-          const int32_t c0 = is_w ? j * 128 + lane * C::kBoxK : kc * C::kBoxK;
+          uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + (ks + i) * C::kKSlot + sub * C::kBox;
+          uint64_t* bar = is_w ? &w_full[ws] : &k_full[ks + i];
+          const int32_t c0 = is_w ? j * 128 + lane * C::kBoxK : (kb + i) * C::kBoxK;
           const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? tile * 128 : j * 128);
           // measurement: debug & 16 skips the G loads, debug & 32 the W loads
           // (the barrier then completes through the arrive with a tx of 0)
@@ -540,14 +546,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kBoxK,
                              tile * 128, pol_stream);
           const int piece = crank + lane * p.gcl;
-          if (XT_RES && piece < 4 * p.kc_count) {
-            const int kc = piece >> 2, qq = piece & 3;
-            tma_load_2d_mc(k_s + (ks + kc) * C::kKSlot + qq * 32 * 128, &tm_g, &k_full[ks + kc], kc * C::kBoxK,
+          if (XT_RES && piece < 4 * nk) {
+            const int i = piece >> 2, qq = piece & 3;
+            tma_load_2d_mc(k_s + (ks + i) * C::kKSlot + qq * 32 * 128, &tm_g, &k_full[ks + i], (kb + i) * C::kBoxK,
                            tile * 128 + qq * 32, gmask, pol_keep);
           }
         }
         __syncwarp();
-        ks += p.kc_count;
+        ks += nk;
         if (ks == KS) { ks = 0; kph ^= 1; }
       } else {
         // more k-chunks than ring slots (bf16, batch 512): slot by slot
@@ -557,14 +563,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kBoxK,
                            tile * 128, pol_stream);
         __syncwarp();
-        for (int kc = 0; kc < p.kc_count; ++kc) {
+        for (int kc = kb; kc < ke; ++kc) {
           mbar_wait(&k_empty[ks], kph ^ 1);
           uint8_t* slot = k_s + ks * C::kKSlot;
-          if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], C::kKSlot);
+          if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], kslot_bytes);
           __syncwarp();
           if (lane == 0) tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
           if constexpr (!XT_RES)
-            if (lane == 1) tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], kc * C::kBoxK, j * 128, pol_keep);
+            if (lane == 1 && p.do_update)
+              tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], kc * C::kBoxK, j * 128, pol_keep);
           __syncwarp();
           if (++ks == KS) { ks = 0; kph ^= 1; }
         }
@@ -592,12 +599,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
       const uint32_t w_addr = smem_u32(w_s + ws * C::kWBytes);
       const uint32_t d_dw = tmem_base + ds * 128;
-      for (int kc = 0; kc < p.kc_count; ++kc) {
-        if (kc == 1 && lane_id() == 0) trace_ev(p.trace, it, 10);
+      for (int kc = kb; kc < ke; ++kc) {
+        if (kc == kb + 1 && lane_id() == 0) trace_ev(p.trace, it, 10);
         mbar_wait(&k_full[ks], kph);
         tc_fence_after();
-        if (kc == 0 && lane_id() == 0) trace_ev(p.trace, it, 9);
-        if (kc == p.kc_count - 1 && lane_id() == 0) trace_ev(p.trace, it, 3);
+        if (kc == kb && lane_id() == 0) trace_ev(p.trace, it, 9);
+        if (kc == ke - 1 && lane_id() == 0) trace_ev(p.trace, it, 3);
         if (elect_one()) {
           const uint32_t g_addr = smem_u32(k_s + ks * C::kKSlot);
           const uint32_t x_addr = XT_RES ? smem_u32(xt_s + kc * C::kBox) : g_addr + C::kBox;
@@ -612,7 +619,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           // dW complete -> hand it to the update epilogue before the grad_X
           // MMAs are queued (commit tracks only the MMAs issued so far)
-          if (C::kOutBuf && kc == p.kc_count - 1) mma_commit(&t_full[ds]);
+          if (C::kOutBuf && kc == ke - 1) mma_commit(&t_full[ds]);
           // grad_X^T: one MMA group with N = all samples of the pass, issued
           // once its G boxes (contiguous ring slots, LBO = slot pitch) landed;
           // W (A operand) is then read from smem once per tile.
@@ -637,7 +644,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           // in place: dW is handed over only after the grad_X MMAs, which read
           // the W_old tile the epilogue overwrites with W_new
-          if (!C::kOutBuf && kc == p.kc_count - 1) mma_commit(&t_full[ds]);
+          if (!C::kOutBuf && kc == ke - 1) mma_commit(&t_full[ds]);
         }
         __syncwarp();
         if (++ks == KS) { ks = 0; kph ^= 1; }
