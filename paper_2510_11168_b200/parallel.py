@@ -56,6 +56,34 @@ def merge_topk(vals: torch.Tensor, idx: torch.Tensor, k: int) -> torch.Tensor:
     return torch.gather(i1, 1, o2)[:, :k]
 
 
+def broadcast_batch(X, sample_idx, label_idx, src: int = 0, group=None):
+    """X broadcast of SURVEY.md 8(e): rank `src` holds the batch (encoder output
+    X, B x d float32, and the positives as GLOBAL label ids); every other rank
+    receives it.  Returns (X, sample_idx, label_idx) tensors on every rank, on
+    the device of the process group's backend (CUDA for NCCL)."""
+    rank = dist.get_rank(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    if rank == src:
+        X = torch.as_tensor(X, dtype=torch.float32).to(dev).contiguous()
+        si = torch.as_tensor(sample_idx, dtype=torch.int32).to(dev).contiguous()
+        li = torch.as_tensor(label_idx, dtype=torch.int32).to(dev).contiguous()
+        meta = torch.tensor([X.shape[0], X.shape[1], si.numel()], dtype=torch.int64, device=dev)
+    else:
+        meta = torch.empty(3, dtype=torch.int64, device=dev)
+    dist.broadcast(meta, src, group=group)
+    b, d, nnz = (int(v) for v in meta.tolist())
+    if rank != src:
+        X = torch.empty((b, d), dtype=torch.float32, device=dev)
+        si = torch.empty(nnz, dtype=torch.int32, device=dev)
+        li = torch.empty(nnz, dtype=torch.int32, device=dev)
+    dist.broadcast(X, src, group=group)
+    if nnz:
+        dist.broadcast(si, src, group=group)
+        dist.broadcast(li, src, group=group)
+    return X, si, li
+
+
 class ShardedHead:
     """A rank's shard of a label-sharded head.
 

@@ -74,6 +74,32 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
+def _bcast_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2510_11168_b200.parallel import broadcast_batch
+    L, W, X, si, li = _problem()
+    if rank == 0:
+        Xb, sib, lib = broadcast_batch(X, si, li)
+    else:
+        Xb, sib, lib = broadcast_batch(None, None, None)
+    out[rank] = (Xb.numpy(), sib.numpy(), lib.numpy())
+    dist.destroy_process_group()
+
+
+def test_broadcast_batch():
+    """X (and the global positives) broadcast from rank 0."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_bcast_worker, args=(world, port, out), nprocs=world, join=True)
+    L, W, X, si, li = _problem()
+    for r in range(world):
+        Xb, sib, lib = out[r]
+        assert np.array_equal(Xb, X) and np.array_equal(sib, si) and np.array_equal(lib, li)
+
+
 def test_sharded_step_matches_single_process():
     world = 2
     port = _free_port()
