@@ -49,7 +49,7 @@ struct FwdParams {
   int32_t* cand_l;
   int64_t label0;            // global label of local row 0 of this launch
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
-  int32_t debug;             // measurement only (XMC_DEBUG_FWD): 1 skip the G epilogue math and stores
+  int32_t debug;             // measurement only (XMC_DEBUG_FWD): 1 skip the G epilogue, 2 skip only its stores
   int32_t sample0;           // first sample of this pass (batch split into BN-wide passes); entries of
                              // other samples are skipped, this pass's are shifted by -sample0
 };
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) abs_sum += fabsf(g[j]);
         }
-        if (row_ok) {
+        if (row_ok && !(p.debug & 2)) {   // debug & 2 (measurement): G math without the stores
           if constexpr (EB == 1) {
             uint32_t pk[8];
 #pragma unroll
