@@ -220,6 +220,9 @@ struct xmc_head {
   uint32_t* tmp_entry; // [max_positives] packed entry per positive
   int64_t* chunk_dev;  // [k+1] chunk starts (local rows) + [k+1] tile bases
   int32_t* status;     // [4]
+  int32_t* ring_ready;      // [max chunk tiles + 1] fused step flags (zeroed per launch)
+  int32_t* ring_consumed;   // [max chunk tiles + 1]
+  int R_step;          // grad_X partial slots written by the current step's backward
   uint8_t* wm;         // [max_chunk_rows + 128][d] masked W chunk (dropout only)
   uint32_t* keep;      // [max_chunk_rows + 128][d / 32] dropout keep bits (dropout only)
   int64_t comp_rows;   // local rows [0, comp_rows) carry a Kahan compensation
@@ -240,8 +243,40 @@ struct xmc_head {
   size_t l2_window_max;
 };
 
+// ---- fused step: forward and backward of a chunk in ONE persistent launch ----
+// Hypothesis: the forward is DRAM-bound (W streams in once) and the backward
+// is bound by shared-memory bandwidth, so they would overlap on disjoint SMs:
+// the first
+// nfwd CTAs run the forward (split layout, cta_group::1 like the backward)
+// and hand G to the other CTAs through an L2-resident ring of 128-row tiles
+// (FwdParams / BwdParams ring_* fields); the backward then re-reads each W
+// tile from L2 shortly after the forward streamed it in.  Every CTA of the
+// grid is resident (one per SM, grid <= SMs), so the flag waits cannot
+// deadlock: the smallest tile not yet written only waits for the backward of
+// a smaller tile, which only waits for tiles written before it.
+// Measured: slower than the two launches at every split
+// (4.97 / 3.90 ms per step with 34 / 44 forward CTAs vs 1.96 ms), because the
+// forward is not idle-SM work: its epilogue and W pipeline cost ~84 SM-ms per
+// step in the pair layout and more in the split one, so moving it beside the
+// backward cannot shorten the sum.  Kept as a tested option.
+template <int KC>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    xmc_step_kernel(const __grid_constant__ CUtensorMap fw, const __grid_constant__ CUtensorMap fx,
+                    const __grid_constant__ CUtensorMap bw, const __grid_constant__ CUtensorMap bg,
+                    const __grid_constant__ CUtensorMap bxt, const __grid_constant__ CUtensorMap bws, FwdParams fp,
+                    BwdParams bp, int nfwd) {
+  static_assert(FwdCfg<1, 128, false, true>::kThreads == kBwdThreads, "one block shape for both roles");
+  const int b = static_cast<int>(blockIdx.x);
+  if (b < nfwd) fwd_body<1, 128, false, false, true>(fw, fx, fp, b >> 1, nfwd >> 1, b & 1);
+  else bwd_body<1, true, KC, 0, true, false>(bw, bg, bxt, bws, bp, b - nfwd, static_cast<int>(gridDim.x) - nfwd);
+}
+
+constexpr int kStepSmem = FwdCfg<1, 128, false, true>::kSmemBytes > BwdCfg<1, true, 2>::kSmemBytes
+                              ? FwdCfg<1, 128, false, true>::kSmemBytes
+                              : BwdCfg<1, true, 2>::kSmemBytes;
+
 struct Layout {
-  size_t xq, xqt, gbuf, gx, cnt, ptr, cur, ent, tmp, chunk, status, wm, keep, cand, total;
+  size_t xq, xqt, gbuf, gx, cnt, ptr, cur, ent, tmp, chunk, status, flags, wm, keep, cand, total;
 };
 
 static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out, int* bp_out, int* R_out,
@@ -282,7 +317,8 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   L->tmp = align_up(L->ent + (size_t)std::max<int64_t>(d->max_positives, 1) * 4, 256);
   L->chunk = align_up(L->tmp + (size_t)std::max<int64_t>(d->max_positives, 1) * 8, 256);
   L->status = align_up(L->chunk + (size_t)(2 * (ch.size() + 1)) * 8, 256);
-  L->wm = align_up(L->status + 64, 1024);
+  L->flags = align_up(L->status + 64, 256);   // fused step: ready + consumed per chunk tile
+  L->wm = align_up(L->flags + (size_t)2 * (cdiv(maxrows, 128) + 1) * 4, 1024);
   L->keep = align_up(L->wm + (d->dropout ? (size_t)(maxrows + 128) * D * eb : 0), 1024);
   L->cand = align_up(L->keep + (d->dropout ? (size_t)(maxrows + 128) * (D / 32) * 4 : 0), 1024);
   L->total = align_up(L->cand + (size_t)bp * 4 * num_sms * kTopK * 8, 1024);
@@ -323,6 +359,9 @@ static void set_fwd_attr() {
   if constexpr (EB == 1 && BN <= 256 && BN >= 128)
     cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, true, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FwdCfg<EB, BN, true, true>::kSmemBytes);
+  if constexpr (EB == 1 && BN == 128)
+    cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FwdCfg<EB, BN, false, true>::kSmemBytes);
 }
 template <int EB, bool XR, int KC>
 static void set_bwd_attr() {
@@ -411,6 +450,7 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->num_sms = sms;
   h->dtiles = desc->dim / 128;
   h->R = R;
+  h->R_step = R;
   h->chunks = partition(desc->num_labels_local, desc->num_chunks);
   h->total_tiles = tiles;
   h->max_chunk_rows = maxrows;
@@ -447,6 +487,8 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->tmp_entry = h->tmp_tile + std::max<int64_t>(desc->max_positives, 1);
   h->chunk_dev = reinterpret_cast<int64_t*>(w + L.chunk);
   h->status = reinterpret_cast<int32_t*>(w + L.status);
+  h->ring_ready = reinterpret_cast<int32_t*>(w + L.flags);
+  h->ring_consumed = h->ring_ready + (cdiv(maxrows, 128) + 1);
   h->wm = desc->dropout ? w + L.wm : nullptr;
   h->keep = desc->dropout ? reinterpret_cast<uint32_t*>(w + L.keep) : nullptr;
   h->comp_rows = desc->comp_bytes == 0 ? 0
@@ -486,6 +528,7 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   set_bwd_attr<2, true, 2>();
   set_bwd_attr<2, true, 4>();
   set_bwd_attr<2, false, 8>();
+  cudaFuncSetAttribute(xmc_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStepSmem);
   choose_bwd_cluster(h);
   // forward pairs: how many CTA pairs are co-resident.  The persistent grid is
   // capped there, which keeps every primary of a PDL chain fully resident.
@@ -1049,6 +1092,13 @@ static bool fwd_pairs_enabled() {
   return v != 0;
 }
 
+// e4m3 batch 256 forward in the split layout instead of CTA pairs (XMC_FWD_SPLIT=1;
+// the fused step always uses it)
+static bool fwd_split_enabled() {
+  static const int v = getenv("XMC_FWD_SPLIT") ? atoi(getenv("XMC_FWD_SPLIT")) : 0;
+  return v != 0;
+}
+
 template <int EB, int BN, bool PAIR>
 static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtensorMap& tx, const FwdParams& p,
                                cudaStream_t st) {
@@ -1076,15 +1126,9 @@ static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtenso
   return XMC_OK;
 }
 
-// rows [row0, row0+rows) of W (local), mode 0 -> G into gbuf, mode 1 -> fp32 logits
-static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t rows, int B, int Bp, int mode,
-                             const int32_t* tile_ptr, void* out, int64_t ld, float* stats, cudaStream_t st,
-                             float logit_scale = 1.0f) {
+static FwdParams fwd_params(xmc_head* h, int64_t rows, int B, int mode, const int32_t* tile_ptr, void* out,
+                            int64_t ld, float* stats, float logit_scale) {
   const int eb = h->eb, D = h->desc.dim;
-  const bool pair = fwd_pairs_enabled() && (Bp == 128 || Bp == 256);
-  CUtensorMap tw, tx;
-  XMC_TRY(make_map(&tw, static_cast<const uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 128));
-  XMC_TRY(make_map(&tx, h->xq, eb, D, Bp, D, std::min(pair ? Bp / 2 : Bp, 256)));
   FwdParams p{};
   p.rows = static_cast<int32_t>(rows);
   p.B = B;
@@ -1101,6 +1145,19 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t r
   p.status = h->status;
   static const int fdbg = getenv("XMC_DEBUG_FWD") ? atoi(getenv("XMC_DEBUG_FWD")) : 0;
   p.debug = fdbg;
+  return p;
+}
+
+// rows [row0, row0+rows) of W (local), mode 0 -> G into gbuf, mode 1 -> fp32 logits
+static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t rows, int B, int Bp, int mode,
+                             const int32_t* tile_ptr, void* out, int64_t ld, float* stats, cudaStream_t st,
+                             float logit_scale = 1.0f) {
+  const int eb = h->eb, D = h->desc.dim;
+  const bool pair = fwd_pairs_enabled() && (Bp == 128 || Bp == 256);
+  CUtensorMap tw, tx;
+  XMC_TRY(make_map(&tw, static_cast<const uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 128));
+  XMC_TRY(make_map(&tx, h->xq, eb, D, Bp, D, std::min(pair ? Bp / 2 : Bp, 256)));
+  FwdParams p = fwd_params(h, rows, B, mode, tile_ptr, out, ld, stats, logit_scale);
   if (eb == 2 && Bp == 512 && fwd_pairs_enabled()) {
     // batch 512 (bf16): two 256-sample passes of the CTA-pair kernel over the
     // same rows (double-buffered accumulators) instead of one 512-column
@@ -1114,6 +1171,20 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t row0, int64_t r
       XMC_TRY(make_map(&txh, h->xq + static_cast<size_t>(pass) * 256 * D * eb, eb, D, 256, D, 128));
       XMC_TRY((launch_fwd_t<2, 256, true>(h, tw, txh, q, st)));
     }
+    return XMC_OK;
+  }
+  if (eb == 1 && Bp == 256 && fwd_split_enabled() && D / 128 <= FwdCfg<1, 128, false, true>::kXResChunks) {
+    // split layout (XMC_FWD_SPLIT=1): single-CTA tcgen05, CTA pair = sample halves
+    using CS = FwdCfg<1, 128, false, true>;
+    CUtensorMap txs;
+    XMC_TRY(make_map(&txs, h->xq, eb, D, Bp, D, 128));
+    const int grid = static_cast<int>(std::min<int64_t>(h->num_sms & ~1, 2 * p.num_tiles));
+    const size_t win = mode == 0 ? static_cast<size_t>(rows) * ld * eb : 0;
+    ProfRec pr;
+    prof_begin(0, st, &pr);
+    CUDA_TRY(launch_ex(xmc_fwd_kernel<1, 128, false, false, true>, grid, CS::kThreads, CS::kSmemBytes, st, h, win, 1,
+                       tw, txs, p));
+    prof_end(st, &pr);
     return XMC_OK;
   }
   if (eb == 1) {
@@ -1170,12 +1241,19 @@ static xmc_status launch_bwd_t(xmc_head* h, int R, const CUtensorMap& tw, const 
 
 // one bwd pass over local rows [row0, row0+rows), G from gbuf; grad_X partials
 // accumulate into the [R][d][Bp] workspace (zeroed by the caller per step)
-static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int64_t rows, int Bp, bool update,
-                             int gx_kc0, int gx_kc_count, bool gx_overwrite, const xmc_step_args* a,
-                             cudaStream_t st, const uint32_t* keep = nullptr, float drop_scale = 1.0f) {
+struct BwdLaunch {
+  CUtensorMap tw, tg, tx, tws;
+  BwdParams p;
+  int R;
+  size_t gb;
+};
+
+static xmc_status setup_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int64_t rows, int Bp, bool update,
+                            int gx_kc0, int gx_kc_count, bool gx_overwrite, const xmc_step_args* a,
+                            const uint32_t* keep, float drop_scale, BwdLaunch* L) {
   const int eb = h->eb, D = h->desc.dim;
   const int box_k = 128 / eb;
-  CUtensorMap tw, tg, tx, tws;
+  CUtensorMap &tw = L->tw, &tg = L->tg, &tx = L->tx, &tws = L->tws;
   XMC_TRY(make_map(&tw, static_cast<uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 128));
   XMC_TRY(make_map(&tws, static_cast<uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 32));
   const int64_t tiles = cdiv(rows, 128);
@@ -1185,7 +1263,8 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   const int gcl = (eb == 2 && Bp == 512) ? 1 : h->gcl;
   XMC_TRY(make_map(&tg, h->gbuf, eb, Bp, rows, Bp, gcl > 1 ? 32 : 128));
   XMC_TRY(make_map(&tx, h->xqt, eb, Bp, D, Bp, 128));
-  BwdParams p{};
+  BwdParams& p = L->p;
+  p = BwdParams{};
   p.rows = static_cast<int32_t>(rows);
   p.d = D;
   p.num_tiles = static_cast<int32_t>(tiles);
@@ -1227,7 +1306,20 @@ static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int
   p.keep = keep;
   p.drop_scale = drop_scale;
   p.status = h->status;
-  const size_t gb = static_cast<size_t>(rows) * Bp * eb;
+  L->R = R;
+  L->gb = static_cast<size_t>(rows) * Bp * eb;
+  return XMC_OK;
+}
+
+static xmc_status launch_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int64_t rows, int Bp, bool update,
+                             int gx_kc0, int gx_kc_count, bool gx_overwrite, const xmc_step_args* a,
+                             cudaStream_t st, const uint32_t* keep = nullptr, float drop_scale = 1.0f) {
+  BwdLaunch L;
+  XMC_TRY(setup_bwd(h, W, comp, row0, rows, Bp, update, gx_kc0, gx_kc_count, gx_overwrite, a, keep, drop_scale, &L));
+  const int eb = h->eb, R = L.R;
+  const size_t gb = L.gb;
+  const CUtensorMap &tw = L.tw, &tg = L.tg, &tx = L.tx, &tws = L.tws;
+  const BwdParams& p = L.p;
   if (eb == 1) {
     if (Bp == 128) return launch_bwd_t<1, true, 1>(h, R, tw, tg, tx, tws, p, gb, st);
     if (Bp == 256) return launch_bwd_t<1, true, 2>(h, R, tw, tg, tx, tws, p, gb, st);
@@ -1257,6 +1349,62 @@ static xmc_status run_backward(xmc_head* h, void* W, void* comp, int64_t row0, i
   return XMC_OK;
 }
 
+// ---- fused step (XMC_FUSED=1; kernel and measurements: xmc_step_kernel) ----
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+// the fused step runs the SR_FAST e4m3 batch-256 step without compensation,
+// dropout, Adam-style moments or measurement knobs (XMC_FUSED=0 turns it off)
+static bool fused_step_ok(const xmc_head* h, void* comp, int Bp, const xmc_step_args* a) {
+  static const int on = env_int("XMC_FUSED", 0);
+  return on && h->eb == 1 && Bp == 256 && comp == nullptr && h->adam.m == nullptr && a &&
+         a->rounding == ROUND_SR_FAST && h->gcl == 1 && h->desc.dim / 128 <= FwdCfg<1, 128, false, true>::kXResChunks &&
+         !getenv("XMC_DEBUG_BWD") && !getenv("XMC_DEBUG_FWD") && trace_buf() == nullptr &&
+         h->num_sms >= 2 * h->dtiles + 2;
+}
+
+// CTAs the fused step gives the forward / backward (R backward CTAs per d-tile)
+static void fused_split(const xmc_head* h, int64_t tiles, int* nfwd, int* R) {
+  int f = env_int("XMC_FUSED_FWD", 34) & ~1;
+  f = std::max(2, std::min(f, h->num_sms - h->dtiles));
+  *R = static_cast<int>(std::min<int64_t>((h->num_sms - f) / h->dtiles, tiles));
+  *nfwd = static_cast<int>(std::min<int64_t>(f, 2 * tiles));
+}
+
+static xmc_status launch_fused(xmc_head* h, void* W, int64_t row0, int64_t rows, int B, int Bp,
+                               const int32_t* tile_ptr, float* stats, bool gx_overwrite, const xmc_step_args* a,
+                               cudaStream_t st) {
+  const int eb = h->eb, D = h->desc.dim;
+  const int64_t tiles = cdiv(rows, 128);
+  int nfwd, R;
+  fused_split(h, tiles, &nfwd, &R);
+  const int ring = static_cast<int>(std::min<int64_t>(std::max(1, env_int("XMC_RING", 256)), tiles));
+  BwdLaunch L;
+  XMC_TRY(setup_bwd(h, W, nullptr, row0, rows, Bp, true, 0, Bp / 128, gx_overwrite, a, nullptr, 1.0f, &L));
+  XMC_TRY(make_map(&L.tg, h->gbuf, eb, Bp, std::min<int64_t>(static_cast<int64_t>(ring) * 128, rows), Bp, 128));
+  L.p.ring_tiles = ring;
+  L.p.ready_target = 2 * FwdCfg<1, 128, false, true>::kEpiWarps;
+  L.p.ready = h->ring_ready;
+  L.p.consumed = h->ring_consumed;
+  CUtensorMap tw, tx;
+  XMC_TRY(make_map(&tw, static_cast<const uint8_t*>(W) + row0 * D * eb, eb, D, rows, D, 128));
+  XMC_TRY(make_map(&tx, h->xq, eb, D, Bp, D, 128));
+  FwdParams fp = fwd_params(h, rows, B, 0, tile_ptr, h->gbuf, Bp, stats, 1.0f);
+  fp.ring_tiles = ring;
+  fp.consumed_target = h->dtiles;
+  fp.ready = h->ring_ready;
+  fp.consumed = h->ring_consumed;
+  CUDA_TRY(cudaMemsetAsync(h->ring_ready, 0, static_cast<size_t>(2) * (cdiv(h->max_chunk_rows, 128) + 1) * 4, st));
+  ProfRec pr;
+  prof_begin(1, st, &pr);
+  CUDA_TRY(launch_ex(xmc_step_kernel<2>, nfwd + R * h->dtiles, kBwdThreads, kStepSmem, st, h, 0, 1, tw, tx, L.tw,
+                     L.tg, L.tx, L.tws, fp, L.p, nfwd));
+  prof_end(st, &pr);
+  return XMC_OK;
+}
+
 // acc[s][c] (+)= scale * sum_r ws[r][c][s]  -- one deterministic reduction per step
 static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumulate, cudaStream_t st,
                             float scale = 1.0f) {
@@ -1271,7 +1419,7 @@ static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumul
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled(h) ? 1 : 0;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, gx_reduce_kernel, static_cast<const float*>(h->gx_ws), h->R, D, Bp, B,
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, gx_reduce_kernel, static_cast<const float*>(h->gx_ws), h->R_step, D, Bp, B,
                               (h->eb == 1 ? (1.0f / 256.0f) : 1.0f) * scale, accumulate ? 1 : 0, acc));
   CUDA_TRY(cudaGetLastError());
   return XMC_OK;
@@ -1342,6 +1490,7 @@ static xmc_status read_status(xmc_head* h, cudaStream_t st, bool clear) {
   if (s & ST_BAD_SAMPLE) return fail(XMC_ERR_INDEX, "positive sample index out of range");
   if (s & ST_LABEL_OUTSIDE) return fail(XMC_ERR_LABEL, "label outside chunk range");
   if (s & ST_NONFINITE_GRAD) return fail(XMC_ERR_NONFINITE, "non-finite values in fused scratch block");
+  if (s & ST_RING_TIMEOUT) return fail(XMC_ERR_CUDA, "fused step: a G ring flag timed out (CTAs not co-resident)");
   return XMC_OK;
 }
 
@@ -1368,18 +1517,28 @@ extern "C" xmc_status xmc_head_step_kahan(xmc_head_t h, void* W, void* comp, con
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int Bp = padded_batch(h->eb, B);
   XMC_TRY(prepare_step(h, X, Bp, pos_sample, pos_label, nnz, B, st));
-  // the first chunk overwrites every partial slot unless it has fewer tiles
-  // than slots; later chunks accumulate
-  // the first chunk overwrites every partial slot unless it has fewer tiles
-  // than slots; later chunks accumulate
-  const bool first_covers = !h->chunks.empty() && cdiv(h->chunks[0].second - h->chunks[0].first, 128) >= h->R;
   DropoutPlan dp;
   XMC_TRY(dropout_plan(h, args, &dp));
+  const bool fused = !dp.on && fused_step_ok(h, comp, Bp, args);
+  // grad_X partial slots of this step (the fused step gives the backward fewer CTAs)
+  h->R_step = h->R;
+  if (fused) {
+    int nf, Rf;
+    fused_split(h, INT64_MAX / 4, &nf, &Rf);
+    h->R_step = Rf;
+  }
+  // the first chunk overwrites every partial slot unless it has fewer tiles
+  // than slots; later chunks accumulate
+  const bool first_covers = !h->chunks.empty() && cdiv(h->chunks[0].second - h->chunks[0].first, 128) >= h->R_step;
   if (!first_covers) XMC_TRY(zero_gx_ws(h, Bp, st));
   if (stats) CUDA_TRY(cudaMemsetAsync(stats, 0, 8, st));
   for (size_t c = 0; c < h->chunks.size(); ++c) {
     const int64_t r0 = h->chunks[c].first, rows = h->chunks[c].second - h->chunks[c].first;
     const int32_t* tp = h->tile_ptr + h->tile_base[c];
+    if (fused) {
+      XMC_TRY(launch_fused(h, W, r0, rows, B, Bp, tp, stats, first_covers && c == 0, args, st));
+      continue;
+    }
     if (!dp.on) {
       XMC_TRY(launch_fwd(h, W, r0, rows, B, Bp, 0, tp, h->gbuf, Bp, stats, st));
       XMC_TRY(run_backward(h, W, comp, r0, rows, Bp, true, true, first_covers && c == 0, args, st));
@@ -1611,6 +1770,7 @@ extern "C" xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, i
   CUDA_TRY(cudaGetLastError());
   DropoutPlan dp;
   XMC_TRY(dropout_plan(h, args, &dp));
+  h->R_step = h->R;
   if (accumulate_gx) XMC_TRY(zero_gx_ws(h, Bp, st));
   if (!dp.on) {
     XMC_TRY(run_backward(h, W, nullptr, row0, rows, Bp, accumulate_gx != 0, update != 0, false, args, st));

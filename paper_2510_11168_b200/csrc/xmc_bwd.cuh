@@ -39,6 +39,7 @@ enum StatusBits : int32_t {
   ST_LABEL_OUTSIDE = 8,
   ST_CAPACITY = 16,
   ST_NONFINITE_MOMENTS = 32,
+  ST_RING_TIMEOUT = 64,   // fused step: a ring flag never arrived (CTAs not co-resident)
 };
 
 struct BwdParams {
@@ -73,6 +74,14 @@ struct BwdParams {
   float* adam_v;
   float b1, b2, omb1, omb2, bc1, bc2, eps;
   uint64_t* trace;       // measurement only (XMC_TRACE): clock64 per tile and event of CTA 0, [kTraceTiles][16]
+  // fused step (xmc_step_kernel): G arrives through a ring of ring_tiles
+  // 128-row tiles written by the forward CTAs of the same launch; tile t is
+  // readable once ready[t] >= ready_target, and each CTA counts its finished
+  // reads of tile t into consumed[t].  ring_tiles 0: G is the whole chunk.
+  int32_t ring_tiles;
+  int32_t ready_target;
+  const int32_t* ready;
+  int32_t* consumed;
 };
 
 constexpr int kTraceTiles = 512;
@@ -395,11 +404,12 @@ XMC_DEV void w_update_pack_adamw(const BwdParams& p, const uint32_t (&acc)[32], 
   for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
 }
 
-template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false, bool ADAMW = false>
-__global__ void __launch_bounds__(kBwdThreads, 1)
-    xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
-                   const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
-                   BwdParams p) {
+// The kernel body: CTA `bid` of `nblk` backward CTAs (d-tile bid % dtiles,
+// row group bid / dtiles).  xmc_bwd_kernel runs it on every CTA of its grid,
+// xmc_step_kernel on the CTAs after its forward ones.
+template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST, bool ADAMW>
+XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CUtensorMap& tm_xt,
+                      const CUtensorMap& tm_ws, BwdParams p, const int bid, const int nblk) {
   using C = BwdCfg<EB, XT_RES, KCMAX>;
   static_assert(!ADAMW || (CE == 4 && !FAST), "the Adam-style head keeps an fp32 compensation");
   if constexpr (FAST) {
@@ -431,9 +441,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gx_full + 1);
 
   const uint32_t warp = warp_id_sync();
-  const int j = blockIdx.x % p.dtiles;
-  const int R = gridDim.x / p.dtiles;
-  const int r0 = blockIdx.x / p.dtiles;
+  const int j = bid % p.dtiles;
+  const int R = nblk / p.dtiles;
+  const int r0 = bid / p.dtiles;
   const bool do_gx = p.gx_kc_count > 0;
   // this CTA's label tiles: r0, r0 + R, ... (the d-tile CTAs of a row group
   // walk them in step, so each G tile is requested by all six at once)
@@ -517,6 +527,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (lane == 0) trace_ev(p.trace, it, 0);
       if (whole) {
         for (int i = 0; i < nk; ++i) mbar_wait(&k_empty[ks + i], kph ^ 1);
+        if (p.ring_tiles) {
+          // fused step: the tile's G rows are written by the forward CTAs
+          spin_until_ge(p.ready + tile, p.ready_target, p.status, ST_RING_TIMEOUT);
+          fence_proxy_async_global();
+        }
         if (lane == 0) {
           mbar_arrive_expect_tx(&w_full[ws], (p.debug & 32) ? 0 : C::kWBytes);
           for (int i = 0; i < nk; ++i) mbar_arrive_expect_tx(&k_full[ks + i], (p.debug & 16) ? 0 : kslot_bytes);
@@ -533,7 +548,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + (ks + i) * C::kKSlot + sub * C::kBox;
           uint64_t* bar = is_w ? &w_full[ws] : &k_full[ks + i];
           const int32_t c0 = is_w ? j * 128 + lane * C::kBoxK : (kb + i) * C::kBoxK;
-          const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? tile * 128 : j * 128);
+          const int gtile = p.ring_tiles ? tile % p.ring_tiles : tile;
+          const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? gtile * 128 : j * 128);
           // measurement: debug & 16 skips the G loads, debug & 32 the W loads
           // (the barrier then completes through the arrive with a tx of 0)
           const bool skip = (p.debug & 16) ? !is_w : ((p.debug & 32) ? is_w : false);
@@ -603,6 +619,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (kc == kb + 1 && lane_id() == 0) trace_ev(p.trace, it, 10);
         mbar_wait(&k_full[ks], kph);
         tc_fence_after();
+        if (p.ring_tiles && kc == ke - 1 && lane_id() == 0) {
+          // every G box of the tile landed: its ring slot may be rewritten
+          fence_proxy_async_global();
+          red_release_gpu_add(p.consumed + tile, 1);
+        }
         if (kc == kb && lane_id() == 0) trace_ev(p.trace, it, 9);
         if (kc == ke - 1 && lane_id() == 0) trace_ev(p.trace, it, 3);
         if (elect_one()) {
@@ -891,6 +912,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
   }
+}
+
+template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false, bool ADAMW = false>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
+                   const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
+                   BwdParams p) {
+  bwd_body<EB, XT_RES, KCMAX, CE, FAST, ADAMW>(tm_w, tm_g, tm_xt, tm_ws, p, static_cast<int>(blockIdx.x),
+                                               static_cast<int>(gridDim.x));
 }
 
 }  // namespace xmc

@@ -52,11 +52,23 @@ struct FwdParams {
   int32_t debug;             // measurement only (XMC_DEBUG_FWD): 1 skip the G epilogue, 2 skip only its stores
   int32_t sample0;           // first sample of this pass (batch split into BN-wide passes); entries of
                              // other samples are skipped, this pass's are shifted by -sample0
+  // fused step (xmc_step_kernel): G goes to a ring of ring_tiles 128-row tiles
+  // (tile t -> ring tile t mod ring_tiles); before writing tile t a warp waits
+  // for consumed[t - ring_tiles] >= consumed_target (every backward CTA of the
+  // row group has read the previous occupant), after writing it adds 1 to
+  // ready[t].  ring_tiles 0: G rows are chunk rows.
+  int32_t ring_tiles;
+  int32_t consumed_target;
+  int32_t* ready;
+  const int32_t* consumed;
 };
 
 // XRES: this CTA's Xq rows stay resident in shared memory for the whole
 // launch (loaded once, kXResChunks K-chunks max, i.e. d <= 768 for e4m3), so a
 // stage carries only its W box: half the TMA work and L2->SM traffic per tile.
+// Without PAIR, XRES is the split layout (BN = 128): CTAs 2c and 2c+1 take the
+// same label tiles for samples [0, 128) and [128, 256) (cta_group::1 only, as
+// the fused step kernel needs).
 template <int EB, int BN, bool PAIR, bool XRES = false>
 struct FwdCfg {
   static constexpr int kBoxK = 128 / EB;                  // K elements per 128-B swizzle atom
@@ -76,7 +88,7 @@ struct FwdCfg {
   static constexpr int kSmemBytes = 1024 /*align slack*/ + kXResBytes + kStages * kStageBytes + kBitmapBytes + 256;
   static constexpr int kMmaN = BN > 256 ? 256 : BN;
   // epilogue: 4 warps per TMEM sub-partition for wide tiles, 2 otherwise
-  static constexpr int kEpiWarps = BN >= 256 ? 16 : 8;
+  static constexpr int kEpiWarps = (BN >= 256 || XRES) ? 16 : 8;
   static constexpr int kThreads = 64 + kEpiWarps * 32;
   static constexpr int kColsPerWarp = BN / (kEpiWarps / 4);
   static constexpr int kChunks = kColsPerWarp / 32;
@@ -104,13 +116,14 @@ XMC_DEV void topk_insert(float (&s)[kTopK], int32_t (&l)[kTopK], float v, int32_
   }
 }
 
-template <int EB, int BN, bool PAIR, bool TOPK = false, bool XRES = false>
-__global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
-    xmc_fwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                   FwdParams p) {
+// The kernel body: work units unit0, unit0 + ustride, ... (tiles, or tile
+// pairs for PAIR); xh = which BN-sample half of the batch (split layout).
+template <int EB, int BN, bool PAIR, bool TOPK, bool XRES>
+XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParams p, const int unit0,
+                      const int ustride, const int xh) {
   using C = FwdCfg<EB, BN, PAIR, XRES>;
   static_assert(!PAIR || BN <= 256, "paired tiles use one N <= 256 accumulator");
-  static_assert(!XRES || PAIR, "resident Xq is a CTA-pair layout (one 128-B box per K-chunk)");
+  static_assert(!XRES || PAIR || BN == 128, "resident Xq: CTA pairs, or the 128-sample split layout");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -131,8 +144,8 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
   const bool leader = rank == 0;
   // work units: single tiles, or tile pairs (2u, 2u+1) for a CTA pair
   const int num_units = PAIR ? (p.num_tiles + 1) / 2 : p.num_tiles;
-  const int unit0 = PAIR ? static_cast<int>(cluster_id_x()) : static_cast<int>(blockIdx.x);
-  const int ustride = PAIR ? static_cast<int>(num_clusters_x()) : static_cast<int>(gridDim.x);
+  // Xq rows (samples) this CTA stages
+  const int xrow0 = PAIR ? static_cast<int>(rank) * C::kXRows : xh * BN;
 
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tm_w);
@@ -145,7 +158,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], (PAIR ? 2 : 1) * C::kEpiWarps);
     }
-    mbar_init(xfull, 2);
+    mbar_init(xfull, PAIR ? 2 : 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -176,18 +189,24 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     constexpr int kIPB = XRES ? 3 : 2;                                 // stages per instruction
     static_assert(kBPI * kIPB <= 32, "one lane per box");
     const int lane = static_cast<int>(lane_id());
-    const uint64_t pol_w = policy_evict_first();
+    // fused step: the backward CTAs re-read each W tile shortly after
+    const uint64_t pol_w = p.ring_tiles ? policy_evict_normal() : policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
     if constexpr (XRES) {
       // this CTA's Xq rows, every K-chunk, once: one warp-wide instruction
-      if (lane == 0) {
-        if (leader) mbar_arrive_expect_tx(xfull, 2 * kc_count * C::kXBytes);
-        else mbar_arrive_cluster(mapa_shared(xfull, 0));
+      if constexpr (PAIR) {
+        if (lane == 0) {
+          if (leader) mbar_arrive_expect_tx(xfull, 2 * kc_count * C::kXBytes);
+          else mbar_arrive_cluster(mapa_shared(xfull, 0));
+        }
+        __syncwarp();
+        if (lane < kc_count)
+          tma_load_2d_2sm(xres + lane * C::kXBytes, &tm_x, mapa_shared(xfull, 0), lane * C::kBoxK, xrow0, pol_x);
+      } else {
+        if (lane == 0) mbar_arrive_expect_tx(xfull, kc_count * C::kXBytes);
+        __syncwarp();
+        if (lane < kc_count) tma_load_2d_hint(xres + lane * C::kXBytes, &tm_x, xfull, lane * C::kBoxK, xrow0, pol_x);
       }
-      __syncwarp();
-      if (lane < kc_count)
-        tma_load_2d_2sm(xres + lane * C::kXBytes, &tm_x, mapa_shared(xfull, 0), lane * C::kBoxK,
-                        static_cast<int>(rank) * C::kXRows, pol_x);
       __syncwarp();
     }
     const int my_units = unit0 < num_units ? (num_units - unit0 + ustride - 1) / ustride : 0;
@@ -218,7 +237,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       __syncwarp();
       const CUtensorMap* m = b == 0 ? &tm_w : &tm_x;
       uint8_t* dst = b == 0 ? sb : sb + C::kWBytes + (b - 1) * C::kXBoxRows * 128;
-      const int32_t c1 = b == 0 ? tile * 128 : static_cast<int>(rank) * C::kXRows + (b - 1) * C::kXBoxRows;
+      const int32_t c1 = b == 0 ? tile * 128 : xrow0 + (b - 1) * C::kXBoxRows;
       const uint64_t pol = b == 0 ? pol_w : pol_x;
       if (active) {
         if constexpr (PAIR) tma_load_2d_2sm(dst, m, mapa_shared(&full[st_i], 0), kc * C::kBoxK, c1, pol);
@@ -379,7 +398,12 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     const int row = q * 32 + lane_id();      // row within the 128-label tile
     const int etid = ew * 32 + lane_id();
     const bool want_stats = p.stats != nullptr && p.mode == 0;
-    const bool pad_cols = p.B < BN;
+    // split layout: this CTA's columns are samples [xs, xs + BN) of the pass
+    // (the host offsets out / B by the pass's sample0 already)
+    const int xs = xh * BN;
+    const int s0 = p.sample0 + xs;               // first sample (positive entries)
+    const int bvalid = p.B - xs;                 // valid columns
+    const bool pad_cols = bvalid < BN;
     const bool use_pos = p.mode == 0 && p.tile_ptr != nullptr;
     const uint64_t pol_g = policy_evict_last();   // G is re-read by the backward kernel
     float abs_sum = 0.f;
@@ -410,7 +434,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
         named_bar_sync(1, NT);
         for (int e = e0 + etid; e < e1; e += NT) {
           const uint32_t v = p.entries[e];
-          const uint32_t r = v >> 16, s = (v & 0xFFFFu) - static_cast<uint32_t>(p.sample0);
+          const uint32_t r = v >> 16, s = (v & 0xFFFFu) - static_cast<uint32_t>(s0);
           if (s < static_cast<uint32_t>(BN)) atomicOr(&bitmap[r * C::kWordsPerRow + (s >> 5)], 1u << (s & 31));
         }
         named_bar_sync(1, NT);
@@ -422,6 +446,13 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       tc_fence_after();
       const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
       const bool row_ok = grow < p.rows;
+      // G row in out: the chunk row, or its ring row (fused step)
+      int64_t orow = grow;
+      if (p.ring_tiles) {
+        orow = static_cast<int64_t>(tile % p.ring_tiles) * 128 + row;
+        if (tile >= p.ring_tiles)
+          spin_until_ge(p.consumed + (tile - p.ring_tiles), p.consumed_target, p.status, 64 /*ST_RING_TIMEOUT*/);
+      }
 #pragma unroll 1
       for (int cc = 0; cc < ((p.debug & 1) ? 0 : C::kChunks); ++cc) {
         const int col0 = grp * C::kColsPerWarp + cc * 32;
@@ -430,10 +461,10 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
         tmem_ld_wait();
         if (p.mode == 1) {
           if (row_ok) {
-            float* o = reinterpret_cast<float*>(p.out) + grow * p.ld;
+            float* o = reinterpret_cast<float*>(p.out) + grow * p.ld + xs;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (col0 + j < p.B) o[col0 + j] = __uint_as_float(r[j]) * p.logit_scale;
+              if (col0 + j < bvalid) o[col0 + j] = __uint_as_float(r[j]) * p.logit_scale;
           }
           continue;
         }
@@ -479,7 +510,7 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
         if (pad_cols) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (col0 + j >= p.B) g[j] = 0.0f;
+            if (col0 + j >= bvalid) g[j] = 0.0f;
         }
         if (want_stats && row_ok) {
 #pragma unroll
@@ -494,14 +525,14 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
               const uint32_t hi = cvt_e4m3x2_rn(g[4 * j + 3], g[4 * j + 2]);
               pk[j] = lo | (hi << 16);
             }
-            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out) + grow * p.ld + col0);
+            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out) + orow * p.ld + xs + col0);
             st_global_v4_hint(o, make_uint4(pk[0], pk[1], pk[2], pk[3]), pol_g);
             st_global_v4_hint(o + 1, make_uint4(pk[4], pk[5], pk[6], pk[7]), pol_g);
           } else {
             uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) pk[j] = cvt_bf16x2_rn(g[2 * j + 1], g[2 * j]);
-            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + grow * p.ld + col0);
+            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + orow * p.ld + xs + col0);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               st_global_v4_hint(o + j, make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]), pol_g);
@@ -513,6 +544,10 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
       if (lane_id() == 0) {
         if (PAIR && !leader) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
         else mbar_arrive(&tempty[acc]);
+        if (p.ring_tiles) {   // this warp's G rows of the tile are written
+          __threadfence();
+          red_release_gpu_add(p.ready + tile, 1);
+        }
       }
       if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
     }
@@ -532,6 +567,21 @@ __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR>::kThreads, 1)
     tc_fence_after();
     if constexpr (PAIR) tmem_dealloc_2sm<C::kTmemCols>(tmem_base);
     else tmem_dealloc<C::kTmemCols>(tmem_base);
+  }
+}
+
+template <int EB, int BN, bool PAIR, bool TOPK = false, bool XRES = false>
+__global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR, XRES>::kThreads, 1)
+    xmc_fwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                   FwdParams p) {
+  if constexpr (PAIR) {
+    fwd_body<EB, BN, PAIR, TOPK, XRES>(tm_w, tm_x, p, static_cast<int>(cluster_id_x()),
+                                       static_cast<int>(num_clusters_x()), 0);
+  } else if constexpr (XRES) {   // split layout: CTA pair (2c, 2c+1) = the two sample halves
+    fwd_body<EB, BN, PAIR, TOPK, XRES>(tm_w, tm_x, p, static_cast<int>(blockIdx.x >> 1),
+                                       static_cast<int>(gridDim.x >> 1), static_cast<int>(blockIdx.x & 1));
+  } else {
+    fwd_body<EB, BN, PAIR, TOPK, XRES>(tm_w, tm_x, p, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), 0);
   }
 }
 

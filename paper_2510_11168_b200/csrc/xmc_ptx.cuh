@@ -162,6 +162,31 @@ XMC_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory");
 // let the next grid in the stream launch (its CTAs take SMs as ours exit)
 XMC_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ------------------------------------------- inter-CTA flags (global memory)
+XMC_DEV int32_t ld_acquire_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+XMC_DEV void red_release_gpu_add(int32_t* p, int32_t v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// later async-proxy (TMA) accesses of this thread observe the generic-proxy
+// global writes it has acquired
+XMC_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// spin until *flag >= target (acquire); after ~4 s latch `bit` in *status and
+// give up, so a broken co-residency assumption reports instead of hanging
+XMC_DEV void spin_until_ge(const int32_t* flag, int32_t target, int32_t* status, int32_t bit) {
+  if (ld_acquire_gpu(flag) >= target) return;
+  const long long t0 = clock64();
+  while (ld_acquire_gpu(flag) < target) {
+    if (clock64() - t0 > (1ll << 33) || (ld_acquire_gpu(status) & bit)) {   // once latched, nobody waits
+      atomicOr(status, bit);
+      return;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ tcgen05
 template <uint32_t kCols>
 XMC_DEV void tmem_alloc(uint32_t* dst_smem) {

@@ -1,0 +1,57 @@
+"""The fused-step launch (XMC_FUSED=1: forward and backward of a chunk in one
+persistent kernel, G handed over through an L2 ring) and the
+split-layout forward (XMC_FWD_SPLIT=1) are measurement options, read from the
+environment once per process.  Each runs in a child process on the same
+seeded step and must reproduce the default path's weights bit for bit (same G,
+same Philox draws) and its grad_X to fp32 summation-order tolerance."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2510_11168_b200 as xmc
+from oracle import lpxmc_oracle as O
+L, B, D, k = 300_001, 256, 768, 2
+g = torch.Generator(device="cuda"); g.manual_seed(5)
+W0 = xmc.cast_native(torch.randn((L, D), generator=g, device="cuda") * 0.02, xmc.E4M3)
+rs = np.random.default_rng(3)
+X = rs.normal(size=(B, D)).astype(np.float32)
+si, li = O.synthetic_positives(L, B, 5.45, seed=4)
+head = xmc.ChunkedHead(xmc.QuantizedMatrix(W0, xmc.E4M3), num_chunks=k, num_labels_global=L)
+cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=xmc.E4M3, rounding="stochastic", sr_impl="philox")
+for step in range(2):
+    gx = xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(11), step)
+torch.cuda.synchronize()
+torch.save({"W": head.weights.values.view(torch.uint8).cpu(), "gx": gx.cpu()}, sys.argv[2])
+"""
+
+
+def _run(tmp_path, name, env_extra):
+    out = str(tmp_path / f"{name}.pt")
+    env = dict(os.environ)
+    for key in ("XMC_FUSED", "XMC_FWD_SPLIT"):
+        env.pop(key, None)
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, "-c", CHILD, ROOT, out], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return torch.load(out)
+
+
+@pytest.mark.parametrize("mode", ["fused", "split"])
+def test_option_matches_default_path(tmp_path, mode):
+    base = _run(tmp_path, "base", {})
+    env = {"XMC_FUSED": "1"} if mode == "fused" else {"XMC_FWD_SPLIT": "1"}
+    got = _run(tmp_path, mode, env)
+    assert torch.equal(got["W"], base["W"])
+    torch.testing.assert_close(got["gx"], base["gx"], rtol=1e-5, atol=1e-4)
