@@ -267,8 +267,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     BwdParams bp, int nfwd) {
   static_assert(FwdCfg<1, 128, false, true>::kThreads == kBwdThreads, "one block shape for both roles");
   const int b = static_cast<int>(blockIdx.x);
-  if (b < nfwd) fwd_body<1, 128, false, false, true>(fw, fx, fp, b >> 1, nfwd >> 1, b & 1);
-  else bwd_body<1, true, KC, 0, true, false>(bw, bg, bxt, bws, bp, b - nfwd, static_cast<int>(gridDim.x) - nfwd);
+  if (b < nfwd) fwd_body<1, 128, false, false, true, true>(fw, fx, fp, b >> 1, nfwd >> 1, b & 1);
+  else bwd_body<1, true, KC, 0, true, false, true>(bw, bg, bxt, bws, bp, b - nfwd, static_cast<int>(gridDim.x) - nfwd);
 }
 
 constexpr int kStepSmem = FwdCfg<1, 128, false, true>::kSmemBytes > BwdCfg<1, true, 2>::kSmemBytes

@@ -77,7 +77,7 @@ struct BwdParams {
   // fused step (xmc_step_kernel): G arrives through a ring of ring_tiles
   // 128-row tiles written by the forward CTAs of the same launch; tile t is
   // readable once ready[t] >= ready_target, and each CTA counts its finished
-  // reads of tile t into consumed[t].  ring_tiles 0: G is the whole chunk.
+  // reads of tile t into consumed[t].  Read only by bwd_body<..., RING>.
   int32_t ring_tiles;
   int32_t ready_target;
   const int32_t* ready;
@@ -407,7 +407,7 @@ XMC_DEV void w_update_pack_adamw(const BwdParams& p, const uint32_t (&acc)[32], 
 // The kernel body: CTA `bid` of `nblk` backward CTAs (d-tile bid % dtiles,
 // row group bid / dtiles).  xmc_bwd_kernel runs it on every CTA of its grid,
 // xmc_step_kernel on the CTAs after its forward ones.
-template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST, bool ADAMW>
+template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST, bool ADAMW, bool RING = false>
 XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CUtensorMap& tm_xt,
                       const CUtensorMap& tm_ws, BwdParams p, const int bid, const int nblk) {
   using C = BwdCfg<EB, XT_RES, KCMAX>;
@@ -527,7 +527,7 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
       if (lane == 0) trace_ev(p.trace, it, 0);
       if (whole) {
         for (int i = 0; i < nk; ++i) mbar_wait(&k_empty[ks + i], kph ^ 1);
-        if (p.ring_tiles) {
+        if constexpr (RING) {
           // fused step: the tile's G rows are written by the forward CTAs
           spin_until_ge(p.ready + tile, p.ready_target, p.status, ST_RING_TIMEOUT);
           fence_proxy_async_global();
@@ -548,7 +548,7 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
           uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + (ks + i) * C::kKSlot + sub * C::kBox;
           uint64_t* bar = is_w ? &w_full[ws] : &k_full[ks + i];
           const int32_t c0 = is_w ? j * 128 + lane * C::kBoxK : (kb + i) * C::kBoxK;
-          const int gtile = p.ring_tiles ? tile % p.ring_tiles : tile;
+          const int gtile = RING ? tile % p.ring_tiles : tile;
           const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? gtile * 128 : j * 128);
           // measurement: debug & 16 skips the G loads, debug & 32 the W loads
           // (the barrier then completes through the arrive with a tx of 0)
@@ -619,7 +619,7 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
         if (kc == kb + 1 && lane_id() == 0) trace_ev(p.trace, it, 10);
         mbar_wait(&k_full[ks], kph);
         tc_fence_after();
-        if (p.ring_tiles && kc == ke - 1 && lane_id() == 0) {
+        if (RING && kc == ke - 1 && lane_id() == 0) {
           // every G box of the tile landed: its ring slot may be rewritten
           fence_proxy_async_global();
           red_release_gpu_add(p.consumed + tile, 1);

@@ -56,7 +56,7 @@ struct FwdParams {
   // (tile t -> ring tile t mod ring_tiles); before writing tile t a warp waits
   // for consumed[t - ring_tiles] >= consumed_target (every backward CTA of the
   // row group has read the previous occupant), after writing it adds 1 to
-  // ready[t].  ring_tiles 0: G rows are chunk rows.
+  // ready[t].  Read only by the RING instantiation (fwd_body<..., RING>).
   int32_t ring_tiles;
   int32_t consumed_target;
   int32_t* ready;
@@ -118,7 +118,7 @@ XMC_DEV void topk_insert(float (&s)[kTopK], int32_t (&l)[kTopK], float v, int32_
 
 // The kernel body: work units unit0, unit0 + ustride, ... (tiles, or tile
 // pairs for PAIR); xh = which BN-sample half of the batch (split layout).
-template <int EB, int BN, bool PAIR, bool TOPK, bool XRES>
+template <int EB, int BN, bool PAIR, bool TOPK, bool XRES, bool RING = false>
 XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParams p, const int unit0,
                       const int ustride, const int xh) {
   using C = FwdCfg<EB, BN, PAIR, XRES>;
@@ -145,7 +145,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
   // work units: single tiles, or tile pairs (2u, 2u+1) for a CTA pair
   const int num_units = PAIR ? (p.num_tiles + 1) / 2 : p.num_tiles;
   // Xq rows (samples) this CTA stages
-  const int xrow0 = PAIR ? static_cast<int>(rank) * C::kXRows : xh * BN;
+  const int xrow0 = PAIR ? static_cast<int>(rank) * C::kXRows : ((!PAIR && XRES) ? xh * BN : 0);
 
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tm_w);
@@ -190,7 +190,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
     static_assert(kBPI * kIPB <= 32, "one lane per box");
     const int lane = static_cast<int>(lane_id());
     // fused step: the backward CTAs re-read each W tile shortly after
-    const uint64_t pol_w = p.ring_tiles ? policy_evict_normal() : policy_evict_first();
+    const uint64_t pol_w = RING ? policy_evict_normal() : policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
     if constexpr (XRES) {
       // this CTA's Xq rows, every K-chunk, once: one warp-wide instruction
@@ -400,7 +400,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
     const bool want_stats = p.stats != nullptr && p.mode == 0;
     // split layout: this CTA's columns are samples [xs, xs + BN) of the pass
     // (the host offsets out / B by the pass's sample0 already)
-    const int xs = xh * BN;
+    const int xs = (!PAIR && XRES) ? xh * BN : 0;
     const int s0 = p.sample0 + xs;               // first sample (positive entries)
     const int bvalid = p.B - xs;                 // valid columns
     const bool pad_cols = bvalid < BN;
@@ -448,7 +448,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
       const bool row_ok = grow < p.rows;
       // G row in out: the chunk row, or its ring row (fused step)
       int64_t orow = grow;
-      if (p.ring_tiles) {
+      if constexpr (RING) {
         orow = static_cast<int64_t>(tile % p.ring_tiles) * 128 + row;
         if (tile >= p.ring_tiles)
           spin_until_ge(p.consumed + (tile - p.ring_tiles), p.consumed_target, p.status, 64 /*ST_RING_TIMEOUT*/);
@@ -544,7 +544,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
       if (lane_id() == 0) {
         if (PAIR && !leader) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
         else mbar_arrive(&tempty[acc]);
-        if (p.ring_tiles) {   // this warp's G rows of the tile are written
+        if constexpr (RING) {   // this warp's G rows of the tile are written
           __threadfence();
           red_release_gpu_add(p.ready + tile, 1);
         }
