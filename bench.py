@@ -281,9 +281,26 @@ def main():
     batch_dev = xmc.BatchInput(Xd, sid, lid)
     gx = torch.empty((a.batch, a.dim), dtype=torch.float32, device=dev)
 
+    # grad_X across ranks: the peer-memory all-reduce fused into the step's own
+    # grad_X reduction (parallel.PeerGroup; XMC_PEER=0 -> NCCL all_reduce)
+    allreduce = "none (1 rank)"
+    peers = None
+    if world > 1:
+        allreduce = "nccl all_reduce"
+        if os.environ.get("XMC_PEER", "1") != "0":
+            from paper_2510_11168_b200.parallel import PeerGroup
+            try:
+                peers = PeerGroup(a.dim, a.batch)
+                peers.attach(head)
+                allreduce = "peer memory (CUDA IPC over NVLink), fused with the partial-slot reduction"
+            except Exception as e:  # noqa: BLE001 - report and keep NCCL
+                print(f"peer all-reduce unavailable ({e}); using NCCL", file=sys.stderr)
+                peers = None
+    config["grad_x_allreduce"] = allreduce
+
     def step_fn(s, batch, out):
         r = xmc.head_update(head, batch, cfg, rng, s, check=False, grad_out=out)
-        if world > 1:
+        if world > 1 and head.peers is None:
             dist.all_reduce(r)
         return r
 
@@ -291,7 +308,23 @@ def main():
     mem0 = torch.cuda.memory_allocated(dev)
     for s in range(a.warmup):
         step_fn(s, batch_dev, gx)
-    _lib.check(_lib.load().xmc_head_check(head.handle(a.batch, len(si)).h, _lib.stream_ptr()))
+    ok = True
+    try:
+        _lib.check(_lib.load().xmc_head_check(head.handle(a.batch, len(si)).h, _lib.stream_ptr()))
+    except Exception as e:  # noqa: BLE001
+        if peers is None:
+            raise
+        print(f"peer all-reduce failed in warm-up ({e}); using NCCL", file=sys.stderr)
+        ok = False
+    if world > 1 and peers is not None:
+        # every rank must agree before the timed region (and on the path taken)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            head.peers = None
+            config["grad_x_allreduce"] = "nccl all_reduce (peer path failed in warm-up)"
+            for s in range(a.warmup):
+                step_fn(s, batch_dev, gx)
     torch.cuda.synchronize()
 
     # ---------------- timed region (device-resident inputs)

@@ -228,6 +228,27 @@ xmc_status xmc_kahan_adamw_step(xmc_grid g, float* w, float* comp, float* m, flo
 /* Native-storage RTN cast, e.g. X -> e4m3 bytes (head.py:265). */
 xmc_status xmc_cast_rn(const float* x, void* out, int64_t n, int32_t fmt, int32_t* status, void* stream);
 
+/* ---- node-local grad_X all-reduce over peer memory ----
+ * Replaces the per-step `ncclAllReduce(sum)` of the ranks' partial grad_X
+ * (the sum head_update's callers need when W is label-sharded; head.py:254-298
+ * returns one rank's partial) together with the step's own reduction of the
+ * grad_X partial slots: ONE kernel pushes each 32x32 tile of the rank's
+ * partial into every peer's exchange buffer over NVLink (CUDA IPC mapping),
+ * waits for the same tile from every peer and sums them in rank order, so all
+ * ranks return bit-identical grad_X.
+ *   xmc_peer_create  allocates this rank's exchange buffer (cudaMalloc) and
+ *                    writes its 64-byte cudaIpcMemHandle_t to `handle`;
+ *   xmc_peer_connect maps every peer's buffer (`handles`: world x 64 bytes,
+ *                    rank order, swapped by the caller, e.g. all_gather);
+ *   xmc_head_attach_peers  makes xmc_head_step* return the node's grad_X
+ *                    (NULL detaches).  Every rank must run the same steps. */
+typedef struct xmc_peer* xmc_peer_t;
+xmc_status xmc_peer_create(int32_t rank, int32_t world, int32_t dim, int32_t max_batch, xmc_peer_t* out,
+                           void* handle);
+xmc_status xmc_peer_connect(xmc_peer_t p, const void* handles);
+xmc_status xmc_peer_destroy(xmc_peer_t p);
+xmc_status xmc_head_attach_peers(xmc_head_t h, xmc_peer_t p);
+
 /* ---- measurement (no reference counterpart; used by bench.py) ---- */
 /* Bracket every logits+G (fwd) and grad_X+update (bwd) launch with CUDA
  * events on its stream; xmc_profile_read syncs them, returns summed device ms

@@ -65,6 +65,10 @@ _SIGNATURES = {
     "xmc_head_workspace_size": ([ctypes.POINTER(HeadDesc), ctypes.POINTER(ctypes.c_size_t)], _I32),
     "xmc_head_create": ([ctypes.POINTER(HeadDesc), _P, ctypes.c_size_t, ctypes.POINTER(_P)], _I32),
     "xmc_head_destroy": ([_P], _I32),
+    "xmc_peer_create": ([_I32, _I32, _I32, _I32, ctypes.POINTER(_P), _P], _I32),
+    "xmc_peer_connect": ([_P, _P], _I32),
+    "xmc_peer_destroy": ([_P], _I32),
+    "xmc_head_attach_peers": ([_P, _P], _I32),
     "xmc_head_step": ([_P, _P, _P, _I32, _P, _P, _I64, ctypes.POINTER(StepArgs), _P, _P, _P], _I32),
     "xmc_head_step_kahan": ([_P, _P, _P, _P, _I32, _P, _P, _I64, ctypes.POINTER(StepArgs), _P, _P, _P], _I32),
     "xmc_head_check": ([_P, _P], _I32),

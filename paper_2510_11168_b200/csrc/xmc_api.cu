@@ -241,6 +241,22 @@ struct xmc_head {
   } adam;
   size_t l2_persist;   // persisting-L2 bytes granted for the G window (0 = off)
   size_t l2_window_max;
+  struct xmc_peer* peer = nullptr;   // node-local grad_X all-reduce group (xmc_head_attach_peers)
+};
+
+// ---- node-local grad_X all-reduce over peer memory (CUDA IPC / NVLink P2P) ----
+// Every rank cudaMallocs one exchange buffer and maps every peer's (IPC
+// handles swapped by the caller).  Layout, identical on all ranks:
+//   xin   [2 parity][world src][nblocks][1024] fp32   32x32 grad_X tiles pushed by rank src
+//   flags [2 parity][world src][nblocks] int32         epoch of the step that pushed the tile
+constexpr int kMaxPeers = 8;
+struct xmc_peer {
+  int rank = 0, world = 1, dim = 0, max_bp = 0, nblocks = 0;
+  uint8_t* local = nullptr;   // own exchange buffer
+  size_t bytes = 0, flag_off = 0;
+  void* base[kMaxPeers] = {};   // every rank's buffer as mapped here (own = local)
+  int32_t epoch = 0;
+  bool connected = false;
 };
 
 // ---- fused step: forward and backward of a chunk in ONE persistent launch ----
@@ -555,6 +571,76 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   return XMC_OK;
 }
 
+// ---- peer group (C ABI) ----
+extern "C" xmc_status xmc_peer_create(int32_t rank, int32_t world, int32_t dim, int32_t max_batch, xmc_peer_t* out,
+                                      void* handle) {
+  if (!out || !handle) return fail(XMC_ERR_ARG, "null argument");
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+    return fail(XMC_ERR_ARG, "rank %d / world %d outside [0, %d)", rank, world, kMaxPeers);
+  if (dim <= 0 || dim % 128 != 0) return fail(XMC_ERR_SHAPE, "dim must be a positive multiple of 128");
+  if (max_batch < 1 || max_batch > 512) return fail(XMC_ERR_ARG, "max_batch outside [1, 512]");
+  auto* p = new xmc_peer();
+  p->rank = rank;
+  p->world = world;
+  p->dim = dim;
+  p->max_bp = std::max(padded_batch(2, max_batch), 128);   // covers either format's padded batch
+  p->nblocks = (dim / 32) * (p->max_bp / 32);
+  const size_t xin = static_cast<size_t>(2) * world * p->nblocks * 1024 * 4;
+  p->flag_off = align_up(xin, 256);
+  p->bytes = p->flag_off + static_cast<size_t>(2) * world * p->nblocks * 4;
+  cudaError_t e = cudaMalloc(&p->local, p->bytes);
+  if (e == cudaSuccess) e = cudaMemset(p->local, 0, p->bytes);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(handle), p->local);
+  if (e != cudaSuccess) {
+    if (p->local) cudaFree(p->local);
+    delete p;
+    cudaGetLastError();
+    return fail(XMC_ERR_CUDA, "peer exchange buffer: %s", cudaGetErrorString(e));
+  }
+  p->base[rank] = p->local;
+  *out = p;
+  return XMC_OK;
+}
+
+extern "C" xmc_status xmc_peer_connect(xmc_peer_t p, const void* handles) {
+  if (!p || !handles) return fail(XMC_ERR_ARG, "null argument");
+  if (p->connected) return XMC_OK;
+  const auto* hs = static_cast<const cudaIpcMemHandle_t*>(handles);
+  for (int r = 0; r < p->world; ++r) {
+    if (r == p->rank) continue;
+    void* q = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&q, hs[r], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      for (int k = 0; k < r; ++k)
+        if (k != p->rank && p->base[k]) cudaIpcCloseMemHandle(p->base[k]);
+      return fail(XMC_ERR_CUDA, "peer %d exchange buffer not mappable: %s", r, cudaGetErrorString(e));
+    }
+    p->base[r] = q;
+  }
+  p->connected = true;
+  return XMC_OK;
+}
+
+extern "C" xmc_status xmc_peer_destroy(xmc_peer_t p) {
+  if (!p) return XMC_OK;
+  cudaDeviceSynchronize();
+  for (int r = 0; r < p->world; ++r)
+    if (r != p->rank && p->base[r]) cudaIpcCloseMemHandle(p->base[r]);
+  if (p->local) cudaFree(p->local);
+  delete p;
+  cudaGetLastError();
+  return XMC_OK;
+}
+
+extern "C" xmc_status xmc_head_attach_peers(xmc_head_t h, xmc_peer_t p) {
+  if (!h) return fail(XMC_ERR_ARG, "null handle");
+  if (p && (!p->connected || p->dim != h->desc.dim || p->max_bp < h->max_bp))
+    return fail(XMC_ERR_ARG, "peer group not connected or built for another dim / batch");
+  h->peer = p;
+  return XMC_OK;
+}
+
 extern "C" xmc_status xmc_head_destroy(xmc_head_t h) {
   delete h;
   return XMC_OK;
@@ -651,6 +737,75 @@ __global__ void __launch_bounds__(1024) gx_reduce_kernel(const float* __restrict
     float* o = gx + (int64_t)s2 * d + c2;
     *o = accumulate ? *o + tile[threadIdx.x][threadIdx.y] : tile[threadIdx.x][threadIdx.y];
   }
+}
+
+struct PeerArgs {
+  uint8_t* base[kMaxPeers];   // every rank's exchange buffer, mapped in this process
+  int32_t rank, world, nblocks;
+  int32_t epoch;
+  int64_t flag_off;           // byte offset of the flags in a buffer
+  int32_t* status;
+};
+
+// grad_X of the node in one kernel: each 32x32 tile of this rank's partial
+// sum (its R slots, as gx_reduce_kernel) is pushed into every rank's exchange
+// buffer over NVLink, released by a per-(rank, tile) epoch flag; then the
+// block waits for the same tile from every peer and sums the world pushes in
+// rank order, so every rank ends with bit-identical grad_X.  A block pushes
+// before it waits and waits only for the same tile index, so the exchange
+// needs no grid-wide co-residency.  Exchange buffers alternate by step parity;
+// a rank rewrites parity p two steps later, after every peer has passed the
+// next step's flags, i.e. finished reading parity p.
+__global__ void __launch_bounds__(1024) gx_reduce_peer_kernel(const float* __restrict__ ws, int R, int d, int ld,
+                                                              int B, float scale, float* __restrict__ gx,
+                                                              const __grid_constant__ PeerArgs pa) {
+  __shared__ float tile[32][33];
+  griddep_wait();
+  const int c = blockIdx.x * 32 + threadIdx.y, s = blockIdx.y * 32 + threadIdx.x;
+  float acc = 0.f;
+  if (s < B) {
+    const float* p = ws + (int64_t)c * ld + s;
+    const int64_t stride = (int64_t)d * ld;
+    float v[8];
+    int r = 0;
+    for (; r + 8 <= R; r += 8) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldg(p + (r + k) * stride);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += v[k];
+    }
+    for (; r < R; ++r) acc += __ldg(p + r * stride);
+  }
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int bid = blockIdx.y * gridDim.x + blockIdx.x;
+  const int par = pa.epoch & 1;
+  const int64_t slot = (static_cast<int64_t>(par) * pa.world + pa.rank) * pa.nblocks + bid;
+  for (int q = 0; q < pa.world; ++q) __stcg(reinterpret_cast<float*>(pa.base[q]) + slot * 1024 + tid, acc * scale);
+  __threadfence_system();
+  __syncthreads();
+  if (tid < pa.world) {   // release this tile to rank tid, then wait for rank tid's tile
+    st_release_sys(reinterpret_cast<int32_t*>(pa.base[tid] + pa.flag_off) + slot, pa.epoch);
+    const int32_t* f = reinterpret_cast<const int32_t*>(pa.base[pa.rank] + pa.flag_off) +
+                       (static_cast<int64_t>(par) * pa.world + tid) * pa.nblocks + bid;
+    if (ld_acquire_sys(f) < pa.epoch) {
+      const long long t0 = clock64();
+      while (ld_acquire_sys(f) < pa.epoch) {
+        if (clock64() - t0 > (1ll << 33)) {
+          atomicOr(pa.status, ST_PEER_TIMEOUT);
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const float* mine = reinterpret_cast<const float*>(pa.base[pa.rank]);
+  float tot = 0.f;
+  for (int q = 0; q < pa.world; ++q)
+    tot += __ldcg(mine + ((static_cast<int64_t>(par) * pa.world + q) * pa.nblocks + bid) * 1024 + tid);
+  tile[threadIdx.y][threadIdx.x] = tot;
+  __syncthreads();
+  const int s2 = blockIdx.y * 32 + threadIdx.y, c2 = blockIdx.x * 32 + threadIdx.x;
+  if (s2 < B) gx[(int64_t)s2 * d + c2] = tile[threadIdx.x][threadIdx.y];
 }
 
 // Bitonic sort of 32 (key, value) pairs across a warp (15 shuffle exchanges).
@@ -1410,6 +1565,32 @@ static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumul
                             float scale = 1.0f) {
   const int D = h->desc.dim;
   dim3 g(D / 32, (Bp + 31) / 32), b(32, 32);
+  if (h->peer && h->peer->connected && !accumulate) {
+    // fused local reduction + node all-reduce (replaces reduce + ncclAllReduce)
+    xmc_peer* pg = h->peer;
+    if (D != pg->dim || Bp > pg->max_bp) return fail(XMC_ERR_SHAPE, "peer group built for another dim / batch");
+    PeerArgs pa{};
+    for (int r = 0; r < pg->world; ++r) pa.base[r] = static_cast<uint8_t*>(pg->base[r]);
+    pa.rank = pg->rank;
+    pa.world = pg->world;
+    pa.nblocks = pg->nblocks;
+    pa.flag_off = static_cast<int64_t>(pg->flag_off);
+    pa.epoch = ++pg->epoch;
+    pa.status = h->status;
+    cudaLaunchConfig_t pc{};
+    pc.gridDim = g;
+    pc.blockDim = b;
+    pc.stream = st;
+    cudaLaunchAttribute pat[1];
+    pat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pat[0].val.programmaticStreamSerializationAllowed = 1;
+    pc.attrs = pat;
+    pc.numAttrs = pdl_enabled(h) ? 1 : 0;
+    CUDA_TRY(cudaLaunchKernelEx(&pc, gx_reduce_peer_kernel, static_cast<const float*>(h->gx_ws), h->R_step, D, Bp,
+                                B, (h->eb == 1 ? (1.0f / 256.0f) : 1.0f) * scale, acc, pa));
+    CUDA_TRY(cudaGetLastError());
+    return XMC_OK;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = g;
   cfg.blockDim = b;
@@ -1491,6 +1672,7 @@ static xmc_status read_status(xmc_head* h, cudaStream_t st, bool clear) {
   if (s & ST_LABEL_OUTSIDE) return fail(XMC_ERR_LABEL, "label outside chunk range");
   if (s & ST_NONFINITE_GRAD) return fail(XMC_ERR_NONFINITE, "non-finite values in fused scratch block");
   if (s & ST_RING_TIMEOUT) return fail(XMC_ERR_CUDA, "fused step: a G ring flag timed out (CTAs not co-resident)");
+  if (s & ST_PEER_TIMEOUT) return fail(XMC_ERR_CUDA, "peer grad_X all-reduce: a peer's tile never arrived");
   return XMC_OK;
 }
 

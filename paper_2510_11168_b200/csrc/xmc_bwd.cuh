@@ -40,6 +40,7 @@ enum StatusBits : int32_t {
   ST_CAPACITY = 16,
   ST_NONFINITE_MOMENTS = 32,
   ST_RING_TIMEOUT = 64,   // fused step: a ring flag never arrived (CTAs not co-resident)
+  ST_PEER_TIMEOUT = 128,  // peer grad_X all-reduce: a peer's tile never arrived
 };
 
 struct BwdParams {

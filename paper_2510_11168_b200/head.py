@@ -150,6 +150,7 @@ class ChunkedHead:
         self._handle = None
         self.last_stats = None
         self.collect_stats = False   # True: head_update also returns sum|G| in last_stats[0]
+        self.peers = None            # parallel.PeerGroup: head_update returns the node's summed grad_X
 
     # -- construction -------------------------------------------------------
     @classmethod
@@ -329,10 +330,14 @@ def head_update(head: ChunkedHead, batch: BatchInput, cfg: SgdSrConfig, rng: Rou
         acc_h = tracker.alloc("input_grad_accumulator", "accumulator", b * head.dim * 4)
     try:
         if probe is not None:
+            if head.peers is not None:
+                raise NotImplementedError("probe + peer all-reduce: use the fused step (probe=None)")
             if head.comp is not None:
                 raise NotImplementedError("probe + head-Kahan: use the fused step (probe=None)")
             return _head_update_unfused(head, X, si, li, cfg, rng, step, tracker, probe)
         h = head.handle(b, si.numel())
+        # node-local peer all-reduce of grad_X (parallel.PeerGroup), or none
+        _lib.check(_lib.load().xmc_head_attach_peers(h.h, head.peers.p if head.peers is not None else None))
         gx = grad_out if grad_out is not None else torch.empty((b, head.dim), dtype=torch.float32, device=dev)
         stats_ptr = None
         if head.collect_stats:  # sum |G| of the step (trainer divergence proxy)

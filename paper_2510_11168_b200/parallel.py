@@ -15,11 +15,13 @@ reference's ``top_k_indices`` order (metrics.py:38-47).
 
 from __future__ import annotations
 
+import ctypes
 from typing import Callable
 
 import torch
 import torch.distributed as dist
 
+from . import _lib
 from .head import ChunkedHead, partition
 
 
@@ -84,6 +86,49 @@ def broadcast_batch(X, sample_idx, label_idx, src: int = 0, group=None):
     return X, si, li
 
 
+class PeerGroup:
+    """Node-local grad_X all-reduce over peer memory (include/xmc_head.h,
+    xmc_peer_*): replaces ``dist.all_reduce(grad_X)`` after the step.  Each
+    rank allocates an exchange buffer, the CUDA IPC handles are swapped with
+    one ``all_gather_object`` on ``group`` (any backend), and every peer buffer
+    is mapped over NVLink.  Attached to a ChunkedHead, head_update's own
+    grad_X reduction pushes each 32x32 tile to every rank and sums the ranks'
+    tiles in rank order: one kernel, bit-identical grad_X on every rank.
+    Raises RuntimeError when a peer buffer cannot be mapped (callers fall back
+    to dist.all_reduce)."""
+
+    def __init__(self, dim: int, max_batch: int, group=None):
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        lib = _lib.load()
+        self.p = ctypes.c_void_p()
+        handle = (ctypes.c_char * 64)()
+        _lib.check(lib.xmc_peer_create(self.rank, self.world, dim, max_batch, ctypes.byref(self.p),
+                                       ctypes.cast(handle, ctypes.c_void_p)))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        buf = (ctypes.c_char * (64 * self.world)).from_buffer_copy(b"".join(handles))
+        try:
+            _lib.check(lib.xmc_peer_connect(self.p, ctypes.cast(buf, ctypes.c_void_p)))
+        except Exception:
+            self.close()
+            raise
+
+    def attach(self, head: ChunkedHead) -> None:
+        head.peers = self
+
+    def close(self) -> None:
+        if self.p:
+            _lib.load().xmc_peer_destroy(self.p)
+            self.p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class ShardedHead:
     """A rank's shard of a label-sharded head.
 
@@ -113,7 +158,7 @@ class ShardedHead:
     def head_update(self, batch, cfg, rng, step: int) -> torch.Tensor:
         """head_update over all shards; returns the full grad_X on every rank."""
         gx = self._step(batch, cfg, rng, step)
-        if self.world > 1:
+        if self.world > 1 and (self.local is None or self.local.peers is None):
             dist.all_reduce(gx, op=dist.ReduceOp.SUM, group=self.group)
         return gx
 
