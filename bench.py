@@ -48,7 +48,7 @@ def parse():
     # k=2 measured fastest on B200 (fewer launch tails), peak HBM ~2.5 GiB
     ap.add_argument("--chunks", type=int, default=2)
     ap.add_argument("--rounding", default="stochastic")
-    ap.add_argument("--sr-impl", default="philox")
+    ap.add_argument("--sr-impl", default="hash", choices=["hash", "philox", "splitmix64"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--cpu-labels", type=int, default=8192)

@@ -44,7 +44,9 @@ typedef enum { XMC_FMT_FP32 = 0, XMC_FMT_BF16 = 1, XMC_FMT_FP16 = 2, XMC_FMT_E4M
 /* SgdSrConfig.rounding (optimizers.py:28-41).  SR_EXACT draws u from the
  * reference's splitmix64 keyed generator (rng.py:36-57) and compares in fp64
  * exactly like round_stochastic (formats.py:209-225): bit-identical decisions.
- * SR_FAST uses Philox4x32-7 bits with the hardware cvt.rs conversion. */
+ * SR_FAST feeds keyed random words to the hardware cvt.rs conversion: a
+ * stateless PCG hash of (element / 4 + key(seed, step, tensor_id)) by default,
+ * or Philox4x32-7 (xmc_step_args.sr_bits = 1). */
 typedef enum { XMC_ROUND_NEAREST = 0, XMC_ROUND_SR_EXACT = 1, XMC_ROUND_SR_FAST = 2 } xmc_rounding;
 
 /* Head geometry: ChunkedHead (head.py:69-112) restricted to one rank's label
@@ -76,7 +78,7 @@ typedef struct {
   float lr;            /* > 0                                   */
   float weight_decay;  /* >= 0                                  */
   int32_t rounding;    /* xmc_rounding                          */
-  int32_t reserved;
+  int32_t sr_bits;     /* XMC_ROUND_SR_FAST bit source: 0 keyed PCG hash (default), 1 Philox4x32-7 */
   uint64_t seed;       /* RoundingRng(seed)                     */
   uint64_t step;       /* step index keying the draws           */
   uint64_t tensor_id;  /* ChunkedHead.tensor_id (HEAD_WEIGHTS_TAG) */

@@ -40,7 +40,7 @@ class HeadDesc(ctypes.Structure):
 
 class StepArgs(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_float), ("weight_decay", ctypes.c_float),
-                ("rounding", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("rounding", ctypes.c_int32), ("sr_bits", ctypes.c_int32),
                 ("seed", ctypes.c_uint64), ("step", ctypes.c_uint64),
                 ("tensor_id", ctypes.c_uint64), ("dropout_p", ctypes.c_double)]
 

@@ -1438,6 +1438,7 @@ static xmc_status setup_bwd(xmc_head* h, void* W, void* comp, int64_t row0, int6
   p.dw_scale = eb == 1 ? (1.0f / 256.0f) : 1.0f;
   p.rounding = a ? a->rounding : 0;
   p.rng_base = a ? sm64_base(a->seed, a->step, a->tensor_id) : 0;
+  p.sr_bits = a ? a->sr_bits : 0;
   p.gx_ws = h->gx_ws;
   p.gx_ld = Bp;
   p.gx_accumulate = gx_overwrite ? 0 : 1;
@@ -1616,6 +1617,7 @@ static xmc_status check_args(const xmc_step_args* a) {
   if (!(a->lr > 0.0f)) return fail(XMC_ERR_ARG, "lr must be positive");
   if (!(a->weight_decay >= 0.0f)) return fail(XMC_ERR_ARG, "weight_decay must be non-negative");
   if (a->rounding < 0 || a->rounding > 2) return fail(XMC_ERR_ARG, "unknown rounding mode %d", a->rounding);
+  if (a->sr_bits < 0 || a->sr_bits > 1) return fail(XMC_ERR_ARG, "unknown SR bit generator %d", a->sr_bits);
   return XMC_OK;
 }
 

@@ -58,7 +58,8 @@ struct BwdParams {
   int64_t row0_global;   // global label of chunk row 0 (RNG key)
   float lr, wd, dw_scale;
   int32_t rounding;      // ROUND_NEAREST / ROUND_SR_EXACT / ROUND_SR_FAST
-  uint64_t rng_base;     // splitmix64 base(seed, step, tensor_id); Philox key
+  uint64_t rng_base;     // splitmix64 base(seed, step, tensor_id); Philox / hash key
+  int32_t sr_bits;       // ROUND_SR_FAST bits: 0 keyed PCG hash, 1 Philox4x32-7
   float* gx_ws;          // [R][d][gx_ld] fp32 partials (gx_ld = padded batch)
   int32_t gx_ld;
   int32_t gx_accumulate; // 1: add into the partial slot, 0: overwrite it
@@ -173,7 +174,25 @@ XMC_DEV void w_decode(const uint4 (&raw)[2 * EB], float (&w)[32]) {
 // of 32).  e4m3: one word per cvt.rs.e4m3x4 (4 elements, 16 random bits per
 // lane, see profiles/r1_probe_cvt_rs.txt); bf16: one word per bf16x2.
 template <int EB>
-XMC_DEV void sr_words(const PhiloxKeys& ks, int64_t flat0, uint32_t (&rw)[8 * EB]) {
+XMC_DEV void sr_words(const PhiloxKeys& ks, int64_t flat0, uint32_t (&rw)[8 * EB], bool philox) {
+#ifdef XMC_WHATIF_NO_RNG   // measurement only: the SR bits without the generator's cost
+#pragma unroll
+  for (int k = 0; k < 8 * EB; ++k) rw[k] = static_cast<uint32_t>(flat0) * 0x9E3779B9u + k;
+  return;
+#endif
+  if (!philox) {
+    // keyed hash: word i of the step = pcg_hash(i + key(seed, step, tensor_id))
+    // (the RXS-M-XS output function of PCG as a stateless integer hash);
+    // word i carries the cvt.rs bits of elements 4i .. 4i+3
+    const uint32_t base = static_cast<uint32_t>(static_cast<uint64_t>(flat0) >> 2) + ks.hk;
+#pragma unroll
+    for (int k = 0; k < 8 * EB; ++k) {
+      const uint32_t st = (base + k) * 747796405u + 2891336453u;
+      const uint32_t w = ((st >> ((st >> 28u) + 4u)) ^ st) * 277803737u;
+      rw[k] = (w >> 22u) ^ w;
+    }
+    return;
+  }
 #pragma unroll
   for (int h = 0; h < 2 * EB; ++h) {
     const uint64_t ctr = static_cast<uint64_t>(flat0) / (16 / EB) + h;
@@ -733,7 +752,7 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
           // W_old decoded and scaled by 1 - lr wd) is computed and pinned in
           // registers BEFORE the dW wait, so it overlaps the MMAs
           uint32_t rw[8];
-          sr_words<1>(pk, flat0, rw);
+          sr_words<1>(pk, flat0, rw, p.sr_bits != 0);
           const float c_wd = 1.0f - p.lr * p.wd;
           const float a_lr = -p.lr * p.dw_scale;
           float wc[32];
@@ -801,7 +820,7 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
         uint32_t km = 0u;   // dropout keep bits of this thread's 32 columns
         if (p.keep != nullptr && grow < p.rows) km = __ldg(p.keep + grow * (p.d >> 5) + ((j * 128 + c0) >> 5));
         uint32_t rw[C::kRandWords];
-        if (p.rounding == ROUND_SR_FAST) sr_words<EB>(pk, flat0, rw);
+        if (p.rounding == ROUND_SR_FAST) sr_words<EB>(pk, flat0, rw, p.sr_bits != 0);
         float w[CE > 0 ? 1 : 32];
         if constexpr (CE == 0) w_decode<EB>(raw, w);
         // --- dW from TMEM, then release the accumulator buffer at once

@@ -91,10 +91,12 @@ constexpr int kPhiloxRounds = 7;
 // schedule is the same for every counter of a launch
 struct PhiloxKeys {
   uint32_t k0[kPhiloxRounds], k1[kPhiloxRounds];
+  uint32_t hk;   // 32-bit key of the hash generator
 };
 XMC_DEV PhiloxKeys philox_keys(uint64_t key) {
   PhiloxKeys ks;
   uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
+  ks.hk = k0 ^ (k1 * 0x85EBCA6Bu);
 #pragma unroll
   for (int i = 0; i < kPhiloxRounds; ++i) {
     ks.k0[i] = k0;

@@ -289,7 +289,8 @@ def _as_idx(a, device) -> torch.Tensor:
 def _step_args(cfg: SgdSrConfig | None, rng: RoundingRng, step: int, tensor_id: int,
                dropout_p: float = 0.0) -> _lib.StepArgs:
     lr, wd, rc = (cfg.lr, cfg.weight_decay, cfg.rounding_code) if cfg is not None else (0.0, 0.0, 0)
-    return _lib.StepArgs(lr, wd, rc, 0, rng.seed, step & (2**64 - 1), tensor_id & (2**64 - 1),
+    bits = cfg.sr_bits if cfg is not None else 0
+    return _lib.StepArgs(lr, wd, rc, bits, rng.seed, step & (2**64 - 1), tensor_id & (2**64 - 1),
                          float(dropout_p))
 
 

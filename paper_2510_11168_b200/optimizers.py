@@ -4,9 +4,13 @@
 (optimizers.py:28-41) and adds ``sr_impl``: the draw generator used when
 ``rounding == "stochastic"``.
 
-* ``"philox"`` (default, the fast product path): Philox4x32-7 random bits
-  fed to the sm_100a hardware stochastic-rounding conversion (cvt.rs).  SR
-  decisions match the reference in distribution (unbiased, same variance).
+* ``"hash"`` (default, the fast product path): keyed random words fed to the
+  sm_100a hardware stochastic-rounding conversion (cvt.rs); word i of a step
+  is a stateless PCG hash (RXS-M-XS) of i + key(seed, step, tensor_id), the
+  same keyed-hash construction as the reference's splitmix64 draws
+  (rng.py:36-57) at a quarter of Philox's instruction cost.  SR decisions
+  match the reference in distribution (unbiased, same variance).
+* ``"philox"``: the same conversion with Philox4x32-7 words.
 * ``"splitmix64"``: the reference's own keyed generator (rng.py:36-57) and
   fp64 neighbour/probability comparison (formats.py:209-225).  Given the same
   fp32 update value the decision is bit-identical to the reference.
@@ -31,7 +35,7 @@ class SgdSrConfig:
     weight_decay: float = 0.0
     fmt: FloatFormat = field(default_factory=lambda: FP32)
     rounding: str = "stochastic"  # or "nearest"
-    sr_impl: str = "philox"       # or "splitmix64" (bit-exact reference draws)
+    sr_impl: str = "hash"         # or "philox", or "splitmix64" (bit-exact reference draws)
 
     def __post_init__(self):
         if self.lr <= 0:
@@ -40,14 +44,19 @@ class SgdSrConfig:
             raise ValueError("weight_decay must be non-negative")
         if self.rounding not in ("stochastic", "nearest"):
             raise ValueError(f"unknown rounding mode {self.rounding!r}")
-        if self.sr_impl not in ("philox", "splitmix64"):
+        if self.sr_impl not in ("hash", "philox", "splitmix64"):
             raise ValueError(f"unknown SR generator {self.sr_impl!r}")
 
     @property
     def rounding_code(self) -> int:
         if self.rounding == "nearest":
             return _lib.ROUND_NEAREST
-        return _lib.ROUND_SR_FAST if self.sr_impl == "philox" else _lib.ROUND_SR_EXACT
+        return _lib.ROUND_SR_EXACT if self.sr_impl == "splitmix64" else _lib.ROUND_SR_FAST
+
+    @property
+    def sr_bits(self) -> int:
+        """xmc_step_args.sr_bits: the SR_FAST word generator (0 hash, 1 Philox)."""
+        return 1 if self.sr_impl == "philox" else 0
 
 
 def sgd_sr_step(w: torch.Tensor, grad, cfg: SgdSrConfig, rng, step: int, tensor_id: int = 0,

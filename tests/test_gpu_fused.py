@@ -3,7 +3,7 @@ persistent kernel, G handed over through an L2 ring) and the
 split-layout forward (XMC_FWD_SPLIT=1) are measurement options, read from the
 environment once per process.  Each runs in a child process on the same
 seeded step and must reproduce the default path's weights bit for bit (same G,
-same Philox draws) and its grad_X to fp32 summation-order tolerance."""
+same SR draws) and its grad_X to fp32 summation-order tolerance."""
 
 import os
 import subprocess
@@ -28,7 +28,7 @@ rs = np.random.default_rng(3)
 X = rs.normal(size=(B, D)).astype(np.float32)
 si, li = O.synthetic_positives(L, B, 5.45, seed=4)
 head = xmc.ChunkedHead(xmc.QuantizedMatrix(W0, xmc.E4M3), num_chunks=k, num_labels_global=L)
-cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=xmc.E4M3, rounding="stochastic", sr_impl="philox")
+cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=xmc.E4M3, rounding="stochastic", sr_impl="hash")
 for step in range(2):
     gx = xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(11), step)
 torch.cuda.synchronize()

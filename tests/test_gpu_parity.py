@@ -385,7 +385,8 @@ def test_chunk_invariance_bitwise(xmc, fmt_name, B):
         assert np.array_equal(bits(o), bits(outs[0]))
 
 
-def test_sr_fast_is_unbiased(xmc):
+@pytest.mark.parametrize("impl", ["hash", "philox"])
+def test_sr_fast_is_unbiased(xmc, impl):
     """acceptance-03 style: many independent keys, mean of SR(x) ~ x."""
     L, d, B = 1024, 256, 128
     fmt = xmc.E4M3
@@ -398,7 +399,7 @@ def test_sr_fast_is_unbiased(xmc):
     X[0, :] = 1.0
     G = np.zeros((L, B), np.float32)
     G[:, 0] = np.float32(0.5)  # dW = 0.5 for every element
-    cfg = xmc.SgdSrConfig(lr=0.0390625, fmt=fmt, rounding="stochastic", sr_impl="philox")
+    cfg = xmc.SgdSrConfig(lr=0.0390625, fmt=fmt, rounding="stochastic", sr_impl=impl)
     xmc.fused_weight_update(head, torch.from_numpy(G).cuda(), torch.from_numpy(X), cfg, xmc.RoundingRng(5), 1,
                             (0, L))
     got = head.weights.values.float().cpu().numpy()
@@ -411,10 +412,11 @@ def test_sr_fast_is_unbiased(xmc):
     assert abs(frac - p) < 4 * np.sqrt(p * (1 - p) / n), (frac, p)
 
 
+@pytest.mark.parametrize("impl", ["hash", "philox"])
 @pytest.mark.parametrize("fmt_name", ["e4m3", "bf16"])
-def test_sr_fast_matches_reference_in_distribution(xmc, fmt_name):
-    """North-star SR check on the fused production path (Philox words into
-    cvt.rs, FAST backward): for every weight the update value x is the
+def test_sr_fast_matches_reference_in_distribution(xmc, fmt_name, impl):
+    """North-star SR check on the fused production path (hash or Philox
+    words into cvt.rs, FAST backward): for every weight the update value x is the
     reference's fp32 update on the same operand G; SR(x) must land on one of
     x's two grid neighbours, be unbiased over all weights (mean error within
     4 sigma of 0) and round up at the rate p = (x - lo) / (hi - lo) within
@@ -428,7 +430,7 @@ def test_sr_fast_matches_reference_in_distribution(xmc, fmt_name):
     lr, wd = 0.05, 1e-4
     head = _make(xmc, W, fmt_name, 1)
     cfg = xmc.SgdSrConfig(lr=lr, weight_decay=wd, fmt=xmc.parse_format(fmt_name), rounding="stochastic",
-                          sr_impl="philox")
+                          sr_impl=impl)
     xmc.fused_weight_update(head, torch.from_numpy(G).cuda(), torch.from_numpy(X), cfg, xmc.RoundingRng(17), 2,
                             (0, L))
     got = head.weights.values.float().cpu().numpy().astype(np.float64)
