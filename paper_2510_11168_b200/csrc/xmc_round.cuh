@@ -4,8 +4,9 @@
 //   * grids, RTN ties-to-even, saturation    formats.py:164-206
 //   * SR neighbours / probability / compare  formats.py:180-194, 209-225
 //   * splitmix64 keyed uniforms              rng.py:15-57
-// The "fast" SR mode replaces splitmix64 by Philox4x32-10 bits and the
-// hardware cvt.rs stochastic-rounding conversion (distributional parity).
+// The "fast" SR mode replaces splitmix64 by keyed hash (or Philox4x32-7)
+// words and the hardware cvt.rs stochastic-rounding conversion
+// (distributional parity).
 #pragma once
 
 #include <cuda_bf16.h>
