@@ -525,17 +525,17 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
               const uint32_t hi = cvt_e4m3x2_rn(g[4 * j + 3], g[4 * j + 2]);
               pk[j] = lo | (hi << 16);
             }
-            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(p.out) + orow * p.ld + xs + col0);
-            st_global_v4_hint(o, make_uint4(pk[0], pk[1], pk[2], pk[3]), pol_g);
-            st_global_v4_hint(o + 1, make_uint4(pk[4], pk[5], pk[6], pk[7]), pol_g);
+            // one 256-bit store: the thread's 32 G bytes are one full sector
+            st_global_v8_hint(reinterpret_cast<uint8_t*>(p.out) + orow * p.ld + xs + col0, pk, pol_g);
           } else {
             uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) pk[j] = cvt_bf16x2_rn(g[2 * j + 1], g[2 * j]);
-            uint4* o = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(p.out) + orow * p.ld + xs + col0);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              st_global_v4_hint(o + j, make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]), pol_g);
+            uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + orow * p.ld + xs + col0;
+            const uint32_t (&pa)[8] = *reinterpret_cast<const uint32_t(*)[8]>(&pk[0]);
+            const uint32_t (&pb)[8] = *reinterpret_cast<const uint32_t(*)[8]>(&pk[8]);
+            st_global_v8_hint(o, pa, pol_g);        // two full 32-B sectors
+            st_global_v8_hint(o + 16, pb, pol_g);
           }
         }
       }

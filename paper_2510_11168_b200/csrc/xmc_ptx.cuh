@@ -127,6 +127,12 @@ XMC_DEV void st_global_v4_hint(void* p, uint4 v, uint64_t policy) {
                "r"(v.w), "l"(policy)
                : "memory");
 }
+// 32-B global store (sm_100: one 256-bit STG, a full sector per thread)
+XMC_DEV void st_global_v8_hint(void* p, const uint32_t (&v)[8], uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(p), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "l"(policy)
+               : "memory");
+}
 XMC_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 XMC_DEV void bulk_wait_read() {
