@@ -460,10 +460,10 @@ def main():
            "step_frac_of_tc_peak": step_flops / (ms_step * 1e-3) / 1e12 / (tc_peak * world),
            "peak_hbm_gib_per_gpu": peak_mem / 2**30,
            # our kernels in the timed region: every fwd / bwd launch (counted by the
-           # library's profiler) + per step: x_prep + single-CTA bucketing for
-           # <= 2048 positives, else x_prep fused with counting + scan + scatter;
-           # and the grad_X reduce
-           "gpu_launches": int(n_fwd + n_bwd + a.steps * ((2 if len(si) <= 2048 else 3) + 1)),
+           # library's profiler) + per step: x_prep fused with single-CTA bucketing
+           # for <= 2048 positives, else x_prep fused with counting + scan +
+           # scatter; and the grad_X reduce (peer all-reduce kernel for N > 1)
+           "gpu_launches": int(n_fwd + n_bwd + a.steps * ((1 if len(si) <= 2048 else 3) + 1)),
            "clocks": clk}
     if rank == 0 and world == 1 and not a.no_cpu:
         cb = cpu_baseline(a, a.cpu_seconds)

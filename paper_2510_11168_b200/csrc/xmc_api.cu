@@ -961,10 +961,10 @@ __global__ void __launch_bounds__(256) pos_scatter_kernel(int64_t nnz, const uin
 // count per (chunk, 128-label tile) -> exclusive scan -> scatter.  Used when
 // the tile count fits shared memory (every BASELINE config per rank).
 constexpr int kPosMaxTiles = 48 * 1024;
-__global__ void __launch_bounds__(1024) pos_bucket_kernel(PosGeom g, const int32_t* __restrict__ ps,
-                                                          const int32_t* __restrict__ pl, int64_t nnz, int32_t T,
-                                                          int32_t* __restrict__ tile_ptr,
-                                                          uint32_t* __restrict__ entries, int32_t* status) {
+__device__ __forceinline__ void pos_bucket_body(PosGeom g, const int32_t* __restrict__ ps,
+                                                const int32_t* __restrict__ pl, int64_t nnz, int32_t T,
+                                                int32_t* __restrict__ tile_ptr, uint32_t* __restrict__ entries,
+                                                int32_t* status) {
   constexpr int kPer = 16;            // positives held in registers per thread per batch
   extern __shared__ int32_t cnt[];    // [T]
   __shared__ int64_t cs[65], tb[65];
@@ -1003,9 +1003,11 @@ __global__ void __launch_bounds__(1024) pos_bucket_kernel(PosGeom g, const int32
       }
     }
     // Zipf labels pile onto a few low tiles: sort each warp's 32 tile ids and
-    // issue one shared atomic per run of equal tiles
+    // issue one shared atomic per run of equal tiles (only the k rounds that
+    // hold positives: nnz is often far below the 16 x 1024 slots)
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
+      if (base0 + static_cast<int64_t>(k) * nth >= nnz) break;   // block-uniform
       uint32_t key = t[k] >= 0 ? static_cast<uint32_t>(t[k]) : 0xffffffffu, val = 0;
       warp_sort_pairs(key, val);
       int st, len;
@@ -1067,6 +1069,7 @@ __global__ void __launch_bounds__(1024) pos_bucket_kernel(PosGeom g, const int32
     }
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
+      if (base0 + static_cast<int64_t>(k) * nth >= nnz) break;   // block-uniform
       uint32_t key = t[k] >= 0 ? static_cast<uint32_t>(t[k]) : 0xffffffffu, val = e[k];
       warp_sort_pairs(key, val);
       int st, len;
@@ -1077,6 +1080,24 @@ __global__ void __launch_bounds__(1024) pos_bucket_kernel(PosGeom g, const int32
       if (key != 0xffffffffu) entries[b + (lane - st)] = val;
     }
   }
+}
+
+// Small batches: the whole step preparation in ONE launch.  Block 0 buckets
+// the positives (pos_bucket_body, 1024 threads); blocks 1.. quantise X into Xq
+// / Xq^T (x_prep_body, one 32x32 tile each).  The two jobs are independent.
+template <int EB>
+__global__ void __launch_bounds__(1024) prep_bucket_kernel(const float* __restrict__ X, int B, int Bp, int d,
+                                                           uint8_t* __restrict__ xq, uint8_t* __restrict__ xqt,
+                                                           PosGeom g, const int32_t* __restrict__ ps,
+                                                           const int32_t* __restrict__ pl, int64_t nnz, int32_t T,
+                                                           int32_t* __restrict__ tile_ptr,
+                                                           uint32_t* __restrict__ entries, int32_t* status) {
+  if (blockIdx.x == 0) {
+    pos_bucket_body(g, ps, pl, nnz, T, tile_ptr, entries, status);
+    return;
+  }
+  const int b = static_cast<int>(blockIdx.x) - 1, nxc = d / 32;
+  x_prep_body<EB>(X, B, Bp, d, xq, xqt, status, b % nxc, b / nxc, threadIdx.x & 31, threadIdx.x >> 5, 32);
 }
 
 // fp32 G (rows x B, ld) -> backward operand format (e4m3 x scale or bf16), [rows][Bp]
@@ -1633,7 +1654,8 @@ static xmc_status prepare_step(xmc_head* h, const float* X, int Bp, const int32_
             h->desc.label_offset, h->desc.num_labels_local, B};
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(pos_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPosMaxTiles * 4);
+    cudaFuncSetAttribute(prep_bucket_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPosMaxTiles * 4);
+    cudaFuncSetAttribute(prep_bucket_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kPosMaxTiles * 4);
     cudaFuncSetAttribute(pos_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPosMaxTiles * 4);
     attr = true;
   }
@@ -1642,9 +1664,14 @@ static xmc_status prepare_step(xmc_head* h, const float* X, int Bp, const int32_
     return fail(XMC_ERR_UNSUPPORTED, "%d label tiles per rank exceed the bucketing capacity %d; use more ranks", T,
                 kPosMaxTiles);
   if (nnz <= 2048) {
-    // tiny batches: one launch, everything in one CTA's shared memory
-    XMC_TRY(launch_x_prep(h, X, B, Bp, st));
-    pos_bucket_kernel<<<1, 1024, T * 4, st>>>(g, ps, pl, nnz, T, h->tile_ptr, h->entries, h->status);
+    // tiny batches: one launch (block 0 buckets in shared memory, the rest prepare Xq)
+    const int nblk = 1 + (h->desc.dim / 32) * (Bp / 32);
+    if (h->eb == 1)
+      prep_bucket_kernel<1><<<nblk, 1024, T * 4, st>>>(X, B, Bp, h->desc.dim, h->xq, h->xqt, g, ps, pl, nnz, T,
+                                                       h->tile_ptr, h->entries, h->status);
+    else
+      prep_bucket_kernel<2><<<nblk, 1024, T * 4, st>>>(X, B, Bp, h->desc.dim, h->xq, h->xqt, g, ps, pl, nnz, T,
+                                                       h->tile_ptr, h->entries, h->status);
     CUDA_TRY(cudaGetLastError());
     return XMC_OK;
   }
