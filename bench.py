@@ -253,10 +253,18 @@ def main():
     import paper_2510_11168_b200 as xmc
     from paper_2510_11168_b200 import _lib
 
+    # test hook (XMC_BENCH_ONE_DEVICE=1): every rank on cuda:0 with gloo, so the
+    # multi-rank flow (peer all-reduce, fallbacks, max-over-ranks timing) runs
+    # on a one-GPU box; its timings are meaningless (the ranks time-slice)
+    one_dev = os.environ.get("XMC_BENCH_ONE_DEVICE") == "1"
+    local = 0 if one_dev else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     lo, hi = xmc.partition(a.labels, world)[rank]
     fmt = xmc.parse_format(a.fmt)
 
@@ -286,7 +294,7 @@ def main():
     allreduce = "none (1 rank)"
     peers = None
     if world > 1:
-        allreduce = "nccl all_reduce"
+        allreduce = "gloo all_reduce (one-device test hook)" if one_dev else "nccl all_reduce"
         if os.environ.get("XMC_PEER", "1") != "0":
             from paper_2510_11168_b200.parallel import PeerGroup
             try:
