@@ -44,9 +44,12 @@ def parse():
     ap.add_argument("--dim", type=int, default=768)
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--fmt", default="e4m3")
-    # label chunks per rank (the reference's memory knob, head.num_chunks):
-    # k=2 measured fastest on B200 (fewer launch tails), peak HBM ~2.5 GiB
-    ap.add_argument("--chunks", type=int, default=2)
+    # label chunks per rank (the reference's memory knob, head.num_chunks).
+    # Default: the fewest chunks of at most --max-chunk-rows rows each, so the
+    # G buffer per GPU stays the same at every N (C4: k=2 on 1 GPU, k=1 per
+    # rank on 2-8 GPUs; fewer, larger chunks have fewer launch tails)
+    ap.add_argument("--chunks", type=int, default=None)
+    ap.add_argument("--max-chunk-rows", type=int, default=1_406_141)
     ap.add_argument("--rounding", default="stochastic")
     ap.add_argument("--sr-impl", default="hash", choices=["hash", "philox", "splitmix64"])
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -231,6 +234,9 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     metric = "head train samples/sec at 3M labels FP8"
+    if a.chunks is None:
+        shard_rows = -(-a.labels // world)
+        a.chunks = max(1, -(-shard_rows // a.max_chunk_rows))
     config = {"workload": f"Amazon-3M head step: L={a.labels}, d={a.dim}, B={a.batch}, {a.fmt} weights, "
                           f"k={a.chunks} chunks, SR={a.rounding}/{a.sr_impl}, lr=0.05, wd=1e-4",
               "labels": a.labels, "dim": a.dim, "global_batch": a.batch, "chunks": a.chunks,
