@@ -88,3 +88,31 @@ def test_positive_bucketing_host_model():
         assert not seen[slot]
         seen[slot] = True
     assert seen.sum() == L
+
+
+def test_peer_group_argument_checks_without_device():
+    """xmc_peer_create validates rank / world / dim / batch before any CUDA
+    call, and the step-args generator field is range-checked (no GPU here)."""
+    import ctypes
+    from paper_2510_11168_b200 import _lib
+    from paper_2510_11168_b200.optimizers import SgdSrConfig
+    lib = _lib.load()
+    p = ctypes.c_void_p()
+    h = (ctypes.c_char * 64)()
+    hv = ctypes.cast(h, ctypes.c_void_p)
+    assert lib.xmc_peer_create(0, 0, 768, 256, ctypes.byref(p), hv) == _lib.XMC_ERR_ARG      # world 0
+    assert lib.xmc_peer_create(2, 2, 768, 256, ctypes.byref(p), hv) == _lib.XMC_ERR_ARG      # rank >= world
+    assert lib.xmc_peer_create(0, 9, 768, 256, ctypes.byref(p), hv) == _lib.XMC_ERR_ARG      # > 8 ranks
+    assert lib.xmc_peer_create(0, 2, 100, 256, ctypes.byref(p), hv) == _lib.XMC_ERR_SHAPE    # dim % 128
+    assert lib.xmc_peer_create(0, 2, 768, 1024, ctypes.byref(p), hv) == _lib.XMC_ERR_ARG     # batch > 512
+    assert lib.xmc_peer_connect(None, hv) == _lib.XMC_ERR_ARG
+    assert lib.xmc_head_attach_peers(None, None) == _lib.XMC_ERR_ARG
+    # SgdSrConfig: generator names map onto (rounding code, sr_bits)
+    from paper_2510_11168_b200.formats import E4M3
+    assert (SgdSrConfig(0.1, fmt=E4M3).rounding_code, SgdSrConfig(0.1, fmt=E4M3).sr_bits) == (_lib.ROUND_SR_FAST, 0)
+    c = SgdSrConfig(0.1, fmt=E4M3, sr_impl="philox")
+    assert (c.rounding_code, c.sr_bits) == (_lib.ROUND_SR_FAST, 1)
+    c = SgdSrConfig(0.1, fmt=E4M3, sr_impl="splitmix64")
+    assert c.rounding_code == _lib.ROUND_SR_EXACT
+    with pytest.raises(ValueError):
+        SgdSrConfig(0.1, fmt=E4M3, sr_impl="xorshift")

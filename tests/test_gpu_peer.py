@@ -1,10 +1,10 @@
 """Peer-memory grad_X all-reduce (parallel.PeerGroup, xmc_peer_* in
-include/xmc_head.h) with two ranks.  The round's GPU box has one B200, so the
-two processes share cuda:0: the exchange buffers are still mapped through CUDA
+include/xmc_head.h) with two and three ranks.  The round's GPU box has one
+B200, so the rank processes share cuda:0: the exchange buffers are still mapped through CUDA
 IPC in the other process and every push / flag / wait runs as it does over
-NVLink.  Per step and rank the peer result must equal the sum of the two
-ranks' partial grad_X from heads without peers (fp32 tolerance), be bitwise
-identical on both ranks, and leave each shard's weights bitwise equal to the
+NVLink.  Per step and rank the peer result must equal the sum of the ranks'
+partial grad_X from heads without peers (fp32 tolerance), be bitwise
+identical on every rank, and leave each shard's weights bitwise equal to the
 peer-less run."""
 
 import os
@@ -66,14 +66,14 @@ def _worker(rank, world, port, fmt_name, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fmt_name", ["e4m3", "bf16"])
-def test_peer_allreduce_two_ranks(tmp_path, fmt_name):
-    world = 2
+@pytest.mark.parametrize("fmt_name,world", [("e4m3", 2), ("bf16", 2), ("e4m3", 3)])
+def test_peer_allreduce_ranks(tmp_path, fmt_name, world):
     mp.spawn(_worker, args=(world, _free_port(), fmt_name, str(tmp_path)), nprocs=world, join=True)
     r = [torch.load(os.path.join(tmp_path, f"rank{k}.pt")) for k in range(world)]
     for k in range(world):
         assert r[k]["w_equal"]
         for step in range(STEPS):
             torch.testing.assert_close(r[k]["got"][step], r[k]["expect"][step], rtol=1e-5, atol=1e-5)
-    for step in range(STEPS):
-        assert torch.equal(r[0]["got"][step], r[1]["got"][step])
+    for k in range(1, world):
+        for step in range(STEPS):
+            assert torch.equal(r[0]["got"][step], r[k]["got"][step])
