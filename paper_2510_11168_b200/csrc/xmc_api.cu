@@ -223,6 +223,7 @@ struct xmc_head {
   int32_t* ring_ready;      // [max chunk tiles + 1] fused step flags (zeroed per launch)
   int32_t* ring_consumed;   // [max chunk tiles + 1]
   int R_step;          // grad_X partial slots written by the current step's backward
+  uint8_t* xq_topk;    // Xq rows of the current top-k launch (sample offset applied)
   uint8_t* wm;         // [max_chunk_rows + 128][d] masked W chunk (dropout only)
   uint32_t* keep;      // [max_chunk_rows + 128][d / 32] dropout keep bits (dropout only)
   int64_t comp_rows;   // local rows [0, comp_rows) carry a Kahan compensation
@@ -378,6 +379,9 @@ static void set_fwd_attr() {
   if constexpr (EB == 1 && BN == 128)
     cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          FwdCfg<EB, BN, false, true>::kSmemBytes);
+  if constexpr (EB == 1 && BN == 256)
+    cudaFuncSetAttribute(xmc_fwd_kernel<EB, BN, true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         FwdCfg<EB, BN, true, true>::kSmemBytes);
 }
 template <int EB, bool XR, int KC>
 static void set_bwd_attr() {
@@ -1858,11 +1862,33 @@ __global__ void __launch_bounds__(256) topk_merge_kernel(const float* __restrict
   }
 }
 
+// e4m3 batch-256 scoring on CTA pairs with resident Xq (the training forward's
+// mainloop), unless XMC_TOPK_PAIR=0
+static bool topk_pairs() {
+  static const int v = getenv("XMC_TOPK_PAIR") ? atoi(getenv("XMC_TOPK_PAIR")) : 1;
+  return v != 0;
+}
+static int topk_grid(const xmc_head* h, int64_t tiles, int eb, int bn, int D) {
+  if (topk_pairs() && eb == 1 && bn == 256 && D / 128 <= FwdCfg<1, 256, true, true>::kXResChunks)
+    return static_cast<int>(std::min<int64_t>(2 * h->fwd_max_clusters, 2 * ((tiles + 1) / 2)));
+  return static_cast<int>(std::min<int64_t>(h->num_sms, tiles));
+}
+
 template <int EB, int BN>
 static xmc_status launch_topk_t(xmc_head* h, const CUtensorMap& tw, const CUtensorMap& tx, const FwdParams& p,
                                 cudaStream_t st) {
   using C = FwdCfg<EB, BN, false>;
-  const int grid = static_cast<int>(std::min<int64_t>(h->num_sms, p.num_tiles));
+  const int grid = topk_grid(h, p.num_tiles, EB, BN, p.d);
+  if constexpr (EB == 1 && BN == 256) {
+    if (topk_pairs() && p.d / 128 <= FwdCfg<1, 256, true, true>::kXResChunks) {
+      using CP = FwdCfg<1, 256, true, true>;
+      CUtensorMap txp;   // each CTA of a pair stages its 128 samples
+      XMC_TRY(make_map(&txp, h->xq_topk, 1, p.d, 256, p.d, 128));
+      CUDA_TRY(launch_ex(xmc_fwd_kernel<1, 256, true, true, true>, grid, CP::kThreads, CP::kSmemBytes, st, h, 0, 2,
+                         tw, txp, p));
+      return XMC_OK;
+    }
+  }
   CUDA_TRY(launch_ex(xmc_fwd_kernel<EB, BN, false, true>, grid, C::kThreads, C::kSmemBytes, st, h, 0, 1, tw, tx, p));
   return XMC_OK;
 }
@@ -1880,13 +1906,15 @@ extern "C" xmc_status xmc_head_topk(xmc_head_t h, const void* W, const float* X,
   XMC_TRY(launch_x_prep(h, X, B, Bp, st));
   CUtensorMap tw;
   XMC_TRY(make_map(&tw, static_cast<const uint8_t*>(W), eb, D, rows, D, 128));
-  const int nslots = 4 * static_cast<int>(std::min<int64_t>(h->num_sms, cdiv(rows, 128)));
+  const int bn0 = std::min(Bp, 256);
+  const int nslots = 4 * topk_grid(h, cdiv(rows, 128), eb, bn0, D);
   // Bp = 512 runs as two N = 256 launches over the sample halves (the 512-wide
   // epilogue would need twice the candidate registers)
   const int bn = std::min(Bp, 256);
   for (int s0 = 0; s0 < B; s0 += bn) {
     CUtensorMap tx;
     XMC_TRY(make_map(&tx, h->xq + static_cast<size_t>(s0) * D * eb, eb, D, bn, D, bn));
+    h->xq_topk = h->xq + static_cast<size_t>(s0) * D * eb;
     FwdParams p{};
     p.rows = static_cast<int32_t>(rows);
     p.B = std::min(bn, B - s0);
