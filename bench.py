@@ -330,14 +330,14 @@ def main():
             raise
         print(f"peer all-reduce failed in warm-up ({e}); using NCCL", file=sys.stderr)
         ok = False
-    if world > 1 and peers is not None and ok:
-        # sanity check of the peer path: the summed grad_X must be bit-identical on every rank
+    if world > 1 and peers is not None:
+        # sanity check of the peer path (every rank takes part): the summed
+        # grad_X must be bit-identical on every rank
         gxs = [torch.empty_like(gx) for _ in range(world)]
         dist.all_gather(gxs, gx)
         if not all(torch.equal(g_, gxs[0]) for g_ in gxs[1:]):
             print("peer all-reduce gave different grad_X across ranks; using NCCL", file=sys.stderr)
             ok = False
-    if world > 1 and peers is not None:
         # every rank must agree before the timed region (and on the path taken)
         flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)

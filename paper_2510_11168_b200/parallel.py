@@ -98,21 +98,36 @@ class PeerGroup:
     to dist.all_reduce)."""
 
     def __init__(self, dim: int, max_batch: int, group=None):
+        # Collective-safe: every rank takes part in both exchanges even when its
+        # own step failed, and all ranks raise together, so no rank is left
+        # waiting in a collective the others skipped.
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         lib = _lib.load()
         self.p = ctypes.c_void_p()
         handle = (ctypes.c_char * 64)()
-        _lib.check(lib.xmc_peer_create(self.rank, self.world, dim, max_batch, ctypes.byref(self.p),
-                                       ctypes.cast(handle, ctypes.c_void_p)))
-        handles = [None] * self.world
-        dist.all_gather_object(handles, bytes(handle), group=group)
-        buf = (ctypes.c_char * (64 * self.world)).from_buffer_copy(b"".join(handles))
+        err = None
         try:
-            _lib.check(lib.xmc_peer_connect(self.p, ctypes.cast(buf, ctypes.c_void_p)))
-        except Exception:
+            _lib.check(lib.xmc_peer_create(self.rank, self.world, dim, max_batch, ctypes.byref(self.p),
+                                           ctypes.cast(handle, ctypes.c_void_p)))
+            mine = bytes(handle)
+        except Exception as e:  # noqa: BLE001 - reported after the exchange
+            err, mine = e, b""
+        handles = [None] * self.world
+        dist.all_gather_object(handles, mine, group=group)
+        if err is None and all(len(h) == 64 for h in handles):
+            buf = (ctypes.c_char * (64 * self.world)).from_buffer_copy(b"".join(handles))
+            try:
+                _lib.check(lib.xmc_peer_connect(self.p, ctypes.cast(buf, ctypes.c_void_p)))
+            except Exception as e:  # noqa: BLE001
+                err = e
+        elif err is None:
+            err = RuntimeError("a peer rank could not create its exchange buffer")
+        oks = [None] * self.world
+        dist.all_gather_object(oks, err is None, group=group)
+        if not all(oks):
             self.close()
-            raise
+            raise RuntimeError(f"peer group unavailable: {err or 'failed on another rank'}")
 
     def attach(self, head: ChunkedHead) -> None:
         head.peers = self
