@@ -11,8 +11,10 @@
  * Error convention (mirrors the reference's exceptions, head.py / formats.py /
  * optimizers.py): every call returns an xmc_status; xmc_last_error() gives a
  * message.  Device-detected errors (non-finite input/gradient, sample index
- * out of range) are latched in the handle and reported by xmc_head_check()
- * or by the next call, and make every later kernel of the step a no-op.
+ * out of range) are latched in the handle's status word: every later kernel
+ * (of this step and of later steps) becomes a no-op that leaves W untouched,
+ * and grad_X comes back as NaN, until xmc_head_check() reports the error and
+ * clears the latch.
  */
 #ifndef XMC_HEAD_H_
 #define XMC_HEAD_H_
@@ -44,9 +46,10 @@ typedef enum { XMC_FMT_FP32 = 0, XMC_FMT_BF16 = 1, XMC_FMT_FP16 = 2, XMC_FMT_E4M
 /* SgdSrConfig.rounding (optimizers.py:28-41).  SR_EXACT draws u from the
  * reference's splitmix64 keyed generator (rng.py:36-57) and compares in fp64
  * exactly like round_stochastic (formats.py:209-225): bit-identical decisions.
- * SR_FAST feeds keyed random words to the hardware cvt.rs conversion: a
- * stateless PCG hash of (element / 4 + key(seed, step, tensor_id)) by default,
- * or Philox4x32-7 (xmc_step_args.sr_bits = 1). */
+ * SR_FAST feeds keyed random words to the hardware cvt.rs conversion: by
+ * default a stateless keyed hash of the word index (one word per cvt.rs
+ * instruction) under the 64-bit key splitmix64(seed, step, tensor_id), or
+ * Philox4x32-7 (xmc_step_args.sr_bits = 1). */
 typedef enum { XMC_ROUND_NEAREST = 0, XMC_ROUND_SR_EXACT = 1, XMC_ROUND_SR_FAST = 2 } xmc_rounding;
 
 /* Head geometry: ChunkedHead (head.py:69-112) restricted to one rank's label
@@ -64,12 +67,30 @@ typedef struct {
   int32_t comp_bytes;        /* Kahan compensation storage: 0 none, 2 bf16, 4 fp32 */
   int32_t dropout;           /* 1: reserve the keyed-dropout scratch (masked W chunk + keep bits),
                                 needed for steps with dropout_p > 0 (head.py:138-161) */
-  int32_t reserved;
+  int32_t precision;         /* xmc_precision of the backward GEMMs (see below) */
   int64_t comp_labels;       /* with comp_bytes > 0: only GLOBAL labels < comp_labels carry a
                                 compensation (top-p% head-Kahan over frequency-sorted labels,
                                 PAPER.md:795); <= 0 = every label.  The comp buffer then holds the
                                 shard's rows [0, clamp(comp_labels - label_offset, 0, local)). */
+  int32_t g_format;          /* XMC_PRECISION_OPERAND only: the G operand format of an e4m3 head,
+                                XMC_FMT_E5M2 (e5m2(2^8 g), the default for 0) or XMC_FMT_E4M3
+                                (e4m3(2^8 g)); ignored for a bf16 head (always bf16(g)) */
+  int32_t reserved;
 } xmc_head_desc;
+
+/* Precision of G in the two backward GEMMs (dW = G.Xq and grad_X += G^T.W).
+ *  XMC_PRECISION_REFERENCE: G exactly as the reference's fp32 logit_gradient
+ *    (head.py:181-196, accurate expf / divide), split exactly into three bf16
+ *    planes g = hi + mid + lo; the backward runs kind::f16 MMAs over the 3x
+ *    longer K, so every product G[l,b] Xq[b,c] and G[l,b] W[l,c] is exact and
+ *    only the fp32 accumulation order differs from the reference's sgemm
+ *    (head.py:193-208, 236; "update computed at working precision
+ *    before the single rounding").  An e4m3 head's W chunk is copied to bf16
+ *    for the MMAs (exact) and the update still rounds onto the e4m3 grid.
+ *  XMC_PRECISION_OPERAND: the production fast path; G is rounded once to the
+ *    tensor-core operand format of the head (e4m3 head: e5m2 or e4m3 of
+ *    2^8 g, all three GEMMs on FP8 kind::f8f6f4; bf16 head: bf16(g)). */
+typedef enum { XMC_PRECISION_OPERAND = 0, XMC_PRECISION_REFERENCE = 1 } xmc_precision;
 
 typedef struct xmc_head* xmc_head_t;
 
@@ -78,7 +99,7 @@ typedef struct {
   float lr;            /* > 0                                   */
   float weight_decay;  /* >= 0                                  */
   int32_t rounding;    /* xmc_rounding                          */
-  int32_t sr_bits;     /* XMC_ROUND_SR_FAST bit source: 0 keyed PCG hash (default), 1 Philox4x32-7 */
+  int32_t sr_bits;     /* XMC_ROUND_SR_FAST bit source: 0 keyed hash (default), 1 Philox4x32-7 */
   uint64_t seed;       /* RoundingRng(seed)                     */
   uint64_t step;       /* step index keying the draws           */
   uint64_t tensor_id;  /* ChunkedHead.tensor_id (HEAD_WEIGHTS_TAG) */
@@ -177,8 +198,9 @@ xmc_status xmc_logit_gradient(const float* logits, int64_t rows, int32_t B, int6
 
 /* input_gradient_accumulate (head.py:199-209) and/or fused_weight_update
  * (head.py:212-251) on local rows [row0, row1) from an fp32 G (rows x B, ld):
- * G is rounded to the backward operand format (e4m3 x 2^8 or bf16) and run
- * through the same tcgen05 kernel as the step.  acc (B x dim fp32) += when
+ * G is converted to the handle's backward operand format (desc.precision:
+ * the exact three-plane bf16 split, or the operand rounding) and run through
+ * the same tcgen05 kernel as the step.  acc (B x dim fp32) += when
  * accumulate_gx != 0; W updated in place when update != 0. */
 xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, int64_t ld, const float* X,
                              int32_t B, int64_t row0, int64_t row1, float* acc, int32_t accumulate_gx,

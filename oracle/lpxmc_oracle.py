@@ -510,22 +510,27 @@ def fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp=None, comp_fmt=
                                                          rng, step, head.tensor_id, idx[n_c:])
 
 
-def quantize_g_operand(G, fmt):
-    """The GPU consumes G in the backward tensor-core operand format: an e4m3
-    head uses e4m3(G * 2^8) * 2^-8 (exact power-of-two scale), a bf16 head
-    uses bf16(G); both RTN.  This is a documented B200 design choice (not in
-    the reference), so parity tests can isolate it by applying it here."""
+def quantize_g_operand(G, fmt, g_format="e5m2"):
+    """The GPU's operand-precision mode (ChunkedHead(precision="operand"))
+    consumes G in the backward tensor-core operand format: an e4m3 head uses
+    e5m2(G * 2^8) * 2^-8 (g_format "e5m2", the default) or e4m3(G * 2^8) * 2^-8
+    ("e4m3") -- exact power-of-two scale -- and a bf16 head uses bf16(G); all
+    RTN.  This is a documented B200 design choice (not in the reference), so
+    parity tests of that mode can isolate it by applying it here.  The default
+    reference-precision mode needs no quantisation (g_quant=False)."""
     G = np.asarray(G, dtype=np.float32)
     if fmt.name == "e4m3":
-        return (round_nearest(E4M3, G * np.float32(256.0)) * np.float32(1.0 / 256.0)).astype(np.float32)
+        q = E5M2 if g_format == "e5m2" else E4M3
+        return (round_nearest(q, G * np.float32(256.0)) * np.float32(1.0 / 256.0)).astype(np.float32)
     return round_nearest(fmt, G)
 
 
 def head_update(head, X, sample_idx, label_idx, cfg, rng, step, comp=None,
                 probe=None, g_quant=False, comp_fmt=None, adam=None):
     """One head step over all chunks; returns grad_X (b, d).  head.py:254-298.
-    ``g_quant=True`` applies quantize_g_operand to each chunk's G before the
-    backward (the GPU's operand precision)."""
+    ``g_quant`` ("e5m2" / "e4m3", or True = "e5m2") applies
+    quantize_g_operand to each chunk's G before the backward (the GPU's
+    operand-precision mode); False (default) is the reference itself."""
     X = np.asarray(X, dtype=np.float32)
     sample_idx = np.asarray(sample_idx, dtype=np.int64)
     label_idx = np.asarray(label_idx, dtype=np.int64)
@@ -542,7 +547,7 @@ def head_update(head, X, sample_idx, label_idx, cfg, rng, step, comp=None,
         if probe is not None:
             probe(step, chunk, G)
         if g_quant:
-            G = quantize_g_operand(G, head.fmt)
+            G = quantize_g_operand(G, head.fmt, "e5m2" if g_quant is True else g_quant)
         input_gradient_accumulate(acc, G, head, chunk, rng, step)
         fused_weight_update(head, G, Xq, cfg, rng, step, chunk, comp, comp_fmt, adam)
     return acc

@@ -32,7 +32,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", os.path.join(HERE, "csrc", "xmc_api.cu")]
+    units = [os.path.join(HERE, "csrc", u) for u in ("xmc_api.cu", "xmc_elementwise.cu")]
+    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *units]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

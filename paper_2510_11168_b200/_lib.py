@@ -26,6 +26,7 @@ XMC_ERR_CAPACITY = 8
 
 FMT_FP32, FMT_BF16, FMT_FP16, FMT_E4M3, FMT_E5M2 = 0, 1, 2, 3, 4
 ROUND_NEAREST, ROUND_SR_EXACT, ROUND_SR_FAST = 0, 1, 2
+PRECISION_OPERAND, PRECISION_REFERENCE = 0, 1
 
 
 class HeadDesc(ctypes.Structure):
@@ -34,8 +35,9 @@ class HeadDesc(ctypes.Structure):
                 ("fmt", ctypes.c_int32), ("num_chunks", ctypes.c_int32),
                 ("max_batch", ctypes.c_int32), ("max_positives", ctypes.c_int64),
                 ("num_sms", ctypes.c_int32), ("comp_bytes", ctypes.c_int32),
-                ("dropout", ctypes.c_int32), ("reserved", ctypes.c_int32),
-                ("comp_labels", ctypes.c_int64)]
+                ("dropout", ctypes.c_int32), ("precision", ctypes.c_int32),
+                ("comp_labels", ctypes.c_int64), ("g_format", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
 
 class StepArgs(ctypes.Structure):

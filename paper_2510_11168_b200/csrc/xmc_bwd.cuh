@@ -20,8 +20,16 @@
 // warps 2..17 update epilogue: 4 warps per TMEM sub-partition, each owning 32
 // of the tile's 128 d-columns for its 32 label rows.  Per tile the epilogue
 // reads W_old and draws its random bits while the MMA is still running,
-// releases the dW buffer right after tcgen05.ld, writes W_new back into the
-// same swizzled smem tile and one thread TMA-stores the tile to HBM.
+// releases the dW buffer right after tcgen05.ld, writes W_new into a swizzled
+// smem tile and one thread per sub-partition TMA-stores its 32-row slab.
+//
+// Operand precision.  EB is the MMA operand / W storage width (1: e4m3 with
+// kind::f8f6f4, 2: bf16 with kind::f16); GE is the grid the update rounds
+// onto (GE = EB normally).  The reference-precision mode of an e4m3 head runs
+// this kernel with EB = 2 on a bf16 copy of the W chunk (exact: every e4m3
+// value is a bf16 value) and GE = 1, so the rounding still lands on the e4m3
+// grid, while G arrives as three bf16 planes hi + mid + lo = fp32 g (a 3x
+// longer K; BwdParams::xt_kc maps a G k-chunk onto its Xq^T k-chunk).
 #pragma once
 
 #include "xmc_ptx.cuh"
@@ -32,26 +40,18 @@ namespace xmc {
 constexpr int kBwdEpiWarps = 16;
 constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32;
 
-enum StatusBits : int32_t {
-  ST_NONFINITE_X = 1,
-  ST_BAD_SAMPLE = 2,
-  ST_NONFINITE_GRAD = 4,
-  ST_LABEL_OUTSIDE = 8,
-  ST_CAPACITY = 16,
-  ST_NONFINITE_MOMENTS = 32,
-  ST_RING_TIMEOUT = 64,   // fused step: a ring flag never arrived (CTAs not co-resident)
-  ST_PEER_TIMEOUT = 128,  // peer grad_X all-reduce: a peer's tile never arrived
-};
 
 struct BwdParams {
   int32_t rows;          // labels in this chunk
   int32_t d;             // feature dim
   int32_t num_tiles;     // ceil(rows / 128)
   int32_t dtiles;        // d / 128
-  int32_t kc_count;      // sample k-chunks (Bp * EB / 128)
+  int32_t kc_count;      // sample k-chunks of G (Bp * EB / 128, x3 for the reference-precision planes)
+  int32_t xt_kc;         // k-chunks of one Xq^T plane: G k-chunk kc multiplies Xq^T k-chunk kc % xt_kc
   int32_t do_update;     // dW + SGD + rounding, W written in place
-  int32_t gx_kc0;        // first sample k-chunk accumulated into grad_X
+  int32_t gx_kc0;        // first G k-chunk accumulated into grad_X
   int32_t gx_kc_count;   // 0 = no grad_X
+  int32_t g_e5m2;        // EB = 1: G is e5m2 (x 2^8) instead of e4m3 (x 2^8)
   uint8_t* W;            // chunk base (row-major rows x d, EB bytes/elem), written in place
   uint8_t* comp;         // Kahan compensation, chunk base (comp_rows x d, CE bytes/elem) or null
   int32_t comp_rows;     // leading chunk rows that carry a compensation (top-p% head-Kahan)
@@ -59,38 +59,19 @@ struct BwdParams {
   float lr, wd, dw_scale;
   int32_t rounding;      // ROUND_NEAREST / ROUND_SR_EXACT / ROUND_SR_FAST
   uint64_t rng_base;     // splitmix64 base(seed, step, tensor_id); Philox / hash key
-  int32_t sr_bits;       // ROUND_SR_FAST bits: 0 keyed PCG hash, 1 Philox4x32-7
-  float* gx_ws;          // [R][d][gx_ld] fp32 partials (gx_ld = padded batch)
+  int32_t sr_bits;       // ROUND_SR_FAST bits: 0 keyed hash, 1 Philox4x32-7
+  float* gx_ws;          // [R][d][gx_ld] fp32 partials (gx_ld = padded batch x planes)
   int32_t gx_ld;
   int32_t gx_accumulate; // 1: add into the partial slot, 0: overwrite it
   const uint32_t* keep;  // keyed dropout keep bits [rows][d / 32] (chunk-local) or null
   float drop_scale;      // f32(1) / f32(1 - p) applied to kept dW (head.py:239-242)
-  int32_t debug;         // measurement only (XMC_DEBUG_BWD): 1 skip dW MMAs, 2 skip update epilogue
-  int32_t pol_normal;    // measurement: evict_normal for every load/store (L2-resident chunk experiments)
-  int32_t gcl;           // CTAs (consecutive d-tiles of one label-tile row group) sharing each G tile
-                         // through TMA multicast: 1 = every CTA loads G itself
   int32_t* status;
   // Adam-style head (ADAMW instantiation): fp32 moments [rows][d] at the chunk
   // base, comp (CE = 4) fp32, constants as kahan_adamw_step forms them
   float* adam_m;
   float* adam_v;
   float b1, b2, omb1, omb2, bc1, bc2, eps;
-  uint64_t* trace;       // measurement only (XMC_TRACE): clock64 per tile and event of CTA 0, [kTraceTiles][16]
-  // fused step (xmc_step_kernel): G arrives through a ring of ring_tiles
-  // 128-row tiles written by the forward CTAs of the same launch; tile t is
-  // readable once ready[t] >= ready_target, and each CTA counts its finished
-  // reads of tile t into consumed[t].  Read only by bwd_body<..., RING>.
-  int32_t ring_tiles;
-  int32_t ready_target;
-  const int32_t* ready;
-  int32_t* consumed;
 };
-
-constexpr int kTraceTiles = 512;
-// trace event e of local tile iteration i (CTA 0 only)
-XMC_DEV void trace_ev(uint64_t* tr, int i, int e) {
-  if (tr != nullptr && blockIdx.x == 0 && i < kTraceTiles) tr[i * 16 + e] = clock64();
-}
 
 template <int EB, bool XT_RES, int KCMAX>
 struct BwdCfg {
@@ -102,30 +83,20 @@ struct BwdCfg {
   // is released right after the epilogue has read it and the update never
   // waits for the grad_X MMAs still reading W_old; bf16 (no smem left for a
   // second tile) writes W_new in place after the grad_X MMAs completed.
-// (measured equal within box noise: in place / 1 / 2 staging tiles with 5 / 4 / 3
-// W stages; two staging tiles need one named barrier per tile, one needs two)
-#ifndef XMC_BWD_OUT
-#define XMC_BWD_OUT 2
-#endif
-#ifndef XMC_BWD_WST
-#define XMC_BWD_WST 3
-#endif
-#ifndef XMC_BWD_KST
-#define XMC_BWD_KST 6
-#endif
-  static constexpr int kOutTiles = EB == 1 ? XMC_BWD_OUT : 0;   // W_new staging tiles (0 = in place)
+  // (measured equal within box noise: in place / 1 / 2 staging tiles with
+  // 5 / 4 / 3 W stages; two staging tiles need one named barrier per tile)
+  static constexpr int kOutTiles = EB == 1 ? 2 : 0;   // W_new staging tiles (0 = in place)
   static constexpr bool kOutBuf = kOutTiles > 0;
-  static constexpr int kWStages = EB == 1 ? XMC_BWD_WST : 3;
+  static constexpr int kWStages = 3;
   static constexpr int kOutBytes = kOutTiles * kWBytes;
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
-  static constexpr int kKStages = EB == 1 ? XMC_BWD_KST : 4;
+  static constexpr int kKStages = EB == 1 ? 6 : 4;
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
   static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2) + 16;
   static constexpr int kSmemBytes =
       1024 + kXtBytes + kWStages * kWBytes + kOutBytes + kKStages * kKSlot + kBarBytes;
   static constexpr int kKmma = 32 / EB;              // K per MMA instruction (elements)
   static constexpr int kChunks16 = 2 * EB;           // 16-B smem chunks per thread (32 elements)
-  static constexpr int kRandWords = 8 * EB;          // cvt.rs words per 32 elements
 };
 
 // byte offset of 16-B chunk `h` of this thread's 32 columns [c0, c0+32) in the
@@ -170,33 +141,26 @@ XMC_DEV void w_decode(const uint4 (&raw)[2 * EB], float (&w)[32]) {
   }
 }
 
-// Philox4x32-7 words for 32 elements starting at flat index flat0 (multiple
-// of 32).  e4m3: one word per cvt.rs.e4m3x4 (4 elements, 16 random bits per
-// lane, see profiles/r1_probe_cvt_rs.txt); bf16: one word per bf16x2.
-template <int EB>
-XMC_DEV void sr_words(const PhiloxKeys& ks, int64_t flat0, uint32_t (&rw)[8 * EB], bool philox) {
-#ifdef XMC_WHATIF_NO_RNG   // measurement only: the SR bits without the generator's cost
-#pragma unroll
-  for (int k = 0; k < 8 * EB; ++k) rw[k] = static_cast<uint32_t>(flat0) * 0x9E3779B9u + k;
-  return;
-#endif
+// SR_FAST random words for the 32 elements [flat0, flat0 + 32) (flat0 a
+// multiple of 32): one word per cvt.rs instruction of the grid GE -- e4m3x4
+// (4 elements; lanes (c,d) / (a,b) draw their 16 bits from rbits[15:0] /
+// [31:16], profiles/r1_probe_cvt_rs.txt) or bf16x2 (2 elements).  Word w of
+// the step is hash(w, key) (sr_hash_word) or Philox4x32-7 at counter w / 4;
+// consecutive threads' word ranges are disjoint.
+template <int GE>
+XMC_DEV void sr_words(const PhiloxKeys& ks, int64_t flat0, uint32_t (&rw)[8 * GE], bool philox) {
+  const uint64_t w0 = static_cast<uint64_t>(flat0) >> (GE == 1 ? 2 : 1);   // multiple of 8 * GE
   if (!philox) {
-    // keyed hash: word i of the step = pcg_hash(i + key(seed, step, tensor_id))
-    // (the RXS-M-XS output function of PCG as a stateless integer hash);
-    // word i carries the cvt.rs bits of elements 4i .. 4i+3
-    const uint32_t base = static_cast<uint32_t>(static_cast<uint64_t>(flat0) >> 2) + ks.hk;
+    const uint32_t ka = sr_hash_ka(ks, w0);
+    const uint32_t lo = static_cast<uint32_t>(w0);
 #pragma unroll
-    for (int k = 0; k < 8 * EB; ++k) {
-      const uint32_t st = (base + k) * 747796405u + 2891336453u;
-      const uint32_t w = ((st >> ((st >> 28u) + 4u)) ^ st) * 277803737u;
-      rw[k] = (w >> 22u) ^ w;
-    }
+    for (int k = 0; k < 8 * GE; ++k) rw[k] = sr_hash_word(lo + k, ka, ks.hk1);
     return;
   }
 #pragma unroll
-  for (int h = 0; h < 2 * EB; ++h) {
-    const uint64_t ctr = static_cast<uint64_t>(flat0) / (16 / EB) + h;
-    const U4 r = philox4x32_keys(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), EB - 1u, 0u}, ks);
+  for (int h = 0; h < 2 * GE; ++h) {
+    const uint64_t ctr = (w0 >> 2) + h;
+    const U4 r = philox4x32_keys(U4{static_cast<uint32_t>(ctr), static_cast<uint32_t>(ctr >> 32), GE - 1u, 0u}, ks);
     rw[4 * h + 0] = r.x;
     rw[4 * h + 1] = r.y;
     rw[4 * h + 2] = r.z;
@@ -204,13 +168,56 @@ XMC_DEV void sr_words(const PhiloxKeys& ks, int64_t flat0, uint32_t (&rw)[8 * EB
   }
 }
 
+// bf16x2 word of two e4m3 values (exact: every e4m3 value is a bf16 value)
+XMC_DEV uint32_t e4m3x2_to_bf16x2(uint16_t v) {
+  const float2 f = dec_e4m3x2(v);
+  return (__float_as_uint(f.x) >> 16) | (__float_as_uint(f.y) & 0xFFFF0000u);
+}
+
+// Round 4 consecutive fp32 values x[0..3] onto the GE grid (RTN, exact SR or
+// hardware SR with word rw4[0] (GE = 1) / rw4[0..1] (GE = 2)), write the
+// rounded values back into x and the EB storage words into out (1 word for
+// EB = 1, 2 words for EB = 2).
+template <int EB, int GE>
+XMC_DEV void round4(const BwdParams& p, int rounding, float (&x)[4], const uint32_t* rw4, int64_t flat,
+                    uint32_t* out) {
+  static_assert(GE <= EB, "the storage holds the grid");
+  if (rounding == ROUND_SR_EXACT) {
+    const GridFmt gf = grid_of(GE == 1 ? FMT_E4M3 : FMT_BF16);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      x[e] = grid_round_stochastic(gf, x[e], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat + e)));
+  }
+  if constexpr (GE == 1) {
+    const uint32_t w4 = rounding == ROUND_SR_FAST
+                            ? cvt_e4m3x4_rs(x[3], x[2], x[1], x[0], rw4[0])
+                            : (cvt_e4m3x2_rn(x[1], x[0]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(x[3], x[2])) << 16));
+    const float2 lo = dec_e4m3x2(static_cast<uint16_t>(w4 & 0xFFFF));
+    const float2 hi = dec_e4m3x2(static_cast<uint16_t>(w4 >> 16));
+    x[0] = lo.x; x[1] = lo.y; x[2] = hi.x; x[3] = hi.y;
+    if constexpr (EB == 1) {
+      out[0] = w4;
+    } else {
+      out[0] = (__float_as_uint(x[0]) >> 16) | (__float_as_uint(x[1]) & 0xFFFF0000u);
+      out[1] = (__float_as_uint(x[2]) >> 16) | (__float_as_uint(x[3]) & 0xFFFF0000u);
+    }
+  } else {
+    const uint32_t w0 = rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[1], x[0], rw4[0]) : cvt_bf16x2_rn(x[1], x[0]);
+    const uint32_t w1 = rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[3], x[2], rw4[1]) : cvt_bf16x2_rn(x[3], x[2]);
+    out[0] = w0;
+    out[1] = w1;
+    x[0] = __uint_as_float(w0 << 16); x[1] = __uint_as_float(w0 & 0xFFFF0000u);
+    x[2] = __uint_as_float(w1 << 16); x[3] = __uint_as_float(w1 & 0xFFFF0000u);
+  }
+}
+
 // updated = w (1 - lr wd) - (lr * dw_scale) acc  (SGD with wd folded,
-// optimizers.py:71-73, one rounding), rounded and packed into the tile's
-// storage bytes.  FMA contraction moves the fp32 update by <= 1 fp32 ulp,
-// far below the tensor-core accumulation noise of acc.
-template <int EB>
+// optimizers.py:71-73, one rounding), rounded onto the GE grid and packed
+// into the tile's EB storage bytes.  FMA contraction moves the fp32 update by
+// <= 1 fp32 ulp, far below the tensor-core accumulation noise of acc.
+template <int EB, int GE>
 XMC_DEV void w_update_pack(const BwdParams& p, int rounding, const uint32_t (&acc)[32], const float (&w)[32],
-                           const uint32_t (&rw)[8 * EB], int64_t flat0, uint4 (&out)[2 * EB]) {
+                           const uint32_t (&rw)[8 * GE], int64_t flat0, uint4 (&out)[2 * EB]) {
   const float a_lr = -p.lr * p.dw_scale;
   const float c_wd = 1.0f - p.lr * p.wd;
   const uint64_t A2 = f2pack(a_lr, a_lr), C2 = f2pack(c_wd, c_wd);
@@ -230,29 +237,38 @@ XMC_DEV void w_update_pack(const BwdParams& p, int rounding, const uint32_t (&ac
       f2unpack(r, u[2 * k], u[2 * k + 1]);
     }
   }
-  if (rounding == ROUND_SR_EXACT) {
-    const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-      u[k] = grid_round_stochastic(gf, u[k], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + k)));
-  }
   uint32_t pk[8 * EB];
-  if constexpr (EB == 1) {
-    if (rounding == ROUND_SR_FAST) {
+  if constexpr (EB == GE) {
+    if (rounding == ROUND_SR_EXACT) {
+      const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) pk[k] = cvt_e4m3x4_rs(u[4 * k + 3], u[4 * k + 2], u[4 * k + 1], u[4 * k], rw[k]);
+      for (int k = 0; k < 32; ++k)
+        u[k] = grid_round_stochastic(gf, u[k], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + k)));
+    }
+    if constexpr (EB == 1) {
+      if (rounding == ROUND_SR_FAST) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pk[k] = cvt_e4m3x4_rs(u[4 * k + 3], u[4 * k + 2], u[4 * k + 1], u[4 * k], rw[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          pk[k] = cvt_e4m3x2_rn(u[4 * k + 1], u[4 * k]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(u[4 * k + 3], u[4 * k + 2])) << 16);
+      }
     } else {
+      if (rounding == ROUND_SR_FAST) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        pk[k] = cvt_e4m3x2_rn(u[4 * k + 1], u[4 * k]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(u[4 * k + 3], u[4 * k + 2])) << 16);
+        for (int k = 0; k < 16; ++k) pk[k] = cvt_bf16x2_rs(u[2 * k + 1], u[2 * k], rw[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) pk[k] = cvt_bf16x2_rn(u[2 * k + 1], u[2 * k]);
+      }
     }
   } else {
-    if (rounding == ROUND_SR_FAST) {
+    // e4m3 grid in bf16 storage (reference-precision mode of an e4m3 head)
 #pragma unroll
-      for (int k = 0; k < 16; ++k) pk[k] = cvt_bf16x2_rs(u[2 * k + 1], u[2 * k], rw[k]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) pk[k] = cvt_bf16x2_rn(u[2 * k + 1], u[2 * k]);
+    for (int g = 0; g < 8; ++g) {
+      float x[4] = {u[4 * g], u[4 * g + 1], u[4 * g + 2], u[4 * g + 3]};
+      round4<EB, GE>(p, rounding, x, &rw[g], flat0 + 4 * g, &pk[2 * g]);
     }
   }
 #pragma unroll
@@ -266,18 +282,33 @@ XMC_DEV uint32_t word_of(const uint4 (&v)[N], int i) {
   return (i & 3) == 0 ? q.x : ((i & 3) == 1 ? q.y : ((i & 3) == 2 ? q.z : q.w));
 }
 
+// elements 4g .. 4g+3 of a thread's 32 storage elements -> floats
+template <int EB>
+XMC_DEV void decode4(const uint4 (&raw)[2 * EB], int g, float (&w)[4]) {
+  if constexpr (EB == 1) {
+    const uint32_t wv = word_of(raw, g);
+    const float2 lo = dec_e4m3x2(static_cast<uint16_t>(wv & 0xFFFF));
+    const float2 hi = dec_e4m3x2(static_cast<uint16_t>(wv >> 16));
+    w[0] = lo.x; w[1] = lo.y; w[2] = hi.x; w[3] = hi.y;
+  } else {
+    const uint32_t w0 = word_of(raw, 2 * g), w1 = word_of(raw, 2 * g + 1);
+    w[0] = __uint_as_float(w0 << 16); w[1] = __uint_as_float(w0 & 0xFFFF0000u);
+    w[2] = __uint_as_float(w1 << 16); w[3] = __uint_as_float(w1 & 0xFFFF0000u);
+  }
+}
+
 // Head-Kahan variant (kahan_add formats.py:246-263 composed
 // with the SGD update optimizers.py:51-74; PAPER.md:795 keeps the
 // compensation in BF16):
 //   v = -lr (g + wd s);  y = v - c;  t = ROUND(s + y);  c' = (t - s) - y;  s' = t
 // Works 4 elements at a time straight from the packed W (`raw`) and comp
-// (`craw`) registers so only acc[32] is live at full width (no spills at
-// 576 threads).  comp (CE = 2: bf16, CE = 4: fp32) is read/written from/to
-// HBM by the owning thread; rows without compensation (top-p% head-Kahan,
-// PAPER.md:795) pass craw = 0 and drop cout.
-template <int EB, int CE>
+// (`craw`) registers so only acc[32] is live at full width.  comp (CE = 2:
+// bf16, CE = 4: fp32) is read/written from/to HBM by the owning thread; rows
+// without compensation (top-p% head-Kahan) pass craw = 0 and
+// drop cout.
+template <int EB, int CE, int GE>
 XMC_DEV void w_update_pack_kahan(const BwdParams& p, int rounding, const uint32_t (&acc)[32], const uint4 (&raw)[2 * EB],
-                                 const uint32_t (&rw)[8 * EB], int64_t flat0, const uint4 (&craw)[CE * 2],
+                                 const uint32_t (&rw)[8 * GE], int64_t flat0, const uint4 (&craw)[CE * 2],
                                  uint4 (&out)[2 * EB], uint4* cdst, uint64_t pol) {
   const float a_lr = -p.lr * p.dw_scale;
   const float b_wd = -p.lr * p.wd;
@@ -286,16 +317,7 @@ XMC_DEV void w_update_pack_kahan(const BwdParams& p, int rounding, const uint32_
 #pragma unroll
   for (int g = 0; g < 8; ++g) {   // elements 4g .. 4g+3
     float w[4], c[4];
-    if constexpr (EB == 1) {
-      const uint32_t wv = word_of(raw, g);
-      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(wv & 0xFFFF));
-      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(wv >> 16));
-      w[0] = lo.x; w[1] = lo.y; w[2] = hi.x; w[3] = hi.y;
-    } else {
-      const uint32_t w0 = word_of(raw, 2 * g), w1 = word_of(raw, 2 * g + 1);
-      w[0] = __uint_as_float(w0 << 16); w[1] = __uint_as_float(w0 & 0xFFFF0000u);
-      w[2] = __uint_as_float(w1 << 16); w[3] = __uint_as_float(w1 & 0xFFFF0000u);
-    }
+    decode4<EB>(raw, g, w);
     if constexpr (CE == 2) {
       const uint32_t c0 = word_of(craw, 2 * g), c1 = word_of(craw, 2 * g + 1);
       c[0] = __uint_as_float(c0 << 16); c[1] = __uint_as_float(c0 & 0xFFFF0000u);
@@ -304,36 +326,14 @@ XMC_DEV void w_update_pack_kahan(const BwdParams& p, int rounding, const uint32_
 #pragma unroll
       for (int e = 0; e < 4; ++e) c[e] = __uint_as_float(word_of(craw, 4 * g + e));
     }
-    float y[4], x[4], t[4];
+    float y[4], t[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float v = fmaf(a_lr, __uint_as_float(acc[4 * g + e]), b_wd * w[e]);
       y[e] = v - c[e];
-      x[e] = w[e] + y[e];
+      t[e] = w[e] + y[e];
     }
-    if (rounding == ROUND_SR_EXACT) {
-      const GridFmt gf = grid_of(EB == 1 ? FMT_E4M3 : FMT_BF16);
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        x[e] = grid_round_stochastic(gf, x[e], sm64_uniform(p.rng_base, static_cast<uint64_t>(flat0 + 4 * g + e)));
-    }
-    if constexpr (EB == 1) {
-      const uint32_t w4 = rounding == ROUND_SR_FAST
-                              ? cvt_e4m3x4_rs(x[3], x[2], x[1], x[0], rw[g])
-                              : (cvt_e4m3x2_rn(x[1], x[0]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(x[3], x[2])) << 16));
-      pk[g] = w4;
-      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(w4 & 0xFFFF));
-      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(w4 >> 16));
-      t[0] = lo.x; t[1] = lo.y; t[2] = hi.x; t[3] = hi.y;
-    } else {
-      const uint32_t w0 = rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[1], x[0], rw[2 * g]) : cvt_bf16x2_rn(x[1], x[0]);
-      const uint32_t w1 =
-          rounding == ROUND_SR_FAST ? cvt_bf16x2_rs(x[3], x[2], rw[2 * g + 1]) : cvt_bf16x2_rn(x[3], x[2]);
-      pk[2 * g] = w0;
-      pk[2 * g + 1] = w1;
-      t[0] = __uint_as_float(w0 << 16); t[1] = __uint_as_float(w0 & 0xFFFF0000u);
-      t[2] = __uint_as_float(w1 << 16); t[3] = __uint_as_float(w1 & 0xFFFF0000u);
-    }
+    round4<EB, GE>(p, rounding, t, &rw[GE == 1 ? g : 2 * g], flat0 + 4 * g, &pk[EB == 1 ? g : 2 * g]);
     float cn[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) cn[e] = (t[e] - w[e]) - y[e];
@@ -351,14 +351,12 @@ XMC_DEV void w_update_pack_kahan(const BwdParams& p, int rounding, const uint32_
   for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
 }
 
-// FAST: the production specialisation (Philox SR, no dropout mask, no
-// measurement hooks, no G sharing) with every runtime mode switch folded away
 // Adam-style head update (kahan_adamw_step optimizers.py:112-137 with the
 // chunk gradient g = dW from TMEM, kahan_add formats.py:246-263 with RTN onto
 // the grid), 4 elements at a time: m, v, comp fp32 read and written from/to
 // HBM by the owning thread.  Every op explicitly rounded in the reference's
 // order, so given the same dW the result is the reference's bit for bit.
-template <int EB>
+template <int EB, int GE>
 XMC_DEV void w_update_pack_adamw(const BwdParams& p, const uint32_t (&acc)[32], const uint4 (&raw)[2 * EB],
                                  int64_t eoff, bool row_ok, uint4 (&out)[2 * EB], uint64_t pol) {
   uint32_t pk[8 * EB];
@@ -366,23 +364,14 @@ XMC_DEV void w_update_pack_adamw(const BwdParams& p, const uint32_t (&acc)[32], 
 #pragma unroll
   for (int g = 0; g < 8; ++g) {
     float w[4];
-    if constexpr (EB == 1) {
-      const uint32_t wv = word_of(raw, g);
-      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(wv & 0xFFFF));
-      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(wv >> 16));
-      w[0] = lo.x; w[1] = lo.y; w[2] = hi.x; w[3] = hi.y;
-    } else {
-      const uint32_t w0 = word_of(raw, 2 * g), w1 = word_of(raw, 2 * g + 1);
-      w[0] = __uint_as_float(w0 << 16); w[1] = __uint_as_float(w0 & 0xFFFF0000u);
-      w[2] = __uint_as_float(w1 << 16); w[3] = __uint_as_float(w1 & 0xFFFF0000u);
-    }
+    decode4<EB>(raw, g, w);
     float4* mp = reinterpret_cast<float4*>(p.adam_m + eoff) + g;
     float4* vp = reinterpret_cast<float4*>(p.adam_v + eoff) + g;
     float4* cp = reinterpret_cast<float4*>(reinterpret_cast<float*>(p.comp) + eoff) + g;
     const float4 m4 = row_ok ? *mp : z4, v4 = row_ok ? *vp : z4, c4 = row_ok ? *cp : z4;
     const float mm[4] = {m4.x, m4.y, m4.z, m4.w}, vv[4] = {v4.x, v4.y, v4.z, v4.w};
     const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
-    float m1[4], v1[4], y[4], x[4], t[4];
+    float m1[4], v1[4], y[4], t[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const float gg = __fmul_rn(__uint_as_float(acc[4 * g + e]), p.dw_scale);
@@ -393,21 +382,9 @@ XMC_DEV void w_update_pack_adamw(const BwdParams& p, const uint32_t (&acc)[32], 
       const float upd = __fmul_rn(-p.lr, __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), p.eps)),
                                                   __fmul_rn(p.wd, w[e])));
       y[e] = __fsub_rn(upd, cc[e]);
-      x[e] = __fadd_rn(w[e], y[e]);
+      t[e] = __fadd_rn(w[e], y[e]);
     }
-    if constexpr (EB == 1) {
-      const uint32_t w4 = cvt_e4m3x2_rn(x[1], x[0]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(x[3], x[2])) << 16);
-      pk[g] = w4;
-      const float2 lo = dec_e4m3x2(static_cast<uint16_t>(w4 & 0xFFFF));
-      const float2 hi = dec_e4m3x2(static_cast<uint16_t>(w4 >> 16));
-      t[0] = lo.x; t[1] = lo.y; t[2] = hi.x; t[3] = hi.y;
-    } else {
-      const uint32_t w0 = cvt_bf16x2_rn(x[1], x[0]), w1 = cvt_bf16x2_rn(x[3], x[2]);
-      pk[2 * g] = w0;
-      pk[2 * g + 1] = w1;
-      t[0] = __uint_as_float(w0 << 16); t[1] = __uint_as_float(w0 & 0xFFFF0000u);
-      t[2] = __uint_as_float(w1 << 16); t[3] = __uint_as_float(w1 & 0xFFFF0000u);
-    }
+    round4<EB, GE>(p, ROUND_NEAREST, t, nullptr, 0, &pk[EB == 1 ? g : 2 * g]);
     if (row_ok) {
       st_global_v4_hint(mp, make_uint4(__float_as_uint(m1[0]), __float_as_uint(m1[1]), __float_as_uint(m1[2]),
                                        __float_as_uint(m1[3])), pol);
@@ -424,30 +401,27 @@ XMC_DEV void w_update_pack_adamw(const BwdParams& p, const uint32_t (&acc)[32], 
   for (int h = 0; h < 2 * EB; ++h) out[h] = make_uint4(pk[4 * h], pk[4 * h + 1], pk[4 * h + 2], pk[4 * h + 3]);
 }
 
-// The kernel body: CTA `bid` of `nblk` backward CTAs (d-tile bid % dtiles,
-// row group bid / dtiles).  xmc_bwd_kernel runs it on every CTA of its grid,
-// xmc_step_kernel on the CTAs after its forward ones.
-template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST, bool ADAMW, bool RING = false>
-XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CUtensorMap& tm_xt,
-                      const CUtensorMap& tm_ws, BwdParams p, const int bid, const int nblk) {
+// The kernel: CTA bid of the grid (d-tile bid % dtiles, row group bid / dtiles).
+// FAST: the production specialisation (SR_FAST, e4m3, no compensation, no
+// dropout mask) with every runtime mode switch folded away.
+template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false, bool ADAMW = false, int GE = EB>
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
+                   const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
+                   const __grid_constant__ BwdParams p) {
   using C = BwdCfg<EB, XT_RES, KCMAX>;
   static_assert(!ADAMW || (CE == 4 && !FAST), "the Adam-style head keeps an fp32 compensation");
-  if constexpr (FAST) {
-    p.debug = 0;
-#ifndef XMC_TRACE_FAST   // measurement builds keep the pipeline trace in the fast path
-    p.trace = nullptr;
-#endif
-    p.keep = nullptr;
-    p.rounding = ROUND_SR_FAST;
-  }
+  static_assert(!FAST || (EB == 1 && GE == 1 && CE == 0), "the fast path is the e4m3 SR_FAST head");
   constexpr int WS = C::kWStages;
   constexpr int KS = C::kKStages;
+  const int bid = static_cast<int>(blockIdx.x), nblk = static_cast<int>(gridDim.x);
+  const int rounding = FAST ? static_cast<int>(ROUND_SR_FAST) : p.rounding;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* xt_s = smem;
   uint8_t* w_s = smem + C::kXtBytes;
-  uint8_t* out_s = w_s + WS * C::kWBytes;      // W_new staging tile (kOutBuf)
+  uint8_t* out_s = w_s + WS * C::kWBytes;      // W_new staging tiles (kOutBuf)
   uint8_t* k_s = out_s + C::kOutBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(k_s + KS * C::kKSlot);
   uint64_t* w_full = bars;                 // [WS]
@@ -459,6 +433,7 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
   uint64_t* xt_full = t_empty + 2;
   uint64_t* gx_full = xt_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gx_full + 1);
+  int32_t* status_s = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id_sync();
   const int j = bid % p.dtiles;
@@ -489,7 +464,7 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], p.gcl);   // one MMA commit from every CTA the slot is multicast to
+      mbar_init(&k_empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&t_full[s], 1);
@@ -500,22 +475,21 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  // G sharing: peers multicast into this CTA's slots and arrive on its
-  // barriers, so every barrier of the cluster is initialised first
-  if (p.gcl > 1) cluster_sync();
-  else __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const uint32_t tmem_gx = tmem_base + 256;   // cols [256, 512): grad_X^T partial
-  // cols [0,128) and [128,256): the two dW buffers
-
   // PDL: the prologue above (barriers, TMEM, tensor maps) overlapped the
   // previous kernel's tail; from here on its outputs are read
   griddep_wait();
   griddep_launch_dependents();
-  // a latched error of an earlier kernel of the step turns this one into a no-op
-  const bool aborted = *p.status != 0;
+  // a latched error of an earlier kernel of the step turns this one into a
+  // no-op; read once so every role of the CTA agrees
+  if (threadIdx.x == 0) *status_s = *p.status;
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const uint32_t tmem_gx = tmem_base + 256;   // cols [256, 512): grad_X^T partial
+  // cols [0,128) and [128,256): the two dW buffers
+  const bool aborted = *status_s != 0;
+
   if (aborted) {
   } else if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -523,76 +497,48 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
     // 128-B lines of all its lanes) cycles (tools/probe_tma.cu), so a tile's
     // boxes go out together as ONE warp-wide instruction, lane l = box l.
     const int lane = static_cast<int>(lane_id());
-    // debug & 4 / pol_normal (measurement): evict_normal everywhere, so a
-    // chunk that fits in L2 stays there across repeated launches
-    const bool pn = (p.debug & 4) || p.pol_normal;
-    const uint64_t pol_stream = pn ? policy_evict_normal() : policy_evict_first();
-    const uint64_t pol_keep = pn ? policy_evict_normal() : policy_evict_last();
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
     if constexpr (XT_RES) {
-      if (lane == 0) mbar_arrive_expect_tx(xt_full, p.kc_count * C::kBox);
+      if (lane == 0) mbar_arrive_expect_tx(xt_full, p.xt_kc * C::kBox);
       __syncwarp();
-      if (lane < p.kc_count)
+      if (lane < p.xt_kc)
         tma_load_2d_hint(xt_s + lane * C::kBox, &tm_xt, xt_full, lane * C::kBoxK, j * 128, pol_keep);
       __syncwarp();
     }
     int ws = 0, ks = 0;
     uint32_t wph = 0, kph = 0;
-    const int crank = p.gcl > 1 ? static_cast<int>(cluster_ctarank()) : 0;
-    const uint16_t gmask = static_cast<uint16_t>((1u << p.gcl) - 1u);
     // the tile's G slots are consecutive ring slots when the ring holds whole tiles
     const bool whole = nk > 0 && nk <= KS && KS % nk == 0;
     for (int it = 0; it < ntl; ++it) {
       const int tile = tile_at(it);
       mbar_wait(&w_empty[ws], wph ^ 1);
-      if (lane == 0) trace_ev(p.trace, it, 0);
       if (whole) {
         for (int i = 0; i < nk; ++i) mbar_wait(&k_empty[ks + i], kph ^ 1);
-        if constexpr (RING) {
-          // fused step: the tile's G rows are written by the forward CTAs
-          spin_until_ge(p.ready + tile, p.ready_target, p.status, ST_RING_TIMEOUT);
-          fence_proxy_async_global();
-        }
         if (lane == 0) {
-          mbar_arrive_expect_tx(&w_full[ws], (p.debug & 32) ? 0 : C::kWBytes);
-          for (int i = 0; i < nk; ++i) mbar_arrive_expect_tx(&k_full[ks + i], (p.debug & 16) ? 0 : kslot_bytes);
+          mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
+          for (int i = 0; i < nk; ++i) mbar_arrive_expect_tx(&k_full[ks + i], kslot_bytes);
         }
         __syncwarp();
-        if (p.gcl == 1) {
-          // W boxes, then per k-chunk the G box (+ the Xq^T box when not resident)
-          const int kGB = (!XT_RES && p.do_update) ? 2 : 1;
-          const int gl = lane - C::kWBoxes;
-          const int i = gl / kGB, sub = gl % kGB;
-          const bool is_w = lane < C::kWBoxes;
-          const bool active = is_w || (gl >= 0 && i < nk);
-          const CUtensorMap* m = is_w ? &tm_w : (sub == 0 ? &tm_g : &tm_xt);
-          uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + (ks + i) * C::kKSlot + sub * C::kBox;
-          uint64_t* bar = is_w ? &w_full[ws] : &k_full[ks + i];
-          const int32_t c0 = is_w ? j * 128 + lane * C::kBoxK : (kb + i) * C::kBoxK;
-          const int gtile = RING ? tile % p.ring_tiles : tile;
-          const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? gtile * 128 : j * 128);
-          // measurement: debug & 16 skips the G loads, debug & 32 the W loads
-          // (the barrier then completes through the arrive with a tx of 0)
-          const bool skip = (p.debug & 16) ? !is_w : ((p.debug & 32) ? is_w : false);
-          if (active && !skip) tma_load_2d_hint(dst, m, bar, c0, c1, is_w ? pol_stream : pol_keep);
-        } else {
-          // G shared over the cluster (measured neutral, XMC_BWD_GCL): this
-          // CTA's 32-row G pieces (id kc*4+qq, owner id mod gcl) multicast to
-          // every CTA of the cluster; k_empty counts every CTA's commit
-          if (lane < C::kWBoxes)
-            tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kBoxK,
-                             tile * 128, pol_stream);
-          const int piece = crank + lane * p.gcl;
-          if (XT_RES && piece < 4 * nk) {
-            const int i = piece >> 2, qq = piece & 3;
-            tma_load_2d_mc(k_s + (ks + i) * C::kKSlot + qq * 32 * 128, &tm_g, &k_full[ks + i], (kb + i) * C::kBoxK,
-                           tile * 128 + qq * 32, gmask, pol_keep);
-          }
-        }
+        // W boxes, then per k-chunk the G box (+ the Xq^T box when not resident)
+        const int kGB = (!XT_RES && p.do_update) ? 2 : 1;
+        const int gl = lane - C::kWBoxes;
+        const int i = gl / kGB, sub = gl % kGB;
+        const bool is_w = lane < C::kWBoxes;
+        const bool active = is_w || (gl >= 0 && i < nk);
+        const CUtensorMap* m = is_w ? &tm_w : (sub == 0 ? &tm_g : &tm_xt);
+        uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + (ks + i) * C::kKSlot + sub * C::kBox;
+        uint64_t* bar = is_w ? &w_full[ws] : &k_full[ks + i];
+        const int kcg = kb + i;
+        const int32_t c0 = is_w ? j * 128 + lane * C::kBoxK : (sub == 0 ? kcg : kcg % p.xt_kc) * C::kBoxK;
+        const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? tile * 128 : j * 128);
+        if (active) tma_load_2d_hint(dst, m, bar, c0, c1, is_w ? pol_stream : pol_keep);
         __syncwarp();
         ks += nk;
         if (ks == KS) { ks = 0; kph ^= 1; }
       } else {
-        // more k-chunks than ring slots (bf16, batch 512): slot by slot
+        // more k-chunks than ring slots (bf16 batch 512, reference-precision
+        // planes): slot by slot
         if (lane == 0) mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
         __syncwarp();
         if (lane < C::kWBoxes)
@@ -607,49 +553,37 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
           if (lane == 0) tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
           if constexpr (!XT_RES)
             if (lane == 1 && p.do_update)
-              tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], kc * C::kBoxK, j * 128, pol_keep);
+              tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], (kc % p.xt_kc) * C::kBoxK, j * 128, pol_keep);
           __syncwarp();
           if (++ks == KS) { ks = 0; kph ^= 1; }
         }
       }
       if (++ws == WS) { ws = 0; wph ^= 1; }
-      if (lane == 0) trace_ev(p.trace, it, 1);
     }
     __syncwarp();
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    constexpr uint32_t fa = EB == 1 ? 0u : 1u;   // e4m3 : bf16
-    constexpr uint32_t idesc_dw = umma_idesc(fa, fa, false, false, 128, 128);
-    const uint32_t idesc_gx = umma_idesc(fa, fa, true, true, 128, p.gx_kc_count * C::kBoxK);
-    const uint16_t gmask = static_cast<uint16_t>((1u << p.gcl) - 1u);
+    // e4m3 head: kind::f8f6f4 with G e4m3 or e5m2 (format code 1); bf16: kind::f16
+    const uint32_t gf = EB == 1 ? (p.g_e5m2 ? 1u : 0u) : 1u;
+    const uint32_t xf = EB == 1 ? 0u : 1u;
+    const uint32_t idesc_dw = umma_idesc(gf, xf, false, false, 128, 128);                         // A = G, B = Xq
+    const uint32_t idesc_gx = umma_idesc(xf, gf, true, true, 128, p.gx_kc_count * C::kBoxK);      // A = W^T, B = G
     if constexpr (XT_RES) mbar_wait(xt_full, 0);
     int ws = 0, ks = 0, ds = 0;
     uint32_t wph = 0, kph = 0, dph = 0;
-    int it = 0;
-    for (; it < ntl; ++it) {
-      const int tile = tile_at(it);
+    for (int it = 0; it < ntl; ++it) {
       mbar_wait(&w_full[ws], wph);
-      if (lane_id() == 0) trace_ev(p.trace, it, 2);
       mbar_wait(&t_empty[ds], dph ^ 1);
-      if (lane_id() == 0) trace_ev(p.trace, it, 8);
       tc_fence_after();
       const uint32_t w_addr = smem_u32(w_s + ws * C::kWBytes);
       const uint32_t d_dw = tmem_base + ds * 128;
       for (int kc = kb; kc < ke; ++kc) {
-        if (kc == kb + 1 && lane_id() == 0) trace_ev(p.trace, it, 10);
         mbar_wait(&k_full[ks], kph);
         tc_fence_after();
-        if (RING && kc == ke - 1 && lane_id() == 0) {
-          // every G box of the tile landed: its ring slot may be rewritten
-          fence_proxy_async_global();
-          red_release_gpu_add(p.consumed + tile, 1);
-        }
-        if (kc == kb && lane_id() == 0) trace_ev(p.trace, it, 9);
-        if (kc == ke - 1 && lane_id() == 0) trace_ev(p.trace, it, 3);
         if (elect_one()) {
           const uint32_t g_addr = smem_u32(k_s + ks * C::kKSlot);
-          const uint32_t x_addr = XT_RES ? smem_u32(xt_s + kc * C::kBox) : g_addr + C::kBox;
-          if (p.do_update && !(p.debug & 1)) {
+          const uint32_t x_addr = XT_RES ? smem_u32(xt_s + (kc % p.xt_kc) * C::kBox) : g_addr + C::kBox;
+          if (p.do_update) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t ad = umma_desc_sw128(g_addr + k * 32, 16, 1024);
@@ -675,13 +609,9 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
               if constexpr (EB == 1) mma_f8(tmem_gx, ad, bd, idesc_gx, (it | k) != 0);
               else mma_f16(tmem_gx, ad, bd, idesc_gx, (it | k) != 0);
             }
-            for (int s = ks - gk; s <= ks; ++s) {
-              if (p.gcl > 1) mma_commit_mc(&k_empty[s], gmask);
-              else mma_commit(&k_empty[s]);
-            }
+            for (int s = ks - gk; s <= ks; ++s) mma_commit(&k_empty[s]);
           } else if (!in_gx) {
-            if (p.gcl > 1) mma_commit_mc(&k_empty[ks], gmask);
-            else mma_commit(&k_empty[ks]);
+            mma_commit(&k_empty[ks]);
           }
           // in place: dW is handed over only after the grad_X MMAs, which read
           // the W_old tile the epilogue overwrites with W_new
@@ -691,7 +621,6 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
         if (++ks == KS) { ks = 0; kph ^= 1; }
       }
       if (elect_one()) mma_commit(&w_empty[ws]);
-      if (lane_id() == 0) trace_ev(p.trace, it, 4);
       __syncwarp();
       if (++ws == WS) { ws = 0; wph ^= 1; }
       if (++ds == 2) { ds = 0; dph ^= 1; }
@@ -709,19 +638,16 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
     // the 4 warps of sub-partition q own rows [32q, 32q+32) of every tile;
     // they sync among themselves and one lane TMA-stores their 32-row slab
     const bool storer = (quarter == 0) && lane_id() == 0;
-    const uint64_t pol_w_out = ((p.debug & 4) || p.pol_normal) ? policy_evict_normal() : policy_evict_first();   // W_new streams out; keep L2 for G
+    const uint64_t pol_w_out = policy_evict_first();   // W_new streams out; keep L2 for G
     int ws = 0, ds = 0, prev_ws = -1;
     int ot_flip = 0;
     uint32_t wph = 0, dph = 0;
-    const bool tracer = warp == 2 && lane_id() == 0;
     const PhiloxKeys pk = philox_keys(p.rng_base);   // round keys, once per launch
-    int it = 0;
-    for (; it < ntl; ++it) {
+    for (int it = 0; it < ntl; ++it) {
       const int tile = tile_at(it);
       uint8_t* wt = w_s + ws * C::kWBytes;
       mbar_wait(&w_full[ws], wph);
-      if (tracer) trace_ev(p.trace, it, 5);
-      if (p.do_update && !(p.debug & 2)) {
+      if (p.do_update) {
         const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
         const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + c0;
         // --- independent of dW: W_old and random bits, overlapping the MMAs
@@ -747,9 +673,9 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
 #pragma unroll
           for (int h = 0; h < CE * 2; ++h) craw[h] = krow ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
         }
-        if constexpr (FAST && EB == 1 && CE == 0 && C::kOutTiles == 2) {
-          // production path: everything independent of dW (Philox words,
-          // W_old decoded and scaled by 1 - lr wd) is computed and pinned in
+        if constexpr (FAST) {
+          // production path: everything independent of dW (SR words, W_old
+          // decoded and scaled by 1 - lr wd) is computed and pinned in
           // registers BEFORE the dW wait, so it overlaps the MMAs
           uint32_t rw[8];
           sr_words<1>(pk, flat0, rw, p.sr_bits != 0);
@@ -780,7 +706,6 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
           for (int k = 0; k < 32; ++k) pin(wc[k]);
           mbar_wait(&t_full[ds], dph);
           tc_fence_after();
-          if (tracer) trace_ev(p.trace, it, 6);
           uint32_t acc[32];
           tmem_ld32(tmem_base + lane_off + ds * 128 + c0, acc);
           tmem_ld_wait();
@@ -811,7 +736,6 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
             tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
             bulk_commit();
           }
-          if (tracer) trace_ev(p.trace, it, 7);
           prev_ws = ws;
           if (++ws == WS) { ws = 0; wph ^= 1; }
           if (++ds == 2) { ds = 0; dph ^= 1; }
@@ -819,14 +743,13 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
         }
         uint32_t km = 0u;   // dropout keep bits of this thread's 32 columns
         if (p.keep != nullptr && grow < p.rows) km = __ldg(p.keep + grow * (p.d >> 5) + ((j * 128 + c0) >> 5));
-        uint32_t rw[C::kRandWords];
-        if (p.rounding == ROUND_SR_FAST) sr_words<EB>(pk, flat0, rw, p.sr_bits != 0);
+        uint32_t rw[8 * GE];
+        if (rounding == ROUND_SR_FAST) sr_words<GE>(pk, flat0, rw, p.sr_bits != 0);
         float w[CE > 0 ? 1 : 32];
         if constexpr (CE == 0) w_decode<EB>(raw, w);
         // --- dW from TMEM, then release the accumulator buffer at once
         mbar_wait(&t_full[ds], dph);
         tc_fence_after();
-        if (tracer) trace_ev(p.trace, it, 6);
         uint32_t acc[32];
         tmem_ld32(tmem_base + lane_off + ds * 128 + c0, acc);
         tmem_ld_wait();
@@ -840,23 +763,18 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
         }
         uint4 out[C::kChunks16];
         if constexpr (ADAMW) {
-          w_update_pack_adamw<EB>(p, acc, raw, grow * p.d + j * 128 + c0, grow < p.rows, out, pol_w_out);
+          w_update_pack_adamw<EB, GE>(p, acc, raw, grow * p.d + j * 128 + c0, grow < p.rows, out, pol_w_out);
         } else if constexpr (CE > 0) {
           uint4* cdst = krow ? reinterpret_cast<uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE) : nullptr;
-          w_update_pack_kahan<EB, CE>(p, p.rounding, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
+          w_update_pack_kahan<EB, CE, GE>(p, rounding, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
         } else {
-          w_update_pack<EB>(p, p.rounding, acc, w, rw, flat0, out);
+          w_update_pack<EB, GE>(p, rounding, acc, w, rw, flat0, out);
         }
         // W_new into a swizzled smem tile (the staging tile, or in place once
         // the grad_X MMAs have read W_old), then one TMA store per 32-row slab
         // (full 128-B lines to HBM, no LSU traffic)
         uint8_t* ot = wt;
-        if constexpr (C::kOutTiles == 1) {
-          ot = out_s;
-          // the previous tile's store of this slab must have read the staging smem
-          if (storer && prev_ws >= 0) bulk_wait_read<0>();
-          named_bar_sync(1 + q, 128);
-        } else if constexpr (C::kOutTiles == 2) {
+        if constexpr (C::kOutTiles == 2) {
           ot = out_s + (ot_flip & 1) * C::kWBytes;
           ++ot_flip;
         }
@@ -872,12 +790,10 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
         if (storer) {
 #pragma unroll
           for (int b = 0; b < C::kWBoxes; ++b)
-            if (!(p.debug & 8))   // measurement: debug & 8 drops the W_new store
-              tma_store_2d_hint(&tm_ws, ot + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK,
-                                tile * 128 + q * 32, pol_w_out);
+            tma_store_2d_hint(&tm_ws, ot + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK, tile * 128 + q * 32,
+                              pol_w_out);
           bulk_commit();
         }
-        if (tracer) trace_ev(p.trace, it, 7);
         prev_ws = ws;
       } else {
         mbar_wait(&t_full[ds], dph);
@@ -897,7 +813,7 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
     if (do_gx) {
       mbar_wait(gx_full, 0);
       tc_fence_after();
-      // this CTA's slot of the [R][d][Bp] partial buffer; chunks of one step
+      // this CTA's slot of the [R][d][gx_ld] partial buffer; chunks of one step
       // accumulate into it (stream-ordered, one owner per slot: deterministic)
       const int nchunks = p.gx_kc_count * C::kBoxK / 32;
       float* dst = p.gx_ws + (static_cast<int64_t>(r0) * p.d + j * 128 + row) * p.gx_ld + p.gx_kc0 * C::kBoxK;
@@ -925,22 +841,11 @@ XMC_DEV void bwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_g, const CU
   }
 
   tc_fence_before();
-  // no CTA leaves while a peer may still multicast into it or arrive on it
-  if (p.gcl > 1) cluster_sync();
-  else __syncthreads();
+  __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);
   }
-}
-
-template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false, bool ADAMW = false>
-__global__ void __launch_bounds__(kBwdThreads, 1)
-    xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
-                   const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
-                   BwdParams p) {
-  bwd_body<EB, XT_RES, KCMAX, CE, FAST, ADAMW>(tm_w, tm_g, tm_xt, tm_ws, p, static_cast<int>(blockIdx.x),
-                                               static_cast<int>(gridDim.x));
 }
 
 }  // namespace xmc

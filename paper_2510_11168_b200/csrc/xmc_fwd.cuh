@@ -18,11 +18,21 @@
 // leader's commits multicast to both CTAs' empty / tmem-full barriers; the
 // peer's epilogue releases the accumulator on the leader's barrier.
 //
-// Epilogue numerics.  sigmoid = 1 / (1 + 2^(-z log2 e)): ex2 on MUFU.  e4m3 G
-// is stored as e4m3(256 g): the 2^8 scale is folded into the reciprocal, which
-// runs on the FMA pipe (magic seed + 3 Newton steps, rel. err < 2^-20), and the
-// [2^-24, 1-2^-24] clip is dropped because both clip edges round to the same
-// e4m3 code (0 / 256) as the unclipped value.  bf16 G keeps MUFU rcp + clip.
+// G output formats (template GOUT, mode 0):
+//   G_OPERAND  e4m3 head: e4m3(256 g); bf16 head: bf16(g).  sigmoid =
+//              1 / (1 + 2^(-z log2 e)): ex2 on MUFU; for e4m3 the 2^8 scale is
+//              folded into the reciprocal, which runs on the FMA pipe (magic
+//              seed + 3 Newton steps, rel. err < 2^-20), and the clip is
+//              dropped because both clip edges round to the same e4m3 code.
+//   G_E5M2     e4m3 head: e5m2(256 g) -- same scale, range down to the
+//              reference's 2^-24 clip (e5m2 subnormals reach 2^-16 = 2^8 * 2^-24),
+//              so trained heads' small sigmoids do not flush to zero.
+//   G_REF      reference precision: g exactly as logit_gradient computes it
+//              (IEEE expf, fp32 add and divide, clip, fp32 "-1" at positives),
+//              split EXACTLY into three bf16 planes hi + mid + lo = g, written
+//              as [hi | mid | lo] (row stride 3 Bp).  The backward consumes the
+//              planes as a 3x longer K (bf16 x bf16 products are exact), so it
+//              multiplies by the fp32 G of the reference (head.py:193-208, 236).
 #pragma once
 
 #include "xmc_ptx.cuh"
@@ -30,17 +40,19 @@
 
 namespace xmc {
 
+enum GOut : int { G_OPERAND = 0, G_E5M2 = 1, G_REF = 2 };
+
 struct FwdParams {
   int32_t rows;        // labels in this chunk
   int32_t B;           // valid samples
   int32_t d;           // feature dim (multiple of 128 B / elem)
   int32_t num_tiles;   // ceil(rows / 128)
-  int32_t mode;        // 0: write quantized G; 1: write fp32 logits
-  int32_t g_fmt;       // FMT_E4M3 (scaled by 256) or FMT_BF16
+  int32_t mode;        // 0: write G; 1: write fp32 logits; 2: top-k (TOPK instantiation)
   const int32_t* tile_ptr;   // [num_tiles + 1] into entries (chunk-local tiles)
   const uint32_t* entries;   // (row_in_tile << 16) | sample
   void* out;                 // G [rows][ld] or logits fp32 [rows][ld]
   int64_t ld;                // leading dimension (elements) of out
+  int64_t plane_ld;          // G_REF: elements between the hi / mid / lo planes of a row
   float* stats;              // [0] += sum |G| over valid entries (optional)
   float logit_scale;         // z = logit_scale * acc (1, or 1/(1-p) under keyed dropout)
   // top-k scoring (TOPK instantiation): per (sample, CTA, sub-partition) the
@@ -49,28 +61,17 @@ struct FwdParams {
   int32_t* cand_l;
   int64_t label0;            // global label of local row 0 of this launch
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
-  int32_t debug;             // measurement only (XMC_DEBUG_FWD): 1 skip the G epilogue, 2 skip only its stores
   int32_t sample0;           // first sample of this pass (batch split into BN-wide passes); entries of
                              // other samples are skipped, this pass's are shifted by -sample0
-  // fused step (xmc_step_kernel): G goes to a ring of ring_tiles 128-row tiles
-  // (tile t -> ring tile t mod ring_tiles); before writing tile t a warp waits
-  // for consumed[t - ring_tiles] >= consumed_target (every backward CTA of the
-  // row group has read the previous occupant), after writing it adds 1 to
-  // ready[t].  Read only by the RING instantiation (fwd_body<..., RING>).
-  int32_t ring_tiles;
-  int32_t consumed_target;
-  int32_t* ready;
-  const int32_t* consumed;
 };
 
-// XRES: this CTA's Xq rows stay resident in shared memory for the whole
-// launch (loaded once, kXResChunks K-chunks max, i.e. d <= 768 for e4m3), so a
-// stage carries only its W box: half the TMA work and L2->SM traffic per tile.
-// Without PAIR, XRES is the split layout (BN = 128): CTAs 2c and 2c+1 take the
-// same label tiles for samples [0, 128) and [128, 256) (cta_group::1 only, as
-// the fused step kernel needs).
+// XRES (CTA pairs only): this CTA's Xq rows stay resident in shared memory
+// for the whole launch (loaded once, kXResChunks K-chunks max, i.e. d <= 768
+// for e4m3), so a stage carries only its W box: half the TMA work and L2->SM
+// traffic per tile.
 template <int EB, int BN, bool PAIR, bool XRES = false>
 struct FwdCfg {
+  static_assert(!XRES || PAIR, "resident Xq runs on CTA pairs");
   static constexpr int kBoxK = 128 / EB;                  // K elements per 128-B swizzle atom
   static constexpr int kWBytes = 128 * 128;               // W box: 128 rows x 128 B
   static constexpr int kXRows = PAIR ? BN / 2 : BN;       // Xq rows staged by this CTA
@@ -116,14 +117,22 @@ XMC_DEV void topk_insert(float (&s)[kTopK], int32_t (&l)[kTopK], float v, int32_
   }
 }
 
+// logit_gradient's sigmoid (head.py:193-195) in the reference's fp32 ops:
+// clip(1 / (1 + exp(-z)), 2^-24, 1 - 2^-24) with IEEE expf / add / divide
+XMC_DEV float ref_sigmoid_clip(float z) {
+  float g = __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-z)));
+  g = g < 5.9604644775390625e-08f ? 5.9604644775390625e-08f : g;   // NaN propagates like np.clip
+  return g > 0.99999994039535522461f ? 0.99999994039535522461f : g;
+}
+
 // The kernel body: work units unit0, unit0 + ustride, ... (tiles, or tile
-// pairs for PAIR); xh = which BN-sample half of the batch (split layout).
-template <int EB, int BN, bool PAIR, bool TOPK, bool XRES, bool RING = false>
-XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParams p, const int unit0,
-                      const int ustride, const int xh) {
+// pairs for PAIR).
+template <int EB, int BN, bool PAIR, bool TOPK, bool XRES, int GOUT>
+XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const FwdParams& p, const int unit0,
+                      const int ustride) {
   using C = FwdCfg<EB, BN, PAIR, XRES>;
   static_assert(!PAIR || BN <= 256, "paired tiles use one N <= 256 accumulator");
-  static_assert(!XRES || PAIR || BN == 128, "resident Xq: CTA pairs, or the 128-sample split layout");
+  static_assert(GOUT != G_E5M2 || EB == 1, "e5m2 G is the e4m3 head's wide-range operand");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -137,6 +146,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
   uint64_t* tempty = tfull + C::kAccStages;       // [kAccStages] (leader's counts both CTAs)
   uint64_t* xfull = tempty + C::kAccStages;       // resident Xq landed (leader's counts both CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfull + 1);
+  int32_t* status_s = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id_sync();
   const int kc_count = p.d / C::kBoxK;
@@ -145,7 +155,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
   // work units: single tiles, or tile pairs (2u, 2u+1) for a CTA pair
   const int num_units = PAIR ? (p.num_tiles + 1) / 2 : p.num_tiles;
   // Xq rows (samples) this CTA stages
-  const int xrow0 = PAIR ? static_cast<int>(rank) * C::kXRows : ((!PAIR && XRES) ? xh * BN : 0);
+  const int xrow0 = PAIR ? static_cast<int>(rank) * C::kXRows : 0;
 
   if (warp == 0 && elect_one()) {
     prefetch_tmap(&tm_w);
@@ -165,18 +175,25 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
     if constexpr (PAIR) tmem_alloc_2sm<C::kTmemCols>(tmem_slot);
     else tmem_alloc<C::kTmemCols>(tmem_slot);
   }
+  // PDL: the prologue above (barriers, TMEM, tensor maps) overlapped the
+  // previous kernel's tail; from here on its outputs are read
+  griddep_wait();
+  griddep_launch_dependents();
+  // A latched error of an earlier kernel of the step turns this one into a
+  // no-op.  The status word is read ONCE (by the pair leader) and every warp of
+  // both CTAs takes that value: the kernel itself may latch an error later, and
+  // roles of one pair must never disagree about skipping (they would hang on
+  // each other's barriers).
+  if (threadIdx.x == 0 && leader) *status_s = *p.status;
   tc_fence_before();
   if constexpr (PAIR) cluster_sync();
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  bool aborted;
+  if constexpr (PAIR) aborted = ld_shared_cluster_s32(mapa_shared(status_s, 0)) != 0;
+  else aborted = *status_s != 0;
 
-  // PDL: the prologue above (barriers, TMEM, tensor maps) overlapped the
-  // previous kernel's tail; from here on its outputs are read
-  griddep_wait();
-  griddep_launch_dependents();
-  // a latched error of an earlier kernel of the step turns this one into a no-op
-  const bool aborted = *p.status != 0;
   if (aborted) {
   } else if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -189,24 +206,17 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
     constexpr int kIPB = XRES ? 3 : 2;                                 // stages per instruction
     static_assert(kBPI * kIPB <= 32, "one lane per box");
     const int lane = static_cast<int>(lane_id());
-    // fused step: the backward CTAs re-read each W tile shortly after
-    const uint64_t pol_w = RING ? policy_evict_normal() : policy_evict_first();
+    const uint64_t pol_w = policy_evict_first();
     const uint64_t pol_x = policy_evict_last();
     if constexpr (XRES) {
       // this CTA's Xq rows, every K-chunk, once: one warp-wide instruction
-      if constexpr (PAIR) {
-        if (lane == 0) {
-          if (leader) mbar_arrive_expect_tx(xfull, 2 * kc_count * C::kXBytes);
-          else mbar_arrive_cluster(mapa_shared(xfull, 0));
-        }
-        __syncwarp();
-        if (lane < kc_count)
-          tma_load_2d_2sm(xres + lane * C::kXBytes, &tm_x, mapa_shared(xfull, 0), lane * C::kBoxK, xrow0, pol_x);
-      } else {
-        if (lane == 0) mbar_arrive_expect_tx(xfull, kc_count * C::kXBytes);
-        __syncwarp();
-        if (lane < kc_count) tma_load_2d_hint(xres + lane * C::kXBytes, &tm_x, xfull, lane * C::kBoxK, xrow0, pol_x);
+      if (lane == 0) {
+        if (leader) mbar_arrive_expect_tx(xfull, 2 * kc_count * C::kXBytes);
+        else mbar_arrive_cluster(mapa_shared(xfull, 0));
       }
+      __syncwarp();
+      if (lane < kc_count)
+        tma_load_2d_2sm(xres + lane * C::kXBytes, &tm_x, mapa_shared(xfull, 0), lane * C::kBoxK, xrow0, pol_x);
       __syncwarp();
     }
     const int my_units = unit0 < num_units ? (num_units - unit0 + ustride - 1) / ustride : 0;
@@ -398,17 +408,16 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
     const int row = q * 32 + lane_id();      // row within the 128-label tile
     const int etid = ew * 32 + lane_id();
     const bool want_stats = p.stats != nullptr && p.mode == 0;
-    // split layout: this CTA's columns are samples [xs, xs + BN) of the pass
-    // (the host offsets out / B by the pass's sample0 already)
-    const int xs = (!PAIR && XRES) ? xh * BN : 0;
-    const int s0 = p.sample0 + xs;               // first sample (positive entries)
-    const int bvalid = p.B - xs;                 // valid columns
+    const int s0 = p.sample0;                    // first sample (positive entries)
+    const int bvalid = p.B;                      // valid columns
     const bool pad_cols = bvalid < BN;
     const bool use_pos = p.mode == 0 && p.tile_ptr != nullptr;
     const uint64_t pol_g = policy_evict_last();   // G is re-read by the backward kernel
     float abs_sum = 0.f;
     bool nan_seen = false;
     const float zk = -1.4426950408889634f * p.logit_scale;   // -log2(e) * scale
+    // operand G of an e4m3 head carries the 2^8 scale (e4m3 / e5m2 encodings)
+    constexpr bool kScaled = EB == 1 && GOUT != G_REF;
     int acc = 0;
     uint32_t acc_phase = 0;
     auto tile_of = [&](int u) { return PAIR ? 2 * u + static_cast<int>(rank) : u; };
@@ -446,22 +455,15 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
       tc_fence_after();
       const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
       const bool row_ok = grow < p.rows;
-      // G row in out: the chunk row, or its ring row (fused step)
-      int64_t orow = grow;
-      if constexpr (RING) {
-        orow = static_cast<int64_t>(tile % p.ring_tiles) * 128 + row;
-        if (tile >= p.ring_tiles)
-          spin_until_ge(p.consumed + (tile - p.ring_tiles), p.consumed_target, p.status, 64 /*ST_RING_TIMEOUT*/);
-      }
 #pragma unroll 1
-      for (int cc = 0; cc < ((p.debug & 1) ? 0 : C::kChunks); ++cc) {
+      for (int cc = 0; cc < C::kChunks; ++cc) {
         const int col0 = grp * C::kColsPerWarp + cc * 32;
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, r);
         tmem_ld_wait();
         if (p.mode == 1) {
           if (row_ok) {
-            float* o = reinterpret_cast<float*>(p.out) + grow * p.ld + xs;
+            float* o = reinterpret_cast<float*>(p.out) + grow * p.ld;
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               if (col0 + j < bvalid) o[col0 + j] = __uint_as_float(r[j]) * p.logit_scale;
@@ -470,7 +472,16 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
         }
         const uint32_t pos = has_pos ? bitmap[row * C::kWordsPerRow + (col0 >> 5)] : 0u;
         float g[32];
-        if constexpr (EB == 1) {
+        if constexpr (GOUT == G_REF) {
+          // the reference's fp32 sigmoid; positives get the fp32 "-1" (head.py:196)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float z = __uint_as_float(r[j]) * p.logit_scale;
+            nan_seen |= (z != z);
+            g[j] = ref_sigmoid_clip(z);
+            if ((pos >> j) & 1u) g[j] = __fsub_rn(g[j], 1.0f);
+          }
+        } else if constexpr (EB == 1) {
           // g256 = 256 sigmoid(z) = 1 / y, y = 2^-8 (1 + 2^(-z log2 e))
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
@@ -489,6 +500,12 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
             for (int it = 0; it < 3; ++it) x = fmul2(x, ffma2(ny, x, two));   // x (2 - y x)
             f2unpack(x, g[j], g[j + 1]);
           }
+          if constexpr (GOUT == G_E5M2) {
+            // the 2^-24 clip (head.py:47-48) is representable in e5m2 x 2^8
+            // (2^-16, its smallest subnormal): keep it
+#pragma unroll
+            for (int j = 0; j < 32; ++j) g[j] = fmaxf(g[j], 1.52587890625e-05f);
+          }
         } else {
           const float SIG_LO = 5.9604644775390625e-08f;   // 2^-24  (head.py:47-48)
           const float SIG_HI = 0.99999994039535522461f;   // 1 - 2^-24
@@ -501,11 +518,13 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
             g[j] = sg > SIG_HI ? SIG_HI : sg;
           }
         }
-        const float one = EB == 1 ? 256.0f : 1.0f;
-        if (pos != 0u) {
+        if constexpr (GOUT != G_REF) {
+          const float one = kScaled ? 256.0f : 1.0f;
+          if (pos != 0u) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if ((pos >> j) & 1u) g[j] -= one;
+            for (int j = 0; j < 32; ++j)
+              if ((pos >> j) & 1u) g[j] -= one;
+          }
         }
         if (pad_cols) {
 #pragma unroll
@@ -516,22 +535,47 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
 #pragma unroll
           for (int j = 0; j < 32; ++j) abs_sum += fabsf(g[j]);
         }
-        if (row_ok && !(p.debug & 2)) {   // debug & 2 (measurement): G math without the stores
-          if constexpr (EB == 1) {
+        if (row_ok) {
+          if constexpr (GOUT == G_REF) {
+            // g = hi + mid + lo exactly: hi = bf16(g), mid = bf16(g - hi),
+            // lo = bf16(g - hi - mid) (each residual is exact in fp32 and the
+            // last one has <= 8 significant bits)
+            uint32_t ph[16], pm[16], pl[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              ph[j] = cvt_bf16x2_rn(g[2 * j + 1], g[2 * j]);
+              const float r0 = g[2 * j] - __uint_as_float(ph[j] << 16);
+              const float r1 = g[2 * j + 1] - __uint_as_float(ph[j] & 0xFFFF0000u);
+              pm[j] = cvt_bf16x2_rn(r1, r0);
+              const float t0 = r0 - __uint_as_float(pm[j] << 16);
+              const float t1 = r1 - __uint_as_float(pm[j] & 0xFFFF0000u);
+              pl[j] = cvt_bf16x2_rn(t1, t0);
+            }
+            uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + grow * p.ld + col0;
+            auto store_plane = [&](uint16_t* dst, const uint32_t (&v)[16]) {
+              st_global_v8_hint(dst, *reinterpret_cast<const uint32_t(*)[8]>(&v[0]), pol_g);
+              st_global_v8_hint(dst + 16, *reinterpret_cast<const uint32_t(*)[8]>(&v[8]), pol_g);
+            };
+            store_plane(o, ph);
+            store_plane(o + p.plane_ld, pm);
+            store_plane(o + 2 * p.plane_ld, pl);
+          } else if constexpr (EB == 1) {
             uint32_t pk[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              const uint32_t lo = cvt_e4m3x2_rn(g[4 * j + 1], g[4 * j + 0]);
-              const uint32_t hi = cvt_e4m3x2_rn(g[4 * j + 3], g[4 * j + 2]);
+              const uint32_t lo = GOUT == G_E5M2 ? cvt_e5m2x2_rn(g[4 * j + 1], g[4 * j + 0])
+                                                 : cvt_e4m3x2_rn(g[4 * j + 1], g[4 * j + 0]);
+              const uint32_t hi = GOUT == G_E5M2 ? cvt_e5m2x2_rn(g[4 * j + 3], g[4 * j + 2])
+                                                 : cvt_e4m3x2_rn(g[4 * j + 3], g[4 * j + 2]);
               pk[j] = lo | (hi << 16);
             }
             // one 256-bit store: the thread's 32 G bytes are one full sector
-            st_global_v8_hint(reinterpret_cast<uint8_t*>(p.out) + orow * p.ld + xs + col0, pk, pol_g);
+            st_global_v8_hint(reinterpret_cast<uint8_t*>(p.out) + grow * p.ld + col0, pk, pol_g);
           } else {
             uint32_t pk[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) pk[j] = cvt_bf16x2_rn(g[2 * j + 1], g[2 * j]);
-            uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + orow * p.ld + xs + col0;
+            uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + grow * p.ld + col0;
             const uint32_t (&pa)[8] = *reinterpret_cast<const uint32_t(*)[8]>(&pk[0]);
             const uint32_t (&pb)[8] = *reinterpret_cast<const uint32_t(*)[8]>(&pk[8]);
             st_global_v8_hint(o, pa, pol_g);        // two full 32-B sectors
@@ -544,15 +588,11 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
       if (lane_id() == 0) {
         if (PAIR && !leader) mbar_arrive_cluster(mapa_shared(&tempty[acc], 0));
         else mbar_arrive(&tempty[acc]);
-        if constexpr (RING) {   // this warp's G rows of the tile are written
-          __threadfence();
-          red_release_gpu_add(p.ready + tile, 1);
-        }
       }
       if (++acc == C::kAccStages) { acc = 0; acc_phase ^= 1; }
     }
     if (want_stats) {
-      abs_sum *= (EB == 1) ? 0.00390625f : 1.0f;
+      abs_sum *= kScaled ? 0.00390625f : 1.0f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) abs_sum += __shfl_xor_sync(0xffffffffu, abs_sum, o);
       if (lane_id() == 0) atomicAdd(p.stats, abs_sum);
@@ -570,18 +610,16 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, FwdParam
   }
 }
 
-template <int EB, int BN, bool PAIR, bool TOPK = false, bool XRES = false>
+template <int EB, int BN, bool PAIR, bool TOPK = false, bool XRES = false, int GOUT = G_OPERAND>
 __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR, XRES>::kThreads, 1)
     xmc_fwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                   FwdParams p) {
+                   const __grid_constant__ FwdParams p) {
   if constexpr (PAIR) {
-    fwd_body<EB, BN, PAIR, TOPK, XRES>(tm_w, tm_x, p, static_cast<int>(cluster_id_x()),
-                                       static_cast<int>(num_clusters_x()), 0);
-  } else if constexpr (XRES) {   // split layout: CTA pair (2c, 2c+1) = the two sample halves
-    fwd_body<EB, BN, PAIR, TOPK, XRES>(tm_w, tm_x, p, static_cast<int>(blockIdx.x >> 1),
-                                       static_cast<int>(gridDim.x >> 1), static_cast<int>(blockIdx.x & 1));
+    fwd_body<EB, BN, PAIR, TOPK, XRES, GOUT>(tm_w, tm_x, p, static_cast<int>(cluster_id_x()),
+                                             static_cast<int>(num_clusters_x()));
   } else {
-    fwd_body<EB, BN, PAIR, TOPK, XRES>(tm_w, tm_x, p, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), 0);
+    fwd_body<EB, BN, PAIR, TOPK, XRES, GOUT>(tm_w, tm_x, p, static_cast<int>(blockIdx.x),
+                                             static_cast<int>(gridDim.x));
   }
 }
 

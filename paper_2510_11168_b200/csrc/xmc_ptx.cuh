@@ -336,6 +336,12 @@ XMC_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// 32-bit load from shared::cluster memory (a peer CTA's smem, mapa address)
+XMC_DEV int32_t ld_shared_cluster_s32(uint32_t cluster_addr) {
+  int32_t v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(cluster_addr) : "memory");
+  return v;
+}
 // Remote arrive with relaxed semantics: the callers only order tcgen05 / TMA
 // work (via tcgen05 fences / complete_tx), never generic memory, so no
 // cluster-scope release (which would wait for prior global stores) is needed.

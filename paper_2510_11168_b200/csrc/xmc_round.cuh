@@ -21,6 +21,17 @@ namespace xmc {
 enum Fmt : int32_t { FMT_FP32 = 0, FMT_BF16 = 1, FMT_FP16 = 2, FMT_E4M3 = 3, FMT_E5M2 = 4 };
 enum Rounding : int32_t { ROUND_NEAREST = 0, ROUND_SR_EXACT = 1, ROUND_SR_FAST = 2 };
 
+// latched device error bits (the handle status word; xmc_head.h error convention)
+enum StatusBits : int32_t {
+  ST_NONFINITE_X = 1,
+  ST_BAD_SAMPLE = 2,
+  ST_NONFINITE_GRAD = 4,
+  ST_LABEL_OUTSIDE = 8,
+  ST_CAPACITY = 16,
+  ST_NONFINITE_MOMENTS = 32,
+  ST_PEER_TIMEOUT = 128,  // peer grad_X all-reduce: a peer's tile never arrived
+};
+
 // Grid parameters of an emulated (E, M) format (formats.py:49-137).
 struct GridFmt {
   int32_t man_bits;
@@ -92,12 +103,13 @@ constexpr int kPhiloxRounds = 7;
 // schedule is the same for every counter of a launch
 struct PhiloxKeys {
   uint32_t k0[kPhiloxRounds], k1[kPhiloxRounds];
-  uint32_t hk;   // 32-bit key of the hash generator
+  uint32_t hk0, hk1;   // 64-bit key of the hash generator (see sr_hash_word)
 };
 XMC_DEV PhiloxKeys philox_keys(uint64_t key) {
   PhiloxKeys ks;
   uint32_t k0 = static_cast<uint32_t>(key), k1 = static_cast<uint32_t>(key >> 32);
-  ks.hk = k0 ^ (k1 * 0x85EBCA6Bu);
+  ks.hk0 = k0;
+  ks.hk1 = k1;
 #pragma unroll
   for (int i = 0; i < kPhiloxRounds; ++i) {
     ks.k0[i] = k0;
@@ -117,6 +129,25 @@ XMC_DEV U4 philox4x32_keys(U4 c, const PhiloxKeys& ks) {
            static_cast<uint32_t>(m0 >> 32) ^ c.w ^ ks.k1[i], static_cast<uint32_t>(m0)};
   }
   return c;
+}
+
+// Keyed hash generator of the SR_FAST words (the default sr_impl "hash").
+// Word i (a 40-bit word index: element / 4 for e4m3x4, element / 2 for
+// bf16x2) of the step keyed by key = splitmix64(seed, step, tensor_id)
+// (rng.py:42-46) = RXS-M-XS(((lo32(i) ^ ka) * 747796405 + k1)), the PCG output
+// permutation applied to a keyed affine image of the index, with
+// ka = k0 ^ (hi32(i) * 0x9E3779B9).  Both key halves enter (XOR before the
+// multiply, add after it), so two steps' word streams are unrelated
+// permutations of the index space instead of shifted windows of one
+// sequence, and indexes past 2^32 words get their own key.  Within a step the
+// map i -> word is a bijection on each 2^32 block (no repeats).
+XMC_DEV uint32_t sr_hash_word(uint32_t ilo, uint32_t ka, uint32_t k1) {
+  const uint32_t st = (ilo ^ ka) * 747796405u + k1;
+  const uint32_t w = ((st >> ((st >> 28u) + 4u)) ^ st) * 277803737u;
+  return (w >> 22u) ^ w;
+}
+XMC_DEV uint32_t sr_hash_ka(const PhiloxKeys& ks, uint64_t word_index) {
+  return ks.hk0 ^ (static_cast<uint32_t>(word_index >> 32) * 0x9E3779B9u);
 }
 
 XMC_DEV U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {

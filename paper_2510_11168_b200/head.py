@@ -9,6 +9,14 @@ Same names, argument meaning and errors as the reference module
 * ``head_update`` (head.py:254-298) runs the whole step in two tcgen05
   kernels per chunk through the C ABI (include/xmc_head.h):
   logits+G (head.py:164-196) then grad_X + dW + SGD/rounding (head.py:199-251).
+* ``ChunkedHead.precision`` selects the precision of G in the two backward
+  GEMMs.  ``"reference"`` (default): G is the reference's fp32 logit gradient,
+  split exactly into three bf16 planes, so dW and grad_X multiply by the same
+  fp32 G as the reference (head.py:193-208, 236) and only the fp32
+  accumulation order differs.  ``"operand"``: the production fast path, G
+  rounded once to the FP8/BF16 tensor-core operand format (e4m3 heads:
+  ``g_format`` "e5m2" (default, e5m2(2^8 g): the reference's whole
+  [2^-24, 1] sigmoid range) or "e4m3" (e4m3(2^8 g)); bf16 heads: bf16(g)).
 * The unfused sub-ops keep the reference signatures for parity isolation.
 
 There is no CPU fallback: every call goes to libxmc_b200.so.
@@ -79,10 +87,12 @@ class _Handle:
         lib = _lib.load()
         self.key = (max_batch, max_positives, head.num_chunks, head.weights.values.device)
         comp_bytes = 0 if head.comp is None else head.comp.element_size()
+        self.precision, self.g_format = head.precision, head.g_format
         self.desc = _lib.HeadDesc(head.num_labels_global, head.label_offset, head.num_labels,
                                   head.dim, head.fmt.code, head.num_chunks, max_batch,
-                                  max_positives, 0, comp_bytes, 1 if head.dropout_p > 0.0 else 0, 0,
-                                  head.kahan_labels or 0)
+                                  max_positives, 0, comp_bytes, 1 if head.dropout_p > 0.0 else 0,
+                                  _PRECISIONS[head.precision], head.kahan_labels or 0,
+                                  _G_FORMATS[head.g_format], 0)
         size = ctypes.c_size_t()
         _lib.check(lib.xmc_head_workspace_size(ctypes.byref(self.desc), ctypes.byref(size)))
         self.workspace = torch.empty(size.value + 1024, dtype=torch.uint8,
@@ -100,21 +110,32 @@ class _Handle:
             pass
 
 
+_PRECISIONS = {"reference": _lib.PRECISION_REFERENCE, "operand": _lib.PRECISION_OPERAND}
+_G_FORMATS = {"e5m2": _lib.FMT_E5M2, "e4m3": _lib.FMT_E4M3}
+
+
 class ChunkedHead:
     """Classifier weights partitioned into contiguous label chunks (head.py:69-112).
 
     ``num_labels_global`` / ``label_offset`` describe this rank's shard when
     the head is label-sharded across GPUs (see parallel.ShardedHead); for a
-    single GPU they are (L, 0)."""
+    single GPU they are (L, 0).  ``precision`` / ``g_format``: the backward's G
+    precision (module docstring)."""
 
     def __init__(self, weights: QuantizedMatrix, num_chunks: int = 1, dropout_p: float = 0.0,
                  block_m: int = 64, block_n: int = 64, tensor_id: int = HEAD_WEIGHTS_TAG,
                  num_labels_global: int | None = None, label_offset: int = 0,
-                 kahan: str | None = None, kahan_labels: int | None = None, adamw: bool = False):
+                 kahan: str | None = None, kahan_labels: int | None = None, adamw: bool = False,
+                 precision: str = "reference", g_format: str = "e5m2"):
         if num_chunks < 1:
             raise ValueError("num_chunks must be >= 1")
         if not (0.0 <= dropout_p < 1.0):
             raise ValueError("dropout_p must lie in [0, 1)")
+        if precision not in _PRECISIONS:
+            raise ValueError(f"precision must be 'reference' or 'operand', got {precision!r}")
+        if g_format not in _G_FORMATS:
+            raise ValueError(f"g_format must be 'e5m2' or 'e4m3', got {g_format!r}")
+        self.precision, self.g_format = precision, g_format
         if weights.values.dtype != weights.fmt.torch_dtype or weights.fmt.code not in (
                 _lib.FMT_BF16, _lib.FMT_E4M3):
             raise NotImplementedError("GPU head stores bf16 or e4m3 weights natively")
@@ -156,12 +177,12 @@ class ChunkedHead:
     @classmethod
     def create(cls, num_labels: int, dim: int, fmt: FloatFormat, seed: int = 0,
                num_chunks: int = 1, dropout_p: float = 0.0, init_scale: float = 0.02,
-               device="cuda") -> "ChunkedHead":
+               device="cuda", **kw) -> "ChunkedHead":
         """Same W0 as the reference (head.py:86-92): numpy N(0, scale^2) then
         RTN onto the grid -- the RTN cast runs on the GPU, bit-exact."""
         w = np.random.default_rng(seed).normal(scale=init_scale, size=(num_labels, dim)).astype(np.float32)
         return cls(QuantizedMatrix(cast_native(torch.from_numpy(w).to(device), fmt), fmt),
-                   num_chunks, dropout_p)
+                   num_chunks, dropout_p, **kw)
 
     @classmethod
     def from_float(cls, values, fmt: FloatFormat, **kw) -> "ChunkedHead":
@@ -217,7 +238,8 @@ class ChunkedHead:
         comp_bytes = 0 if self.comp is None else self.comp.element_size()
         if (h is None or batch > h.max_batch or nnz > h.max_positives
                 or h.key[2] != self.num_chunks or h.key[3] != dev or h.desc.comp_bytes != comp_bytes
-                or h.desc.dropout != (1 if self.dropout_p > 0.0 else 0)):
+                or h.desc.dropout != (1 if self.dropout_p > 0.0 else 0)
+                or h.precision != self.precision or h.g_format != self.g_format):
             mb = max(batch, h.max_batch if h else 0)
             mp = max(nnz, h.max_positives if h else 0, 1024)
             self._handle = _Handle(self, mb, mp)
@@ -416,8 +438,8 @@ def logit_gradient(logits: torch.Tensor, sample_idx, label_idx, chunk) -> torch.
 
 def input_gradient_accumulate(acc: torch.Tensor, G: torch.Tensor, head: ChunkedHead, chunk,
                               rng, step) -> torch.Tensor:
-    """acc += G^T @ W_chunk (head.py:199-209).  G is consumed in the backward
-    operand format (e4m3 x 2^8 for an e4m3 head, bf16 for a bf16 head)."""
+    """acc += G^T @ W_chunk (head.py:199-209).  G is consumed at the head's
+    backward precision (exact three-plane bf16 split by default)."""
     start, stop = chunk
     if tuple(acc.shape) != (G.shape[1], head.dim):
         raise ValueError("accumulator shape mismatch")
@@ -477,7 +499,7 @@ def save_head(head: ChunkedHead, fp) -> None:
             fp.close()
 
 
-def load_head(fp, num_chunks: int = 1, dropout_p: float = 0.0, device="cuda") -> ChunkedHead:
+def load_head(fp, num_chunks: int = 1, dropout_p: float = 0.0, device="cuda", **kw) -> ChunkedHead:
     """head.py:375-392."""
     close = isinstance(fp, (str, bytes))
     if close:
@@ -494,7 +516,7 @@ def load_head(fp, num_chunks: int = 1, dropout_p: float = 0.0, device="cuda") ->
         if raw.size != L * m:
             raise ValueError("truncated head checkpoint")
         t = torch.from_numpy(raw.copy()).reshape(L, m).to(device).view(fmt.torch_dtype)
-        return ChunkedHead(QuantizedMatrix(t, fmt), num_chunks, dropout_p)
+        return ChunkedHead(QuantizedMatrix(t, fmt), num_chunks, dropout_p, **kw)
     finally:
         if close:
             fp.close()
