@@ -1,11 +1,15 @@
 """Benchmark of the ELMO head step on B200 (BASELINE.json metric).
 
 Workload (BASELINE.json configs[3]): Amazon-3M shape,
-L = 2,812,281 labels, d = 768, batch 256, FP8 e4m3 weights, SR on (Philox +
-cvt.rs), lr 0.05, wd 1e-4, dropout 0, synthetic data: W0 ~ N(0, 0.02^2) RTN to
-e4m3, X ~ N(0, 1), positives per sample max(1, Poisson(36.17)) distinct labels
-drawn Zipf(1.0).  Labels are sharded contiguously across ranks (strong
+L = 2,812,281 labels, d = 768, batch 256, FP8 e4m3 weights, SR on (keyed hash
+words + cvt.rs), lr 0.05, wd 1e-4, dropout 0, synthetic data: W0 ~ N(0, 0.02^2)
+RTN to e4m3, X ~ N(0, 1), positives per sample max(1, Poisson(36.17)) distinct
+labels drawn Zipf(1.0).  Labels are sharded contiguously across ranks (strong
 scaling: the 3M-label problem is fixed, each rank owns L/N rows).
+
+The headline runs the production operand precision (all three GEMMs on FP8
+tensor cores, G as e5m2(2^8 g)); `reference_precision` in the same line is the
+same step with the reference's fp32 G (ChunkedHead(precision="reference")).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -52,6 +56,10 @@ def parse():
     ap.add_argument("--max-chunk-rows", type=int, default=1_406_141)
     ap.add_argument("--rounding", default="stochastic")
     ap.add_argument("--sr-impl", default="hash", choices=["hash", "philox", "splitmix64"])
+    ap.add_argument("--precision", default="operand", choices=["operand", "reference"])
+    ap.add_argument("--g-format", default="e5m2", choices=["e5m2", "e4m3"])
+    ap.add_argument("--ref-steps", type=int, default=5,
+                    help="timed steps of the reference-precision mode reported beside the headline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--cpu-labels", type=int, default=8192)
@@ -240,7 +248,9 @@ def main():
     config = {"workload": f"Amazon-3M head step: L={a.labels}, d={a.dim}, B={a.batch}, {a.fmt} weights, "
                           f"k={a.chunks} chunks, SR={a.rounding}/{a.sr_impl}, lr=0.05, wd=1e-4",
               "labels": a.labels, "dim": a.dim, "global_batch": a.batch, "chunks": a.chunks,
-              "parallelism": f"label-shard x{world}", "l2": "inputs larger than L2 (W >> 126 MB)"}
+              "precision": a.precision, "g_format": a.g_format if a.fmt == "e4m3" else "bf16",
+              "parallelism": f"label-shard x{world}", "l2": "inputs larger than L2 (W >> 126 MB)",
+              "cpu_sample_labels": min(a.cpu_labels, a.labels)}
 
     if a.impl == "reference":
         if rank != 0:
@@ -283,7 +293,7 @@ def main():
         r1 = min(r0 + blk, hi - lo)
         W[r0:r1] = xmc.cast_native(torch.randn((r1 - r0, a.dim), generator=g, device=dev) * 0.02, fmt)
     head = xmc.ChunkedHead(xmc.QuantizedMatrix(W, fmt), num_chunks=a.chunks, num_labels_global=a.labels,
-                           label_offset=lo)
+                           label_offset=lo, precision=a.precision, g_format=a.g_format)
     rs = np.random.default_rng(0)
     Xh = rs.normal(size=(a.batch, a.dim)).astype(np.float32)
     si, li = synthetic_positives(a.labels, a.batch, PAPER_MEAN_LABELS.get(a.labels, 5.0), seed=1)
@@ -310,7 +320,7 @@ def main():
             except Exception as e:  # noqa: BLE001 - report and keep NCCL
                 print(f"peer all-reduce unavailable ({e}); using NCCL", file=sys.stderr)
                 peers = None
-    config["grad_x_allreduce"] = allreduce
+    gx_allreduce = [allreduce]
 
     def step_fn(s, batch, out):
         r = xmc.head_update(head, batch, cfg, rng, s, check=False, grad_out=out)
@@ -343,7 +353,7 @@ def main():
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         if int(flag.item()) == 0:
             head.peers = None
-            config["grad_x_allreduce"] = "nccl all_reduce (peer path failed in warm-up)"
+            gx_allreduce[0] = "nccl all_reduce (peer path failed in warm-up)"
             for s in range(a.warmup):
                 step_fn(s, batch_dev, gx)
     torch.cuda.synchronize()
@@ -411,6 +421,32 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te.item()) / a.e2e_steps
 
+    # ---------------- the reference-precision mode on the same workload
+    ref_prec = None
+    if a.ref_steps > 0 and a.precision == "operand":
+        head.precision = "reference"
+        for s in range(2):
+            step_fn(20_000 + s, batch_dev, gx)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        r0_, r1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0_.record(stream)
+        for s in range(a.ref_steps):
+            step_fn(20_100 + s, batch_dev, gx)
+        r1_.record(stream)
+        torch.cuda.synchronize()
+        tr_ = torch.tensor([r0_.elapsed_time(r1_)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tr_, op=dist.ReduceOp.MAX)
+        ms_ref = float(tr_.item()) / a.ref_steps
+        _lib.check(_lib.load().xmc_head_check(head.handle(a.batch, len(si)).h, _lib.stream_ptr()))
+        ref_prec = {"value": a.batch / (ms_ref * 1e-3), "unit": "samples/s", "ms_per_step": ms_ref,
+                    "steps": a.ref_steps,
+                    "what": "same step with ChunkedHead(precision='reference'): the reference's fp32 G as three "
+                            "exact bf16 planes, kind::f16 backward GEMMs (device-resident inputs)"}
+        head.precision = a.precision
+
     # ---------------- roofline of the dominant kernel
     peaks = load_peaks()
     L_r, B, D = hi - lo, a.batch, a.dim
@@ -422,12 +458,18 @@ def main():
     n_launch = max(per_step[dom][1], 1)
     ms_launch = per_step[dom][0] / n_launch
     rows_launch = L_r / n_launch
-    if dom == "bwd":   # grad_X + dW GEMMs, W read+write, G read once per d-tile group
+    # algorithmic work per launch: flops of its GEMMs and the
+    # bytes of W it must move (bwd: read + write, fwd: read); the G buffer
+    # round trip is a design cost, reported separately as design_bytes
+    gb = 1 if eb == 1 else 2
+    if dom == "bwd":   # grad_X + dW GEMMs, W read+write
         flops = 4.0 * B * rows_launch * D
-        bytes_ = 2.0 * rows_launch * D * eb + rows_launch * Bp * eb
-    else:              # logits GEMM, W read, G write
+        bytes_ = 2.0 * rows_launch * D * eb
+        design = bytes_ + rows_launch * Bp * gb
+    else:              # logits GEMM, W read
         flops = 2.0 * B * rows_launch * D
-        bytes_ = rows_launch * D * eb + rows_launch * Bp * eb
+        bytes_ = rows_launch * D * eb
+        design = bytes_ + rows_launch * Bp * gb
     # Burst vs sustained peak by the clocks seen in the timed region: a short
     # region runs at boost clocks (burst peak); a long one hits the ~1 kW power
     # cap, the SM clock drops to ~1.3-1.4 GHz and the sustained peak applies.
@@ -469,6 +511,9 @@ def main():
                  else "xmc_fwd_kernel (logits + sigmoid - Y)", "traffic": traffic,
                  "ms_per_launch": ms_launch, "launches_per_step": n_launch,
                  "algorithmic_flops_per_launch": flops, "algorithmic_bytes_per_launch": bytes_,
+                 "design_bytes_per_launch": design,
+                 "tensor_frac_of_nominal": (flops / (ms_launch * 1e-3) / 1e12) / (4500.0 if eb == 1 else 2250.0),
+                 "hbm_frac": (bytes_ / (ms_launch * 1e-3) / 1e9) / peaks["hbm_gbs"],
                  "peak_source": tc_src if bound == "tensor" else f"hbm {peaks['source']}",
                  "peak_regime": regime,
                  "step_kernel_ms": {"fwd": per_step["fwd"][0], "bwd": per_step["bwd"][0]}})
@@ -482,6 +527,8 @@ def main():
                    "h2d_bytes_per_step": int(Xh.nbytes + 8 * len(si)),
                    "d2h_bytes_per_step": int(B * D * 4), "ms_per_step": e2e_ms},
            "roofline": roof,
+           "grad_x_allreduce": gx_allreduce[0],
+           "reference_precision": ref_prec,
            "step_tflops": step_flops / (ms_step * 1e-3) / 1e12,
            "step_frac_of_tc_peak": step_flops / (ms_step * 1e-3) / 1e12 / (tc_peak * world),
            "peak_hbm_gib_per_gpu": peak_mem / 2**30,

@@ -128,7 +128,7 @@ XMC_DEV float ref_sigmoid_clip(float z) {
 // The kernel body: work units unit0, unit0 + ustride, ... (tiles, or tile
 // pairs for PAIR).
 template <int EB, int BN, bool PAIR, bool TOPK, bool XRES, int GOUT>
-XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const FwdParams& p, const int unit0,
+XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const FwdParams p, const int unit0,
                       const int ustride) {
   using C = FwdCfg<EB, BN, PAIR, XRES>;
   static_assert(!PAIR || BN <= 256, "paired tiles use one N <= 256 accumulator");
@@ -190,9 +190,12 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  bool aborted;
-  if constexpr (PAIR) aborted = ld_shared_cluster_s32(mapa_shared(status_s, 0)) != 0;
-  else aborted = *status_s != 0;
+  // (shuffled from lane 0: provably warp-uniform, which keeps the role code
+  // below on the uniform datapath)
+  int32_t st_word;
+  if constexpr (PAIR) st_word = ld_shared_cluster_s32(mapa_shared(status_s, 0));
+  else st_word = *status_s;
+  const bool aborted = __shfl_sync(0xffffffffu, st_word, 0) != 0;
 
   if (aborted) {
   } else if (warp == 0) {
@@ -613,7 +616,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
 template <int EB, int BN, bool PAIR, bool TOPK = false, bool XRES = false, int GOUT = G_OPERAND>
 __global__ void __launch_bounds__(FwdCfg<EB, BN, PAIR, XRES>::kThreads, 1)
     xmc_fwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
-                   const __grid_constant__ FwdParams p) {
+                   const FwdParams p) {
   if constexpr (PAIR) {
     fwd_body<EB, BN, PAIR, TOPK, XRES, GOUT>(tm_w, tm_x, p, static_cast<int>(cluster_id_x()),
                                              static_cast<int>(num_clusters_x()));

@@ -38,4 +38,4 @@ def test_bench_two_ranks_one_device(peer):
     for key in ("e2e", "roofline", "clocks", "gpu_launches"):
         assert key in d
     want = "peer memory" if peer == "1" else "gloo all_reduce"
-    assert d["config"]["grad_x_allreduce"].startswith(want), d["config"]["grad_x_allreduce"]
+    assert d["grad_x_allreduce"].startswith(want), d["grad_x_allreduce"]

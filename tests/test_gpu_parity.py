@@ -54,7 +54,7 @@ def assert_update_within_bound(got, ref, fmt, lr, Xq, G_gpu, G_ref=None, wd=0.0,
     if G_ref is not None:
         err += np.abs(np.asarray(G_gpu, np.float64) - np.asarray(G_ref, np.float64)) @ Xa
     if g_flips:
-        gfmt, scale = (O.E4M3, 256.0) if fmt.name == "e4m3" else (fmt, 1.0)
+        gfmt, scale = (O.E5M2, 256.0) if fmt.name == "e4m3" else (fmt, 1.0)
         uG = O._ulp_of(gfmt, Ga * scale) / scale                       # (L, B)
         mx = np.zeros_like(err)
         for r0 in range(0, uG.shape[0], 64):
@@ -177,10 +177,14 @@ def _golden_case(ci):
                 fmt=str(GOLD[p + "fmt"]), rounding=str(GOLD[p + "rounding"]), p=p)
 
 
-def _make(xmc, W, fmt_name, k, device="cuda", dropout_p=0.0):
+def _make(xmc, W, fmt_name, k, device="cuda", dropout_p=0.0, precision="operand"):
+    """The head under test.  This file pins the OPERAND-precision mode (G
+    rounded to the tensor-core operand, e5m2(2^8 g) for e4m3 heads) against
+    the oracle given the same operand G; tests/test_gpu_reference.py pins the
+    default reference-precision mode against the unmodified reference."""
     fmt = xmc.parse_format(fmt_name)
     return xmc.ChunkedHead.from_float(torch.from_numpy(np.ascontiguousarray(W)), fmt, num_chunks=k,
-                                      dropout_p=dropout_p)
+                                      dropout_p=dropout_p, precision=precision)
 
 
 def _w_eff(W, p, seed, step):
@@ -272,7 +276,7 @@ def test_fused_update_matches_oracle_on_operand_G(xmc, fmt_name, B, rmode, impl)
 
 
 @pytest.mark.parametrize("ci", range(NCASES))
-def test_head_update_matches_reference_golden(xmc, ci):
+def test_head_update_operand_matches_golden(xmc, ci):
     c = _golden_case(ci)
     p, drop = c["p"], c["drop"]
     fmt = xmc.parse_format(c["fmt"])
@@ -571,7 +575,7 @@ def test_head_kahan_matches_oracle(xmc, fmt_name, kahan, rmode, n_comp):
     L, d, B = 700, 256, 128
     fmt, W, X, si, li = _rand_problem(L, d, B, fmt_name, 61)
     head = xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.parse_format(fmt_name), num_chunks=2, kahan=kahan,
-                                      kahan_labels=n_comp)
+                                      kahan_labels=n_comp, precision="operand")
     cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=xmc.parse_format(fmt_name), rounding=rmode,
                           sr_impl="splitmix64")
     oh = O.OracleHead(W.copy(), fmt, 2)
@@ -611,7 +615,7 @@ def test_head_adamw_matches_oracle(xmc, fmt_name, B, chunks):
     L, d = 700, 256
     fmt, W, X, si, li = _rand_problem(L, d, B, fmt_name, 71)
     head = xmc.ChunkedHead.from_float(torch.from_numpy(W), xmc.parse_format(fmt_name), num_chunks=chunks,
-                                      adamw=True)
+                                      adamw=True, precision="operand")
     cfg = xmc.KahanAdamWConfig(lr=0.01, beta1=0.9, beta2=0.99, eps=1e-6, weight_decay=0.05,
                                fmt=xmc.parse_format(fmt_name))
     cfg_o = O.KahanAdamWConfig(lr=0.01, beta1=0.9, beta2=0.99, eps=1e-6, weight_decay=0.05, fmt=fmt)
