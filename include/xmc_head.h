@@ -58,7 +58,7 @@ typedef struct {
   int64_t num_labels_global; /* L                                        */
   int64_t label_offset;      /* first global label owned by this rank     */
   int64_t num_labels_local;  /* labels owned by this rank                 */
-  int32_t dim;               /* d (multiple of 128 for e4m3, 64 for bf16) */
+  int32_t dim;               /* d, a multiple of 32 (partial last 128-column tile is zero-filled) */
   int32_t fmt;               /* xmc_fmt of W: XMC_FMT_E4M3 or XMC_FMT_BF16 */
   int32_t num_chunks;        /* k: chunks = partition(num_labels_local, k) (head.py:51-57) */
   int32_t max_batch;         /* B capacity of the workspace               */

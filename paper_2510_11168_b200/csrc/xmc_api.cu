@@ -293,8 +293,10 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   if (d->fmt != XMC_FMT_E4M3 && d->fmt != XMC_FMT_BF16)
     return fail(XMC_ERR_UNSUPPORTED, "head format must be e4m3 or bf16 (got %d)", d->fmt);
   const int eb = elem_bytes(d->fmt);
-  if (d->dim <= 0 || d->dim % 128 != 0)
-    return fail(XMC_ERR_SHAPE, "dim must be a positive multiple of 128 (got %d)", d->dim);
+  // d-tiles of 128 columns; a partial last tile is zero-filled by TMA on load
+  // and clipped on store (the 32-column epilogue chunks need d % 32 == 0)
+  if (d->dim <= 0 || d->dim % 32 != 0)
+    return fail(XMC_ERR_SHAPE, "dim must be a positive multiple of 32 (got %d)", d->dim);
   if (d->num_chunks < 1) return fail(XMC_ERR_ARG, "num_chunks must be >= 1");
   if (d->comp_bytes != 0 && d->comp_bytes != 2 && d->comp_bytes != 4)
     return fail(XMC_ERR_ARG, "comp_bytes must be 0 (none), 2 (bf16) or 4 (fp32)");
@@ -320,7 +322,7 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
     tiles += cdiv(c.second - c.first, 128);
     maxrows = std::max(maxrows, c.second - c.first);
   }
-  const int dtiles = d->dim / 128;
+  const int dtiles = (d->dim + 127) / 128;
   int R = std::max(1, num_sms / dtiles);
   const int64_t D = d->dim;
   L->xq = 0;
@@ -386,7 +388,7 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->gout = h->ref ? G_REF : ((eb == 1 && desc->g_format != XMC_FMT_E4M3) ? G_E5M2 : G_OPERAND);
   h->max_bp = bp;
   h->num_sms = sms;
-  h->dtiles = desc->dim / 128;
+  h->dtiles = (desc->dim + 127) / 128;
   h->R = R;
   h->R_step = R;
   h->chunks = partition(desc->num_labels_local, desc->num_chunks);
@@ -467,7 +469,7 @@ extern "C" xmc_status xmc_peer_create(int32_t rank, int32_t world, int32_t dim, 
   if (!out || !handle) return fail(XMC_ERR_ARG, "null argument");
   if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
     return fail(XMC_ERR_ARG, "rank %d / world %d outside [0, %d)", rank, world, kMaxPeers);
-  if (dim <= 0 || dim % 128 != 0) return fail(XMC_ERR_SHAPE, "dim must be a positive multiple of 128");
+  if (dim <= 0 || dim % 32 != 0) return fail(XMC_ERR_SHAPE, "dim must be a positive multiple of 32");
   if (max_batch < 1 || max_batch > 512) return fail(XMC_ERR_ARG, "max_batch outside [1, 512]");
   auto* p = new xmc_peer();
   p->rank = rank;
@@ -624,7 +626,7 @@ static xmc_status launch_fwd_t(xmc_head* h, const CUtensorMap& tw, const CUtenso
   prof_begin(0, st, &pr);
   if constexpr (PAIR && EB == 1) {
     using CX = FwdCfg<EB, BN, true, true>;
-    if (p.d / CX::kBoxK <= CX::kXResChunks) {   // resident Xq (e4m3 pairs, d <= 768)
+    if ((p.d + CX::kBoxK - 1) / CX::kBoxK <= CX::kXResChunks) {   // resident Xq (e4m3 pairs, d <= 768)
       auto k = xmc_fwd_kernel<EB, BN, true, false, true, GOUT>;
       smem_attr_once<xmc_fwd_kernel<EB, BN, true, false, true, GOUT>>(CX::kSmemBytes);
       CUDA_TRY(launch_ex(k, grid, CX::kThreads, CX::kSmemBytes, st, h, 2, tw, tx, p));
@@ -1144,7 +1146,7 @@ static xmc_status launch_topk_t(xmc_head* h, const CUtensorMap& tw, const CUtens
   using C = FwdCfg<EB, BN, false>;
   const int grid = topk_grid(h, p.num_tiles, EB, BN, p.d);
   if constexpr (EB == 1 && BN == 256) {
-    if (p.d / 128 <= FwdCfg<1, 256, true, true>::kXResChunks) {
+    if ((p.d + 127) / 128 <= FwdCfg<1, 256, true, true>::kXResChunks) {
       using CP = FwdCfg<1, 256, true, true>;
       CUtensorMap txp;   // each CTA of a pair stages its 128 samples
       XMC_TRY(make_map(&txp, h->xq_topk, 1, p.d, 256, p.d, 128));

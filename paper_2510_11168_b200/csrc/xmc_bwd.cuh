@@ -45,7 +45,7 @@ struct BwdParams {
   int32_t rows;          // labels in this chunk
   int32_t d;             // feature dim
   int32_t num_tiles;     // ceil(rows / 128)
-  int32_t dtiles;        // d / 128
+  int32_t dtiles;        // ceil(d / 128); the last d-tile may be partial (d % 32 == 0)
   int32_t kc_count;      // sample k-chunks of G (Bp * EB / 128, x3 for the reference-precision planes)
   int32_t xt_kc;         // k-chunks of one Xq^T plane: G k-chunk kc multiplies Xq^T k-chunk kc % xt_kc
   int32_t do_update;     // dW + SGD + rounding, W written in place
@@ -697,7 +697,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           prev_ws = -1;
         }
         uint4 craw[CE > 0 ? CE * 2 : 1];
-        const bool krow = CE > 0 && grow < p.comp_rows;   // this row carries a compensation
+        // columns past d (partial last d-tile) are computed on TMA's zero fill
+        // and clipped by the TMA store; per-thread side buffers skip them
+        const bool col_ok = j * 128 + c0 < p.d;
+        const bool krow = CE > 0 && grow < p.comp_rows && col_ok;   // this row carries a compensation
         if constexpr (CE > 0 && !ADAMW) {   // Kahan compensation of this thread's 32 elements (HBM)
           const uint4* csrc = reinterpret_cast<const uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE);
 #pragma unroll
@@ -772,7 +775,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           continue;
         }
         uint32_t km = 0u;   // dropout keep bits of this thread's 32 columns
-        if (p.keep != nullptr && grow < p.rows) km = __ldg(p.keep + grow * (p.d >> 5) + ((j * 128 + c0) >> 5));
+        if (p.keep != nullptr && grow < p.rows && col_ok)
+          km = __ldg(p.keep + grow * (p.d >> 5) + ((j * 128 + c0) >> 5));
         uint32_t rw[8 * GE];
         if (rounding == ROUND_SR_FAST) sr_words<GE>(pk, flat0, rw, p.sr_bits != 0);
         float w[CE > 0 ? 1 : 32];
@@ -793,7 +797,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         uint4 out[C::kChunks16];
         if constexpr (ADAMW) {
-          w_update_pack_adamw<EB, GE>(p, acc, raw, grow * p.d + j * 128 + c0, grow < p.rows, out, pol_w_out);
+          w_update_pack_adamw<EB, GE>(p, acc, raw, grow * p.d + j * 128 + c0, grow < p.rows && col_ok, out, pol_w_out);
         } else if constexpr (CE > 0) {
           uint4* cdst = krow ? reinterpret_cast<uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE) : nullptr;
           w_update_pack_kahan<EB, CE, GE>(p, rounding, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
@@ -845,7 +849,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
       // this CTA's slot of the [R][d][gx_ld] partial buffer; chunks of one step
       // accumulate into it (stream-ordered, one owner per slot: deterministic)
-      const int nchunks = p.gx_kc_count * C::kBoxK / 32;
+      const int nchunks = j * 128 + row < p.d ? p.gx_kc_count * C::kBoxK / 32 : 0;   // TMEM lane = d index
       float* dst = p.gx_ws + (static_cast<int64_t>(r0) * p.d + j * 128 + row) * p.gx_ld + p.gx_kc0 * C::kBoxK;
 #pragma unroll 1
       for (int cch = quarter; cch < nchunks; cch += 4) {

@@ -149,7 +149,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
   int32_t* status_s = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id_sync();
-  const int kc_count = p.d / C::kBoxK;
+  const int kc_count = (p.d + C::kBoxK - 1) / C::kBoxK;   // a partial last K-chunk is zero-filled by TMA
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   // work units: single tiles, or tile pairs (2u, 2u+1) for a CTA pair

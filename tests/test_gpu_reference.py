@@ -320,3 +320,43 @@ def test_fullsize_c4_grad_x_and_rows_vs_unmodified_reference(xmc):
     got = head.weights.values[torch.from_numpy(rows).cuda()].float().cpu().numpy()
     same, over1, ok = reference_weight_report(got, ref, O.E4M3, 0.05, G, Xq, sr=True)
     assert same >= 0.999 and ok, (same, over1)
+
+
+@pytest.mark.parametrize("fname,d,B,extra", [("e4m3", 32, 32, None), ("bf16", 32, 64, "kahan"), ("e4m3", 96, 256, "dropout"),
+                                             ("bf16", 160, 128, None), ("e4m3", 800, 128, "kahan")])
+def test_partial_d_tiles(xmc, fname, d, B, extra):
+    """d a multiple of 32 but not of 128 (the reference takes any d; the
+    kernels need d % 32 == 0): the last 128-column tile is zero-filled by TMA
+    on load and clipped on store, the per-thread side buffers (compensation,
+    keep bits, grad_X rows) skip the columns past d."""
+    L = 900
+    fmt_o, W, X, si, li = _rand_problem(L, d, B, fname, 501)
+    fmt = xmc.parse_format(fname)
+    p = 0.2 if extra == "dropout" else 0.0
+    head = xmc.ChunkedHead.from_float(torch.from_numpy(W), fmt, num_chunks=2, dropout_p=p,
+                                      kahan="bf16" if extra == "kahan" else None)
+    oh = O.OracleHead(W.copy(), fmt_o, 2, dropout_p=p)
+    cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt, rounding="stochastic", sr_impl="splitmix64")
+    cfg_o = O.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt_o, rounding="stochastic")
+    comp = np.zeros((L, d), np.float32) if extra == "kahan" else None
+    gx = xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(3), 1)
+    gx_o = O.head_update(oh, X, si, li, cfg_o, O.RoundingRng(3), 1, comp=comp,
+                         comp_fmt=O.BF16 if extra == "kahan" else None)
+    _gx_close(gx.cpu().numpy(), gx_o)
+    got = head.weights.values.float().cpu().numpy()
+    assert np.mean(got.view(np.uint32) == oh.values.view(np.uint32)) >= 0.999
+    if extra == "kahan":
+        assert np.isfinite(head.comp.float().cpu().numpy()).all()
+    # the operand mode on the same shape (oracle given the same operand G)
+    head = xmc.ChunkedHead.from_float(torch.from_numpy(W), fmt, num_chunks=2, dropout_p=p, precision="operand")
+    oh = O.OracleHead(W.copy(), fmt_o, 2, dropout_p=p)
+    gx = xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(3), 1)
+    gx_o = O.head_update(oh, X, si, li, cfg_o, O.RoundingRng(3), 1, g_quant=True)
+    _gx_close(gx.cpu().numpy(), gx_o)
+    assert np.mean(head.weights.values.float().cpu().numpy().view(np.uint32) == oh.values.view(np.uint32)) >= 0.99
+    # scores / fused top-k on the partial tile
+    sc = head.scores(torch.from_numpy(X)).cpu().numpy()
+    np.testing.assert_allclose(sc, oh.scores(X), rtol=1e-5, atol=1e-5)
+    _, labs = head.topk(torch.from_numpy(X), 3)
+    for s in range(B):
+        assert np.array_equal(labs[s].cpu().numpy(), O.top_k_indices(sc[s], 3))
