@@ -14,6 +14,6 @@ from .head import (DROPOUT_TAG, HEAD_WEIGHTS_TAG, N_CELLS, BatchInput, ChunkedHe
                    head_update, input_gradient_accumulate, load_head, logit_gradient, partition,
                    save_head)
 
-from . import metrics
+from . import metrics, trainer_hooks
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
