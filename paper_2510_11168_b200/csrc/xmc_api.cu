@@ -787,7 +787,8 @@ static xmc_status launch_bwd_v(xmc_head* h, const BwdLaunch& L, cudaStream_t st)
   if (ce == 2) return launch_bwd_k<EB, XR, KC, 2, false, false, GE>(h, L, st);
   if (ce == 4) return launch_bwd_k<EB, XR, KC, 4, false, false, GE>(h, L, st);
   if constexpr (EB == 1 && GE == 1)
-    if (p.rounding == ROUND_SR_FAST && p.keep == nullptr) return launch_bwd_k<1, XR, KC, 0, true, false, 1>(h, L, st);
+    if (p.do_update && p.rounding == ROUND_SR_FAST && p.keep == nullptr)
+      return launch_bwd_k<1, XR, KC, 0, true, false, 1>(h, L, st);
   return launch_bwd_k<EB, XR, KC, 0, false, false, GE>(h, L, st);
 }
 

@@ -37,6 +37,12 @@
 
 namespace xmc {
 
+// Epilogue warps: 16, i.e. 4 per TMEM sub-partition.  The general path gives
+// each warp 32 of the tile's 128 columns on every tile.  The FAST path runs
+// them as two ping-pong groups of 8 warps (2 per sub-partition, 64 columns
+// each) that take alternate tiles, so one tile's update may take two tiles'
+// worth of MMA time without stalling the tensor pipe (each group owns one of
+// the two dW accumulator buffers).
 constexpr int kBwdEpiWarps = 16;
 constexpr int kBwdThreads = 64 + kBwdEpiWarps * 32;
 
@@ -463,7 +469,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&w_full[s], 1);
       // MMA commit + (kOutBuf) every epilogue warp once it has read W_old, or
       // (in place) one store thread per TMEM sub-partition once W_new is stored
-      mbar_init(&w_empty[s], C::kOutBuf ? 1 + kBwdEpiWarps : 5);
+      mbar_init(&w_empty[s], FAST ? 1 + kBwdEpiWarps / 2 : (C::kOutBuf ? 1 + kBwdEpiWarps : 5));
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -471,7 +477,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&t_full[s], 1);
-      mbar_init(&t_empty[s], kBwdEpiWarps);
+      mbar_init(&t_empty[s], FAST ? kBwdEpiWarps / 2 : kBwdEpiWarps);
     }
     mbar_init(xt_full, 1);
     mbar_init(gx_full, 1);
@@ -517,7 +523,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const bool whole = nk > 0 && nk <= KS && KS % nk == 0;
     for (int it = 0; it < ntl; ++it) {
       const int tile = tile_at(it);
-      mbar_wait(&w_empty[ws], wph ^ 1);
+      mbar_wait_sleep(&w_empty[ws], wph ^ 1);
       if (whole) {
         for (int i = 0; i < nk; ++i) mbar_wait(&k_empty[ks + i], kph ^ 1);
         if (lane == 0) {
@@ -578,9 +584,58 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t idesc_dw = umma_idesc(gf, xf, false, false, 128, 128);                         // A = G, B = Xq
     const uint32_t idesc_gx = umma_idesc(xf, gf, true, true, 128, p.gx_kc_count * C::kBoxK);      // A = W^T, B = G
     if constexpr (XT_RES) mbar_wait(xt_full, 0);
+    if constexpr (FAST) {
+      // Production path, lean instruction stream (the MMA warp shares its
+      // scheduler with 4 epilogue warps; with ~275 instructions per tile it
+      // was itself the pipeline's critical path).  Descriptors are affine in
+      // the smem address: built once, advanced by (byte offset >> 4).
+      // Every tile's KCMAX G k-chunks are consecutive ring slots (KS % KCMAX == 0).
+      static_assert(KS % KCMAX == 0, "whole tiles in the G ring");
+      const uint64_t dG = umma_desc_sw128(smem_u32(k_s), 16, 1024);            // dW A: G, K-major
+      const uint64_t dX = umma_desc_sw128(smem_u32(xt_s), 16, 1024);           // dW B: Xq^T, K-major
+      const uint64_t dWt = umma_desc_sw128(smem_u32(w_s), C::kBox, 1024);      // grad_X A: W^T, MN-major
+      const uint64_t dGt = umma_desc_sw128(smem_u32(k_s), C::kKSlot, 1024);    // grad_X B: G, MN-major
+      int ws = 0, ks = 0, ds = 0;
+      uint32_t wph = 0, kph = 0, dph = 0;
+      for (int it = 0; it < ntl; ++it) {
+        mbar_wait(&w_full[ws], wph);
+        mbar_wait(&t_empty[ds], dph ^ 1);
+        tc_fence_after();
+        const uint32_t d_dw = tmem_base + ds * 128;
+#pragma unroll
+        for (int kc = 0; kc < KCMAX; ++kc) {
+          mbar_wait(&k_full[ks + kc], kph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint64_t ga = dG + ((static_cast<uint32_t>(ks + kc) * C::kKSlot) >> 4);
+            const uint64_t xb = dX + ((kc * C::kBox) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mma_f8(d_dw, ga + 2 * k, xb + 2 * k, idesc_dw, (kc | k) != 0);
+            if (kc == KCMAX - 1) mma_commit(&t_full[ds]);   // dW complete -> update epilogue
+          }
+          __syncwarp();
+        }
+        if (elect_one()) {
+          if (do_gx) {
+            const uint64_t wa = dWt + ((static_cast<uint32_t>(ws) * C::kWBytes) >> 4);
+            const uint64_t gb = dGt + ((static_cast<uint32_t>(ks) * C::kKSlot) >> 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) mma_f8(tmem_gx, wa + 256 * k, gb + 256 * k, idesc_gx, (it | k) != 0);
+          }
+#pragma unroll
+          for (int kc = 0; kc < KCMAX; ++kc) mma_commit(&k_empty[ks + kc]);
+          mma_commit(&w_empty[ws]);
+        }
+        __syncwarp();
+        ks += KCMAX;
+        if (ks == KS) { ks = 0; kph ^= 1; }
+        if (++ws == WS) { ws = 0; wph ^= 1; }
+        if (++ds == 2) { ds = 0; dph ^= 1; }
+      }
+    }
     int ws = 0, ks = 0, ds = 0;
     uint32_t wph = 0, kph = 0, dph = 0;
-    for (int it = 0; it < ntl; ++it) {
+    for (int it = 0; it < (FAST ? 0 : ntl); ++it) {
       mbar_wait(&w_full[ws], wph);
       mbar_wait(&t_empty[ds], dph ^ 1);
       tc_fence_after();
@@ -659,7 +714,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     __syncwarp();
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 2;                 // 0..15
+    const int ew = warp - 2;                 // 0 .. kBwdEpiWarps-1
     const int q = warp & 3;                  // TMEM sub-partition
     const int quarter = ew >> 2;             // which 32 of the 128 d-columns
     const int row = q * 32 + lane_id();
@@ -673,15 +728,124 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     int ot_flip = 0;
     uint32_t wph = 0, dph = 0;
     const PhiloxKeys pk = philox_keys(p.rng_base);   // round keys, once per launch
-    for (int it = 0; it < ntl; ++it) {
+    if constexpr (FAST) {
+      // ---- production path (e4m3, SR_FAST, no compensation / dropout):
+      // ping-pong groups.  Group g = ew / 8 takes tiles it = g, g + 2, ... and
+      // owns dW buffer g; its warp (q, half) updates rows [32q, 32q+32) x
+      // columns [64 half, 64 half + 64).  Per tile: W_old of both 32-column
+      // groups and the first group's SR words / decoded, (1 - lr wd)-scaled
+      // W_old are ready BEFORE the dW wait (they overlap the MMAs).
+      const int g = ew >> 3;
+      const int half = (ew >> 2) & 1;
+      const int cw0 = half * 64;
+      const bool gstorer = half == 0 && lane_id() == 0;
+      const float c_wd = 1.0f - p.lr * p.wd;
+      const float a_lr = -p.lr * p.dw_scale;
+      uint8_t* ot = out_s + g * C::kWBytes;          // this group's W_new staging tile
+      const uint32_t ot_s = smem_u32(ot);
+      bool stored = false;
+      for (int it = g; it < ntl; it += 2) {
+        const int tile = tile_at(it);
+        const int wsi = it % WS;
+        const uint32_t wphi = static_cast<uint32_t>(it / WS) & 1u;
+        const uint32_t dphi = static_cast<uint32_t>(it >> 1) & 1u;
+        const uint32_t wt_s = smem_u32(w_s + wsi * C::kWBytes);
+        mbar_wait(&w_full[wsi], wphi);
+        const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
+        const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + cw0;
+        uint4 raw[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) raw[h] = lds128(wt_s + w_chunk_off<EB>(row, cw0 + (h >> 1) * 32, h & 1));
+        // W_old is in registers: the slot can be refilled once the MMAs are done too
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&w_empty[wsi]);
+        auto prep = [&](int cg, uint32_t (&rw)[8], float (&wc)[32]) {
+          sr_words<1>(pk, flat0 + cg * 32, rw, p.sr_bits != 0);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint4 r4 = raw[2 * cg + h];
+            const uint32_t wv[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 lo = dec_e4m3x2(static_cast<uint16_t>(wv[k] & 0xFFFF));
+              const float2 hi = dec_e4m3x2(static_cast<uint16_t>(wv[k] >> 16));
+              wc[h * 16 + 4 * k + 0] = lo.x;
+              wc[h * 16 + 4 * k + 1] = lo.y;
+              wc[h * 16 + 4 * k + 2] = hi.x;
+              wc[h * 16 + 4 * k + 3] = hi.y;
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {   // w (1 - lr wd)  (optimizers.py:71-73, wd folded)
+            const uint64_t r = fmul2(f2pack(wc[2 * k], wc[2 * k + 1]), f2pack(c_wd, c_wd));
+            f2unpack(r, wc[2 * k], wc[2 * k + 1]);
+          }
+        };
+        // updated = w (1 - lr wd) - lr dW, one SR rounding onto e4m3 (cvt.rs)
+        auto finish = [&](int cg, const uint32_t (&acc)[32], const uint32_t (&rw)[8], const float (&wc)[32]) {
+          uint32_t pk8[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            float u[4];
+#pragma unroll
+            for (int e = 0; e < 4; e += 2) {
+              const uint64_t r = ffma2(f2pack(__uint_as_float(acc[4 * k + e]), __uint_as_float(acc[4 * k + e + 1])),
+                                       f2pack(a_lr, a_lr), f2pack(wc[4 * k + e], wc[4 * k + e + 1]));
+              f2unpack(r, u[e], u[e + 1]);
+            }
+            pk8[k] = cvt_e4m3x4_rs(u[3], u[2], u[1], u[0], rw[k]);
+          }
+          const int cc = cw0 + cg * 32;
+          sts128(ot_s + w_chunk_off<EB>(row, cc, 0), make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]));
+          sts128(ot_s + w_chunk_off<EB>(row, cc, 1), make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]));
+        };
+        uint32_t rw[8];
+        float wc[32];
+        prep(0, rw, wc);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pin(rw[k]);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) pin(wc[k]);
+        // this group's previous W_new store must have read the staging tile
+        if (gstorer && stored) bulk_wait_read<0>();
+        named_bar_sync(1 + q + 4 * g, 64);
+        mbar_wait_sleep(&t_full[g], dphi);   // off the critical path: do not steal issue slots
+        tc_fence_after();
+        {
+          uint32_t acc[32];
+          tmem_ld32(tmem_base + lane_off + g * 128 + cw0, acc);
+          tmem_ld_wait();
+          finish(0, acc, rw, wc);
+        }
+        {
+          uint32_t acc[32];
+          tmem_ld32(tmem_base + lane_off + g * 128 + cw0 + 32, acc);
+          tmem_ld_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&t_empty[g]);
+          prep(1, rw, wc);
+          finish(1, acc, rw, wc);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1 + q + 4 * g, 64);
+        if (gstorer) {
+          tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
+          bulk_commit();
+          stored = true;
+        }
+      }
+      if (gstorer && stored) bulk_wait<0>();
+    }
+    for (int it = 0; it < (FAST ? 0 : ntl); ++it) {
       const int tile = tile_at(it);
       uint8_t* wt = w_s + ws * C::kWBytes;
       mbar_wait(&w_full[ws], wph);
       if (p.do_update) {
         const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
+        const uint32_t wt_s = smem_u32(wt);
         const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + c0;
         // --- independent of dW: W_old and random bits, overlapping the MMAs
-        const uint32_t wt_s = smem_u32(wt);
         uint4 raw[C::kChunks16];
 #pragma unroll
         for (int h = 0; h < C::kChunks16; ++h) raw[h] = lds128(wt_s + w_chunk_off<EB>(row, c0, h));
@@ -705,74 +869,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const uint4* csrc = reinterpret_cast<const uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE);
 #pragma unroll
           for (int h = 0; h < CE * 2; ++h) craw[h] = krow ? __ldg(csrc + h) : make_uint4(0u, 0u, 0u, 0u);
-        }
-        if constexpr (FAST) {
-          // production path: everything independent of dW (SR words, W_old
-          // decoded and scaled by 1 - lr wd) is computed and pinned in
-          // registers BEFORE the dW wait, so it overlaps the MMAs
-          uint32_t rw[8];
-          sr_words<1>(pk, flat0, rw, p.sr_bits != 0);
-          const float c_wd = 1.0f - p.lr * p.wd;
-          const float a_lr = -p.lr * p.dw_scale;
-          float wc[32];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t wv[4] = {raw[h].x, raw[h].y, raw[h].z, raw[h].w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float2 lo = dec_e4m3x2(static_cast<uint16_t>(wv[k] & 0xFFFF));
-              const float2 hi = dec_e4m3x2(static_cast<uint16_t>(wv[k] >> 16));
-              wc[h * 16 + 4 * k + 0] = lo.x;
-              wc[h * 16 + 4 * k + 1] = lo.y;
-              wc[h * 16 + 4 * k + 2] = hi.x;
-              wc[h * 16 + 4 * k + 3] = hi.y;
-            }
-          }
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {   // w (1 - lr wd)  (optimizers.py:71-73, wd folded)
-            const uint64_t r = fmul2(f2pack(wc[2 * k], wc[2 * k + 1]), f2pack(c_wd, c_wd));
-            f2unpack(r, wc[2 * k], wc[2 * k + 1]);
-          }
-#pragma unroll
-          for (int k = 0; k < 8; ++k) pin(rw[k]);
-#pragma unroll
-          for (int k = 0; k < 32; ++k) pin(wc[k]);
-          mbar_wait(&t_full[ds], dph);
-          tc_fence_after();
-          uint32_t acc[32];
-          tmem_ld32(tmem_base + lane_off + ds * 128 + c0, acc);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane_id() == 0) mbar_arrive(&t_empty[ds]);
-          uint32_t pk8[8];
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            float u[4];
-#pragma unroll
-            for (int e = 0; e < 4; e += 2) {
-              const uint64_t r = ffma2(f2pack(__uint_as_float(acc[4 * k + e]), __uint_as_float(acc[4 * k + e + 1])),
-                                       f2pack(a_lr, a_lr), f2pack(wc[4 * k + e], wc[4 * k + e + 1]));
-              f2unpack(r, u[e], u[e + 1]);
-            }
-            pk8[k] = cvt_e4m3x4_rs(u[3], u[2], u[1], u[0], rw[k]);
-          }
-          uint8_t* ot = out_s + (ot_flip & 1) * C::kWBytes;
-          ++ot_flip;
-          const uint32_t ot_s = smem_u32(ot);
-          sts128(ot_s + w_chunk_off<EB>(row, c0, 0), make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]));
-          sts128(ot_s + w_chunk_off<EB>(row, c0, 1), make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]));
-          fence_proxy_async_smem();
-          if (storer && prev_ws >= 0) bulk_wait_read<0>();
-          named_bar_sync(1 + q, 128);
-          if (storer) {
-            tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
-            bulk_commit();
-          }
-          prev_ws = ws;
-          if (++ws == WS) { ws = 0; wph ^= 1; }
-          if (++ds == 2) { ds = 0; dph ^= 1; }
-          continue;
         }
         uint32_t km = 0u;   // dropout keep bits of this thread's 32 columns
         if (p.keep != nullptr && grow < p.rows && col_ok)
@@ -840,7 +936,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (++ws == WS) { ws = 0; wph ^= 1; }
       if (++ds == 2) { ds = 0; dph ^= 1; }
     }
-    if (storer && p.do_update) {
+    if (!FAST && storer && p.do_update) {
       bulk_wait<0>();
       if (!C::kOutBuf && prev_ws >= 0) mbar_arrive(&w_empty[prev_ws]);
     }

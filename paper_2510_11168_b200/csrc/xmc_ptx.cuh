@@ -51,6 +51,8 @@ XMC_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 
 XMC_DEV bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  // (a suspendTimeHint operand, i.e. sleeping until the phase completes,
+  // measured 2-3 % slower in the backward than re-polling)
   uint32_t ok;
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -62,6 +64,21 @@ XMC_DEV bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// try_wait that suspends the thread in hardware until the phase completes
+// (or the hint expires): for waits off the critical path, so the waiting
+// warp does not take issue slots from the warps doing the work
+XMC_DEV bool mbar_try_wait_sleep(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+
 // Spin on an mbarrier phase.  A watchdog traps (turning a would-be hang into
 // a reported launch failure) if the phase never completes within ~2^34 cycles.
 XMC_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -69,6 +86,14 @@ XMC_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(a, parity)) return;
   const long long t0 = clock64();
   while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
+}
+XMC_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait_sleep(a, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait_sleep(a, parity)) {
     if (clock64() - t0 > (1ll << 34)) __trap();
   }
 }

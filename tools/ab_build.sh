@@ -16,6 +16,7 @@ else
   git -C "$root" archive "$rev" paper_2510_11168_b200/csrc include | tar -x -C "$tmp"
 fi
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared $extra \
-  -o "$root/paper_2510_11168_b200/libxmc_b200_$tag.so" "$tmp/paper_2510_11168_b200/csrc/xmc_api.cu"
+  -o "$root/paper_2510_11168_b200/libxmc_b200_$tag.so" "$tmp/paper_2510_11168_b200/csrc/xmc_api.cu" \
+  "$tmp/paper_2510_11168_b200/csrc/xmc_elementwise.cu"
 rm -rf "$tmp"
 echo "built paper_2510_11168_b200/libxmc_b200_$tag.so from $rev"
