@@ -239,7 +239,7 @@ struct xmc_head {
   uint8_t* xq;         // [max_bp][d] (eb)
   uint8_t* xqt;        // [d][max_bp] (beb)
   uint8_t* gbuf;       // [max_chunk_rows + 128][planes * max_bp] (beb)
-  float* gx_ws;        // [R][d][planes * max_bp]
+  float* gx_ws;        // [R][d][gx_planes * max_bp]
   int32_t* tile_cnt;   // [total_tiles + 1]
   int32_t* tile_ptr;   // [total_tiles + 1]
   int32_t* tile_cur;   // [total_tiles + 1] scatter cursors (tile_cnt is re-zeroed by the scan)
@@ -252,7 +252,6 @@ struct xmc_head {
   uint8_t* xq_topk;    // Xq rows of the current top-k launch (sample offset applied)
   uint8_t* wm;         // [max_chunk_rows + 128][d] masked W chunk (dropout only)
   uint32_t* keep;      // [max_chunk_rows + 128][d / 32] dropout keep bits (dropout only)
-  uint16_t* w16;       // [max_chunk_rows + 128][d] bf16 copy of an e4m3 W chunk (reference precision)
   int64_t comp_rows;   // local rows [0, comp_rows) carry a Kahan compensation
   float* cand_s;       // [max_bp][4 num_sms][kTopK] streaming top-k candidates (scores)
   int32_t* cand_l;     // [max_bp][4 num_sms][kTopK] (global labels)
@@ -284,8 +283,14 @@ struct xmc_peer {
 };
 
 struct Layout {
-  size_t xq, xqt, gbuf, gx, cnt, ptr, cur, ent, tmp, chunk, status, wm, keep, w16, cand, total;
+  size_t xq, xqt, gbuf, gx, cnt, ptr, cur, ent, tmp, chunk, status, wm, keep, cand, total;
 };
+
+// grad_X partial column groups per sample: the reference-precision planes
+// accumulate into one TMEM accumulator (grad_X^T = sum_p W^T G_p) when the
+// padded batch fits its 256 columns; bf16 batch 512 keeps one column group
+// per plane (two passes, summed by the reduce kernel)
+static int gx_planes(bool ref, int planes, int bp) { return (ref && bp <= 256) ? 1 : planes; }
 
 static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out, int* bp_out, int* R_out,
                                  int64_t* tiles_out, int64_t* maxrows_out, int num_sms) {
@@ -329,7 +334,7 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   L->xqt = align_up(L->xq + (size_t)bp * D * eb, 1024);
   L->gbuf = align_up(L->xqt + (size_t)bp * D * beb, 1024);
   L->gx = align_up(L->gbuf + (size_t)(maxrows + 128) * planes * bp * beb, 1024);
-  L->cnt = align_up(L->gx + (size_t)R * D * planes * bp * 4, 256);
+  L->cnt = align_up(L->gx + (size_t)R * D * gx_planes(ref, planes, bp) * bp * 4, 256);
   L->ptr = align_up(L->cnt + (size_t)(tiles + 1) * 4, 256);
   L->cur = align_up(L->ptr + (size_t)(tiles + 1) * 4, 256);
   L->ent = align_up(L->cur + (size_t)(tiles + 1) * 4, 256);
@@ -338,8 +343,7 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   L->status = align_up(L->chunk + (size_t)(2 * (ch.size() + 1)) * 8, 256);
   L->wm = align_up(L->status + 64, 1024);
   L->keep = align_up(L->wm + (d->dropout ? (size_t)(maxrows + 128) * D * eb : 0), 1024);
-  L->w16 = align_up(L->keep + (d->dropout ? (size_t)(maxrows + 128) * (D / 32) * 4 : 0), 1024);
-  L->cand = align_up(L->w16 + ((ref && eb == 1) ? (size_t)(maxrows + 128) * D * 2 : 0), 1024);
+  L->cand = align_up(L->keep + (d->dropout ? (size_t)(maxrows + 128) * (D / 32) * 4 : 0), 1024);
   L->total = align_up(L->cand + (size_t)bp * 4 * num_sms * kTopK * 8, 1024);
   *eb_out = eb;
   *bp_out = bp;
@@ -409,7 +413,6 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   h->status = reinterpret_cast<int32_t*>(w + L.status);
   h->wm = desc->dropout ? w + L.wm : nullptr;
   h->keep = desc->dropout ? reinterpret_cast<uint32_t*>(w + L.keep) : nullptr;
-  h->w16 = (h->ref && eb == 1) ? reinterpret_cast<uint16_t*>(w + L.w16) : nullptr;
   h->comp_rows = desc->comp_bytes == 0 ? 0
                  : desc->comp_labels <= 0
                      ? desc->num_labels_local
@@ -712,15 +715,18 @@ struct BwdLaunch {
 // One bwd pass over `rows` chunk rows whose W starts at Wc (the chunk's first
 // row: W itself, the masked dropout copy or the bf16 reference-precision copy)
 // and whose global label / compensation row is the local row row0.  G from
-// gbuf; grad_X partials into the [R][d][planes * Bp] workspace.
+// gbuf; grad_X partials into the [R][d][gx_planes * Bp] workspace.
 static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int64_t rows, int Bp, bool update,
                             int gx_kc0, int gx_kc_count, bool gx_overwrite, const xmc_step_args* a,
                             const uint32_t* keep, float drop_scale, BwdLaunch* L) {
   const int beb = h->beb, D = h->desc.dim;
   const int box_k = 128 / beb;
   const int ldg = h->planes * Bp;
-  XMC_TRY(make_map(&L->tw, Wc, beb, D, rows, D, 128));
-  XMC_TRY(make_map(&L->tws, Wc, beb, D, rows, D, 32));
+  const int gxp = gx_planes(h->ref, h->planes, Bp);
+  // W in its storage format (an e4m3 head's reference-precision kernel
+  // converts each tile to bf16 operands in shared memory)
+  XMC_TRY(make_map(&L->tw, Wc, h->eb, D, rows, D, 128));
+  XMC_TRY(make_map(&L->tws, Wc, h->eb, D, rows, D, 32));
   const int64_t tiles = cdiv(rows, 128);
   const int R = static_cast<int>(std::min<int64_t>(h->R, tiles));
   XMC_TRY(make_map(&L->tg, h->gbuf, beb, ldg, rows, ldg, 128));
@@ -736,6 +742,16 @@ static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int
   p.do_update = update ? 1 : 0;
   p.gx_kc0 = gx_kc0;
   p.gx_kc_count = gx_kc_count;
+  // reference-precision planes accumulated in TMEM: grad_X MMA groups of
+  // N = 128 samples (2 k-chunks), so the 4-slot G ring holds two groups and the
+  // producer loads one while the other multiplies
+  const bool acc_planes = gxp == 1 && h->planes > 1;
+  p.gx_group = acc_planes ? std::min(2, Bp / box_k) : gx_kc_count;
+  p.gx_cols = acc_planes ? Bp : gx_kc_count * box_k;
+  p.g_prefetch = h->planes > 1 ? 1 : 0;
+  // reference precision: drain grad_X every 32 tiles (fp32 accumulation
+  // chains of <= 32 x 3 x 128 products per TMEM window)
+  p.gx_flush = h->planes > 1 ? 32 : 0;
   p.g_e5m2 = h->gout == G_E5M2 ? 1 : 0;
   p.W = static_cast<uint8_t*>(Wc);
   const int64_t crows = comp ? std::min<int64_t>(rows, std::max<int64_t>(0, h->comp_rows - row0)) : 0;
@@ -749,7 +765,7 @@ static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int
   p.rng_base = a ? sm64_base(a->seed, a->step, a->tensor_id) : 0;
   p.sr_bits = a ? a->sr_bits : 0;
   p.gx_ws = h->gx_ws;
-  p.gx_ld = ldg;
+  p.gx_ld = gxp * Bp;
   p.gx_accumulate = gx_overwrite ? 0 : 1;
   if (h->adam.m && update) {
     p.adam_m = h->adam.m + row0 * D;
@@ -769,27 +785,28 @@ static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int
   return XMC_OK;
 }
 
-template <int EB, bool XR, int KC, int CE, bool FAST, bool ADAMW, int GE>
+template <int EB, bool XR, int KC, int CE, bool FAST, bool ADAMW, int GE, int SB>
 static xmc_status launch_bwd_k(xmc_head* h, const BwdLaunch& L, cudaStream_t st) {
-  constexpr int sm = BwdCfg<EB, XR, KC>::kSmemBytes;
-  auto k = xmc_bwd_kernel<EB, XR, KC, CE, FAST, ADAMW, GE>;
-  smem_attr_once<xmc_bwd_kernel<EB, XR, KC, CE, FAST, ADAMW, GE>>(sm);
+  constexpr int sm = BwdCfg<EB, XR, KC, SB>::kSmemBytes;
+  static_assert(sm <= 232448, "bwd shared memory over the 227 KB opt-in limit");
+  auto k = xmc_bwd_kernel<EB, XR, KC, CE, FAST, ADAMW, GE, SB>;
+  smem_attr_once<xmc_bwd_kernel<EB, XR, KC, CE, FAST, ADAMW, GE, SB>>(sm);
   CUDA_TRY(launch_ex(k, L.R * h->dtiles, kBwdThreads, sm, st, h, 1, L.tw, L.tg, L.tx, L.tws, L.p));
   return XMC_OK;
 }
 
 // compensation / optimizer variant of one kernel geometry
-template <int EB, bool XR, int KC, int GE>
+template <int EB, bool XR, int KC, int GE, int SB = EB>
 static xmc_status launch_bwd_v(xmc_head* h, const BwdLaunch& L, cudaStream_t st) {
   const BwdParams& p = L.p;
-  if (p.adam_m != nullptr) return launch_bwd_k<EB, XR, KC, 4, false, true, GE>(h, L, st);
+  if (p.adam_m != nullptr) return launch_bwd_k<EB, XR, KC, 4, false, true, GE, SB>(h, L, st);
   const int ce = p.comp ? h->desc.comp_bytes : 0;
-  if (ce == 2) return launch_bwd_k<EB, XR, KC, 2, false, false, GE>(h, L, st);
-  if (ce == 4) return launch_bwd_k<EB, XR, KC, 4, false, false, GE>(h, L, st);
+  if (ce == 2) return launch_bwd_k<EB, XR, KC, 2, false, false, GE, SB>(h, L, st);
+  if (ce == 4) return launch_bwd_k<EB, XR, KC, 4, false, false, GE, SB>(h, L, st);
   if constexpr (EB == 1 && GE == 1)
     if (p.do_update && p.rounding == ROUND_SR_FAST && p.keep == nullptr)
-      return launch_bwd_k<1, XR, KC, 0, true, false, 1>(h, L, st);
-  return launch_bwd_k<EB, XR, KC, 0, false, false, GE>(h, L, st);
+      return launch_bwd_k<1, XR, KC, 0, true, false, 1, 1>(h, L, st);
+  return launch_bwd_k<EB, XR, KC, 0, false, false, GE, SB>(h, L, st);
 }
 
 static xmc_status launch_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int64_t rows, int Bp, bool update,
@@ -800,10 +817,12 @@ static xmc_status launch_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, in
   ProfRec pr;
   prof_begin(1, st, &pr);
   xmc_status s = XMC_ERR_UNSUPPORTED;
-  if (h->ref) {
-    // reference precision: bf16 operands (three G planes, streamed Xq^T),
-    // rounding onto the head's own grid
-    s = h->eb == 1 ? launch_bwd_v<2, false, 8, 1>(h, L, st) : launch_bwd_v<2, false, 8, 2>(h, L, st);
+  if (h->ref && h->eb == 1) {
+    // reference precision of an e4m3 head: W stays e4m3 in HBM, each tile is
+    // converted to bf16 operands in shared memory; three G planes, resident
+    // Xq^T, rounding onto the e4m3 grid
+    if (Bp == 128) s = launch_bwd_v<2, true, 2, 1, 1>(h, L, st);
+    else if (Bp == 256) s = launch_bwd_v<2, true, 4, 1, 1>(h, L, st);
   } else if (h->eb == 1) {
     if (Bp == 128) s = launch_bwd_v<1, true, 1, 1>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<1, true, 2, 1>(h, L, st);
@@ -828,6 +847,8 @@ static xmc_status run_backward(xmc_head* h, void* Wc, void* comp, int64_t row0, 
                                const uint32_t* keep = nullptr, float drop_scale = 1.0f) {
   if (!gx) return launch_bwd(h, Wc, comp, row0, rows, Bp, update, 0, 0, false, a, st, keep, drop_scale);
   const int kcs = h->planes * Bp * h->beb / 128;
+  if (h->planes > 1 && gx_planes(h->ref, h->planes, Bp) == 1)   // one pass; the planes accumulate in TMEM
+    return launch_bwd(h, Wc, comp, row0, rows, Bp, update, 0, kcs, gx_overwrite, a, st, keep, drop_scale);
   const int per = 256 * h->beb / 128;   // k-chunks whose grad_X columns fit 256 TMEM columns
   const int groups = (kcs + per - 1) / per;
   for (int gi = groups - 1; gi >= 0; --gi) {
@@ -839,46 +860,17 @@ static xmc_status run_backward(xmc_head* h, void* Wc, void* comp, int64_t row0, 
   return XMC_OK;
 }
 
-static int copy_blocks(int64_t n16) { return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cdiv(n16, 256), 148 * 8))); }
-
-// e4m3 W rows -> the bf16 scratch (reference-precision backward operand)
-static xmc_status w_to_bf16(xmc_head* h, const void* Wc, int64_t rows, cudaStream_t st) {
-  const int64_t n16 = rows * h->desc.dim / 16;
-  w_e4m3_to_bf16_kernel<<<copy_blocks(n16), 256, 0, st>>>(static_cast<const uint8_t*>(Wc), n16, h->w16);
-  CUDA_TRY(cudaGetLastError());
-  return XMC_OK;
-}
-static xmc_status w_from_bf16(xmc_head* h, void* Wc, int64_t rows, cudaStream_t st) {
-  const int64_t n16 = rows * h->desc.dim / 16;
-  w_bf16_to_e4m3_kernel<<<copy_blocks(n16), 256, 0, st>>>(h->w16, n16, static_cast<uint8_t*>(Wc));
-  CUDA_TRY(cudaGetLastError());
-  return XMC_OK;
-}
-
 // The backward of one chunk (local rows [r0, r0 + rows)), G in gbuf:
 // grad_X partials from Wgx (W, or the masked dropout copy at its chunk base)
-// and, if update, the update of W (dW masked by keep under dropout).  In
-// reference precision an e4m3 head's operands go through the bf16 scratch.
+// and, if update, the update of W (dW masked by keep under dropout).
 static xmc_status chunk_backward(xmc_head* h, void* W, const void* Wgx, void* comp, int64_t r0, int64_t rows,
                                  int Bp, bool gx, bool update, bool gx_overwrite, const xmc_step_args* a,
                                  cudaStream_t st, const uint32_t* keep = nullptr, float drop_scale = 1.0f) {
   const int D = h->desc.dim, eb = h->eb;
   uint8_t* Wr = static_cast<uint8_t*>(W) + r0 * D * eb;
-  const bool same = Wgx == Wr;
-  if (!h->w16) {
-    if (same || !gx) return run_backward(h, Wr, comp, r0, rows, Bp, gx, update, gx_overwrite, a, st, keep, drop_scale);
-    XMC_TRY(run_backward(h, const_cast<void*>(Wgx), nullptr, r0, rows, Bp, true, false, gx_overwrite, a, st));
-    return update ? launch_bwd(h, Wr, comp, r0, rows, Bp, true, 0, 0, false, a, st, keep, drop_scale) : XMC_OK;
-  }
-  if (gx && !same) {
-    XMC_TRY(w_to_bf16(h, Wgx, rows, st));
-    XMC_TRY(run_backward(h, h->w16, nullptr, r0, rows, Bp, true, false, gx_overwrite, a, st));
-    if (!update) return XMC_OK;
-    gx = false;
-  }
-  XMC_TRY(w_to_bf16(h, Wr, rows, st));
-  XMC_TRY(run_backward(h, h->w16, comp, r0, rows, Bp, gx, update, gx_overwrite, a, st, keep, drop_scale));
-  return update ? w_from_bf16(h, Wr, rows, st) : XMC_OK;
+  if (Wgx == Wr || !gx) return run_backward(h, Wr, comp, r0, rows, Bp, gx, update, gx_overwrite, a, st, keep, drop_scale);
+  XMC_TRY(run_backward(h, const_cast<void*>(Wgx), nullptr, r0, rows, Bp, true, false, gx_overwrite, a, st));
+  return update ? launch_bwd(h, Wr, comp, r0, rows, Bp, true, 0, 0, false, a, st, keep, drop_scale) : XMC_OK;
 }
 
 // acc[s][c] (+)= scale * sum_r sum_planes ws[r][c][plane * Bp + s] -- one
@@ -886,7 +878,8 @@ static xmc_status chunk_backward(xmc_head* h, void* W, const void* Wgx, void* co
 static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumulate, cudaStream_t st,
                             float scale = 1.0f) {
   const int D = h->desc.dim;
-  const int ldg = h->planes * Bp;
+  const int gxp = gx_planes(h->ref, h->planes, Bp);
+  const int ldg = gxp * Bp;
   const float sc = ((h->eb == 1 && !h->ref) ? (1.0f / 256.0f) : 1.0f) * scale;
   dim3 g(D / 32, (Bp + 31) / 32), b(32, 32);
   cudaLaunchConfig_t cfg{};
@@ -911,16 +904,16 @@ static xmc_status reduce_gx(xmc_head* h, int B, int Bp, float* acc, bool accumul
     pa.epoch = ++pg->epoch;
     pa.status = h->status;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, gx_reduce_peer_kernel, static_cast<const float*>(h->gx_ws), h->R_step, D, ldg,
-                                h->planes, Bp, B, sc, acc, pa));
+                                gxp, Bp, B, sc, acc, pa));
     return XMC_OK;
   }
   CUDA_TRY(cudaLaunchKernelEx(&cfg, gx_reduce_kernel, static_cast<const float*>(h->gx_ws), h->R_step, D, ldg,
-                              h->planes, Bp, B, sc, accumulate ? 1 : 0, static_cast<const int32_t*>(h->status), acc));
+                              gxp, Bp, B, sc, accumulate ? 1 : 0, static_cast<const int32_t*>(h->status), acc));
   return XMC_OK;
 }
 
 static xmc_status zero_gx_ws(xmc_head* h, int Bp, cudaStream_t st) {
-  CUDA_TRY(cudaMemsetAsync(h->gx_ws, 0, (size_t)h->R * h->desc.dim * h->planes * Bp * 4, st));
+  CUDA_TRY(cudaMemsetAsync(h->gx_ws, 0, (size_t)h->R * h->desc.dim * gx_planes(h->ref, h->planes, Bp) * Bp * 4, st));
   return XMC_OK;
 }
 

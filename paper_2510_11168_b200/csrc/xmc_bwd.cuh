@@ -57,7 +57,14 @@ struct BwdParams {
   int32_t do_update;     // dW + SGD + rounding, W written in place
   int32_t gx_kc0;        // first G k-chunk accumulated into grad_X
   int32_t gx_kc_count;   // 0 = no grad_X
+  int32_t gx_group;      // G k-chunks per grad_X MMA group (N = gx_group x 128 / EB samples): gx_kc_count for one
+                         // column group, xt_kc for the reference-precision planes, which accumulate into the
+                         // same TMEM columns (grad_X^T = sum over planes of W^T G_plane)
   int32_t g_e5m2;        // EB = 1: G is e5m2 (x 2^8) instead of e4m3 (x 2^8)
+  int32_t gx_cols;       // TMEM columns of the grad_X accumulator (samples of one column group / plane)
+  int32_t g_prefetch;    // 1: the producer prefetches the next tile's G boxes into L2 (slot-by-slot path)
+  int32_t gx_flush;      // > 0 (general path): drain the grad_X accumulator into the partial slot every
+                         // gx_flush tiles, bounding the length of the tensor core's fp32 accumulation chain
   uint8_t* W;            // chunk base (row-major rows x d, EB bytes/elem), written in place
   uint8_t* comp;         // Kahan compensation, chunk base (comp_rows x d, CE bytes/elem) or null
   int32_t comp_rows;     // leading chunk rows that carry a compensation (top-p% head-Kahan)
@@ -79,32 +86,39 @@ struct BwdParams {
   float b1, b2, omb1, omb2, bc1, bc2, eps;
 };
 
-template <int EB, bool XT_RES, int KCMAX>
+// SB: bytes per stored W element (the HBM tile, the update epilogue, W_new).
+// SB < EB (reference precision of an e4m3 head): the epilogue converts each
+// e4m3 W tile into a bf16 operand tile (kOpBytes) for the grad_X MMAs.
+template <int EB, bool XT_RES, int KCMAX, int SB = EB>
 struct BwdCfg {
-  static constexpr int kBoxK = 128 / EB;             // elements per 128-B atom row
+  static_assert(SB == EB || (SB == 1 && EB == 2), "bf16 operands of an e4m3 head only");
+  static constexpr bool kW8 = SB != EB;              // W stored e4m3, MMA operands bf16
+  static constexpr int kBoxK = 128 / EB;             // elements per 128-B atom row (operands)
+  static constexpr int kWBoxK = 128 / SB;            // elements per 128-B atom row (stored W)
   static constexpr int kBox = 128 * 128;             // one [128 rows x 128 B] box
-  static constexpr int kWBoxes = EB;                 // d-tile of 128 elements
+  static constexpr int kWBoxes = SB;                 // d-tile of 128 stored elements
   static constexpr int kWBytes = kWBoxes * kBox;
+  static constexpr int kOpBytes = kW8 ? EB * kBox : 0;   // bf16 W^T operand tile (kW8)
   // e4m3: W_new is staged in its own smem tile (kOutBytes), so the W_old slot
   // is released right after the epilogue has read it and the update never
   // waits for the grad_X MMAs still reading W_old; bf16 (no smem left for a
   // second tile) writes W_new in place after the grad_X MMAs completed.
   // (measured equal within box noise: in place / 1 / 2 staging tiles with
   // 5 / 4 / 3 W stages; two staging tiles need one named barrier per tile)
-  static constexpr int kOutTiles = EB == 1 ? 2 : 0;   // W_new staging tiles (0 = in place)
+  static constexpr int kOutTiles = SB == 1 ? 2 : 0;   // W_new staging tiles (0 = in place)
   static constexpr bool kOutBuf = kOutTiles > 0;
   // e4m3: 4 W stages (224 KB with the staging tiles; 3 -> 4 measured -1.5 %
   // bwd); the G ring (6 slots = 3 tiles) must not get shallower (4 slots: +10 %)
-  static constexpr int kWStages = EB == 1 ? 4 : 3;
+  static constexpr int kWStages = kW8 ? (KCMAX > 2 ? 2 : 4) : (EB == 1 ? 4 : 3);
   static constexpr int kOutBytes = kOutTiles * kWBytes;
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
   static constexpr int kKStages = EB == 1 ? 6 : 4;
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
-  static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2) + 16;
+  static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2 + 2 + 2) + 16;
   static constexpr int kSmemBytes =
-      1024 + kXtBytes + kWStages * kWBytes + kOutBytes + kKStages * kKSlot + kBarBytes;
+      1024 + kXtBytes + kWStages * kWBytes + kOpBytes + kOutBytes + kKStages * kKSlot + kBarBytes;
   static constexpr int kKmma = 32 / EB;              // K per MMA instruction (elements)
-  static constexpr int kChunks16 = 2 * EB;           // 16-B smem chunks per thread (32 elements)
+  static constexpr int kChunks16 = 2 * SB;           // 16-B smem chunks per thread (32 stored elements)
 };
 
 // byte offset of 16-B chunk `h` of this thread's 32 columns [c0, c0+32) in the
@@ -412,7 +426,7 @@ XMC_DEV void w_update_pack_adamw(const BwdParams& p, const uint32_t (&acc)[32], 
 // The kernel: CTA bid of the grid (d-tile bid % dtiles, row group bid / dtiles).
 // FAST: the production specialisation (SR_FAST, e4m3, no compensation, no
 // dropout mask) with every runtime mode switch folded away.
-template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false, bool ADAMW = false, int GE = EB>
+template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false, bool ADAMW = false, int GE = EB, int SB = EB>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
                    const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
@@ -420,7 +434,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // a by-value copy: the compiler keeps launch-uniform fields in uniform
   // registers (a __grid_constant__ reference measured 17 % slower)
   BwdParams p = p_arg;
-  using C = BwdCfg<EB, XT_RES, KCMAX>;
+  using C = BwdCfg<EB, XT_RES, KCMAX, SB>;
   static_assert(!ADAMW || (CE == 4 && !FAST), "the Adam-style head keeps an fp32 compensation");
   static_assert(!FAST || (EB == 1 && GE == 1 && CE == 0), "the fast path is the e4m3 SR_FAST head");
   constexpr int WS = C::kWStages;
@@ -432,7 +446,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* xt_s = smem;
   uint8_t* w_s = smem + C::kXtBytes;
-  uint8_t* out_s = w_s + WS * C::kWBytes;      // W_new staging tiles (kOutBuf)
+  uint8_t* op_s = w_s + WS * C::kWBytes;       // bf16 W^T operand tile (kW8)
+  uint8_t* out_s = op_s + C::kOpBytes;         // W_new staging tiles (kOutBuf)
   uint8_t* k_s = out_s + C::kOutBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(k_s + KS * C::kKSlot);
   uint64_t* w_full = bars;                 // [WS]
@@ -443,7 +458,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* t_empty = t_full + 2;          // [2]
   uint64_t* xt_full = t_empty + 2;
   uint64_t* gx_full = xt_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gx_full + 1);
+  uint64_t* op_full = gx_full + 1;         // kW8: operand tile converted (every epilogue warp)
+  uint64_t* op_empty = op_full + 1;        // kW8: the tile's grad_X MMAs have read it
+  uint64_t* gxw_full = op_empty + 1;       // a grad_X accumulation window is complete (gx_flush)
+  uint64_t* gxw_empty = gxw_full + 1;      // ... and drained into the partial slot
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gxw_empty + 1);
   int32_t* status_s = reinterpret_cast<int32_t*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id_sync();
@@ -451,6 +470,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int R = nblk / p.dtiles;
   const int r0 = bid / p.dtiles;
   const bool do_gx = p.gx_kc_count > 0;
+  // kW8: the epilogue converts each e4m3 W tile to the bf16 operand tile
+  const bool conv = C::kW8 && do_gx;
+  // grad_X accumulation windows of gx_win tiles (general path only)
+  const int gx_win = (!FAST && p.gx_flush > 0) ? p.gx_flush : 0x7fffffff;
   // this CTA's label tiles: r0, r0 + R, ... (the d-tile CTAs of a row group
   // walk them in step, so each G tile is requested by all six at once)
   const int ntl = r0 < p.num_tiles ? (p.num_tiles - r0 + R - 1) / R : 0;
@@ -471,7 +494,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&w_full[s], 1);
       // MMA commit + (kOutBuf) every epilogue warp once it has read W_old, or
       // (in place) one store thread per TMEM sub-partition once W_new is stored
-      mbar_init(&w_empty[s], FAST ? 1 + kBwdEpiWarps / 2 : (C::kOutBuf ? 1 + kBwdEpiWarps : 5));
+      // (kW8: the MMAs read the bf16 operand tile, not the stage: epilogue warps only)
+      mbar_init(&w_empty[s], FAST ? 1 + kBwdEpiWarps / 2
+                                  : (C::kW8 ? kBwdEpiWarps : (C::kOutBuf ? 1 + kBwdEpiWarps : 5)));
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -483,6 +508,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     mbar_init(xt_full, 1);
     mbar_init(gx_full, 1);
+    mbar_init(op_full, kBwdEpiWarps);
+    mbar_init(op_empty, 1);
+    mbar_init(gxw_full, 1);
+    mbar_init(gxw_empty, kBwdEpiWarps);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -545,7 +574,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int kcg = kb + i;
         int xk = kcg;   // Xq^T k-chunk of G k-chunk kcg (kcg < 3 xt_kc)
         while (xk >= p.xt_kc) xk -= p.xt_kc;
-        const int32_t c0 = is_w ? j * 128 + lane * C::kBoxK : (sub == 0 ? kcg : xk) * C::kBoxK;
+        const int32_t c0 = is_w ? j * 128 + lane * C::kWBoxK : (sub == 0 ? kcg : xk) * C::kBoxK;
         const int32_t c1 = is_w ? tile * 128 : (sub == 0 ? tile * 128 : j * 128);
         if (active) tma_load_2d_hint(dst, m, bar, c0, c1, is_w ? pol_stream : pol_keep);
         __syncwarp();
@@ -557,22 +586,41 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (lane == 0) mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
         __syncwarp();
         if (lane < C::kWBoxes)
-          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kBoxK,
+          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kWBoxK,
                            tile * 128, pol_stream);
         __syncwarp();
-        int xk = 0;   // Xq^T k-chunk of kc (kb = 0 whenever Xq^T is loaded)
-        for (int kc = kb; kc < ke; ++kc) {
-          mbar_wait(&k_empty[ks], kph ^ 1);
-          uint8_t* slot = k_s + ks * C::kKSlot;
-          if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], kslot_bytes);
-          __syncwarp();
-          if (lane == 0) tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
-          if constexpr (!XT_RES)
+        // the next tile's G boxes into L2 while this one streams from the ring
+        // (the reference-precision planes: the ring holds only a plane or two)
+        if (p.g_prefetch && it + 1 < ntl && lane < nk) tma_prefetch_2d(&tm_g, (kb + lane) * C::kBoxK, tile_at(it + 1) * 128);
+        if constexpr (XT_RES) {
+          // G boxes in batches of one grad_X group (one warp-wide instruction,
+          // lane = box); groups never straddle the ring end (KS % bat == 0)
+          const int bat = (KS % p.gx_group == 0 && nk % p.gx_group == 0) ? p.gx_group : 1;
+          for (int kc = kb; kc < ke; kc += bat) {
+            for (int i = 0; i < bat; ++i) mbar_wait(&k_empty[ks + i], kph ^ 1);
+            if (lane < bat) {
+              mbar_arrive_expect_tx(&k_full[ks + lane], kslot_bytes);
+              tma_load_2d_hint(k_s + (ks + lane) * C::kKSlot, &tm_g, &k_full[ks + lane], (kc + lane) * C::kBoxK,
+                               tile * 128, pol_keep);
+            }
+            __syncwarp();
+            ks += bat;
+            if (ks == KS) { ks = 0; kph ^= 1; }
+          }
+        } else {
+          int xk = 0;   // Xq^T k-chunk of kc (kb = 0 whenever Xq^T is loaded)
+          for (int kc = kb; kc < ke; ++kc) {
+            mbar_wait(&k_empty[ks], kph ^ 1);
+            uint8_t* slot = k_s + ks * C::kKSlot;
+            if (lane == 0) mbar_arrive_expect_tx(&k_full[ks], kslot_bytes);
+            __syncwarp();
+            if (lane == 0) tma_load_2d_hint(slot, &tm_g, &k_full[ks], kc * C::kBoxK, tile * 128, pol_keep);
             if (lane == 1 && p.do_update)
               tma_load_2d_hint(slot + C::kBox, &tm_xt, &k_full[ks], xk * C::kBoxK, j * 128, pol_keep);
-          __syncwarp();
-          if (++xk == p.xt_kc) xk = 0;
-          if (++ks == KS) { ks = 0; kph ^= 1; }
+            __syncwarp();
+            if (++xk == p.xt_kc) xk = 0;
+            if (++ks == KS) { ks = 0; kph ^= 1; }
+          }
         }
       }
       if (++ws == WS) { ws = 0; wph ^= 1; }
@@ -584,7 +632,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t gf = EB == 1 ? (p.g_e5m2 ? 1u : 0u) : 1u;
     const uint32_t xf = EB == 1 ? 0u : 1u;
     const uint32_t idesc_dw = umma_idesc(gf, xf, false, false, 128, 128);                         // A = G, B = Xq
-    const uint32_t idesc_gx = umma_idesc(xf, gf, true, true, 128, p.gx_kc_count * C::kBoxK);      // A = W^T, B = G
+    const uint32_t idesc_gx = umma_idesc(xf, gf, true, true, 128, p.gx_group * C::kBoxK);         // A = W^T, B = G
     if constexpr (XT_RES) mbar_wait(xt_full, 0);
     if constexpr (FAST) {
       // Production path, lean instruction stream (the MMA warp shares its
@@ -637,19 +685,37 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     int ws = 0, ks = 0, ds = 0;
     uint32_t wph = 0, kph = 0, dph = 0;
+    const int gsz = p.gx_group;   // k-chunks per grad_X MMA group
+    // groups per accumulator: the column groups of one plane (reference
+    // precision with N = 128 groups); group gi writes columns (gi % gpp) x N
+    const int gpp = p.gx_cols / (gsz * C::kBoxK) > 0 ? p.gx_cols / (gsz * C::kBoxK) : 1;
     for (int it = 0; it < (FAST ? 0 : ntl); ++it) {
       mbar_wait(&w_full[ws], wph);
       mbar_wait(&t_empty[ds], dph ^ 1);
       tc_fence_after();
-      const uint32_t w_addr = smem_u32(w_s + ws * C::kWBytes);
+      // grad_X A operand: the W stage, or (kW8) the bf16 tile the epilogue converted
+      const uint32_t w_addr = C::kW8 ? smem_u32(op_s) : smem_u32(w_s + ws * C::kWBytes);
       const uint32_t d_dw = tmem_base + ds * 128;
+      bool op_ready = !C::kW8;
+      int xk = kb;   // Xq^T k-chunk of G k-chunk kc (the planes repeat it)
+      while (xk >= p.xt_kc) xk -= p.xt_kc;
       for (int kc = kb; kc < ke; ++kc) {
         mbar_wait(&k_full[ks], kph);
+        const int gk = kc - p.gx_kc0;
+        const bool in_gx = do_gx && gk >= 0 && gk < p.gx_kc_count;
+        const bool gx_last = in_gx && gk % gsz == gsz - 1;   // a grad_X group's G boxes are all in
+        if (C::kW8 && gx_last && !op_ready) {
+          mbar_wait(op_full, static_cast<uint32_t>(it) & 1u);
+          op_ready = true;
+        }
+        // a new accumulation window starts once the epilogue drained the last one
+        const bool fresh = it % gx_win == 0;
+        if (gx_last && fresh && it > 0 && gk < gsz)   // the window's first group
+          mbar_wait(gxw_empty, static_cast<uint32_t>(it / gx_win - 1) & 1u);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t g_addr = smem_u32(k_s + ks * C::kKSlot);
-          // resident Xq^T only with one G plane (xt_kc == kc_count)
-          const uint32_t x_addr = XT_RES ? smem_u32(xt_s + kc * C::kBox) : g_addr + C::kBox;
+          const uint32_t x_addr = XT_RES ? smem_u32(xt_s + xk * C::kBox) : g_addr + C::kBox;
           if (p.do_update) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -662,37 +728,38 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           // dW complete -> hand it to the update epilogue before the grad_X
           // MMAs are queued (commit tracks only the MMAs issued so far)
           if (C::kOutBuf && kc == ke - 1) mma_commit(&t_full[ds]);
-          // grad_X^T: one MMA group with N = all samples of the pass, issued
+          // grad_X^T: one MMA group with N = gsz k-chunks of samples, issued
           // once its G boxes (contiguous ring slots, LBO = slot pitch) landed;
-          // W (A operand) is then read from smem once per tile.
-          const int gk = kc - p.gx_kc0;
-          const bool in_gx = do_gx && gk >= 0 && gk < p.gx_kc_count;
-          if (in_gx && gk == p.gx_kc_count - 1) {
-            const int s0 = ks - gk;   // ring slot of the group's first k-chunk
+          // W (A operand) is then read from smem once per group.  Groups of
+          // the reference-precision planes accumulate into the same columns.
+          if (gx_last) {
+            const int gi = gk / gsz;
+            const bool acc0 = !fresh || gi >= gpp;
+            const uint32_t d_gx = tmem_gx + (gi % gpp) * gsz * C::kBoxK;
+            const int s0 = ks - gk % gsz;   // ring slot of the group's first k-chunk
             if (s0 >= 0) {
               const uint32_t g0 = smem_u32(k_s + s0 * C::kKSlot);
 #pragma unroll
               for (int k = 0; k < 128 / C::kKmma; ++k) {
                 const uint64_t ad = umma_desc_sw128(w_addr + k * C::kKmma * 128, C::kBox, 1024);
                 const uint64_t bd = umma_desc_sw128(g0 + k * C::kKmma * 128, C::kKSlot, 1024);
-                if constexpr (EB == 1) mma_f8(tmem_gx, ad, bd, idesc_gx, (it | k) != 0);
-                else mma_f16(tmem_gx, ad, bd, idesc_gx, (it | k) != 0);
+                if constexpr (EB == 1) mma_f8(d_gx, ad, bd, idesc_gx, acc0 || k != 0);
+                else mma_f16(d_gx, ad, bd, idesc_gx, acc0 || k != 0);
               }
               for (int s = s0; s <= ks; ++s) mma_commit(&k_empty[s]);
             } else {
-              // the group wraps around the ring (kc_count not a multiple of
-              // KS, e.g. the reference-precision planes at batch <= 128):
-              // one N = kBoxK MMA group per k-chunk into its TMEM columns
+              // the group wraps around the ring: one N = kBoxK MMA group per
+              // k-chunk into its TMEM columns
               const uint32_t idesc_c = umma_idesc(xf, gf, true, true, 128, C::kBoxK);
-              for (int c = 0; c <= gk; ++c) {
+              for (int c = 0; c <= gk % gsz; ++c) {
                 const int sc = s0 + c < 0 ? s0 + c + KS : s0 + c;
                 const uint32_t gc = smem_u32(k_s + sc * C::kKSlot);
 #pragma unroll
                 for (int k = 0; k < 128 / C::kKmma; ++k) {
                   const uint64_t ad = umma_desc_sw128(w_addr + k * C::kKmma * 128, C::kBox, 1024);
                   const uint64_t bd = umma_desc_sw128(gc + k * C::kKmma * 128, C::kKSlot, 1024);
-                  if constexpr (EB == 1) mma_f8(tmem_gx + c * C::kBoxK, ad, bd, idesc_c, (it | k) != 0);
-                  else mma_f16(tmem_gx + c * C::kBoxK, ad, bd, idesc_c, (it | k) != 0);
+                  if constexpr (EB == 1) mma_f8(d_gx + c * C::kBoxK, ad, bd, idesc_c, acc0 || k != 0);
+                  else mma_f16(d_gx + c * C::kBoxK, ad, bd, idesc_c, acc0 || k != 0);
                 }
                 mma_commit(&k_empty[sc]);
               }
@@ -705,9 +772,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (!C::kOutBuf && kc == ke - 1) mma_commit(&t_full[ds]);
         }
         __syncwarp();
+        if (++xk == p.xt_kc) xk = 0;
         if (++ks == KS) { ks = 0; kph ^= 1; }
       }
-      if (elect_one()) mma_commit(&w_empty[ws]);
+      if (elect_one()) {
+        if constexpr (C::kW8) {
+          if (conv) mma_commit(op_empty);   // the stage itself is released by the epilogue
+        } else {
+          mma_commit(&w_empty[ws]);
+        }
+        if (do_gx && (it + 1) % gx_win == 0 && it + 1 < ntl) mma_commit(gxw_full);
+      }
       __syncwarp();
       if (++ws == WS) { ws = 0; wph ^= 1; }
       if (++ds == 2) { ds = 0; dph ^= 1; }
@@ -730,6 +805,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     int ot_flip = 0;
     uint32_t wph = 0, dph = 0;
     const PhiloxKeys pk = philox_keys(p.rng_base);   // round keys, once per launch
+    // grad_X^T accumulator (TMEM lane = d index) into this CTA's slot of the
+    // [R][d][gx_ld] partial buffer; the chunks (and accumulation windows) of
+    // one step add into it (stream-ordered, one owner per slot: deterministic)
+    auto gx_drain = [&](bool accumulate) {
+      const int nchunks = j * 128 + row < p.d ? p.gx_cols / 32 : 0;
+      float* dst = p.gx_ws + (static_cast<int64_t>(r0) * p.d + j * 128 + row) * p.gx_ld + p.gx_kc0 * C::kBoxK;
+#pragma unroll 1
+      for (int cch = quarter; cch < nchunks; cch += 4) {
+        uint32_t r[32];
+        tmem_ld32(tmem_gx + lane_off + cch * 32, r);
+        tmem_ld_wait();
+        float4* o = reinterpret_cast<float4*>(dst + cch * 32);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          float4 v = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                                 __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+          if (accumulate) {
+            const float4 old = o[k];
+            v.x += old.x;
+            v.y += old.y;
+            v.z += old.z;
+            v.w += old.w;
+          }
+          o[k] = v;
+        }
+      }
+    };
     if constexpr (FAST) {
       // ---- production path (e4m3, SR_FAST, no compensation / dropout):
       // ping-pong groups.  Group g = ew / 8 takes tiles it = g, g + 2, ... and
@@ -843,14 +945,36 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int tile = tile_at(it);
       uint8_t* wt = w_s + ws * C::kWBytes;
       mbar_wait(&w_full[ws], wph);
+      const uint32_t wt_s = smem_u32(wt);
+      uint4 raw[C::kChunks16];
+      if (p.do_update || conv) {
+#pragma unroll
+        for (int h = 0; h < C::kChunks16; ++h) raw[h] = lds128(wt_s + w_chunk_off<SB>(row, c0, h));
+      }
+      if constexpr (C::kW8) {
+        if (conv) {
+          // e4m3 W_old -> the bf16 grad_X operand tile (exact), same swizzled
+          // layout a bf16 TMA box would have; the MMA warp waits on op_full
+          mbar_wait(op_empty, (static_cast<uint32_t>(it) & 1u) ^ 1u);
+          const uint32_t op = smem_u32(op_s);
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {   // bf16 16-B chunk h = e4m3 elements [8h, 8h + 8)
+            const uint32_t w0 = word_of(raw, 2 * h), w1 = word_of(raw, 2 * h + 1);
+            sts128(op + w_chunk_off<2>(row, c0, h),
+                   make_uint4(e4m3x2_to_bf16x2(static_cast<uint16_t>(w0 & 0xFFFF)),
+                              e4m3x2_to_bf16x2(static_cast<uint16_t>(w0 >> 16)),
+                              e4m3x2_to_bf16x2(static_cast<uint16_t>(w1 & 0xFFFF)),
+                              e4m3x2_to_bf16x2(static_cast<uint16_t>(w1 >> 16))));
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(op_full);
+        }
+      }
       if (p.do_update) {
         const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
-        const uint32_t wt_s = smem_u32(wt);
         const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + c0;
         // --- independent of dW: W_old and random bits, overlapping the MMAs
-        uint4 raw[C::kChunks16];
-#pragma unroll
-        for (int h = 0; h < C::kChunks16; ++h) raw[h] = lds128(wt_s + w_chunk_off<EB>(row, c0, h));
         if constexpr (C::kOutBuf) {
           // W_old is in registers: the slot can be refilled once the MMAs are done too
           __syncwarp();
@@ -878,7 +1002,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t rw[8 * GE];
         if (rounding == ROUND_SR_FAST) sr_words<GE>(pk, flat0, rw, p.sr_bits != 0);
         float w[CE > 0 ? 1 : 32];
-        if constexpr (CE == 0) w_decode<EB>(raw, w);
+        if constexpr (CE == 0) w_decode<SB>(raw, w);
         // --- dW from TMEM, then release the accumulator buffer at once
         mbar_wait(&t_full[ds], dph);
         tc_fence_after();
@@ -895,12 +1019,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         uint4 out[C::kChunks16];
         if constexpr (ADAMW) {
-          w_update_pack_adamw<EB, GE>(p, acc, raw, grow * p.d + j * 128 + c0, grow < p.rows && col_ok, out, pol_w_out);
+          w_update_pack_adamw<SB, GE>(p, acc, raw, grow * p.d + j * 128 + c0, grow < p.rows && col_ok, out, pol_w_out);
         } else if constexpr (CE > 0) {
           uint4* cdst = krow ? reinterpret_cast<uint4*>(p.comp + (grow * p.d + j * 128 + c0) * CE) : nullptr;
-          w_update_pack_kahan<EB, CE, GE>(p, rounding, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
+          w_update_pack_kahan<SB, CE, GE>(p, rounding, acc, raw, rw, flat0, craw, out, cdst, pol_w_out);
         } else {
-          w_update_pack<EB, GE>(p, rounding, acc, w, rw, flat0, out);
+          w_update_pack<SB, GE>(p, rounding, acc, w, rw, flat0, out);
         }
         // W_new into a swizzled smem tile (the staging tile, or in place once
         // the grad_X MMAs have read W_old), then one TMA store per 32-row slab
@@ -912,7 +1036,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         const uint32_t ot_s = smem_u32(ot);
 #pragma unroll
-        for (int h = 0; h < C::kChunks16; ++h) sts128(ot_s + w_chunk_off<EB>(row, c0, h), out[h]);
+        for (int h = 0; h < C::kChunks16; ++h) sts128(ot_s + w_chunk_off<SB>(row, c0, h), out[h]);
         fence_proxy_async_smem();
         // two staging tiles: before this barrier the storer waits until the
         // previous tile's store (the only one outstanding) has read its smem,
@@ -922,7 +1046,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (storer) {
 #pragma unroll
           for (int b = 0; b < C::kWBoxes; ++b)
-            tma_store_2d_hint(&tm_ws, ot + b * C::kBox + q * 32 * 128, j * 128 + b * C::kBoxK, tile * 128 + q * 32,
+            tma_store_2d_hint(&tm_ws, ot + b * C::kBox + q * 32 * 128, j * 128 + b * C::kWBoxK, tile * 128 + q * 32,
                               pol_w_out);
           bulk_commit();
         }
@@ -935,6 +1059,17 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (lane_id() == 0) mbar_arrive(&t_empty[ds]);
         if (C::kOutBuf ? lane_id() == 0 : storer) mbar_arrive(&w_empty[ws]);
       }
+      if (do_gx && (it + 1) % gx_win == 0 && it + 1 < ntl) {
+        // drain a complete accumulation window; the MMA warp restarts the
+        // accumulator after every epilogue warp has read its part
+        const int w = it / gx_win;
+        mbar_wait(gxw_full, static_cast<uint32_t>(w) & 1u);
+        tc_fence_after();
+        gx_drain(w > 0 || p.gx_accumulate != 0);
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(gxw_empty);
+      }
       if (++ws == WS) { ws = 0; wph ^= 1; }
       if (++ds == 2) { ds = 0; dph ^= 1; }
     }
@@ -945,30 +1080,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (do_gx) {
       mbar_wait(gx_full, 0);
       tc_fence_after();
-      // this CTA's slot of the [R][d][gx_ld] partial buffer; chunks of one step
-      // accumulate into it (stream-ordered, one owner per slot: deterministic)
-      const int nchunks = j * 128 + row < p.d ? p.gx_kc_count * C::kBoxK / 32 : 0;   // TMEM lane = d index
-      float* dst = p.gx_ws + (static_cast<int64_t>(r0) * p.d + j * 128 + row) * p.gx_ld + p.gx_kc0 * C::kBoxK;
-#pragma unroll 1
-      for (int cch = quarter; cch < nchunks; cch += 4) {
-        uint32_t r[32];
-        tmem_ld32(tmem_gx + lane_off + cch * 32, r);
-        tmem_ld_wait();
-        float4* o = reinterpret_cast<float4*>(dst + cch * 32);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          float4 v = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
-                                 __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
-          if (p.gx_accumulate) {
-            const float4 old = o[k];
-            v.x += old.x;
-            v.y += old.y;
-            v.z += old.z;
-            v.w += old.w;
-          }
-          o[k] = v;
-        }
-      }
+      gx_drain(ntl > gx_win || p.gx_accumulate != 0);
     }
   }
 

@@ -513,43 +513,6 @@ __global__ void g_quant_kernel(const float* __restrict__ G, int64_t ld, int64_t 
   if (bad) atomicOr(status, ST_NONFINITE_GRAD);
 }
 
-// Reference-precision backward of an e4m3 head: the W chunk as bf16 for the
-// kind::f16 MMAs (exact), and back to e4m3 after the update (exact: the
-// update rounded onto the e4m3 grid).  16 elements per thread-iteration.
-__global__ void w_e4m3_to_bf16_kernel(const uint8_t* __restrict__ w, int64_t n16, uint16_t* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 v = reinterpret_cast<const uint4*>(w)[i];
-    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-    uint32_t o[8];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float2 a = dec_e4m3x2(static_cast<uint16_t>(wv[k] & 0xFFFF));
-      const float2 b = dec_e4m3x2(static_cast<uint16_t>(wv[k] >> 16));
-      o[2 * k] = (__float_as_uint(a.x) >> 16) | (__float_as_uint(a.y) & 0xFFFF0000u);
-      o[2 * k + 1] = (__float_as_uint(b.x) >> 16) | (__float_as_uint(b.y) & 0xFFFF0000u);
-    }
-    uint4* dst = reinterpret_cast<uint4*>(out) + 2 * i;
-    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
-  }
-}
-
-__global__ void w_bf16_to_e4m3_kernel(const uint16_t* __restrict__ w, int64_t n16, uint8_t* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint4* src = reinterpret_cast<const uint4*>(w) + 2 * i;
-    const uint4 a = src[0], b = src[1];
-    const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    uint32_t o[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t p = wv[2 * k], q = wv[2 * k + 1];
-      o[k] = cvt_e4m3x2_rn(__uint_as_float(p & 0xFFFF0000u), __uint_as_float(p << 16)) |
-             (static_cast<uint32_t>(cvt_e4m3x2_rn(__uint_as_float(q & 0xFFFF0000u), __uint_as_float(q << 16))) << 16);
-    }
-    reinterpret_cast<uint4*>(out)[i] = make_uint4(o[0], o[1], o[2], o[3]);
-  }
-}
-
 // ---- keyed weight dropout (head.py:138-161) ---------------------------------
 // keep = u >= p with u = (mix(base + flat * gamma) >> 11) * 2^-53, i.e.
 // (mix(...) >> 11) >= ceil(p * 2^53) exactly.  One thread per 32 consecutive

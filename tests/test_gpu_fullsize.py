@@ -94,12 +94,17 @@ def test_chunk_invariance_and_shard_linearity(setup, precision):
     h1, gx1 = _run(xmc, W0, X, si, li, k=1, rmode="stochastic", impl="hash", precision=precision)
     h2, gx2 = _run(xmc, W0, X, si, li, k=2, rmode="stochastic", impl="hash", precision=precision)
     assert torch.equal(h1.weights.values.view(torch.uint8), h2.weights.values.view(torch.uint8))
-    torch.testing.assert_close(gx1, gx2, rtol=1e-5, atol=1e-4)
+    # grad_X: the chunking changes the fp32 summation order of 2.8M label
+    # contributions (TMEM windows of 32 tiles, then the partial slots); in
+    # reference precision every contribution is the sum of three exact plane
+    # products, so values that cancel to near zero keep a few ulps of max|grad_X|
+    atol = 1e-4 if precision == "operand" else max(1e-4, 2e-6 * float(gx1.abs().max()))
+    torch.testing.assert_close(gx1, gx2, rtol=1e-5, atol=atol)
     del h2
     half = L // 2
     ha, gxa = _run(xmc, W0, X, si, li, k=1, impl="hash", lo=0, hi=half, precision=precision)
     hb, gxb = _run(xmc, W0, X, si, li, k=1, impl="hash", lo=half, hi=L, precision=precision)
-    torch.testing.assert_close(gxa + gxb, gx1, rtol=1e-5, atol=1e-4)
+    torch.testing.assert_close(gxa + gxb, gx1, rtol=1e-5, atol=atol)
     # global-row RNG keys: shard weights equal the single-GPU rows bit for bit
     assert torch.equal(ha.weights.values.view(torch.uint8), h1.weights.values[:half].view(torch.uint8))
     assert torch.equal(hb.weights.values.view(torch.uint8), h1.weights.values[half:].view(torch.uint8))

@@ -15,7 +15,14 @@ KEYS = {
     "dram_read_MB": "dram__bytes_read.sum",
     "dram_write_MB": "dram__bytes_write.sum",
     "dram_pct": "dram__throughput.avg.pct_of_peak_sustained_elapsed",
-    "tensor_pipe_pct": "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    # tensor pipe: sm__pipe_tensor_cycles_active (SM clock domain) is the one that
+    # equals the flop-derived utilisation (flops / (16384 flop/clk/SM fp8 x SMs x
+    # SM clock x duration)); the *_realtime variant counts in another clock domain
+    "tensor_pipe_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+    "tensor_pipe_realtime_pct": "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "dram_TBps": "dram__bytes.sum.per_second",
+    "smem_lsu_wavefronts_pct": "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "inst_executed": "smsp__inst_executed.sum",
     "tensor_mem_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "l2_pct": "lts__throughput.avg.pct_of_peak_sustained_elapsed",
     "l1tex_pct": "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -56,6 +63,8 @@ def summarize(path):
                     v *= 1000.0
                 elif u == "nsecond" and k == "duration_us":
                     v /= 1000.0
+                if k == "dram_TBps":
+                    v = v if u == "Tbyte/s" else (v / 1000.0 if u == "Gbyte/s" else v)
                 if k == "sm_clock_mhz":
                     v = v / 1e6 if u in ("cycle/second", "") else v * (1000.0 if u.startswith("G") else 1.0)
                 d[k] = round(v, 3)
@@ -75,8 +84,22 @@ def summarize(path):
     return out
 
 
+def reconcile(d, flops, per_clk):
+    """flop-derived tensor utilisation next to the ncu metric"""
+    if "duration_us" in d and "sm_clock_mhz" in d:
+        peak = per_clk * 148 * d["sm_clock_mhz"] * 1e6
+        d["algorithmic_flops"] = flops
+        d["flop_derived_tensor_pct"] = round(100.0 * flops / (d["duration_us"] * 1e-6) / peak, 1)
+        d["flop_peak_note"] = f"{per_clk} flop/clk/SM x 148 SMs x {d['sm_clock_mhz']:.0f} MHz"
+
+
 if __name__ == "__main__":
     res = summarize(sys.argv[1])
+    if "--flops" in sys.argv:
+        fl = float(sys.argv[sys.argv.index("--flops") + 1])
+        pc = float(sys.argv[sys.argv.index("--per-clk") + 1]) if "--per-clk" in sys.argv else 16384.0
+        for d in res:
+            reconcile(d, fl, pc)
     if "--json" in sys.argv:
         with open(sys.argv[sys.argv.index("--json") + 1], "w") as f:
             json.dump(res, f, indent=1)
