@@ -396,10 +396,17 @@ def main():
     Xe = torch.empty_like(Xd)
     sie = torch.empty_like(sid)
     lie = torch.empty_like(lid)
+    from paper_2510_11168_b200.parallel import broadcast_batch
+
     def e2e_step(s):
-        Xe.copy_(Xp, non_blocking=True)
-        sie.copy_(sip, non_blocking=True)
-        lie.copy_(lip, non_blocking=True)
+        if world > 1:
+            # rank 0 holds the batch (pinned host X + global positives): H2D
+            # on rank 0, broadcast to every rank (SURVEY 8(e) X broadcast)
+            broadcast_batch(Xp, sip, lip, src=0, out=(Xe, sie, lie))
+        else:
+            Xe.copy_(Xp, non_blocking=True)
+            sie.copy_(sip, non_blocking=True)
+            lie.copy_(lip, non_blocking=True)
         r = step_fn(s, xmc.BatchInput(Xe, sie, lie), gx)
         gxh.copy_(r, non_blocking=True)
         stream.synchronize()

@@ -58,12 +58,29 @@ def merge_topk(vals: torch.Tensor, idx: torch.Tensor, k: int) -> torch.Tensor:
     return torch.gather(i1, 1, o2)[:, :k]
 
 
-def broadcast_batch(X, sample_idx, label_idx, src: int = 0, group=None):
+def broadcast_batch(X, sample_idx, label_idx, src: int = 0, group=None, out=None):
     """X broadcast of SURVEY.md 8(e): rank `src` holds the batch (encoder output
     X, B x d float32, and the positives as GLOBAL label ids); every other rank
     receives it.  Returns (X, sample_idx, label_idx) tensors on every rank, on
-    the device of the process group's backend (CUDA for NCCL)."""
+    the device of the process group's backend (CUDA for NCCL).
+
+    ``out=(X, sample_idx, label_idx)``: preallocated receive tensors (float32,
+    int32, int32) whose shapes every rank already knows, e.g. a training loop
+    with a fixed batch and positive count: rank `src` copies its batch into
+    them (host -> device when the inputs are pinned host tensors) and the
+    shape exchange is skipped."""
     rank = dist.get_rank(group)
+    if out is not None:
+        Xo, so, lo_ = out
+        if rank == src:
+            Xo.copy_(torch.as_tensor(X), non_blocking=True)
+            so.copy_(torch.as_tensor(sample_idx), non_blocking=True)
+            lo_.copy_(torch.as_tensor(label_idx), non_blocking=True)
+        dist.broadcast(Xo, src, group=group)
+        if so.numel():
+            dist.broadcast(so, src, group=group)
+            dist.broadcast(lo_, src, group=group)
+        return Xo, so, lo_
     dev = torch.device("cuda", torch.cuda.current_device()) \
         if dist.get_backend(group) == "nccl" else torch.device("cpu")
     if rank == src:
@@ -187,9 +204,13 @@ class ShardedHead:
             sc = self._scores(X)
             vals, idx = topk_stable(sc, min(k, sc.shape[1]), offset=self.lo)
         if self.world > 1:
+            # gloo gathers host tensors only (the one-GPU test harness)
+            dev = vals.device
+            if dist.get_backend(self.group) != "nccl":
+                vals, idx = vals.cpu(), idx.cpu()
             vs = [torch.empty_like(vals) for _ in range(self.world)]
             ix = [torch.empty_like(idx) for _ in range(self.world)]
             dist.all_gather(vs, vals.contiguous(), group=self.group)
             dist.all_gather(ix, idx.contiguous(), group=self.group)
-            vals, idx = torch.cat(vs, dim=1), torch.cat(ix, dim=1)
+            vals, idx = torch.cat(vs, dim=1).to(dev), torch.cat(ix, dim=1).to(dev)
         return merge_topk(vals, idx, k)

@@ -83,7 +83,13 @@ def _bcast_worker(rank, world, port, out):
         Xb, sib, lib = broadcast_batch(X, si, li)
     else:
         Xb, sib, lib = broadcast_batch(None, None, None)
-    out[rank] = (Xb.numpy(), sib.numpy(), lib.numpy())
+    # preallocated receive buffers (fixed batch shape): no shape exchange
+    bufs = (torch.empty(X.shape, dtype=torch.float32), torch.empty(len(si), dtype=torch.int32),
+            torch.empty(len(li), dtype=torch.int32))
+    src = (torch.from_numpy(X), torch.from_numpy(si.astype(np.int32)), torch.from_numpy(li.astype(np.int32)))
+    Xo, sio, lio = broadcast_batch(*(src if rank == 1 else (None, None, None)), src=1, out=bufs)
+    assert Xo is bufs[0]
+    out[rank] = (Xb.numpy(), sib.numpy(), lib.numpy(), Xo.numpy(), sio.numpy(), lio.numpy())
     dist.destroy_process_group()
 
 
@@ -96,8 +102,9 @@ def test_broadcast_batch():
     mp.spawn(_bcast_worker, args=(world, port, out), nprocs=world, join=True)
     L, W, X, si, li = _problem()
     for r in range(world):
-        Xb, sib, lib = out[r]
+        Xb, sib, lib, Xo, sio, lio = out[r]
         assert np.array_equal(Xb, X) and np.array_equal(sib, si) and np.array_equal(lib, li)
+        assert np.array_equal(Xo, X) and np.array_equal(sio, si) and np.array_equal(lio, li)
 
 
 def test_sharded_step_matches_single_process():

@@ -23,7 +23,8 @@ L, D, B = 2_812_281, 768, 256
 lo, hi = xmc.partition(L, world)[0]
 dev = torch.device("cuda")
 W = xmc.cast_native(torch.randn((hi - lo, D), device=dev) * 0.02, xmc.E4M3)
-head = xmc.ChunkedHead(xmc.QuantizedMatrix(W, xmc.E4M3), num_chunks=k, num_labels_global=L, label_offset=lo)
+head = xmc.ChunkedHead(xmc.QuantizedMatrix(W, xmc.E4M3), num_chunks=k, num_labels_global=L, label_offset=lo,
+                       precision="operand")
 si, li = synthetic_positives(L, B, mean, seed=1)
 X = torch.randn((B, D), device=dev)
 batch = xmc.BatchInput(X, torch.from_numpy(si.astype(np.int32)).to(dev), torch.from_numpy(li.astype(np.int32)).to(dev))
