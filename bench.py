@@ -93,35 +93,56 @@ def synthetic_positives(num_labels, batch, mean_labels, seed=0):
 
 class ClockSampler:
     """SM clocks / clock-event (throttle) reasons sampled DURING the timed
-    region: NVML polled every ~2 ms from a thread (the timed region is tens of
-    ms), nvidia-smi -lms 100 as the fallback when NVML is unavailable."""
+    region by a separate process polling NVML every ~1 ms (a thread of this
+    process would share the GIL with the launch loop and get a sample or two
+    in a tens-of-ms region); nvidia-smi -lms 100 as the fallback."""
 
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    POLL = r"""
+import sys, time, pynvml as nv
+nv.nvmlInit()
+h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+print("max", nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM), flush=True)
+out = []
+import select
+while True:
+    r, _, _ = select.select([sys.stdin], [], [], 0.001)
+    if r:
+        break
+    try:
+        out.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                    nv.nvmlDeviceGetCurrentClocksEventReasons(h),
+                    nv.nvmlDeviceGetPowerUsage(h) / 1000.0))
+    except Exception:
+        pass
+for s in out:
+    print(*s)
+"""
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.nvml = None
         self.lines = []
-        self.samples = []
-        self.stop_evt = threading.Event()
 
     def start(self):
         try:
-            import pynvml
-            pynvml.nvmlInit()
-            self.nvml = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-            self.t = threading.Thread(target=self._poll, daemon=True)
-            self.t.start()
-            return
+            import pynvml  # noqa: F401  (the poller needs it)
+            self.proc = subprocess.Popen([sys.executable, "-c", self.POLL, str(self.index)], stdin=subprocess.PIPE,
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            first = self.proc.stdout.readline().split()
+            if len(first) == 2 and first[0] == "max":
+                self.nvml = True
+                self.smax = int(first[1])
+                return
+            self.proc.kill()
         except Exception:
-            self.nvml = None
+            pass
+        self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -131,32 +152,25 @@ class ClockSampler:
         except FileNotFoundError:
             self.proc = None
 
-    def _poll(self):
-        nv = self.nvml
-        while not self.stop_evt.is_set():
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
-                self.samples.append((sm, rs, pw))
-            except Exception:
-                pass
-            time.sleep(0.002)
-
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
         if self.nvml is not None:
-            self.stop_evt.set()
-            self.t.join(timeout=5)
-            sm = [s[0] for s in self.samples]
-            reasons = sorted({n for _, rs, _ in self.samples for n, bit in self.REASONS.items() if rs & bit})
-            pw = [s[2] for s in self.samples]
+            out, _ = self.proc.communicate(input="stop\n", timeout=30)
+            samples = []
+            for ln in out.splitlines():
+                f = ln.split()
+                if len(f) == 3:
+                    samples.append((int(f[0]), int(f[1]), float(f[2])))
+            sm = [s[0] for s in samples]
+            reasons = sorted({n for _, rs, _ in samples for n, bit in self.REASONS.items() if rs & bit})
+            pw = [s[2] for s in samples]
             return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
                     "sm_max_mhz": self.smax, "reasons": reasons, "samples": len(sm),
-                    "power_w_median": statistics.median(pw) if pw else None, "source": "nvml 2 ms poll"}
+                    "power_w_median": statistics.median(pw) if pw else None,
+                    "power_w_max": max(pw) if pw else None, "source": "nvml ~1 ms poll (separate process)"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -184,6 +198,14 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- peaks
+
+def fp8_gemm_peak():
+    path = os.path.join(ROOT, "profiles", "fp8_peak.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f).get("tflops")
+    return None
+
 
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -362,6 +384,7 @@ def main():
     stream = torch.cuda.current_stream()
     clocks = ClockSampler(local)
     _lib.profile_read()
+    _lib.profile_clock()
     _lib.profile_enable(True)
     if world > 1:
         dist.barrier()
@@ -380,6 +403,10 @@ def main():
     clk = clocks.stop()
     _lib.profile_enable(False)
     ms_fwd, n_fwd, ms_bwd, n_bwd = _lib.profile_read()
+    # effective SM clock inside the kernels (block 0's clock64 / globaltimer):
+    # NVML's clock reading lags; the heavy kernels run power-limited below it
+    kclk = _lib.profile_clock()
+    clk["kernel_mhz"] = {k: (round(v, 1) if v else None) for k, v in kclk.items()}
     t_ms = ev0.elapsed_time(ev1)
     t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -489,11 +516,13 @@ def main():
     # region.  This is the hardware ceiling (4.77 PF fp8 at 1965 MHz, 4.4-4.5 PF
     # at the ~1.84 GHz a dense MMA loop holds); cuBLAS-class library GEMMs reach
     # less (torch._scaled_mm 8192^3: 3.1 PF, profiles/fp8_peak.json).
-    sm_mhz = clk.get("sm_mhz") or smax
+    # the clock the dominant kernel actually ran at (in-kernel clock64 /
+    # globaltimer), else NVML's reading
+    sm_mhz = (clk.get("kernel_mhz") or {}).get(dom) or clk.get("sm_mhz") or smax
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
     tc_peak = (16384.0 if eb == 1 else 8192.0) * n_sms * sm_mhz * 1e6 / 1e12
     tc_src = (f"tensor pipe {'16384' if eb == 1 else '8192'} flop/clk/SM (probe_mma) x {n_sms} SMs x "
-              f"{sm_mhz:.0f} MHz observed ({regime})")
+              f"{sm_mhz:.0f} MHz in-kernel clock ({regime})")
     t_tc = flops / (tc_peak * 1e12)
     t_hbm = bytes_ / (peaks["hbm_gbs"] * 1e9)
     bound = "tensor" if t_tc >= t_hbm else "hbm"
@@ -537,6 +566,12 @@ def main():
            "grad_x_allreduce": gx_allreduce[0],
            "reference_precision": ref_prec,
            "step_tflops": step_flops / (ms_step * 1e-3) / 1e12,
+           # against dense FP8 at B200's nominal 4.5 PF and the measured
+           # torch._scaled_mm FP8 GEMM (profiles/fp8_peak.json, burst)
+           "step_frac_of_nominal_fp8": (step_flops / (ms_step * 1e-3) / 1e12 / (4500.0 * world)
+                                        if eb == 1 else None),
+           "step_frac_of_measured_fp8_gemm": (step_flops / (ms_step * 1e-3) / 1e12 / (fp8_gemm_peak() * world)
+                                              if eb == 1 and fp8_gemm_peak() else None),
            "step_frac_of_tc_peak": step_flops / (ms_step * 1e-3) / 1e12 / (tc_peak * world),
            "peak_hbm_gib_per_gpu": peak_mem / 2**30,
            # our kernels in the timed region: every fwd / bwd launch (counted by the

@@ -279,6 +279,10 @@ xmc_status xmc_head_attach_peers(xmc_head_t h, xmc_peer_t p);
  * and launch counts since the previous read, and clears the record. */
 xmc_status xmc_profile_enable(int32_t on);
 xmc_status xmc_profile_read(double* ms_fwd, int64_t* n_fwd, double* ms_bwd, int64_t* n_bwd);
+/* Effective SM clock of the same kernels: block 0 of every fwd / bwd launch
+ * adds its clock64 cycles and globaltimer ns; out4 = {fwd cycles, fwd ns,
+ * bwd cycles, bwd ns} since the previous read (cleared; synchronises). */
+xmc_status xmc_profile_clock(uint64_t* out4);
 
 #ifdef __cplusplus
 }

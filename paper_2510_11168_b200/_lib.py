@@ -93,6 +93,7 @@ _SIGNATURES = {
     "xmc_profile_enable": ([_I32], _I32),
     "xmc_profile_read": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
                           ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64)], _I32),
+    "xmc_profile_clock": ([ctypes.POINTER(ctypes.c_uint64)], _I32),
 }
 
 
@@ -106,6 +107,18 @@ def profile_read():
     na, nb = _I64(), _I64()
     load().xmc_profile_read(ctypes.byref(a), ctypes.byref(na), ctypes.byref(b), ctypes.byref(nb))
     return a.value, na.value, b.value, nb.value
+
+
+
+def profile_clock():
+    """-> {"fwd": MHz or None, "bwd": MHz or None}: effective SM clock of the
+    fwd / bwd launches since the previous read (block 0's clock64 / globaltimer)."""
+    out = (ctypes.c_uint64 * 4)()
+    check(load().xmc_profile_clock(out))
+    res = {}
+    for k, i in (("fwd", 0), ("bwd", 2)):
+        res[k] = out[i] / out[i + 1] * 1e3 if out[i + 1] else None
+    return res
 
 _lib = None
 

@@ -195,6 +195,19 @@ extern "C" xmc_status xmc_profile_read(double* ms_fwd, int64_t* n_fwd, double* m
   return XMC_OK;
 }
 
+// Effective SM clock of the fwd / bwd kernels since the last read: summed
+// clock64 cycles and globaltimer ns of block 0 per kind (out[0..3] = fwd
+// cycles, fwd ns, bwd cycles, bwd ns).  Synchronises the device.
+extern "C" xmc_status xmc_profile_clock(uint64_t* out4) {
+  unsigned long long h[4] = {0, 0, 0, 0};
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  if (cudaMemcpyFromSymbol(h, g_xmc_clk, sizeof(h)) != cudaSuccess ||
+      cudaMemcpyToSymbol(g_xmc_clk, z, sizeof(z)) != cudaSuccess)
+    return fail(XMC_ERR_CUDA, "xmc_profile_clock: %s", cudaGetErrorString(cudaGetLastError()));
+  for (int i = 0; i < 4; ++i) out4[i] = h[i];
+  return XMC_OK;
+}
+
 // ============================================================== helpers
 
 static int elem_bytes(int fmt) { return fmt == XMC_FMT_E4M3 || fmt == XMC_FMT_E5M2 ? 1 : (fmt == XMC_FMT_FP32 ? 4 : 2); }

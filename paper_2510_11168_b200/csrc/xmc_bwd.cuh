@@ -519,6 +519,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // previous kernel's tail; from here on its outputs are read
   griddep_wait();
   griddep_launch_dependents();
+  ClkSpan clk;
+  clk.begin();
   // a latched error of an earlier kernel of the step turns this one into a
   // no-op; read once so every role of the CTA agrees
   if (threadIdx.x == 0) *status_s = *p.status;
@@ -558,7 +560,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (whole) {
         for (int i = 0; i < nk; ++i) mbar_wait(&k_empty[ks + i], kph ^ 1);
         if (lane == 0) {
+#ifdef XMC_WHATIF_NO_WLOAD
+          mbar_arrive_expect_tx(&w_full[ws], 0);
+#else
           mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
+#endif
           for (int i = 0; i < nk; ++i) mbar_arrive_expect_tx(&k_full[ks + i], kslot_bytes);
         }
         __syncwarp();
@@ -567,7 +573,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int gl = lane - C::kWBoxes;
         const int i = gl / kGB, sub = gl % kGB;
         const bool is_w = lane < C::kWBoxes;
+#ifdef XMC_WHATIF_NO_WLOAD
+        const bool active = !is_w && (gl >= 0 && i < nk);
+#else
         const bool active = is_w || (gl >= 0 && i < nk);
+#endif
         const CUtensorMap* m = is_w ? &tm_w : (sub == 0 ? &tm_g : &tm_xt);
         uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + (ks + i) * C::kKSlot + sub * C::kBox;
         uint64_t* bar = is_w ? &w_full[ws] : &k_full[ks + i];
@@ -666,7 +676,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           __syncwarp();
         }
         if (elect_one()) {
+#ifdef XMC_WHATIF_NO_GX
+          if (false) {
+#else
           if (do_gx) {
+#endif
             const uint64_t wa = dWt + ((static_cast<uint32_t>(ws) * C::kWBytes) >> 4);
             const uint64_t gb = dGt + ((static_cast<uint32_t>(ks) * C::kKSlot) >> 4);
 #pragma unroll
@@ -860,10 +874,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint4 raw[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) raw[h] = lds128(wt_s + w_chunk_off<EB>(row, cw0 + (h >> 1) * 32, h & 1));
+#ifdef XMC_WHATIF_NO_WLOAD
+        for (int h = 0; h < 4; ++h) raw[h] = make_uint4(raw[h].x & 0x3F3F3F3Fu, raw[h].y & 0x3F3F3F3Fu, raw[h].z & 0x3F3F3F3Fu, raw[h].w & 0x3F3F3F3Fu);
+#endif
         // W_old is in registers: the slot can be refilled once the MMAs are done too
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&w_empty[wsi]);
         auto prep = [&](int cg, uint32_t (&rw)[8], float (&wc)[32]) {
+#ifdef XMC_WHATIF_NO_EPI_MATH
+          for (int k = 0; k < 8; ++k) rw[k] = word_of(raw, 4 * cg + (k & 3)) ^ k;
+          for (int k = 0; k < 32; ++k) wc[k] = 0.f;
+          return;
+#endif
           sr_words<1>(pk, flat0 + cg * 32, rw, p.sr_bits != 0);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -888,6 +910,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // updated = w (1 - lr wd) - lr dW, one SR rounding onto e4m3 (cvt.rs)
         auto finish = [&](int cg, const uint32_t (&acc)[32], const uint32_t (&rw)[8], const float (&wc)[32]) {
           uint32_t pk8[8];
+#ifdef XMC_WHATIF_NO_EPI_MATH
+          for (int k = 0; k < 8; ++k) pk8[k] = (acc[4 * k] ^ rw[k]) & 0x3F3F3F3Fu;
+          if (false)
+#endif
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             float u[4];
@@ -933,7 +959,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         fence_proxy_async_smem();
         named_bar_sync(1 + q + 4 * g, 64);
+#ifdef XMC_WHATIF_NO_WSTORE
+        if (false) {
+#else
         if (gstorer) {
+#endif
           tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
           bulk_commit();
           stored = true;
@@ -1086,6 +1116,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  clk.end(1);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);

@@ -189,6 +189,31 @@ XMC_DEV uint64_t policy_evict_last() {
 // ------------------------------------------------- programmatic dependent launch
 // wait until the previous grid in the stream completed and its writes are
 // visible (no-op when the kernel was not launched as a dependent)
+// Effective SM clock of the heavy kernels (measurement only): thread 0 of
+// block 0 adds its clock64 / globaltimer span to [2 kind] / [2 kind + 1]
+// (kind 0 fwd, 1 bwd); xmc_profile_clock reads and clears the sums.
+static __device__ unsigned long long g_xmc_clk[4];
+XMC_DEV uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct ClkSpan {
+  uint64_t c0 = 0, t0 = 0;
+  XMC_DEV void begin() {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      c0 = clock64();
+      t0 = globaltimer_ns();
+    }
+  }
+  XMC_DEV void end(int kind) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      atomicAdd(&g_xmc_clk[2 * kind], static_cast<unsigned long long>(clock64() - c0));
+      atomicAdd(&g_xmc_clk[2 * kind + 1], static_cast<unsigned long long>(globaltimer_ns() - t0));
+    }
+  }
+};
+
 XMC_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // let the next grid in the stream launch (its CTAs take SMs as ours exit)
 XMC_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
