@@ -946,8 +946,8 @@ template <int EB, int XTB>
 static void launch_prep(xmc_head* h, const float* X, int Bp, const PosGeom& g, const int32_t* ps, const int32_t* pl,
                         int64_t nnz, int B, int32_t T, cudaStream_t st) {
   const int D = h->desc.dim;
-  if (nnz <= 2048) {
-    // tiny batches: one launch (block 0 buckets in shared memory, the rest prepare Xq)
+  if (nnz <= kPosOneCta) {
+    // up to 12k positives: one launch (block 0 buckets in shared memory, the rest prepare Xq)
     smem_attr_once<prep_bucket_kernel<EB, XTB>>(kPosMaxTiles * 4);
     const int nblk = 1 + (D / 32) * (Bp / 32);
     prep_bucket_kernel<EB, XTB><<<nblk, 1024, T * 4, st>>>(X, B, Bp, D, h->xq, h->xqt, g, ps, pl, nnz, T, h->tile_ptr,
