@@ -946,7 +946,7 @@ template <int EB, int XTB>
 static void launch_prep(xmc_head* h, const float* X, int Bp, const PosGeom& g, const int32_t* ps, const int32_t* pl,
                         int64_t nnz, int B, int32_t T, cudaStream_t st) {
   const int D = h->desc.dim;
-  if (nnz <= kPosOneCta) {
+  if (nnz <= kPosOneCta && T <= kPosMaxTiles && h->chunks.size() <= 64) {
     // up to 12k positives: one launch (block 0 buckets in shared memory, the rest prepare Xq)
     smem_attr_once<prep_bucket_kernel<EB, XTB>>(kPosMaxTiles * 4);
     const int nblk = 1 + (D / 32) * (Bp / 32);
@@ -959,7 +959,7 @@ static void launch_prep(xmc_head* h, const float* X, int Bp, const PosGeom& g, c
   prep_count_kernel<EB, XTB><<<nx + blocks, 256, 0, st>>>(X, B, Bp, D, h->xq, h->xqt, nx, g, ps, pl, nnz,
                                                          h->tile_cnt, h->tmp_tile, h->tmp_entry, h->status);
   smem_attr_once<pos_scan_kernel>(kPosMaxTiles * 4);
-  pos_scan_kernel<<<1, 1024, T * 4, st>>>(h->tile_cnt, h->tile_ptr, h->tile_cur, T);
+  pos_scan_kernel<<<1, 1024, T <= kPosMaxTiles ? T * 4 : 0, st>>>(h->tile_cnt, h->tile_ptr, h->tile_cur, T);
   pos_scatter_kernel<<<blocks, 256, 0, st>>>(nnz, h->tmp_tile, h->tmp_entry, h->tile_cur, h->entries);
 }
 
@@ -971,9 +971,6 @@ static xmc_status prepare_step(xmc_head* h, const float* X, int Bp, const int32_
   PosGeom g{h->chunk_dev, h->chunk_dev + h->chunks.size() + 1, static_cast<int32_t>(h->chunks.size()),
             h->desc.label_offset, h->desc.num_labels_local, B};
   const int32_t T = static_cast<int32_t>(h->total_tiles);
-  if (T > kPosMaxTiles || h->chunks.size() > 64)
-    return fail(XMC_ERR_UNSUPPORTED, "%d label tiles per rank exceed the bucketing capacity %d; use more ranks", T,
-                kPosMaxTiles);
   if (h->eb == 1 && h->beb == 2) launch_prep<1, 2>(h, X, Bp, g, ps, pl, nnz, B, T, st);
   else if (h->eb == 1) launch_prep<1, 1>(h, X, Bp, g, ps, pl, nnz, B, T, st);
   else launch_prep<2, 2>(h, X, Bp, g, ps, pl, nnz, B, T, st);

@@ -273,13 +273,18 @@ __global__ void __launch_bounds__(256) prep_count_kernel(const float* __restrict
   pos_count_body(g, ps, pl, nnz, cnt, tmp_tile, tmp_entry, status, blockIdx.x - nx);
 }
 
-// K2: exclusive scan of the T tile counters (one CTA; smem-staged segments)
+// K2: exclusive scan of the T tile counters (one CTA; a contiguous segment
+// per thread, staged in shared memory when T fits, else straight from global)
+constexpr int kPosMaxTiles = 48 * 1024;
 __global__ void __launch_bounds__(1024) pos_scan_kernel(int32_t* __restrict__ cnt, int32_t* __restrict__ ptr,
                                                         int32_t* __restrict__ cur, int32_t T) {
-  extern __shared__ int32_t sc[];   // [T]
+  extern __shared__ int32_t sc_smem[];   // [T] when T <= kPosMaxTiles
   __shared__ int32_t wsum[32];
+  const bool staged = T <= kPosMaxTiles;
+  int32_t* sc = staged ? sc_smem : cnt;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, w = tid >> 5;
-  for (int i = tid; i < T; i += nth) sc[i] = cnt[i];
+  if (staged)
+    for (int i = tid; i < T; i += nth) sc[i] = cnt[i];
   __syncthreads();
   const int per = (T + nth - 1) / nth;
   const int a = min(T, tid * per), b = min(T, a + per);
@@ -306,14 +311,16 @@ __global__ void __launch_bounds__(1024) pos_scan_kernel(int32_t* __restrict__ cn
   int32_t pre = (w > 0 ? wsum[w - 1] : 0) + x - run;
   for (int i = a; i < b; ++i) {
     const int32_t c = sc[i];
-    sc[i] = pre;
+    if (staged) sc[i] = pre;
+    else ptr[i] = pre;
     pre += c;
   }
   if (tid == nth - 1) ptr[T] = pre;
   __syncthreads();
   for (int i = tid; i < T; i += nth) {
-    ptr[i] = sc[i];
-    cur[i] = sc[i];   // the scatter cursor
+    const int32_t v = staged ? sc[i] : ptr[i];
+    if (staged) ptr[i] = v;
+    cur[i] = v;       // the scatter cursor
     cnt[i] = 0;       // counters start the next step at zero (no memset launch)
   }
 }
@@ -347,7 +354,6 @@ __global__ void __launch_bounds__(256) pos_scatter_kernel(int64_t nnz, const uin
 // (The earlier version warp-sorted every round of tile ids for run-aggregated
 // atomics and re-read the positives for the scatter: 23 us per call at
 // L = 351,536 under ncu, latency- and instruction-cache-bound.)
-constexpr int kPosMaxTiles = 48 * 1024;
 constexpr int kPosPer = 12;
 constexpr int kPosOneCta = kPosPer * 1024;
 __device__ __forceinline__ void pos_bucket_body(PosGeom g, const int32_t* __restrict__ ps,

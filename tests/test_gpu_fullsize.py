@@ -127,3 +127,41 @@ def test_fused_topk_full_size(setup):
     from paper_2510_11168_b200.parallel import merge_topk
     ref = merge_topk(torch.cat(cand_v, 1), torch.cat(cand_l, 1), 5)
     assert torch.equal(labs, ref)
+
+
+def test_more_label_tiles_than_shared_memory_counters():
+    """A rank with more than 48k label tiles (> 6.3M labels; the bucketing
+    scan then runs from global memory) and more than 12k positives (the
+    multi-CTA bucketing path): rows [hi - 100k, hi) must equal, bit for bit,
+    the same rows updated by a small shard (single-CTA bucketing), and the
+    positives near the end of the label range must be applied."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_11168_b200 as xmc
+    Lb, lo_s = 6_500_000, 6_400_000
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    W0 = torch.empty((Lb, D), dtype=torch.float8_e4m3fn, device="cuda")
+    for r0 in range(0, Lb, 524_288):
+        r1 = min(Lb, r0 + 524_288)
+        W0[r0:r1] = xmc.cast_native(torch.randn((r1 - r0, D), generator=g, device="cuda") * 0.02, xmc.E4M3)
+    rs = np.random.default_rng(13)
+    X = rs.normal(size=(B, D)).astype(np.float32)
+    si, li = O.synthetic_positives(Lb, B, 60.0, seed=14)
+    # plus 40 positives per sample inside the compared shard
+    si2 = np.repeat(np.arange(B, dtype=np.int64), 40)
+    li2 = rs.integers(lo_s, Lb, size=si2.size)
+    si, li = np.concatenate([si, si2]), np.concatenate([li, li2])
+    assert si.size > 12_288
+    cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=xmc.E4M3, rounding="stochastic", sr_impl="splitmix64")
+    full = xmc.ChunkedHead(xmc.QuantizedMatrix(W0.clone(), xmc.E4M3), num_chunks=5)
+    xmc.head_update(full, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(11), 0)
+    # the shard run sees the same global labels (out-of-shard ones are skipped)
+    head = xmc.ChunkedHead(xmc.QuantizedMatrix(W0[lo_s:].clone(), xmc.E4M3), num_chunks=1,
+                           num_labels_global=Lb, label_offset=lo_s)
+    xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(11), 0)
+    a = full.weights.values[lo_s:].view(torch.uint8)
+    b_ = head.weights.values.view(torch.uint8)
+    assert torch.equal(a, b_), f"{int((a != b_).sum())} bytes differ"
+    # the positives moved their rows (sigma - 1 < 0 pushes W up along X)
+    assert not torch.equal(a, W0[lo_s:].view(torch.uint8))
