@@ -214,8 +214,10 @@ static int elem_bytes(int fmt) { return fmt == XMC_FMT_E4M3 || fmt == XMC_FMT_E5
 
 // padded batch = N of the logits MMA = G leading dimension
 static int padded_batch(int eb, int B) {
-  const int opts1[] = {128, 256};
-  const int opts2[] = {64, 128, 256, 512};
+  // > 256: the forward runs 256-sample passes, the backward grad_X passes of
+  // 256 TMEM columns (the update rides on the last); up to 1024 samples
+  const int opts1[] = {128, 256, 512, 1024};
+  const int opts2[] = {64, 128, 256, 512, 1024};
   if (eb == 1) {
     for (int o : opts1) if (B <= o) return o;
   } else {
@@ -332,6 +334,9 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   const int bp = padded_batch(eb, d->max_batch);
   if (bp < 0) return fail(XMC_ERR_UNSUPPORTED, "batch %d too large for format", d->max_batch);
   const bool ref = d->precision == XMC_PRECISION_REFERENCE;
+  if (ref && eb == 1 && bp > 256)
+    return fail(XMC_ERR_UNSUPPORTED, "reference precision of an e4m3 head supports batch <= 256 (got %d)",
+                d->max_batch);
   const int planes = ref ? 3 : 1;
   const int beb = ref ? 2 : eb;
   auto ch = partition(d->num_labels_local, d->num_chunks);
@@ -486,7 +491,7 @@ extern "C" xmc_status xmc_peer_create(int32_t rank, int32_t world, int32_t dim, 
   if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
     return fail(XMC_ERR_ARG, "rank %d / world %d outside [0, %d)", rank, world, kMaxPeers);
   if (dim <= 0 || dim % 32 != 0) return fail(XMC_ERR_SHAPE, "dim must be a positive multiple of 32");
-  if (max_batch < 1 || max_batch > 512) return fail(XMC_ERR_ARG, "max_batch outside [1, 512]");
+  if (max_batch < 1 || max_batch > 1024) return fail(XMC_ERR_ARG, "max_batch outside [1, 1024]");
   auto* p = new xmc_peer();
   p->rank = rank;
   p->world = world;
@@ -697,8 +702,8 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t rows, int B, in
   p.status = h->status;
   CUtensorMap tw;
   XMC_TRY(make_map(&tw, W, eb, D, rows, D, 128));
-  // batch 512 (bf16) runs as two 256-sample passes of the pair kernel
-  const int pass_n = Bp == 512 ? 256 : Bp;
+  // batches over 256 run as 256-sample passes of the pair kernel
+  const int pass_n = Bp > 256 ? 256 : Bp;
   for (int pass = 0; pass * pass_n < B || pass == 0; ++pass) {
     FwdParams q = p;
     q.sample0 = pass * pass_n;
@@ -713,7 +718,7 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t rows, int B, in
     else if (h->gout == G_E5M2) s = launch_fwd_g<G_E5M2>(h, pass_n, tw, tx, q, st);
     else s = launch_fwd_g<G_REF>(h, pass_n, tw, tx, q, st);
     XMC_TRY(s);
-    if (Bp != 512) break;
+    if (Bp <= 256) break;
   }
   return XMC_OK;
 }
@@ -816,7 +821,8 @@ static xmc_status launch_bwd_v(xmc_head* h, const BwdLaunch& L, cudaStream_t st)
   const int ce = p.comp ? h->desc.comp_bytes : 0;
   if (ce == 2) return launch_bwd_k<EB, XR, KC, 2, false, false, GE, SB>(h, L, st);
   if (ce == 4) return launch_bwd_k<EB, XR, KC, 4, false, false, GE, SB>(h, L, st);
-  if constexpr (EB == 1 && GE == 1)
+  // the FAST instantiation keeps Xq^T resident and whole tiles in the G ring
+  if constexpr (EB == 1 && GE == 1 && XR && BwdCfg<EB, XR, KC, SB>::kKStages % KC == 0)
     if (p.do_update && p.rounding == ROUND_SR_FAST && p.keep == nullptr)
       return launch_bwd_k<1, XR, KC, 0, true, false, 1, 1>(h, L, st);
   return launch_bwd_k<EB, XR, KC, 0, false, false, GE, SB>(h, L, st);
@@ -839,11 +845,14 @@ static xmc_status launch_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, in
   } else if (h->eb == 1) {
     if (Bp == 128) s = launch_bwd_v<1, true, 1, 1>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<1, true, 2, 1>(h, L, st);
+    else if (Bp == 512) s = launch_bwd_v<1, true, 4, 1>(h, L, st);
+    else if (Bp == 1024) s = launch_bwd_v<1, false, 8, 1>(h, L, st);
   } else {
     if (Bp == 64) s = launch_bwd_v<2, true, 1, 2>(h, L, st);
     else if (Bp == 128) s = launch_bwd_v<2, true, 2, 2>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<2, true, 4, 2>(h, L, st);
     else if (Bp == 512) s = launch_bwd_v<2, false, 8, 2>(h, L, st);
+    else if (Bp == 1024) s = launch_bwd_v<2, false, 16, 2>(h, L, st);
   }
   if (s == XMC_ERR_UNSUPPORTED) return fail(s, "no backward kernel for padded batch %d", Bp);
   XMC_TRY(s);

@@ -112,7 +112,9 @@ struct BwdCfg {
   static constexpr int kWStages = kW8 ? (KCMAX > 2 ? 2 : 4) : (EB == 1 ? 4 : 3);
   static constexpr int kOutBytes = kOutTiles * kWBytes;
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
-  static constexpr int kKStages = EB == 1 ? 6 : 4;
+  // e4m3: 6 G slots (3 tiles at batch 256); batch 512 / 1024 (4 / 8 k-chunks
+  // per tile) 4 slots to stay within the 227 KB
+  static constexpr int kKStages = EB == 1 ? (KCMAX > 2 ? 4 : 6) : 4;
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
   static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2 + 2 + 2) + 16;
   static constexpr int kSmemBytes =
@@ -519,8 +521,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // previous kernel's tail; from here on its outputs are read
   griddep_wait();
   griddep_launch_dependents();
-  ClkSpan clk;
-  clk.begin();
+  ClkSpan::begin(1);
   // a latched error of an earlier kernel of the step turns this one into a
   // no-op; read once so every role of the CTA agrees
   if (threadIdx.x == 0) *status_s = *p.status;
@@ -1116,7 +1117,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  clk.end(1);
+  ClkSpan::end(1);
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem_base);

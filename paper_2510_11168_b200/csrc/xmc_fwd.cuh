@@ -179,8 +179,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
   // previous kernel's tail; from here on its outputs are read
   griddep_wait();
   griddep_launch_dependents();
-  ClkSpan clk;
-  clk.begin();
+  ClkSpan::begin(0);
   // A latched error of an earlier kernel of the step turns this one into a
   // no-op.  The status word is read ONCE (by the pair leader) and every warp of
   // both CTAs takes that value: the kernel itself may latch an error later, and
@@ -608,7 +607,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
   tc_fence_before();
   if constexpr (PAIR) cluster_sync();
   else __syncthreads();
-  clk.end(0);
+  ClkSpan::end(0);
   if (warp == 1) {
     tc_fence_after();
     if constexpr (PAIR) tmem_dealloc_2sm<C::kTmemCols>(tmem_base);

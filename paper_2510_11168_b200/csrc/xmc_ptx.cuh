@@ -198,18 +198,19 @@ XMC_DEV uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// begin() subtracts the start stamps, end() adds the end stamps (mod 2^64),
+// so nothing stays live in registers across the kernel
 struct ClkSpan {
-  uint64_t c0 = 0, t0 = 0;
-  XMC_DEV void begin() {
+  XMC_DEV static void begin(int kind) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      c0 = clock64();
-      t0 = globaltimer_ns();
+      atomicAdd(&g_xmc_clk[2 * kind], 0ull - static_cast<unsigned long long>(clock64()));
+      atomicAdd(&g_xmc_clk[2 * kind + 1], 0ull - static_cast<unsigned long long>(globaltimer_ns()));
     }
   }
-  XMC_DEV void end(int kind) {
+  XMC_DEV static void end(int kind) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      atomicAdd(&g_xmc_clk[2 * kind], static_cast<unsigned long long>(clock64() - c0));
-      atomicAdd(&g_xmc_clk[2 * kind + 1], static_cast<unsigned long long>(globaltimer_ns() - t0));
+      atomicAdd(&g_xmc_clk[2 * kind], static_cast<unsigned long long>(clock64()));
+      atomicAdd(&g_xmc_clk[2 * kind + 1], static_cast<unsigned long long>(globaltimer_ns()));
     }
   }
 };
