@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--rounding", default="stochastic")
     ap.add_argument("--sr-impl", default="hash", choices=["hash", "philox", "splitmix64"])
     ap.add_argument("--precision", default="operand", choices=["operand", "reference"])
-    ap.add_argument("--g-format", default="e5m2", choices=["e5m2", "e4m3"])
+    ap.add_argument("--g-format", default="e5m2", choices=["e5m2", "e4m3", "bf16"])
     ap.add_argument("--ref-steps", type=int, default=5,
                     help="timed steps of the reference-precision mode reported beside the headline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=10)

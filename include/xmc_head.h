@@ -73,8 +73,10 @@ typedef struct {
                                 PAPER.md:795); <= 0 = every label.  The comp buffer then holds the
                                 shard's rows [0, clamp(comp_labels - label_offset, 0, local)). */
   int32_t g_format;          /* XMC_PRECISION_OPERAND only: the G operand format of an e4m3 head,
-                                XMC_FMT_E5M2 (e5m2(2^8 g), the default for 0) or XMC_FMT_E4M3
-                                (e4m3(2^8 g)); ignored for a bf16 head (always bf16(g)) */
+                                XMC_FMT_E5M2 (e5m2(2^8 g), the default for 0), XMC_FMT_E4M3
+                                (e4m3(2^8 g)) or XMC_FMT_BF16 (bf16(g): FP8 weights with BF16 logit
+                                gradients as in the paper; e4m3 W tiles become bf16 operands in
+                                shared memory, batch <= 256); ignored for a bf16 head (always bf16(g)) */
   int32_t reserved;
 } xmc_head_desc;
 

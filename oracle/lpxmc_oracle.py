@@ -514,11 +514,14 @@ def quantize_g_operand(G, fmt, g_format="e5m2"):
     """The GPU's operand-precision mode (ChunkedHead(precision="operand"))
     consumes G in the backward tensor-core operand format: an e4m3 head uses
     e5m2(G * 2^8) * 2^-8 (g_format "e5m2", the default) or e4m3(G * 2^8) * 2^-8
-    ("e4m3") -- exact power-of-two scale -- and a bf16 head uses bf16(G); all
+    ("e4m3") -- exact power-of-two scale -- or bf16(G) ("bf16", the paper's
+    BF16 logit gradients), and a bf16 head uses bf16(G); all
     RTN.  This is a documented B200 design choice (not in the reference), so
     parity tests of that mode can isolate it by applying it here.  The default
     reference-precision mode needs no quantisation (g_quant=False)."""
     G = np.asarray(G, dtype=np.float32)
+    if fmt.name == "e4m3" and g_format == "bf16":
+        return round_nearest(BF16, G)   # the paper's BF16 logit gradients, unscaled
     if fmt.name == "e4m3":
         q = E5M2 if g_format == "e5m2" else E4M3
         return (round_nearest(q, G * np.float32(256.0)) * np.float32(1.0 / 256.0)).astype(np.float32)

@@ -324,8 +324,6 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
     return fail(XMC_ERR_ARG, "precision must be XMC_PRECISION_OPERAND or XMC_PRECISION_REFERENCE");
   if (d->g_format != 0 && d->g_format != XMC_FMT_E4M3 && d->g_format != XMC_FMT_E5M2 && d->g_format != XMC_FMT_BF16)
     return fail(XMC_ERR_ARG, "g_format must be 0 (default), e4m3, e5m2 or bf16");
-  if (d->precision == XMC_PRECISION_OPERAND && eb == 1 && d->g_format == XMC_FMT_BF16)
-    return fail(XMC_ERR_UNSUPPORTED, "an e4m3 head's operand G is e5m2 or e4m3 (FP8 tensor cores)");
   if (d->num_labels_local < 1 || d->label_offset < 0 ||
       d->label_offset + d->num_labels_local > d->num_labels_global)
     return fail(XMC_ERR_ARG, "bad label shard [%lld, +%lld) of %lld", (long long)d->label_offset,
@@ -333,11 +331,16 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   if (d->max_batch < 1 || d->max_batch > 65535) return fail(XMC_ERR_ARG, "max_batch out of range");
   const int bp = padded_batch(eb, d->max_batch);
   if (bp < 0) return fail(XMC_ERR_UNSUPPORTED, "batch %d too large for format", d->max_batch);
-  const bool ref = d->precision == XMC_PRECISION_REFERENCE;
+  // bf16-operand backward: the reference precision (three planes) or, for an
+  // e4m3 head, the operand mode with g_format bf16 (one plane, the paper's
+  // FP8 weights with BF16 logit gradients); both convert e4m3 W tiles to bf16
+  // operands in shared memory
+  const bool ref = d->precision == XMC_PRECISION_REFERENCE ||
+                   (eb == 1 && d->g_format == XMC_FMT_BF16);
   if (ref && eb == 1 && bp > 256)
-    return fail(XMC_ERR_UNSUPPORTED, "reference precision of an e4m3 head supports batch <= 256 (got %d)",
+    return fail(XMC_ERR_UNSUPPORTED, "bf16-G backward of an e4m3 head supports batch <= 256 (got %d)",
                 d->max_batch);
-  const int planes = ref ? 3 : 1;
+  const int planes = d->precision == XMC_PRECISION_REFERENCE ? 3 : 1;
   const int beb = ref ? 2 : eb;
   auto ch = partition(d->num_labels_local, d->num_chunks);
   int64_t tiles = 0, maxrows = 0;
@@ -402,12 +405,13 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
   xmc_head* h = new xmc_head();
   h->desc = *desc;
   h->eb = eb;
-  h->ref = desc->precision == XMC_PRECISION_REFERENCE;
-  h->planes = h->ref ? 3 : 1;
+  h->ref = desc->precision == XMC_PRECISION_REFERENCE || (eb == 1 && desc->g_format == XMC_FMT_BF16);
+  h->planes = desc->precision == XMC_PRECISION_REFERENCE ? 3 : 1;
   h->beb = h->ref ? 2 : eb;
   // the e4m3 head's operand G: e5m2 x 2^8 by default (covers the reference's
   // whole [2^-24, 1] sigmoid range), e4m3 x 2^8 on request
-  h->gout = h->ref ? G_REF : ((eb == 1 && desc->g_format != XMC_FMT_E4M3) ? G_E5M2 : G_OPERAND);
+  h->gout = h->planes == 3 ? G_REF
+                           : (h->ref ? G_BF16 : ((eb == 1 && desc->g_format != XMC_FMT_E4M3) ? G_E5M2 : G_OPERAND));
   h->max_bp = bp;
   h->num_sms = sms;
   h->dtiles = (desc->dim + 127) / 128;
@@ -670,7 +674,7 @@ static xmc_status launch_fwd_g(xmc_head* h, int Bp, const CUtensorMap& tw, const
   if (h->eb == 1) {
     if (Bp == 128) return launch_fwd_t<1, 128, true, GOUT>(h, tw, tx, p, st);
     if (Bp == 256) return launch_fwd_t<1, 256, true, GOUT>(h, tw, tx, p, st);
-  } else if constexpr (GOUT != G_E5M2) {
+  } else if constexpr (GOUT != G_E5M2 && GOUT != G_BF16) {
     if (Bp == 64) return launch_fwd_t<2, 64, false, GOUT>(h, tw, tx, p, st);
     if (Bp == 128) return launch_fwd_t<2, 128, true, GOUT>(h, tw, tx, p, st);
     if (Bp == 256) return launch_fwd_t<2, 256, true, GOUT>(h, tw, tx, p, st);
@@ -697,6 +701,7 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t rows, int B, in
   p.out = out;
   p.ld = ld;
   p.plane_ld = Bp;
+  p.g_planes = h->planes;
   p.stats = stats;
   p.logit_scale = logit_scale;
   p.status = h->status;
@@ -716,6 +721,7 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t rows, int B, in
     xmc_status s;
     if (mode == 1 || h->gout == G_OPERAND) s = launch_fwd_g<G_OPERAND>(h, pass_n, tw, tx, q, st);
     else if (h->gout == G_E5M2) s = launch_fwd_g<G_E5M2>(h, pass_n, tw, tx, q, st);
+    else if (h->gout == G_BF16) s = launch_fwd_g<G_BF16>(h, pass_n, tw, tx, q, st);
     else s = launch_fwd_g<G_REF>(h, pass_n, tw, tx, q, st);
     XMC_TRY(s);
     if (Bp <= 256) break;
@@ -1258,8 +1264,8 @@ extern "C" xmc_status xmc_head_backward(xmc_head_t h, void* W, const float* G, i
   const int64_t rows = row1 - row0;
   const int blocks = static_cast<int>(std::min<int64_t>(cdiv(rows * Bp, 256), 4096));
   // G into the operand format the step's forward would have written
-  if (h->ref) g_quant_kernel<3><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, h->gbuf, h->status);
-  else if (h->eb == 2) g_quant_kernel<2><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, h->gbuf, h->status);
+  if (h->ref && h->planes == 3) g_quant_kernel<3><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, h->gbuf, h->status);
+  else if (h->eb == 2 || h->ref) g_quant_kernel<2><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, h->gbuf, h->status);
   else if (h->gout == G_E5M2) g_quant_kernel<1><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, h->gbuf, h->status);
   else g_quant_kernel<0><<<blocks, 256, 0, st>>>(G, ld, rows, B, Bp, h->gbuf, h->status);
   CUDA_TRY(cudaGetLastError());

@@ -33,6 +33,10 @@
 //              as [hi | mid | lo] (row stride 3 Bp).  The backward consumes the
 //              planes as a 3x longer K (bf16 x bf16 products are exact), so it
 //              multiplies by the fp32 G of the reference (head.py:193-208, 236).
+//              With g_planes = 1 only hi = bf16(g) is written.
+//   G_BF16     e4m3 head, bf16(g) computed as a bf16 head computes it (fast
+//              sigmoid, clip): the bf16-G operand mode (the paper's FP8
+//              weights with BF16 logit gradients).
 #pragma once
 
 #include "xmc_ptx.cuh"
@@ -40,7 +44,7 @@
 
 namespace xmc {
 
-enum GOut : int { G_OPERAND = 0, G_E5M2 = 1, G_REF = 2 };
+enum GOut : int { G_OPERAND = 0, G_E5M2 = 1, G_REF = 2, G_BF16 = 3 };
 
 struct FwdParams {
   int32_t rows;        // labels in this chunk
@@ -53,6 +57,7 @@ struct FwdParams {
   void* out;                 // G [rows][ld] or logits fp32 [rows][ld]
   int64_t ld;                // leading dimension (elements) of out
   int64_t plane_ld;          // G_REF: elements between the hi / mid / lo planes of a row
+  int32_t g_planes;          // G_REF: 3 (hi | mid | lo, reference precision) or 1 (hi = bf16(g) only)
   float* stats;              // [0] += sum |G| over valid entries (optional)
   float logit_scale;         // z = logit_scale * acc (1, or 1/(1-p) under keyed dropout)
   // top-k scoring (TOPK instantiation): per (sample, CTA, sub-partition) the
@@ -421,7 +426,9 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
     bool nan_seen = false;
     const float zk = -1.4426950408889634f * p.logit_scale;   // -log2(e) * scale
     // operand G of an e4m3 head carries the 2^8 scale (e4m3 / e5m2 encodings)
-    constexpr bool kScaled = EB == 1 && GOUT != G_REF;
+    // FP8 G (2^8-scaled e4m3 / e5m2) of an e4m3 head; G_BF16 computes and
+    // stores G exactly as a bf16 head does (unscaled, clipped, bf16)
+    constexpr bool kScaled = EB == 1 && GOUT != G_REF && GOUT != G_BF16;
     int acc = 0;
     uint32_t acc_phase = 0;
     auto tile_of = [&](int u) { return PAIR ? 2 * u + static_cast<int>(rank) : u; };
@@ -485,7 +492,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
             g[j] = ref_sigmoid_clip(z);
             if ((pos >> j) & 1u) g[j] = __fsub_rn(g[j], 1.0f);
           }
-        } else if constexpr (EB == 1) {
+        } else if constexpr (kScaled) {
           // g256 = 256 sigmoid(z) = 1 / y, y = 2^-8 (1 + 2^(-z log2 e))
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
@@ -561,9 +568,11 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
               st_global_v8_hint(dst + 16, *reinterpret_cast<const uint32_t(*)[8]>(&v[8]), pol_g);
             };
             store_plane(o, ph);
-            store_plane(o + p.plane_ld, pm);
-            store_plane(o + 2 * p.plane_ld, pl);
-          } else if constexpr (EB == 1) {
+            if (p.g_planes > 1) {
+              store_plane(o + p.plane_ld, pm);
+              store_plane(o + 2 * p.plane_ld, pl);
+            }
+          } else if constexpr (kScaled) {
             uint32_t pk[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {

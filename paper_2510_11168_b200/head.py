@@ -16,7 +16,10 @@ Same names, argument meaning and errors as the reference module
   accumulation order differs.  ``"operand"``: the production fast path, G
   rounded once to the FP8/BF16 tensor-core operand format (e4m3 heads:
   ``g_format`` "e5m2" (default, e5m2(2^8 g): the reference's whole
-  [2^-24, 1] sigmoid range) or "e4m3" (e4m3(2^8 g)); bf16 heads: bf16(g)).
+  [2^-24, 1] sigmoid range), "e4m3" (e4m3(2^8 g)) or "bf16" (bf16(g): the
+  paper's FP8 weights with BF16 logit gradients -- the e4m3 W tiles become
+  bf16 operands in shared memory, kind::f16 backward GEMMs, batch <= 256);
+  bf16 heads: bf16(g)).
 * The unfused sub-ops keep the reference signatures for parity isolation.
 
 There is no CPU fallback: every call goes to libxmc_b200.so.
@@ -111,7 +114,7 @@ class _Handle:
 
 
 _PRECISIONS = {"reference": _lib.PRECISION_REFERENCE, "operand": _lib.PRECISION_OPERAND}
-_G_FORMATS = {"e5m2": _lib.FMT_E5M2, "e4m3": _lib.FMT_E4M3}
+_G_FORMATS = {"e5m2": _lib.FMT_E5M2, "e4m3": _lib.FMT_E4M3, "bf16": _lib.FMT_BF16}
 
 
 class ChunkedHead:
@@ -134,7 +137,7 @@ class ChunkedHead:
         if precision not in _PRECISIONS:
             raise ValueError(f"precision must be 'reference' or 'operand', got {precision!r}")
         if g_format not in _G_FORMATS:
-            raise ValueError(f"g_format must be 'e5m2' or 'e4m3', got {g_format!r}")
+            raise ValueError(f"g_format must be 'e5m2', 'e4m3' or 'bf16', got {g_format!r}")
         self.precision, self.g_format = precision, g_format
         if weights.values.dtype != weights.fmt.torch_dtype or weights.fmt.code not in (
                 _lib.FMT_BF16, _lib.FMT_E4M3):

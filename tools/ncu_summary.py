@@ -80,6 +80,10 @@ def summarize(path):
         tot = sum(stalls.values()) or 1.0
         d["top_stalls_pct"] = {k: round(100 * v / tot, 1) for k, v in
                                sorted(stalls.items(), key=lambda kv: -kv[1])[:6]}
+        # the exact ncu metric behind every key (the tensor-pipe figure is
+        # tensor_pipe_pct = sm__pipe_tensor_cycles_active; tensor_mem_pct is the
+        # tensor core's shared/tensor-memory traffic, not its math pipe)
+        d["metrics"] = {k: m for k, m in KEYS.items() if k in d}
         out.append(d)
     return out
 
