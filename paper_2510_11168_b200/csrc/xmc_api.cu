@@ -769,10 +769,12 @@ static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int
   // reference-precision planes accumulated in TMEM: grad_X MMA groups of
   // N = 128 samples (2 k-chunks), so the 4-slot G ring holds two groups and the
   // producer loads one while the other multiplies
-  const bool acc_planes = gxp == 1 && h->planes > 1;
+  // (also the one-plane bf16-G backward of an e4m3 head: N = 128 groups free
+  // the 6-slot G ring half a tile at a time)
+  const bool acc_planes = gxp == 1 && (h->planes > 1 || (h->ref && h->eb == 1));
   p.gx_group = acc_planes ? std::min(2, Bp / box_k) : gx_kc_count;
   p.gx_cols = acc_planes ? Bp : gx_kc_count * box_k;
-  p.g_prefetch = h->planes > 1 ? 1 : 0;
+  p.g_prefetch = h->ref ? 1 : 0;
   // reference precision: drain grad_X every 32 tiles (fp32 accumulation
   // chains of <= 32 x 3 x 128 products per TMEM window)
   p.gx_flush = h->planes > 1 ? 32 : 0;

@@ -105,7 +105,10 @@ struct BwdCfg {
   // second tile) writes W_new in place after the grad_X MMAs completed.
   // (measured equal within box noise: in place / 1 / 2 staging tiles with
   // 5 / 4 / 3 W stages; two staging tiles need one named barrier per tile)
-  static constexpr int kOutTiles = SB == 1 ? 2 : 0;   // W_new staging tiles (0 = in place)
+  // (kW8: the MMAs read the converted operand tile, never the W stage, so
+  // W_new goes in place and the freed 32 KB deepen the G ring to 1.5 tiles:
+  // the next tile's first G boxes load while this tile's grad_X runs)
+  static constexpr int kOutTiles = (SB == 1 && !kW8) ? 2 : 0;   // W_new staging tiles (0 = in place)
   static constexpr bool kOutBuf = kOutTiles > 0;
   // e4m3: 4 W stages (224 KB with the staging tiles; 3 -> 4 measured -1.5 %
   // bwd); the G ring (6 slots = 3 tiles) must not get shallower (4 slots: +10 %)
@@ -114,7 +117,7 @@ struct BwdCfg {
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
   // e4m3: 6 G slots (3 tiles at batch 256); batch 512 / 1024 (4 / 8 k-chunks
   // per tile) 4 slots to stay within the 227 KB
-  static constexpr int kKStages = EB == 1 ? (KCMAX > 2 ? 4 : 6) : 4;
+  static constexpr int kKStages = kW8 ? 6 : (EB == 1 ? (KCMAX > 2 ? 4 : 6) : 4);
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
   static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2 + 2 + 2) + 16;
   static constexpr int kSmemBytes =
@@ -498,7 +501,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // (in place) one store thread per TMEM sub-partition once W_new is stored
       // (kW8: the MMAs read the bf16 operand tile, not the stage: epilogue warps only)
       mbar_init(&w_empty[s], FAST ? 1 + kBwdEpiWarps / 2
-                                  : (C::kW8 ? kBwdEpiWarps : (C::kOutBuf ? 1 + kBwdEpiWarps : 5)));
+                                  : (C::kOutBuf ? 1 + kBwdEpiWarps : (C::kW8 ? 4 : 5)));
     }
     for (int s = 0; s < KS; ++s) {
       mbar_init(&k_full[s], 1);
