@@ -745,7 +745,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           // dW complete -> hand it to the update epilogue before the grad_X
           // MMAs are queued (commit tracks only the MMAs issued so far)
-          if (C::kOutBuf && kc == ke - 1) mma_commit(&t_full[ds]);
+          // (kW8: the grad_X MMAs read the operand tile, so W_new in place
+          // does not have to wait for them either)
+          if ((C::kOutBuf || C::kW8) && kc == ke - 1) mma_commit(&t_full[ds]);
           // grad_X^T: one MMA group with N = gsz k-chunks of samples, issued
           // once its G boxes (contiguous ring slots, LBO = slot pitch) landed;
           // W (A operand) is then read from smem once per group.  Groups of
@@ -787,7 +789,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           // in place: dW is handed over only after the grad_X MMAs, which read
           // the W_old tile the epilogue overwrites with W_new
-          if (!C::kOutBuf && kc == ke - 1) mma_commit(&t_full[ds]);
+          if (!(C::kOutBuf || C::kW8) && kc == ke - 1) mma_commit(&t_full[ds]);
         }
         __syncwarp();
         if (++xk == p.xt_kc) xk = 0;
