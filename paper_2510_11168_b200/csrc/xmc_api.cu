@@ -702,6 +702,11 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t rows, int B, in
   p.ld = ld;
   p.plane_ld = Bp;
   p.g_planes = h->planes;
+  // training forward (one pass): the last ~120 MB of each CTA pair's W tiles
+  // stay in L2 for the backward, which walks the tiles in reverse (C4: 8
+  // units of 256 rows per pair; same-box A/B -1.5 % bwd, +0.6 % step)
+  const int64_t unit_bytes = static_cast<int64_t>(h->num_sms / 2) * 256 * D * eb;
+  p.w_keep_units = (mode == 0 && pair && Bp <= 256) ? static_cast<int32_t>(120000000 / unit_bytes) : 0;
   p.stats = stats;
   p.logit_scale = logit_scale;
   p.status = h->status;

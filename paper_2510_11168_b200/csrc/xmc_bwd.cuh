@@ -482,7 +482,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // this CTA's label tiles: r0, r0 + R, ... (the d-tile CTAs of a row group
   // walk them in step, so each G tile is requested by all six at once)
   const int ntl = r0 < p.num_tiles ? (p.num_tiles - r0 + R - 1) / R : 0;
+  // label tiles in DESCENDING order: the forward walks them ascending, so
+  // the first tiles here are the ones whose G (written evict_last) is still
+  // in L2 when the backward starts
+#ifdef XMC_BWD_ASCENDING
   auto tile_at = [&](int k) { return r0 + k * R; };
+#else
+  auto tile_at = [&](int k) { return p.num_tiles - 1 - (r0 + k * R); };
+#endif
   // k-chunks (batch slices) a tile needs: all of them when the update runs
   // (dW sums over the whole batch), else only the grad_X column group's
   const int kb = p.do_update ? 0 : p.gx_kc0;

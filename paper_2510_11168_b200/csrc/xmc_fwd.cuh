@@ -58,6 +58,8 @@ struct FwdParams {
   int64_t ld;                // leading dimension (elements) of out
   int64_t plane_ld;          // G_REF: elements between the hi / mid / lo planes of a row
   int32_t g_planes;          // G_REF: 3 (hi | mid | lo, reference precision) or 1 (hi = bf16(g) only)
+  int32_t w_keep_units;      // training forward: the last units of each CTA load W with evict_last (the
+                             // backward walks the tiles in reverse, so it finds them, and their G, in L2)
   float* stats;              // [0] += sum |G| over valid entries (optional)
   float logit_scale;         // z = logit_scale * acc (1, or 1/(1-p) under keyed dropout)
   // top-k scoring (TOPK instantiation): per (sample, CTA, sub-partition) the
@@ -216,7 +218,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
     static_assert(kBPI * kIPB <= 32, "one lane per box");
     const int lane = static_cast<int>(lane_id());
     const uint64_t pol_w = policy_evict_first();
-    const uint64_t pol_x = policy_evict_last();
+    const uint64_t pol_x = policy_evict_last();   // (also W of the last w_keep_units units)
     if constexpr (XRES) {
       // this CTA's Xq rows, every K-chunk, once: one warp-wide instruction
       if (lane == 0) {
@@ -257,7 +259,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
       const CUtensorMap* m = b == 0 ? &tm_w : &tm_x;
       uint8_t* dst = b == 0 ? sb : sb + C::kWBytes + (b - 1) * C::kXBoxRows * 128;
       const int32_t c1 = b == 0 ? tile * 128 : xrow0 + (b - 1) * C::kXBoxRows;
-      const uint64_t pol = b == 0 ? pol_w : pol_x;
+      const uint64_t pol = (b == 0 && n / kc_count < my_units - p.w_keep_units) ? pol_w : pol_x;
       if (active) {
         if constexpr (PAIR) tma_load_2d_2sm(dst, m, mapa_shared(&full[st_i], 0), kc * C::kBoxK, c1, pol);
         else tma_load_2d_hint(dst, m, &full[st_i], kc * C::kBoxK, c1, pol);
