@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--sr-impl", default="hash", choices=["hash", "philox", "splitmix64"])
     ap.add_argument("--precision", default="operand", choices=["operand", "reference"])
     ap.add_argument("--g-format", default="e5m2", choices=["e5m2", "e4m3", "bf16"])
+    ap.add_argument("--kahan", default=None, choices=["bf16", "fp32"],
+                    help="head-Kahan compensation (PAPER.md:795), fused into the backward")
+    ap.add_argument("--kahan-labels", type=int, default=None,
+                    help="top-p%% head-Kahan: only the first N (frequency-sorted) labels carry a compensation")
     ap.add_argument("--ref-steps", type=int, default=5,
                     help="timed steps of the reference-precision mode reported beside the headline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -273,6 +277,8 @@ def main():
               "precision": a.precision, "g_format": a.g_format if a.fmt == "e4m3" else "bf16",
               "parallelism": f"label-shard x{world}", "l2": "inputs larger than L2 (W >> 126 MB)",
               "cpu_sample_labels": min(a.cpu_labels, a.labels)}
+    if a.kahan:
+        config["kahan"] = {"comp": a.kahan, "labels": a.kahan_labels or a.labels}
 
     if a.impl == "reference":
         if rank != 0:
@@ -315,7 +321,8 @@ def main():
         r1 = min(r0 + blk, hi - lo)
         W[r0:r1] = xmc.cast_native(torch.randn((r1 - r0, a.dim), generator=g, device=dev) * 0.02, fmt)
     head = xmc.ChunkedHead(xmc.QuantizedMatrix(W, fmt), num_chunks=a.chunks, num_labels_global=a.labels,
-                           label_offset=lo, precision=a.precision, g_format=a.g_format)
+                           label_offset=lo, precision=a.precision, g_format=a.g_format,
+                           kahan=a.kahan, kahan_labels=a.kahan_labels)
     rs = np.random.default_rng(0)
     Xh = rs.normal(size=(a.batch, a.dim)).astype(np.float32)
     si, li = synthetic_positives(a.labels, a.batch, PAPER_MEAN_LABELS.get(a.labels, 5.0), seed=1)
@@ -413,6 +420,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_ms = float(t.item())
     peak_mem = torch.cuda.max_memory_allocated(dev) - mem0 + W.numel() * W.element_size()
+    if head.comp is not None:   # allocated with the head, before mem0
+        peak_mem += head.comp.numel() * head.comp.element_size()
     _lib.check(_lib.load().xmc_head_check(head.handle(a.batch, len(si)).h, _lib.stream_ptr()))
 
     # ---------------- end-to-end through the public API, host buffers

@@ -736,7 +736,7 @@ static xmc_status launch_fwd(xmc_head* h, const void* W, int64_t rows, int B, in
 
 // ---- backward ----
 struct BwdLaunch {
-  CUtensorMap tw, tg, tx, tws;
+  CUtensorMap tw, tg, tx, tws, tc;   // tc: the staged bf16 compensation (fast head-Kahan), else a copy of tw
   BwdParams p;
   int R;
 };
@@ -788,6 +788,9 @@ static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int
   const int64_t crows = comp ? std::min<int64_t>(rows, std::max<int64_t>(0, h->comp_rows - row0)) : 0;
   p.comp = crows > 0 ? static_cast<uint8_t*>(comp) + row0 * D * h->desc.comp_bytes : nullptr;
   p.comp_rows = static_cast<int32_t>(crows);
+  L->tc = L->tw;
+  if (crows > 0 && h->desc.comp_bytes == 2)   // [crows][d] bf16, 64-column boxes of 128 rows
+    XMC_TRY(make_map(&L->tc, p.comp, 2, D, crows, D, 128));
   p.row0_global = h->desc.label_offset + row0;
   p.lr = a ? a->lr : 0.f;
   p.wd = a ? a->weight_decay : 0.f;
@@ -818,11 +821,11 @@ static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int
 
 template <int EB, bool XR, int KC, int CE, bool FAST, bool ADAMW, int GE, int SB>
 static xmc_status launch_bwd_k(xmc_head* h, const BwdLaunch& L, cudaStream_t st) {
-  constexpr int sm = BwdCfg<EB, XR, KC, SB>::kSmemBytes;
+  constexpr int sm = BwdCfg<EB, XR, KC, SB, bwd_comp_staged<CE, FAST>()>::kSmemBytes;
   static_assert(sm <= 232448, "bwd shared memory over the 227 KB opt-in limit");
   auto k = xmc_bwd_kernel<EB, XR, KC, CE, FAST, ADAMW, GE, SB>;
   smem_attr_once<xmc_bwd_kernel<EB, XR, KC, CE, FAST, ADAMW, GE, SB>>(sm);
-  CUDA_TRY(launch_ex(k, L.R * h->dtiles, kBwdThreads, sm, st, h, 1, L.tw, L.tg, L.tx, L.tws, L.p));
+  CUDA_TRY(launch_ex(k, L.R * h->dtiles, kBwdThreads, sm, st, h, 1, L.tw, L.tg, L.tx, L.tws, L.tc, L.p));
   return XMC_OK;
 }
 
@@ -832,12 +835,18 @@ static xmc_status launch_bwd_v(xmc_head* h, const BwdLaunch& L, cudaStream_t st)
   const BwdParams& p = L.p;
   if (p.adam_m != nullptr) return launch_bwd_k<EB, XR, KC, 4, false, true, GE, SB>(h, L, st);
   const int ce = p.comp ? h->desc.comp_bytes : 0;
+  // (XMC_BWD_GENERAL=1: test knob, the general instantiation for everything,
+  // so tests can compare the fast specialisations against it bit for bit)
+  static const bool force_general = getenv("XMC_BWD_GENERAL") != nullptr;
+  const bool fast_ok = p.do_update && p.rounding == ROUND_SR_FAST && p.keep == nullptr && !force_general;
+  // the fast head-Kahan (bf16 compensation staged by TMA with the W tile)
+  if constexpr (EB == 1 && GE == 1 && XR && KC <= 2)
+    if (ce == 2 && fast_ok) return launch_bwd_k<1, XR, KC, 2, true, false, 1, 1>(h, L, st);
   if (ce == 2) return launch_bwd_k<EB, XR, KC, 2, false, false, GE, SB>(h, L, st);
   if (ce == 4) return launch_bwd_k<EB, XR, KC, 4, false, false, GE, SB>(h, L, st);
   // the FAST instantiation keeps Xq^T resident and whole tiles in the G ring
   if constexpr (EB == 1 && GE == 1 && XR && BwdCfg<EB, XR, KC, SB>::kKStages % KC == 0)
-    if (p.do_update && p.rounding == ROUND_SR_FAST && p.keep == nullptr)
-      return launch_bwd_k<1, XR, KC, 0, true, false, 1, 1>(h, L, st);
+    if (fast_ok) return launch_bwd_k<1, XR, KC, 0, true, false, 1, 1>(h, L, st);
   return launch_bwd_k<EB, XR, KC, 0, false, false, GE, SB>(h, L, st);
 }
 

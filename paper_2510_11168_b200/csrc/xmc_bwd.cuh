@@ -89,7 +89,9 @@ struct BwdParams {
 // SB: bytes per stored W element (the HBM tile, the update epilogue, W_new).
 // SB < EB (reference precision of an e4m3 head): the epilogue converts each
 // e4m3 W tile into a bf16 operand tile (kOpBytes) for the grad_X MMAs.
-template <int EB, bool XT_RES, int KCMAX, int SB = EB>
+// CS: bytes per element of a compensation tile staged by TMA next to each W
+// stage (2: the bf16 head-Kahan compensation of the fast path; 0: none)
+template <int EB, bool XT_RES, int KCMAX, int SB = EB, int CS = 0>
 struct BwdCfg {
   static_assert(SB == EB || (SB == 1 && EB == 2), "bf16 operands of an e4m3 head only");
   static constexpr bool kW8 = SB != EB;              // W stored e4m3, MMA operands bf16
@@ -112,16 +114,19 @@ struct BwdCfg {
   static constexpr bool kOutBuf = kOutTiles > 0;
   // e4m3: 4 W stages (224 KB with the staging tiles; 3 -> 4 measured -1.5 %
   // bwd); the G ring (6 slots = 3 tiles) must not get shallower (4 slots: +10 %)
-  static constexpr int kWStages = kW8 ? (KCMAX > 2 ? 2 : 4) : (EB == 1 ? 4 : 3);
+  // (staged compensation: 2 stages of W + comp and a 4-slot G ring fit 227 KB)
+  static constexpr int kWStages = CS ? 2 : (kW8 ? (KCMAX > 2 ? 2 : 4) : (EB == 1 ? 4 : 3));
+  static constexpr int kCompBytes = CS * kBox;        // [128 rows x 128 cols] comp tile (CS = 2: two boxes)
+  static constexpr int kWStride = kWBytes + kCompBytes;
   static constexpr int kOutBytes = kOutTiles * kWBytes;
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
   // e4m3: 6 G slots (3 tiles at batch 256); batch 512 / 1024 (4 / 8 k-chunks
   // per tile) 4 slots to stay within the 227 KB
-  static constexpr int kKStages = kW8 ? 6 : (EB == 1 ? (KCMAX > 2 ? 4 : 6) : 4);
+  static constexpr int kKStages = kW8 ? 6 : (EB == 1 ? ((KCMAX > 2 || CS) ? 4 : 6) : 4);
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
   static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2 + 2 + 2) + 16;
   static constexpr int kSmemBytes =
-      1024 + kXtBytes + kWStages * kWBytes + kOpBytes + kOutBytes + kKStages * kKSlot + kBarBytes;
+      1024 + kXtBytes + kWStages * kWStride + kOpBytes + kOutBytes + kKStages * kKSlot + kBarBytes;
   static constexpr int kKmma = 32 / EB;              // K per MMA instruction (elements)
   static constexpr int kChunks16 = 2 * SB;           // 16-B smem chunks per thread (32 stored elements)
 };
@@ -431,17 +436,23 @@ XMC_DEV void w_update_pack_adamw(const BwdParams& p, const uint32_t (&acc)[32], 
 // The kernel: CTA bid of the grid (d-tile bid % dtiles, row group bid / dtiles).
 // FAST: the production specialisation (SR_FAST, e4m3, no compensation, no
 // dropout mask) with every runtime mode switch folded away.
+// the fast path stages a bf16 head-Kahan compensation by TMA
+template <int CE, bool FAST>
+__host__ __device__ constexpr int bwd_comp_staged() { return (FAST && CE == 2) ? 2 : 0; }
+
 template <int EB, bool XT_RES, int KCMAX, int CE, bool FAST = false, bool ADAMW = false, int GE = EB, int SB = EB>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     xmc_bwd_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_g,
                    const __grid_constant__ CUtensorMap tm_xt, const __grid_constant__ CUtensorMap tm_ws,
-                   const BwdParams p_arg) {
+                   const __grid_constant__ CUtensorMap tm_c, const BwdParams p_arg) {
   // a by-value copy: the compiler keeps launch-uniform fields in uniform
   // registers (a __grid_constant__ reference measured 17 % slower)
   BwdParams p = p_arg;
-  using C = BwdCfg<EB, XT_RES, KCMAX, SB>;
+  constexpr int CS = bwd_comp_staged<CE, FAST>();
+  using C = BwdCfg<EB, XT_RES, KCMAX, SB, CS>;
   static_assert(!ADAMW || (CE == 4 && !FAST), "the Adam-style head keeps an fp32 compensation");
-  static_assert(!FAST || (EB == 1 && GE == 1 && CE == 0), "the fast path is the e4m3 SR_FAST head");
+  static_assert(!FAST || (EB == 1 && GE == 1 && (CE == 0 || CE == 2)),
+                "the fast path is the e4m3 SR_FAST head (optionally with a bf16 Kahan compensation)");
   constexpr int WS = C::kWStages;
   constexpr int KS = C::kKStages;
   const int bid = static_cast<int>(blockIdx.x), nblk = static_cast<int>(gridDim.x);
@@ -451,7 +462,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* xt_s = smem;
   uint8_t* w_s = smem + C::kXtBytes;
-  uint8_t* op_s = w_s + WS * C::kWBytes;       // bf16 W^T operand tile (kW8)
+  uint8_t* op_s = w_s + WS * C::kWStride;      // bf16 W^T operand tile (kW8)
   uint8_t* out_s = op_s + C::kOpBytes;         // W_new staging tiles (kOutBuf)
   uint8_t* k_s = out_s + C::kOutBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(k_s + KS * C::kKSlot);
@@ -502,6 +513,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     prefetch_tmap(&tm_w);
     prefetch_tmap(&tm_g);
     prefetch_tmap(&tm_xt);
+    if constexpr (CS > 0) prefetch_tmap(&tm_c);
     for (int s = 0; s < WS; ++s) {
       mbar_init(&w_full[s], 1);
       // MMA commit + (kOutBuf) every epilogue warp once it has read W_old, or
@@ -570,11 +582,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait_sleep(&w_empty[ws], wph ^ 1);
       if (whole) {
         for (int i = 0; i < nk; ++i) mbar_wait(&k_empty[ks + i], kph ^ 1);
+        // staged compensation: the tile's comp boxes ride with its W stage
+        // (only tiles with rows inside the compensated prefix)
+        const int ncb = (CS > 0 && tile * 128 < p.comp_rows) ? CS : 0;
         if (lane == 0) {
 #ifdef XMC_WHATIF_NO_WLOAD
           mbar_arrive_expect_tx(&w_full[ws], 0);
 #else
-          mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
+          mbar_arrive_expect_tx(&w_full[ws], C::kWBytes + ncb * C::kBox);
 #endif
           for (int i = 0; i < nk; ++i) mbar_arrive_expect_tx(&k_full[ks + i], kslot_bytes);
         }
@@ -584,13 +599,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int gl = lane - C::kWBoxes;
         const int i = gl / kGB, sub = gl % kGB;
         const bool is_w = lane < C::kWBoxes;
+        if constexpr (CS > 0) {   // comp box cb = lane - (W boxes + G boxes)
+          const int cb = gl - nk * kGB;
+          if (cb >= 0 && cb < ncb)
+            tma_load_2d_hint(w_s + ws * C::kWStride + C::kWBytes + cb * C::kBox, &tm_c, &w_full[ws],
+                             j * 128 + cb * 64, tile * 128, pol_stream);
+        }
 #ifdef XMC_WHATIF_NO_WLOAD
         const bool active = !is_w && (gl >= 0 && i < nk);
 #else
         const bool active = is_w || (gl >= 0 && i < nk);
 #endif
         const CUtensorMap* m = is_w ? &tm_w : (sub == 0 ? &tm_g : &tm_xt);
-        uint8_t* dst = is_w ? w_s + ws * C::kWBytes + lane * C::kBox : k_s + (ks + i) * C::kKSlot + sub * C::kBox;
+        uint8_t* dst = is_w ? w_s + ws * C::kWStride + lane * C::kBox : k_s + (ks + i) * C::kKSlot + sub * C::kBox;
         uint64_t* bar = is_w ? &w_full[ws] : &k_full[ks + i];
         const int kcg = kb + i;
         int xk = kcg;   // Xq^T k-chunk of G k-chunk kcg (kcg < 3 xt_kc)
@@ -607,7 +628,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (lane == 0) mbar_arrive_expect_tx(&w_full[ws], C::kWBytes);
         __syncwarp();
         if (lane < C::kWBoxes)
-          tma_load_2d_hint(w_s + ws * C::kWBytes + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kWBoxK,
+          tma_load_2d_hint(w_s + ws * C::kWStride + lane * C::kBox, &tm_w, &w_full[ws], j * 128 + lane * C::kWBoxK,
                            tile * 128, pol_stream);
         __syncwarp();
         // the next tile's G boxes into L2 while this one streams from the ring
@@ -665,6 +686,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t dG = umma_desc_sw128(smem_u32(k_s), 16, 1024);            // dW A: G, K-major
       const uint64_t dX = umma_desc_sw128(smem_u32(xt_s), 16, 1024);           // dW B: Xq^T, K-major
       const uint64_t dWt = umma_desc_sw128(smem_u32(w_s), C::kBox, 1024);      // grad_X A: W^T, MN-major
+      static_assert(C::kWStride % 16 == 0, "stage stride in descriptor units");
       const uint64_t dGt = umma_desc_sw128(smem_u32(k_s), C::kKSlot, 1024);    // grad_X B: G, MN-major
       int ws = 0, ks = 0, ds = 0;
       uint32_t wph = 0, kph = 0, dph = 0;
@@ -692,7 +714,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #else
           if (do_gx) {
 #endif
-            const uint64_t wa = dWt + ((static_cast<uint32_t>(ws) * C::kWBytes) >> 4);
+            const uint64_t wa = dWt + ((static_cast<uint32_t>(ws) * C::kWStride) >> 4);
             const uint64_t gb = dGt + ((static_cast<uint32_t>(ks) * C::kKSlot) >> 4);
 #pragma unroll
             for (int k = 0; k < 4; ++k) mma_f8(tmem_gx, wa + 256 * k, gb + 256 * k, idesc_gx, (it | k) != 0);
@@ -719,7 +741,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(&t_empty[ds], dph ^ 1);
       tc_fence_after();
       // grad_X A operand: the W stage, or (kW8) the bf16 tile the epilogue converted
-      const uint32_t w_addr = C::kW8 ? smem_u32(op_s) : smem_u32(w_s + ws * C::kWBytes);
+      const uint32_t w_addr = C::kW8 ? smem_u32(op_s) : smem_u32(w_s + ws * C::kWStride);
       const uint32_t d_dw = tmem_base + ds * 128;
       bool op_ready = !C::kW8;
       int xk = kb;   // Xq^T k-chunk of G k-chunk kc (the planes repeat it)
@@ -875,12 +897,109 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       uint8_t* ot = out_s + g * C::kWBytes;          // this group's W_new staging tile
       const uint32_t ot_s = smem_u32(ot);
       bool stored = false;
-      for (int it = g; it < ntl; it += 2) {
+      if constexpr (CE == 2) {
+        // ---- head-Kahan (bf16 compensation, formats.py:246-263 composed
+        // with sgd_sr_step): the comp tile rides with the W
+        // stage (TMA), both are read into registers before the stage is
+        // released; dW is read 16 columns at a time to keep W_old, comp and
+        // the SR words live; comp' goes out by st.global (rows inside the
+        // compensated prefix only), W_new through the staging tile.
+        const float b_wd = -p.lr * p.wd;
+        const uint64_t pol_c = policy_evict_first();
+        for (int it = g; it < ntl; it += 2) {
+          const int tile = tile_at(it);
+          const int wsi = it % WS;
+          const uint32_t wphi = static_cast<uint32_t>(it / WS) & 1u;
+          const uint32_t dphi = static_cast<uint32_t>(it >> 1) & 1u;
+          const uint32_t wt_s = smem_u32(w_s + wsi * C::kWStride);
+          const uint32_t ct_s = wt_s + C::kWBytes;
+          mbar_wait(&w_full[wsi], wphi);
+          const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
+          const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + cw0;
+          const bool tile_c = tile * 128 < p.comp_rows;           // the producer loaded its comp boxes
+          const bool krow = grow < p.comp_rows && j * 128 + cw0 < p.d;   // this thread stores comp'
+          uint4 raw[4], craw[8];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) raw[h] = lds128(wt_s + w_chunk_off<EB>(row, cw0 + (h >> 1) * 32, h & 1));
+#pragma unroll
+          for (int h = 0; h < 8; ++h)
+            craw[h] = tile_c ? lds128(ct_s + w_chunk_off<2>(row, cw0 + (h >> 2) * 32, h & 3)) : make_uint4(0, 0, 0, 0);
+          __syncwarp();
+          if (lane_id() == 0) mbar_arrive(&w_empty[wsi]);
+          uint32_t rw[8];
+          sr_words<1>(pk, flat0, rw, p.sr_bits != 0);
+          if (gstorer && stored) bulk_wait_read<0>();
+          named_bar_sync(1 + q + 4 * g, 64);
+          mbar_wait_sleep(&t_full[g], dphi);
+          tc_fence_after();
+#pragma unroll
+          for (int cg = 0; cg < 2; ++cg) {
+            if (cg == 1) sr_words<1>(pk, flat0 + 32, rw, p.sr_bits != 0);
+            uint32_t pk8[8];
+#pragma unroll
+            for (int qt = 0; qt < 2; ++qt) {
+              uint32_t acc[16];
+              tmem_ld16(tmem_base + lane_off + g * 128 + cw0 + cg * 32 + qt * 16, acc);
+              tmem_ld_wait();
+              if (cg == 1 && qt == 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane_id() == 0) mbar_arrive(&t_empty[g]);
+              }
+              uint32_t cw[8];
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4) {
+                const int e = cg * 32 + qt * 16 + 4 * k4;   // element of the thread's 64
+                const uint32_t wv = word_of(raw, e >> 2);
+                const float2 w01 = dec_e4m3x2(static_cast<uint16_t>(wv & 0xFFFF));
+                const float2 w23 = dec_e4m3x2(static_cast<uint16_t>(wv >> 16));
+                const float w[4] = {w01.x, w01.y, w23.x, w23.y};
+                const uint32_t c0w = word_of(craw, e >> 1), c1w = word_of(craw, (e >> 1) + 1);
+                const float c[4] = {__uint_as_float(c0w << 16), __uint_as_float(c0w & 0xFFFF0000u),
+                                    __uint_as_float(c1w << 16), __uint_as_float(c1w & 0xFFFF0000u)};
+                float y[4], t[4];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) {
+                  const float v = fmaf(a_lr, __uint_as_float(acc[4 * k4 + x]), b_wd * w[x]);
+                  y[x] = v - c[x];
+                  t[x] = w[x] + y[x];
+                }
+                const uint32_t w4 = cvt_e4m3x4_rs(t[3], t[2], t[1], t[0], rw[qt * 4 + k4]);
+                pk8[qt * 4 + k4] = w4;
+                const float2 r01 = dec_e4m3x2(static_cast<uint16_t>(w4 & 0xFFFF));
+                const float2 r23 = dec_e4m3x2(static_cast<uint16_t>(w4 >> 16));
+                const float tr[4] = {r01.x, r01.y, r23.x, r23.y};
+                float cn[4];
+#pragma unroll
+                for (int x = 0; x < 4; ++x) cn[x] = (tr[x] - w[x]) - y[x];
+                cw[2 * k4] = cvt_bf16x2_rn(cn[1], cn[0]);
+                cw[2 * k4 + 1] = cvt_bf16x2_rn(cn[3], cn[2]);
+              }
+              if (krow) {
+                uint4* cdst = reinterpret_cast<uint4*>(p.comp + (grow * p.d + j * 128 + cw0 + cg * 32 + qt * 16) * 2);
+                st_global_v4_hint(cdst, make_uint4(cw[0], cw[1], cw[2], cw[3]), pol_c);
+                st_global_v4_hint(cdst + 1, make_uint4(cw[4], cw[5], cw[6], cw[7]), pol_c);
+              }
+            }
+            const int cc = cw0 + cg * 32;
+            sts128(ot_s + w_chunk_off<EB>(row, cc, 0), make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]));
+            sts128(ot_s + w_chunk_off<EB>(row, cc, 1), make_uint4(pk8[4], pk8[5], pk8[6], pk8[7]));
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(1 + q + 4 * g, 64);
+          if (gstorer) {
+            tma_store_2d_hint(&tm_ws, ot + q * 32 * 128, j * 128, tile * 128 + q * 32, pol_w_out);
+            bulk_commit();
+            stored = true;
+          }
+        }
+      }
+      for (int it = g; it < (CE == 2 ? 0 : ntl); it += 2) {
         const int tile = tile_at(it);
         const int wsi = it % WS;
         const uint32_t wphi = static_cast<uint32_t>(it / WS) & 1u;
         const uint32_t dphi = static_cast<uint32_t>(it >> 1) & 1u;
-        const uint32_t wt_s = smem_u32(w_s + wsi * C::kWBytes);
+        const uint32_t wt_s = smem_u32(w_s + wsi * C::kWStride);
         mbar_wait(&w_full[wsi], wphi);
         const int64_t grow = static_cast<int64_t>(tile) * 128 + row;
         const int64_t flat0 = (p.row0_global + grow) * static_cast<int64_t>(p.d) + j * 128 + cw0;
@@ -986,7 +1105,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     for (int it = 0; it < (FAST ? 0 : ntl); ++it) {
       const int tile = tile_at(it);
-      uint8_t* wt = w_s + ws * C::kWBytes;
+      uint8_t* wt = w_s + ws * C::kWStride;
       mbar_wait(&w_full[ws], wph);
       const uint32_t wt_s = smem_u32(wt);
       uint4 raw[C::kChunks16];
