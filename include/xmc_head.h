@@ -87,11 +87,14 @@ typedef struct {
  *    longer K, so every product G[l,b] Xq[b,c] and G[l,b] W[l,c] is exact and
  *    only the fp32 accumulation order differs from the reference's sgemm
  *    (head.py:193-208, 236; "update computed at working precision
- *    before the single rounding").  An e4m3 head's W chunk is copied to bf16
- *    for the MMAs (exact) and the update still rounds onto the e4m3 grid.
- *  XMC_PRECISION_OPERAND: the production fast path; G is rounded once to the
- *    tensor-core operand format of the head (e4m3 head: e5m2 or e4m3 of
- *    2^8 g, all three GEMMs on FP8 kind::f8f6f4; bf16 head: bf16(g)). */
+ *    before the single rounding").  An e4m3 head's W tiles are converted to
+ *    bf16 operand tiles in shared memory (exact) and the update still rounds
+ *    onto the e4m3 grid.
+ *  XMC_PRECISION_OPERAND: G is rounded once to a tensor-core operand format
+ *    (desc.g_format): an e4m3 head uses e5m2 or e4m3 of 2^8 g with all three
+ *    GEMMs on FP8 kind::f8f6f4 (the production fast path), or bf16(g) with
+ *    bf16 operand tiles as for the reference precision (the paper's BF16 logit
+ *    gradients); a bf16 head uses bf16(g). */
 typedef enum { XMC_PRECISION_OPERAND = 0, XMC_PRECISION_REFERENCE = 1 } xmc_precision;
 
 typedef struct xmc_head* xmc_head_t;

@@ -2,6 +2,7 @@
 header declares (no compute without a GPU), and the host-side mirror of the
 reference interface agrees with the oracle."""
 
+import ctypes
 import os
 import re
 
@@ -116,3 +117,20 @@ def test_peer_group_argument_checks_without_device():
     assert c.rounding_code == _lib.ROUND_SR_EXACT
     with pytest.raises(ValueError):
         SgdSrConfig(0.1, fmt=E4M3, sr_impl="xorshift")
+
+
+def test_integration_stub_matches_the_abi():
+    """INTEGRATION.md's reference-side ctypes stub declares xmc_head_desc /
+    xmc_step_args with the same fields, in the same order, as the binding the
+    package uses (paper_2510_11168_b200/_lib.py)."""
+    import re
+    from paper_2510_11168_b200 import _lib
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+
+    def fields(cls_name):
+        m = re.search(r"class " + cls_name + r"\(ctypes\.Structure\):\s*_fields_ = \[(.*?)\]\n", text, re.S)
+        assert m, cls_name
+        return [(n, getattr(ctypes, t)) for n, t in re.findall(r'\("(\w+)", ctypes\.(\w+)\)', m.group(1))]
+
+    assert fields("_Desc") == list(_lib.HeadDesc._fields_)
+    assert fields("_Step") == list(_lib.StepArgs._fields_)
