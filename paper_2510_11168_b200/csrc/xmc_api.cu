@@ -833,6 +833,9 @@ static xmc_status launch_bwd_k(xmc_head* h, const BwdLaunch& L, cudaStream_t st)
 template <int EB, bool XR, int KC, int GE, int SB = EB>
 static xmc_status launch_bwd_v(xmc_head* h, const BwdLaunch& L, cudaStream_t st) {
   const BwdParams& p = L.p;
+  if constexpr (KC == 0) {   // grad_X-only pass: no update, no compensation / optimizer state
+    return launch_bwd_k<EB, XR, 0, 0, false, false, GE, SB>(h, L, st);
+  } else {
   if (p.adam_m != nullptr) return launch_bwd_k<EB, XR, KC, 4, false, true, GE, SB>(h, L, st);
   const int ce = p.comp ? h->desc.comp_bytes : 0;
   // (XMC_BWD_GENERAL=1: test knob, the general instantiation for everything,
@@ -848,6 +851,7 @@ static xmc_status launch_bwd_v(xmc_head* h, const BwdLaunch& L, cudaStream_t st)
   if constexpr (EB == 1 && GE == 1 && XR && BwdCfg<EB, XR, KC, SB>::kKStages % KC == 0)
     if (fast_ok) return launch_bwd_k<1, XR, KC, 0, true, false, 1, 1>(h, L, st);
   return launch_bwd_k<EB, XR, KC, 0, false, false, GE, SB>(h, L, st);
+  }
 }
 
 static xmc_status launch_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int64_t rows, int Bp, bool update,
@@ -864,6 +868,11 @@ static xmc_status launch_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, in
     // Xq^T, rounding onto the e4m3 grid
     if (Bp == 128) s = launch_bwd_v<2, true, 2, 1, 1>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<2, true, 4, 1, 1>(h, L, st);
+  } else if (!update && gx_kc_count > 0 && Bp > 256) {
+    // grad_X-only pass of a batch over 256 (the update rides on the last
+    // pass): G boxes only, a two-tile G ring
+    if (h->eb == 1) s = launch_bwd_v<1, true, 0, 1>(h, L, st);
+    else s = launch_bwd_v<2, true, 0, 2>(h, L, st);
   } else if (h->eb == 1) {
     if (Bp == 128) s = launch_bwd_v<1, true, 1, 1>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<1, true, 2, 1>(h, L, st);

@@ -122,7 +122,10 @@ struct BwdCfg {
   static constexpr int kKSlot = kBox + (XT_RES ? 0 : kBox);
   // e4m3: 6 G slots (3 tiles at batch 256); batch 512 / 1024 (4 / 8 k-chunks
   // per tile) 4 slots to stay within the 227 KB
-  static constexpr int kKStages = kW8 ? 6 : (EB == 1 ? ((KCMAX > 2 || CS) ? 4 : 6) : 4);
+  // KCMAX = 0: the grad_X-only pass of a batch > 256 (no Xq^T, no update):
+  // the freed space deepens the G ring to two tiles
+  static constexpr int kKStages = KCMAX == 0 ? (EB == 1 ? 6 : 8)
+                                             : (kW8 ? 6 : (EB == 1 ? ((KCMAX > 2 || CS) ? 4 : 6) : 4));
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
   static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2 + 2 + 2) + 16;
   static constexpr int kSmemBytes =
@@ -566,7 +569,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int lane = static_cast<int>(lane_id());
     const uint64_t pol_stream = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
-    if constexpr (XT_RES) {
+    if constexpr (XT_RES && KCMAX > 0) {
       if (lane == 0) mbar_arrive_expect_tx(xt_full, p.xt_kc * C::kBox);
       __syncwarp();
       if (lane < p.xt_kc)
@@ -675,7 +678,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint32_t xf = EB == 1 ? 0u : 1u;
     const uint32_t idesc_dw = umma_idesc(gf, xf, false, false, 128, 128);                         // A = G, B = Xq
     const uint32_t idesc_gx = umma_idesc(xf, gf, true, true, 128, p.gx_group * C::kBoxK);         // A = W^T, B = G
-    if constexpr (XT_RES) mbar_wait(xt_full, 0);
+    if constexpr (XT_RES && KCMAX > 0) mbar_wait(xt_full, 0);
     if constexpr (FAST) {
       // Production path, lean instruction stream (the MMA warp shares its
       // scheduler with 4 epilogue warps; with ~275 instructions per tile it
