@@ -270,6 +270,8 @@ struct xmc_head {
   int64_t comp_rows;   // local rows [0, comp_rows) carry a Kahan compensation
   float* cand_s;       // [max_bp][4 num_sms][kTopK] streaming top-k candidates (scores)
   int32_t* cand_l;     // [max_bp][4 num_sms][kTopK] (global labels)
+  float* topk_pre_s;   // [max_bp][kTopK] top-8 scores of the top-k prologue (a strided label sample)
+  int64_t* topk_pre_l; // [max_bp][kTopK] their labels (unused)
   int R;               // bwd CTAs per d-tile
   int fwd_max_clusters;   // co-resident CTA pairs of the forward (grid cap, PDL safety)
   bool pdl_ok;
@@ -365,7 +367,7 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   L->wm = align_up(L->status + 64, 1024);
   L->keep = align_up(L->wm + (d->dropout ? (size_t)(maxrows + 128) * D * eb : 0), 1024);
   L->cand = align_up(L->keep + (d->dropout ? (size_t)(maxrows + 128) * (D / 32) * 4 : 0), 1024);
-  L->total = align_up(L->cand + (size_t)bp * 4 * num_sms * kTopK * 8, 1024);
+  L->total = align_up(L->cand + (size_t)bp * 4 * num_sms * kTopK * 8 + (size_t)bp * kTopK * 12, 1024);
   *eb_out = eb;
   *bp_out = bp;
   *R_out = R;
@@ -442,6 +444,8 @@ extern "C" xmc_status xmc_head_create(const xmc_head_desc* desc, void* workspace
                                          std::max<int64_t>(0, desc->comp_labels - desc->label_offset));
   h->cand_s = reinterpret_cast<float*>(w + L.cand);
   h->cand_l = reinterpret_cast<int32_t*>(w + L.cand + (size_t)bp * 4 * sms * kTopK * 4);
+  h->topk_pre_l = reinterpret_cast<int64_t*>(w + L.cand + (size_t)bp * 4 * sms * kTopK * 8);
+  h->topk_pre_s = reinterpret_cast<float*>(w + L.cand + (size_t)bp * 4 * sms * kTopK * 8 + (size_t)bp * kTopK * 8);
   std::vector<int64_t> host(2 * (h->chunks.size() + 1));
   int64_t tb = 0;
   for (size_t c = 0; c < h->chunks.size(); ++c) {
@@ -1239,16 +1243,32 @@ extern "C" xmc_status xmc_head_topk(xmc_head_t h, const void* W, const float* X,
     p.cand_l = h->cand_l + static_cast<size_t>(s0) * nslots * kTopK;
     p.label0 = h->desc.label_offset;
     p.status = h->status;
-    xmc_status r = XMC_ERR_UNSUPPORTED;
-    if (eb == 1) {
-      if (bn == 128) r = launch_topk_t<1, 128>(h, tw, tx, p, st);
-      else if (bn == 256) r = launch_topk_t<1, 256>(h, tw, tx, p, st);
-    } else {
-      if (bn == 64) r = launch_topk_t<2, 64>(h, tw, tx, p, st);
-      else if (bn == 128) r = launch_topk_t<2, 128>(h, tw, tx, p, st);
-      else if (bn == 256) r = launch_topk_t<2, 256>(h, tw, tx, p, st);
+    auto run = [&](const FwdParams& q) -> xmc_status {
+      xmc_status r = XMC_ERR_UNSUPPORTED;
+      if (eb == 1) {
+        if (bn == 128) r = launch_topk_t<1, 128>(h, tw, tx, q, st);
+        else if (bn == 256) r = launch_topk_t<1, 256>(h, tw, tx, q, st);
+      } else {
+        if (bn == 64) r = launch_topk_t<2, 64>(h, tw, tx, q, st);
+        else if (bn == 128) r = launch_topk_t<2, 128>(h, tw, tx, q, st);
+        else if (bn == 256) r = launch_topk_t<2, 256>(h, tw, tx, q, st);
+      }
+      return r == XMC_ERR_UNSUPPORTED ? fail(r, "no top-k kernel for padded batch %d", Bp) : r;
+    };
+    // Prologue on every 16th work unit (a strided label sample): its top-8
+    // per sample bounds the final 8th score from below, so the full pass
+    // skips almost every block in its pre-filter (the lists of one warp see
+    // too few labels to warm up on their own)
+    constexpr int kPreStride = 16;
+    if (p.num_tiles >= 64 * kPreStride) {
+      FwdParams q = p;
+      q.unit_mul = kPreStride;
+      XMC_TRY(run(q));
+      topk_merge_kernel<<<p.B, 256, 0, st>>>(p.cand_s, p.cand_l, nslots, kTopK, h->topk_pre_s, h->topk_pre_l);
+      CUDA_TRY(cudaGetLastError());
+      p.topk_bound = h->topk_pre_s;
     }
-    if (r != XMC_OK) return r == XMC_ERR_UNSUPPORTED ? fail(r, "no top-k kernel for padded batch %d", Bp) : r;
+    XMC_TRY(run(p));
   }
   topk_merge_kernel<<<B, 256, 0, st>>>(h->cand_s, h->cand_l, nslots, k, top_scores, top_labels);
   CUDA_TRY(cudaGetLastError());

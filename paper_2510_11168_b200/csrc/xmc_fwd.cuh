@@ -66,6 +66,8 @@ struct FwdParams {
   // kTopK best (score, global label) of that warp's rows, [Bp][nslots][kTopK]
   float* cand_s;
   int32_t* cand_l;
+  int32_t unit_mul;          // TOPK prologue: only every unit_mul-th work unit (a strided label sample)
+  const float* topk_bound;   // TOPK: [B][8] top-8 scores of that sample (slot 7 <= the final 8th), or null
   int64_t label0;            // global label of local row 0 of this launch
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
   int32_t sample0;           // first sample of this pass (batch split into BN-wide passes); entries of
@@ -160,7 +162,9 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   // work units: single tiles, or tile pairs (2u, 2u+1) for a CTA pair
-  const int num_units = PAIR ? (p.num_tiles + 1) / 2 : p.num_tiles;
+  // (unit_mul > 1: the top-k prologue visits units 0, unit_mul, 2 unit_mul, ...)
+  const int umul = p.unit_mul > 1 ? p.unit_mul : 1;
+  const int num_units = ((PAIR ? (p.num_tiles + 1) / 2 : p.num_tiles) + umul - 1) / umul;
   // Xq rows (samples) this CTA stages
   const int xrow0 = PAIR ? static_cast<int>(rank) * C::kXRows : 0;
 
@@ -244,7 +248,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
       const int st_i = n % C::kStages;
       const int u = unit0 + (n / kc_count) * ustride;
       const int kc = n % kc_count;
-      const int tile = PAIR ? 2 * u + static_cast<int>(rank) : u;
+      const int tile = PAIR ? 2 * u * umul + static_cast<int>(rank) : u * umul;
       uint8_t* sb = stage_base + st_i * C::kStageBytes;
       const bool active = it < cnt;
       if (active && b == 0) {
@@ -339,7 +343,26 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
         ls[cc][i] = -INFINITY;
         ll[cc][i] = 0x7fffffff;
       }
-    auto tile_of = [&](int u) { return PAIR ? 2 * u + static_cast<int>(rank) : u; };
+    // Pre-filter without the transpose.  Each lane's sample threshold (its
+    // list's k-th score, raised to just below the prologue's bound) is
+    // mirrored in shared memory (the positives bitmap region, unused here:
+    // 16 x BN bytes = warps x chunks x 32 floats), so a 32 x 32 block whose
+    // scores are all <= the thresholds costs 8 broadcast LDS.128 and 32
+    // compares instead of the 5-stage shuffle transpose.  Blocks with a
+    // candidate take the exact transpose + insert path (same strict ">").
+    // The bound: the prologue's 8th score over a strided label sample is <=
+    // the final 8th score, so an item under it cannot reach the top-k; one
+    // EQUAL to it still can (lower-label tie rule), hence nextafter(-inf).
+    float* th_s = reinterpret_cast<float*>(bitmap) + ew * C::kChunks * 32;
+#pragma unroll
+    for (int cc = 0; cc < C::kChunks; ++cc) {
+      const int sc = grp * C::kColsPerWarp + cc * 32 + lane;
+      float t0 = INFINITY;
+      if (sc < p.B) t0 = p.topk_bound ? nextafterf(p.topk_bound[sc * kTopK + kTopK - 1], -INFINITY) : -INFINITY;
+      th_s[cc * 32 + lane] = t0;
+    }
+    __syncwarp();
+    auto tile_of = [&](int u) { return PAIR ? 2 * u * umul + static_cast<int>(rank) : u * umul; };
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = unit0; u < num_units; u += ustride) {
@@ -357,6 +380,19 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, r);
         tmem_ld_wait();
+        {
+          // lane = row here: r[c] = score(row, sample col0 + c)
+          bool cand = false;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4) {
+            const float4 t = *reinterpret_cast<const float4*>(th_s + cc * 32 + 4 * c4);
+            cand |= __uint_as_float(r[4 * c4 + 0]) > t.x;
+            cand |= __uint_as_float(r[4 * c4 + 1]) > t.y;
+            cand |= __uint_as_float(r[4 * c4 + 2]) > t.z;
+            cand |= __uint_as_float(r[4 * c4 + 3]) > t.w;
+          }
+          if (!__any_sync(0xffffffffu, cand && lane < vrows)) continue;
+        }
         // butterfly transpose: afterwards r[i] of lane c = score(row i, sample col0 + c)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -370,7 +406,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
             r[i | o] = up ? b : recv;
           }
         }
-        const float th = ls[cc][kTopK - 1];
+        const float th = th_s[cc * 32 + lane];
         uint32_t pm = 0u;
 #pragma unroll
         for (int i = 0; i < 32; ++i) pm |= (__uint_as_float(r[i]) > th ? 1u : 0u) << i;
@@ -387,6 +423,8 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
             topk_insert(ls[cc], ll[cc], rv[i], lab0 + i);
           }
         }
+        if (col0 + lane < p.B) th_s[cc * 32 + lane] = fmaxf(th, ls[cc][kTopK - 1]);
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -433,7 +471,7 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
     constexpr bool kScaled = EB == 1 && GOUT != G_REF && GOUT != G_BF16;
     int acc = 0;
     uint32_t acc_phase = 0;
-    auto tile_of = [&](int u) { return PAIR ? 2 * u + static_cast<int>(rank) : u; };
+    auto tile_of = [&](int u) { return PAIR ? 2 * u * umul + static_cast<int>(rank) : u * umul; };
     // tile_ptr bounds of the first tile; the next tile's are prefetched below
     int e0 = 0, e1 = 0;
     if (use_pos && unit0 < num_units && tile_of(unit0) < p.num_tiles) {
