@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--ref-steps", type=int, default=5,
                     help="timed steps of the reference-precision mode reported beside the headline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--bf16g-steps", type=int, default=5,
+                    help="timed steps of the bf16-G mode (the paper's BF16 logit gradients) reported beside "
+                         "the headline (0: skip)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--cpu-labels", type=int, default=8192)
     ap.add_argument("--no-cpu", action="store_true")
@@ -490,6 +493,31 @@ def main():
                             "exact bf16 planes, kind::f16 backward GEMMs (device-resident inputs)"}
         head.precision = a.precision
 
+    # ---------------- the bf16-G operand mode (FP8 weights, BF16 logit
+    # gradients as in the paper; e4m3 heads) on the same workload
+    bf16g = None
+    if a.bf16g_steps > 0 and world == 1 and a.fmt == "e4m3" and a.precision == "operand" \
+            and a.g_format != "bf16" and a.batch <= 256 and not a.kahan:
+        hg = xmc.ChunkedHead(xmc.QuantizedMatrix(W, fmt), num_chunks=a.chunks, num_labels_global=a.labels,
+                             label_offset=lo, precision="operand", g_format="bf16")
+        for s in range(2):
+            xmc.head_update(hg, batch_dev, cfg, rng, 30_000 + s, grad_out=gx, check=False)
+        torch.cuda.synchronize()
+        b0_, b1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0_.record(stream)
+        for s in range(a.bf16g_steps):
+            xmc.head_update(hg, batch_dev, cfg, rng, 30_100 + s, grad_out=gx, check=False)
+        b1_.record(stream)
+        torch.cuda.synchronize()
+        ms_b = b0_.elapsed_time(b1_) / a.bf16g_steps
+        _lib.check(_lib.load().xmc_head_check(hg.handle(a.batch, len(si)).h, _lib.stream_ptr()))
+        bf16g = {"value": a.batch / (ms_b * 1e-3), "unit": "samples/s", "ms_per_step": ms_b,
+                 "steps": a.bf16g_steps,
+                 "what": "same step with ChunkedHead(precision='operand', g_format='bf16'): FP8 weights with BF16 "
+                         "logit gradients (the paper's Algorithm 1), kind::f16 backward GEMMs on bf16 operand "
+                         "tiles (device-resident inputs)"}
+        del hg
+
     # ---------------- roofline of the dominant kernel
     peaks = load_peaks()
     L_r, B, D = hi - lo, a.batch, a.dim
@@ -574,6 +602,7 @@ def main():
            "roofline": roof,
            "grad_x_allreduce": gx_allreduce[0],
            "reference_precision": ref_prec,
+           "bf16_g_precision": bf16g,
            "step_tflops": step_flops / (ms_step * 1e-3) / 1e12,
            # against dense FP8 at B200's nominal 4.5 PF and the measured
            # torch._scaled_mm FP8 GEMM (profiles/fp8_peak.json, burst)
@@ -585,9 +614,9 @@ def main():
            "peak_hbm_gib_per_gpu": peak_mem / 2**30,
            # our kernels in the timed region: every fwd / bwd launch (counted by the
            # library's profiler) + per step: x_prep fused with single-CTA bucketing
-           # for <= 2048 positives, else x_prep fused with counting + scan +
+           # for <= 12,288 positives, else x_prep fused with counting + scan +
            # scatter; and the grad_X reduce (peer all-reduce kernel for N > 1)
-           "gpu_launches": int(n_fwd + n_bwd + a.steps * ((1 if len(si) <= 2048 else 3) + 1)),
+           "gpu_launches": int(n_fwd + n_bwd + a.steps * ((1 if len(si) <= 12288 else 3) + 1)),
            "clocks": clk}
     if rank == 0 and world == 1 and not a.no_cpu:
         cb = cpu_baseline(a, a.cpu_seconds)
