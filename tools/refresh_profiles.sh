@@ -28,11 +28,11 @@ tail -1 $out/bench_$tag.json
 tail -1 $out/bench_ref_$tag.json
 timeout 300 python bench.py --steps 1000 --no-cpu --e2e-steps 2 --ref-steps 0 > $out/bench_sustained_$tag.json 2>/dev/null
 timeout 300 python tools/bench_topk.py > $out/topk_$tag.json 2>/dev/null
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:xmc_fwd_kernel -c 1 -f \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:xmc_fwd_kernel --launch-skip 1 -c 1 -f \
   -o $out/prof_topk_$tag python tools/bench_topk.py --iters 1 > /dev/null 2>&1
 python tools/ncu_summary.py $out/prof_topk_$tag.ncu-rep --flops $(python -c "print(2*256*2812281*768)") --json $out/ncu_topk_$tag.json > /dev/null
 rm -f $out/prof_topk_$tag.ncu-rep
-for cfg in "c2:--labels 131073 --batch 512 --fmt bf16" "c3:--labels 670091" "c5r0:--labels 1077981 --batch 128" "c4b512:--batch 512"; do
+for cfg in "c2:--labels 131073 --batch 512 --fmt bf16" "c3:--labels 670091" "c5r0:--labels 1077981 --batch 128" "c4b512:--batch 512" "c4s8:--labels 351536" "c4kahan_top10:--kahan bf16 --kahan-labels 281228" "c4kahan_all:--kahan bf16" "c4bf16g:--g-format bf16"; do
   t=${cfg%%:*}; args=${cfg#*:}
   timeout 300 python bench.py --no-cpu --ref-steps 0 --e2e-steps 2 $args 2>/dev/null | tail -1 >> $out/configs_$tag.jsonl
 done
