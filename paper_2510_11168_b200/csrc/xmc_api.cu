@@ -780,7 +780,7 @@ static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int
   // producer loads one while the other multiplies
   // (also the one-plane bf16-G backward of an e4m3 head: N = 128 groups free
   // the 6-slot G ring half a tile at a time)
-  const bool acc_planes = gxp == 1 && (h->planes > 1 || (h->ref && h->eb == 1));
+  const bool acc_planes = gxp == 1 && (h->planes > 1 || (h->ref && h->eb == 1) || (h->eb == 2 && Bp == 256));
   p.gx_group = acc_planes ? std::min(2, Bp / box_k) : gx_kc_count;
   p.gx_cols = acc_planes ? Bp : gx_kc_count * box_k;
   p.g_prefetch = h->ref ? 1 : 0;

@@ -115,7 +115,9 @@ struct BwdCfg {
   // e4m3: 4 W stages (224 KB with the staging tiles; 3 -> 4 measured -1.5 %
   // bwd); the G ring (6 slots = 3 tiles) must not get shallower (4 slots: +10 %)
   // (staged compensation: 2 stages of W + comp and a 4-slot G ring fit 227 KB)
-  static constexpr int kWStages = CS ? 2 : (kW8 ? (KCMAX > 2 ? 2 : 4) : (EB == 1 ? 4 : 3));
+  // (bf16 head, batch 256: 2 W stages free room for a 6-slot G ring, 1.5 tiles)
+  static constexpr bool kBf16Deep = EB == 2 && !kW8 && XT_RES && KCMAX == 4;
+  static constexpr int kWStages = CS ? 2 : (kW8 ? (KCMAX > 2 ? 2 : 4) : (EB == 1 ? 4 : (kBf16Deep ? 2 : 3)));
   static constexpr int kCompBytes = CS * kBox;        // [128 rows x 128 cols] comp tile (CS = 2: two boxes)
   static constexpr int kWStride = kWBytes + kCompBytes;
   static constexpr int kOutBytes = kOutTiles * kWBytes;
@@ -125,7 +127,7 @@ struct BwdCfg {
   // KCMAX = 0: the grad_X-only pass of a batch > 256 (no Xq^T, no update):
   // the freed space deepens the G ring to two tiles
   static constexpr int kKStages = KCMAX == 0 ? (EB == 1 ? 6 : 8)
-                                             : (kW8 ? 6 : (EB == 1 ? ((KCMAX > 2 || CS) ? 4 : 6) : 4));
+                                             : ((kW8 || kBf16Deep) ? 6 : (EB == 1 ? ((KCMAX > 2 || CS) ? 4 : 6) : 4));
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
   static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2 + 2 + 2) + 16;
   static constexpr int kSmemBytes =
