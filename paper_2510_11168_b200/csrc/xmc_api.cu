@@ -845,7 +845,8 @@ static xmc_status launch_bwd_v(xmc_head* h, const BwdLaunch& L, cudaStream_t st)
   // (XMC_BWD_GENERAL=1: test knob, the general instantiation for everything,
   // so tests can compare the fast specialisations against it bit for bit)
   static const bool force_general = getenv("XMC_BWD_GENERAL") != nullptr;
-  const bool fast_ok = p.do_update && p.rounding == ROUND_SR_FAST && p.keep == nullptr && !force_general;
+  const bool fast_ok = p.do_update && (p.rounding == ROUND_SR_FAST || p.rounding == ROUND_NEAREST) &&
+                       p.keep == nullptr && !force_general;
   // the fast head-Kahan (bf16 compensation staged by TMA with the W tile)
   if constexpr (EB == 1 && GE == 1 && XR && KC <= 2)
     if (ce == 2 && fast_ok) return launch_bwd_k<1, XR, KC, 2, true, false, 1, 1>(h, L, st);

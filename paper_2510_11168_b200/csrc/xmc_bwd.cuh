@@ -461,7 +461,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   constexpr int WS = C::kWStages;
   constexpr int KS = C::kKStages;
   const int bid = static_cast<int>(blockIdx.x), nblk = static_cast<int>(gridDim.x);
-  const int rounding = FAST ? static_cast<int>(ROUND_SR_FAST) : p.rounding;
+  // FAST: SR_FAST or RTN (a warp-uniform branch at the rounding step)
+  const int rounding = p.rounding;
+  const bool fast_sr = !FAST || rounding == ROUND_SR_FAST;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -932,14 +934,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           __syncwarp();
           if (lane_id() == 0) mbar_arrive(&w_empty[wsi]);
           uint32_t rw[8];
-          sr_words<1>(pk, flat0, rw, p.sr_bits != 0);
+          if (fast_sr) sr_words<1>(pk, flat0, rw, p.sr_bits != 0);
           if (gstorer && stored) bulk_wait_read<0>();
           named_bar_sync(1 + q + 4 * g, 64);
           mbar_wait_sleep(&t_full[g], dphi);
           tc_fence_after();
 #pragma unroll
           for (int cg = 0; cg < 2; ++cg) {
-            if (cg == 1) sr_words<1>(pk, flat0 + 32, rw, p.sr_bits != 0);
+            if (cg == 1 && fast_sr) sr_words<1>(pk, flat0 + 32, rw, p.sr_bits != 0);
             uint32_t pk8[8];
 #pragma unroll
             for (int qt = 0; qt < 2; ++qt) {
@@ -969,7 +971,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                   y[x] = v - c[x];
                   t[x] = w[x] + y[x];
                 }
-                const uint32_t w4 = cvt_e4m3x4_rs(t[3], t[2], t[1], t[0], rw[qt * 4 + k4]);
+                const uint32_t w4 = fast_sr ? cvt_e4m3x4_rs(t[3], t[2], t[1], t[0], rw[qt * 4 + k4])
+                                            : (cvt_e4m3x2_rn(t[1], t[0]) |
+                                               (static_cast<uint32_t>(cvt_e4m3x2_rn(t[3], t[2])) << 16));
                 pk8[qt * 4 + k4] = w4;
                 const float2 r01 = dec_e4m3x2(static_cast<uint16_t>(w4 & 0xFFFF));
                 const float2 r23 = dec_e4m3x2(static_cast<uint16_t>(w4 >> 16));
@@ -1023,7 +1027,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int k = 0; k < 32; ++k) wc[k] = 0.f;
           return;
 #endif
-          sr_words<1>(pk, flat0 + cg * 32, rw, p.sr_bits != 0);
+          if (fast_sr) sr_words<1>(pk, flat0 + cg * 32, rw, p.sr_bits != 0);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const uint4 r4 = raw[2 * cg + h];
@@ -1060,7 +1064,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                        f2pack(a_lr, a_lr), f2pack(wc[4 * k + e], wc[4 * k + e + 1]));
               f2unpack(r, u[e], u[e + 1]);
             }
-            pk8[k] = cvt_e4m3x4_rs(u[3], u[2], u[1], u[0], rw[k]);
+            pk8[k] = fast_sr ? cvt_e4m3x4_rs(u[3], u[2], u[1], u[0], rw[k])
+                             : (cvt_e4m3x2_rn(u[1], u[0]) | (static_cast<uint32_t>(cvt_e4m3x2_rn(u[3], u[2])) << 16));
           }
           const int cc = cw0 + cg * 32;
           sts128(ot_s + w_chunk_off<EB>(row, cc, 0), make_uint4(pk8[0], pk8[1], pk8[2], pk8[3]));
