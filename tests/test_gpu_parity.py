@@ -729,8 +729,8 @@ def test_fused_topk_rejects_large_k(xmc):
         head.topk(torch.zeros((4, 128)), 0)
 
 
-@pytest.mark.parametrize("fmt_name,B", [("e4m3", 256), ("bf16", 100)])
-def test_fused_topk_prologue_bound_with_massive_ties(xmc, fmt_name, B):
+@pytest.mark.parametrize("fmt_name,B,offset", [("e4m3", 256, 0), ("bf16", 100, 0), ("e4m3", 40, 777_777)])
+def test_fused_topk_prologue_bound_with_massive_ties(xmc, fmt_name, B, offset):
     """Large enough for the top-k prologue (>= 1024 tiles: a strided label
     sample bounds every sample's final 8th score from below, and the full
     pass skips blocks under that bound).  W rows come from a pool of 40
@@ -743,11 +743,13 @@ def test_fused_topk_prologue_bound_with_massive_ties(xmc, fmt_name, B):
     pool = O.round_nearest(fmt, rs.normal(scale=0.05, size=(40, d)).astype(np.float32))
     W = pool[rs.integers(0, 40, size=L)]
     X = rs.normal(size=(B, d)).astype(np.float32)
-    head = _make(xmc, W, fmt_name, 1)
+    f = xmc.parse_format(fmt_name)
+    head = xmc.ChunkedHead(xmc.QuantizedMatrix(xmc.cast_native(torch.from_numpy(W).cuda(), f), f),
+                           num_labels_global=offset + L, label_offset=offset)
     sc = head.scores(torch.from_numpy(X)).cpu().numpy()
     for k in (1, 5, 8):
         vals, labs = head.topk(torch.from_numpy(X), k)
         labs = labs.cpu().numpy()
         for s in range(B):
-            ref = O.top_k_indices(sc[s], k)
+            ref = O.top_k_indices(sc[s], k) + offset
             assert np.array_equal(labs[s], ref), (k, s, labs[s], ref)
