@@ -495,27 +495,29 @@ def test_step_edge_cases(xmc):
     assert torch.equal(before.view(torch.int16), head.weights.values.view(torch.int16))
 
 
-def test_multi_cta_bucketing_steps_and_errors(xmc):
-    """More than 2048 positives take the multi-CTA path (x_prep fused with the
-    counting pass, scan re-zeroing the counters for the next step): three
+@pytest.mark.parametrize("B,mean,multi", [(96, 40.0, False), (256, 60.0, True)])
+def test_bucketing_paths_steps_and_errors(xmc, B, mean, multi):
+    """Up to 12,288 positives are bucketed by one CTA in the prep launch;
+    more take the multi-CTA path (x_prep fused with the counting pass, scan
+    re-zeroing the counters for the next step).  On each path: three
     consecutive steps with different positive lists match the oracle, and a
-    bad sample index / non-finite X on that path leave W untouched."""
-    L, d, B = 3000, 128, 96
+    bad sample index / non-finite X leave W untouched."""
+    L, d = 3000, 128
     fmt, W, X, _, _ = _rand_problem(L, d, B, "bf16", 43)
     cfg = xmc.SgdSrConfig(lr=0.05, fmt=xmc.BF16, rounding="nearest")
     cfg_o = O.SgdSrConfig(lr=0.05, fmt=O.BF16, rounding="nearest")
     head = _make(xmc, W, "bf16", 2)
     oh = O.OracleHead(W.copy(), O.BF16, 2)
     for step in range(3):
-        si, li = O.synthetic_positives(L, B, 40.0, seed=100 + step)
-        assert len(si) > 2048
+        si, li = O.synthetic_positives(L, B, mean, seed=100 + step)
+        assert (len(si) > 12288) == multi and len(si) > 2048
         gx = xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(0), step)
         gx_o = O.head_update(oh, X, si, li, cfg_o, O.RoundingRng(0), step, g_quant=True)
         np.testing.assert_allclose(gx.cpu().numpy(), gx_o, rtol=1e-3, atol=2e-3)
         got = head.weights.values.float().cpu().numpy()
         assert np.mean(bits(got) == bits(oh.values)) > 0.98
         head.weights.values.copy_(xmc.cast_native(torch.from_numpy(oh.values).cuda(), xmc.BF16))
-    si, li = O.synthetic_positives(L, B, 40.0, seed=7)
+    si, li = O.synthetic_positives(L, B, mean, seed=7)
     before = head.weights.values.clone()
     with pytest.raises(IndexError):
         xmc.head_update(head, xmc.BatchInput(X, np.concatenate([si, [B]]), np.concatenate([li, [0]])), cfg,
