@@ -536,9 +536,18 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
           // g256 = 256 sigmoid(z) = 1 / y, y = 2^-8 (1 + 2^(-z log2 e))
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
-            // e clamped to 2^100 keeps y finite (g then rounds to 0 in e4m3)
-            const float ea = fminf(fast_ex2(__uint_as_float(r[j]) * zk), 1.2676506e30f);
-            const float eb = fminf(fast_ex2(__uint_as_float(r[j + 1]) * zk), 1.2676506e30f);
+            float za, zb;
+            f2unpack(fmul2(f2pack(__uint_as_float(r[j]), __uint_as_float(r[j + 1])), f2pack(zk, zk)), za, zb);
+            // e clamped to 2^100 keeps y finite (g then rounds to 0 in e4m3).
+            // e5m2 needs no clamp: an infinite / huge e makes the Newton
+            // iterate NaN or -inf, and the 2^-16 clip below (fmaxf returns
+            // the non-NaN operand) yields exactly the clipped value 256 * 2^-24
+            // that sigmoid(z) < 2^-100 has in the reference
+            float ea = fast_ex2(za), eb = fast_ex2(zb);
+            if constexpr (GOUT != G_E5M2) {
+              ea = fminf(ea, 1.2676506e30f);
+              eb = fminf(eb, 1.2676506e30f);
+            }
             const uint64_t y = ffma2(f2pack(ea, eb), f2pack(0.00390625f, 0.00390625f),
                                      f2pack(0.00390625f, 0.00390625f));
             float y0, y1;
