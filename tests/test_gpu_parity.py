@@ -755,3 +755,31 @@ def test_fused_topk_prologue_bound_with_massive_ties(xmc, fmt_name, B, offset):
         for s in range(B):
             ref = O.top_k_indices(sc[s], k) + offset
             assert np.array_equal(labs[s], ref), (k, s, labs[s], ref)
+
+
+@pytest.mark.parametrize("fmt_name,precision", [("e4m3", "operand"), ("bf16", "reference")])
+def test_checkpoint_resume_is_bitwise(xmc, tmp_path, fmt_name, precision):
+    """SURVEY F3 / test_trainer.py:71-83: training 3 steps, saving, loading
+    into a fresh head and training 3 more gives the same weights, bit for
+    bit, as 6 uninterrupted steps (keyed SR: the draws depend only on seed,
+    step and global row, not on the process history)."""
+    L, d, B = 2000, 256, 128
+    fmt, W, X, si, li = _rand_problem(L, d, B, fmt_name, 91)
+    f = xmc.parse_format(fmt_name)
+    cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=f, rounding="stochastic", sr_impl="hash")
+
+    def steps(head, s0, s1):
+        for s in range(s0, s1):
+            xs = np.roll(X, s, axis=0)
+            xmc.head_update(head, xmc.BatchInput(xs, si, li), cfg, xmc.RoundingRng(3), s)
+
+    a = _make(xmc, W, fmt_name, 2, precision=precision)
+    steps(a, 0, 6)
+    b = _make(xmc, W, fmt_name, 2, precision=precision)
+    steps(b, 0, 3)
+    xmc.save_head(b, str(tmp_path / "h.lpxh"))
+    c = xmc.load_head(str(tmp_path / "h.lpxh"), num_chunks=2, precision=precision)
+    steps(c, 3, 6)
+    va = a.weights.values.view(torch.uint8 if fmt_name == "e4m3" else torch.int16)
+    vc = c.weights.values.view(torch.uint8 if fmt_name == "e4m3" else torch.int16)
+    assert torch.equal(va, vc)
