@@ -995,14 +995,16 @@ static void launch_prep(xmc_head* h, const float* X, int Bp, const PosGeom& g, c
     // up to 12k positives: one launch (block 0 buckets in shared memory, the rest prepare Xq)
     smem_attr_once<prep_bucket_kernel<EB, XTB>>(kPosMaxTiles * 4);
     const int nblk = 1 + (D / 32) * (Bp / 32);
-    prep_bucket_kernel<EB, XTB><<<nblk, 1024, T * 4, st>>>(X, B, Bp, D, h->xq, h->xqt, g, ps, pl, nnz, T, h->tile_ptr,
-                                                          h->entries, h->status);
+    // (programmatic launch: its CTAs start as the previous step's reduce
+    // vacates SMs, then wait in griddepcontrol.wait)
+    launch_ex(prep_bucket_kernel<EB, XTB>, nblk, 1024, T * 4, st, h, 1, X, B, Bp, D, h->xq, h->xqt, g, ps, pl, nnz, T,
+              h->tile_ptr, h->entries, h->status);
     return;
   }
   const int blocks = static_cast<int>(cdiv(nnz, 256));
   const int nx = (D / 32) * (Bp / 32);
-  prep_count_kernel<EB, XTB><<<nx + blocks, 256, 0, st>>>(X, B, Bp, D, h->xq, h->xqt, nx, g, ps, pl, nnz,
-                                                         h->tile_cnt, h->tmp_tile, h->tmp_entry, h->status);
+  launch_ex(prep_count_kernel<EB, XTB>, nx + blocks, 256, 0, st, h, 1, X, B, Bp, D, h->xq, h->xqt, nx, g, ps, pl, nnz,
+            h->tile_cnt, h->tmp_tile, h->tmp_entry, h->status);
   smem_attr_once<pos_scan_kernel>(kPosMaxTiles * 4);
   pos_scan_kernel<<<1, 1024, T <= kPosMaxTiles ? T * 4 : 0, st>>>(h->tile_cnt, h->tile_ptr, h->tile_cur, T);
   pos_scatter_kernel<<<blocks, 256, 0, st>>>(nnz, h->tmp_tile, h->tmp_entry, h->tile_cur, h->entries);

@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(256) prep_count_kernel(const float* __restrict
                                                          const int32_t* __restrict__ pl, int64_t nnz,
                                                          int32_t* __restrict__ cnt, uint32_t* __restrict__ tmp_tile,
                                                          uint32_t* __restrict__ tmp_entry, int32_t* status) {
+  griddep_wait();   // a PDL dependent of the previous step's last kernel
   if (static_cast<int>(blockIdx.x) < nx) {
     x_prep_body<EB, XTB>(X, B, Bp, d, xq, xqt, status, blockIdx.x % (d / 32), blockIdx.x / (d / 32), threadIdx.x & 31,
                     threadIdx.x >> 5, 8);
@@ -453,6 +454,7 @@ __global__ void __launch_bounds__(1024) prep_bucket_kernel(const float* __restri
                                                            const int32_t* __restrict__ pl, int64_t nnz, int32_t T,
                                                            int32_t* __restrict__ tile_ptr,
                                                            uint32_t* __restrict__ entries, int32_t* status) {
+  griddep_wait();   // a PDL dependent of the previous step's last kernel
   if (blockIdx.x == 0) {
     pos_bucket_body(g, ps, pl, nnz, T, tile_ptr, entries, status);
     return;
