@@ -1006,8 +1006,10 @@ static void launch_prep(xmc_head* h, const float* X, int Bp, const PosGeom& g, c
   launch_ex(prep_count_kernel<EB, XTB>, nx + blocks, 256, 0, st, h, 1, X, B, Bp, D, h->xq, h->xqt, nx, g, ps, pl, nnz,
             h->tile_cnt, h->tmp_tile, h->tmp_entry, h->status);
   smem_attr_once<pos_scan_kernel>(kPosMaxTiles * 4);
-  pos_scan_kernel<<<1, 1024, T <= kPosMaxTiles ? T * 4 : 0, st>>>(h->tile_cnt, h->tile_ptr, h->tile_cur, T);
-  pos_scatter_kernel<<<blocks, 256, 0, st>>>(nnz, h->tmp_tile, h->tmp_entry, h->tile_cur, h->entries);
+  launch_ex(pos_scan_kernel, 1, 1024, T <= kPosMaxTiles ? T * 4 : 0, st, h, 1, h->tile_cnt, h->tile_ptr, h->tile_cur,
+            T);
+  launch_ex(pos_scatter_kernel, blocks, 256, 0, st, h, 1, nnz, static_cast<const uint32_t*>(h->tmp_tile),
+            static_cast<const uint32_t*>(h->tmp_entry), h->tile_cur, h->entries);
 }
 
 static xmc_status prepare_step(xmc_head* h, const float* X, int Bp, const int32_t* ps, const int32_t* pl,

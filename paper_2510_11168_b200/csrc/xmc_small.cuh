@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(1024) pos_scan_kernel(int32_t* __restrict__ cn
                                                         int32_t* __restrict__ cur, int32_t T) {
   extern __shared__ int32_t sc_smem[];   // [T] when T <= kPosMaxTiles
   __shared__ int32_t wsum[32];
+  griddep_wait();   // PDL dependent of the counting pass
   const bool staged = T <= kPosMaxTiles;
   int32_t* sc = staged ? sc_smem : cnt;
   const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, w = tid >> 5;
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(1024) pos_scan_kernel(int32_t* __restrict__ cn
 __global__ void __launch_bounds__(256) pos_scatter_kernel(int64_t nnz, const uint32_t* __restrict__ tmp_tile,
                                                           const uint32_t* __restrict__ tmp_entry,
                                                           int32_t* __restrict__ cursor, uint32_t* __restrict__ entries) {
+  griddep_wait();   // PDL dependent of the scan
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   uint32_t key = 0xffffffffu, val = 0;
   if (i < nnz) {
