@@ -134,3 +134,19 @@ def test_integration_stub_matches_the_abi():
 
     assert fields("_Desc") == list(_lib.HeadDesc._fields_)
     assert fields("_Step") == list(_lib.StepArgs._fields_)
+
+
+def test_bench_reference_arm_line():
+    """`bench.py --impl reference` (the driver's reference arm) runs on the
+    host cores without a GPU and prints the contract's JSON line."""
+    import json
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0", "--cpu-seconds", "0.5", "--cpu-labels", "512"],
+                         capture_output=True, text=True, timeout=600, check=True).stdout
+    d = json.loads(out.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["unit"] == "samples/s" and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    assert d["config"]["labels"] == 2_812_281 and d["metric"] == "head train samples/sec at 3M labels FP8"
