@@ -339,9 +339,10 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   // operands in shared memory
   const bool ref = d->precision == XMC_PRECISION_REFERENCE ||
                    (eb == 1 && d->g_format == XMC_FMT_BF16);
-  if (ref && eb == 1 && bp > 256)
-    return fail(XMC_ERR_UNSUPPORTED, "bf16-G backward of an e4m3 head supports batch <= 256 (got %d)",
-                d->max_batch);
+  if (ref && eb == 1 && bp > 512)
+    return fail(XMC_ERR_UNSUPPORTED,
+                "the bf16-operand backward of an e4m3 head (reference precision, bf16 G) supports batch <= 512 "
+                "(got %d)", d->max_batch);
   const int planes = d->precision == XMC_PRECISION_REFERENCE ? 3 : 1;
   const int beb = ref ? 2 : eb;
   auto ch = partition(d->num_labels_local, d->num_chunks);
@@ -780,7 +781,8 @@ static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int
   // producer loads one while the other multiplies
   // (also the one-plane bf16-G backward of an e4m3 head: N = 128 groups free
   // the 6-slot G ring half a tile at a time)
-  const bool acc_planes = gxp == 1 && (h->planes > 1 || (h->ref && h->eb == 1) || (h->eb == 2 && Bp == 256));
+  // (only while the whole padded batch fits the 256 grad_X TMEM columns)
+  const bool acc_planes = gxp == 1 && Bp <= 256 && (h->planes > 1 || (h->ref && h->eb == 1) || (h->eb == 2 && Bp == 256));
   p.gx_group = acc_planes ? std::min(2, Bp / box_k) : gx_kc_count;
   p.gx_cols = acc_planes ? Bp : gx_kc_count * box_k;
   p.g_prefetch = h->ref ? 1 : 0;
@@ -871,8 +873,12 @@ static xmc_status launch_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, in
     // reference precision of an e4m3 head: W stays e4m3 in HBM, each tile is
     // converted to bf16 operands in shared memory; three G planes, resident
     // Xq^T, rounding onto the e4m3 grid
-    if (Bp == 128) s = launch_bwd_v<2, true, 2, 1, 1>(h, L, st);
+    // batch 512: grad_X-only passes without Xq^T on a deep G ring, the
+    // update pass streams Xq^T with G
+    if (!update && gx_kc_count > 0 && Bp > 256) s = launch_bwd_v<2, true, 0, 1, 1>(h, L, st);
+    else if (Bp == 128) s = launch_bwd_v<2, true, 2, 1, 1>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<2, true, 4, 1, 1>(h, L, st);
+    else if (Bp == 512) s = launch_bwd_v<2, false, 8, 1, 1>(h, L, st);
   } else if (!update && gx_kc_count > 0 && Bp > 256) {
     // grad_X-only pass of a batch over 256 (the update rides on the last
     // pass): G boxes only, a two-tile G ring

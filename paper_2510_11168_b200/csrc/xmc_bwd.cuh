@@ -127,7 +127,8 @@ struct BwdCfg {
   // KCMAX = 0: the grad_X-only pass of a batch > 256 (no Xq^T, no update):
   // the freed space deepens the G ring to two tiles
   static constexpr int kKStages = KCMAX == 0 ? (EB == 1 ? 6 : 8)
-                                             : ((kW8 || kBf16Deep) ? 6 : (EB == 1 ? ((KCMAX > 2 || CS) ? 4 : 6) : 4));
+                                             : (kW8 ? (XT_RES ? 6 : 4)
+                                                    : (kBf16Deep ? 6 : (EB == 1 ? ((KCMAX > 2 || CS) ? 4 : 6) : 4)));
   static constexpr int kXtBytes = XT_RES ? KCMAX * kBox : 0;
   static constexpr int kBarBytes = 8 * (2 * kWStages + 2 * kKStages + 4 + 2 + 2 + 2) + 16;
   static constexpr int kSmemBytes =

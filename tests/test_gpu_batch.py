@@ -1,5 +1,6 @@
 """Batches above 256 samples (the reference takes any batch): e4m3 heads up to
-1024 samples, bf16 up to 1024.  The forward runs 256-sample passes of the
+1024 samples (512 in the bf16-operand modes: reference precision, bf16 G),
+bf16 up to 1024.  The forward runs 256-sample passes of the
 pair kernel; the backward accumulates grad_X in passes of 256 TMEM columns
 and applies the update on the last pass, so every pass reads the pre-update
 weights (head.py:290-291).
@@ -36,9 +37,10 @@ def _problem(L, d, B, fmt_name, seed):
     return fmt, W, X, si, li
 
 
-def _gpu_step(xmc, W, X, si, li, fmt_name, k, precision, rounding="stochastic", impl="splitmix64"):
+def _gpu_step(xmc, W, X, si, li, fmt_name, k, precision, rounding="stochastic", impl="splitmix64", g_format="e5m2"):
     fmt = xmc.parse_format(fmt_name)
-    head = xmc.ChunkedHead.from_float(torch.from_numpy(W), fmt, num_chunks=k, precision=precision)
+    head = xmc.ChunkedHead.from_float(torch.from_numpy(W), fmt, num_chunks=k, precision=precision,
+                                      g_format=g_format)
     cfg = xmc.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt, rounding=rounding, sr_impl=impl)
     gx = xmc.head_update(head, xmc.BatchInput(X, si, li), cfg, xmc.RoundingRng(5), 2)
     return head, gx
@@ -46,14 +48,16 @@ def _gpu_step(xmc, W, X, si, li, fmt_name, k, precision, rounding="stochastic", 
 
 @pytest.mark.parametrize("fmt_name,B,precision", [
     ("e4m3", 512, "operand"), ("e4m3", 1000, "operand"), ("bf16", 1024, "operand"), ("bf16", 700, "operand"),
-    ("bf16", 1024, "reference")])
+    ("bf16", 1024, "reference"), ("e4m3", 512, "reference"), ("e4m3", 400, "operand-bf16")])
 def test_large_batch_step_matches_oracle(xmc, fmt_name, B, precision):
     L, d, k = 700, 256, 2
     fmt, W, X, si, li = _problem(L, d, B, fmt_name, 31)
-    head, gx = _gpu_step(xmc, W, X, si, li, fmt_name, k, precision)
+    gfmt = "bf16" if precision == "operand-bf16" else "e5m2"
+    precision = "operand" if precision == "operand-bf16" else precision
+    head, gx = _gpu_step(xmc, W, X, si, li, fmt_name, k, precision, g_format=gfmt)
     oh = O.OracleHead(W.copy(), fmt, k)
     cfg_o = O.SgdSrConfig(lr=0.05, weight_decay=1e-4, fmt=fmt, rounding="stochastic")
-    g_quant = False if precision == "reference" else ("e5m2" if fmt_name == "e4m3" else True)
+    g_quant = False if precision == "reference" else (gfmt if fmt_name == "e4m3" else True)
     gx_o = O.head_update(oh, X, si, li, cfg_o, O.RoundingRng(5), 2, g_quant=g_quant)
     # bf16 operand G: a G value on the other side of a bf16 rounding boundary
     # (fp32 logits summed in another order) moves grad_X by ulp_bf16(G) |W|
@@ -77,7 +81,8 @@ def test_e4m3_batch_512_chunk_invariance_fast_path(xmc):
 
 
 def test_e4m3_reference_precision_batch_limit(xmc):
-    _, W, X, si, li = _problem(300, 128, 512, "e4m3", 51)
+    """The bf16-operand backward of an e4m3 head goes up to batch 512."""
+    _, W, X, si, li = _problem(300, 128, 600, "e4m3", 51)
     with pytest.raises(NotImplementedError):
         _gpu_step(xmc, W, X, si, li, "e4m3", 1, "reference")
 
