@@ -339,10 +339,6 @@ static xmc_status compute_layout(const xmc_head_desc* d, Layout* L, int* eb_out,
   // operands in shared memory
   const bool ref = d->precision == XMC_PRECISION_REFERENCE ||
                    (eb == 1 && d->g_format == XMC_FMT_BF16);
-  if (ref && eb == 1 && bp > 512)
-    return fail(XMC_ERR_UNSUPPORTED,
-                "the bf16-operand backward of an e4m3 head (reference precision, bf16 G) supports batch <= 512 "
-                "(got %d)", d->max_batch);
   const int planes = d->precision == XMC_PRECISION_REFERENCE ? 3 : 1;
   const int beb = ref ? 2 : eb;
   auto ch = partition(d->num_labels_local, d->num_chunks);
@@ -873,12 +869,13 @@ static xmc_status launch_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, in
     // reference precision of an e4m3 head: W stays e4m3 in HBM, each tile is
     // converted to bf16 operands in shared memory; three G planes, resident
     // Xq^T, rounding onto the e4m3 grid
-    // batch 512: grad_X-only passes without Xq^T on a deep G ring, the
-    // update pass streams Xq^T with G
+    // batch 512 / 1024: grad_X-only passes without Xq^T on a deep G ring,
+    // the update pass streams Xq^T with G
     if (!update && gx_kc_count > 0 && Bp > 256) s = launch_bwd_v<2, true, 0, 1, 1>(h, L, st);
     else if (Bp == 128) s = launch_bwd_v<2, true, 2, 1, 1>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<2, true, 4, 1, 1>(h, L, st);
     else if (Bp == 512) s = launch_bwd_v<2, false, 8, 1, 1>(h, L, st);
+    else if (Bp == 1024) s = launch_bwd_v<2, false, 16, 1, 1>(h, L, st);
   } else if (!update && gx_kc_count > 0 && Bp > 256) {
     // grad_X-only pass of a batch over 256 (the update rides on the last
     // pass): G boxes only, a two-tile G ring

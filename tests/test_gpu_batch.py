@@ -1,5 +1,5 @@
 """Batches above 256 samples (the reference takes any batch): e4m3 heads up to
-1024 samples (512 in the bf16-operand modes: reference precision, bf16 G),
+1024 samples (also in the bf16-operand modes: reference precision, bf16 G),
 bf16 up to 1024.  The forward runs 256-sample passes of the
 pair kernel; the backward accumulates grad_X in passes of 256 TMEM columns
 and applies the update on the last pass, so every pass reads the pre-update
@@ -48,7 +48,8 @@ def _gpu_step(xmc, W, X, si, li, fmt_name, k, precision, rounding="stochastic", 
 
 @pytest.mark.parametrize("fmt_name,B,precision", [
     ("e4m3", 512, "operand"), ("e4m3", 1000, "operand"), ("bf16", 1024, "operand"), ("bf16", 700, "operand"),
-    ("bf16", 1024, "reference"), ("e4m3", 512, "reference"), ("e4m3", 400, "operand-bf16")])
+    ("bf16", 1024, "reference"), ("e4m3", 512, "reference"), ("e4m3", 400, "operand-bf16"),
+    ("e4m3", 1000, "reference")])
 def test_large_batch_step_matches_oracle(xmc, fmt_name, B, precision):
     L, d, k = 700, 256, 2
     fmt, W, X, si, li = _problem(L, d, B, fmt_name, 31)
@@ -80,9 +81,9 @@ def test_e4m3_batch_512_chunk_invariance_fast_path(xmc):
     torch.testing.assert_close(gxa, gxb, rtol=1e-5, atol=1e-4)
 
 
-def test_e4m3_reference_precision_batch_limit(xmc):
-    """The bf16-operand backward of an e4m3 head goes up to batch 512."""
-    _, W, X, si, li = _problem(300, 128, 600, "e4m3", 51)
+def test_batch_limit(xmc):
+    """Batches up to 1024 in every mode; beyond that a clear error."""
+    _, W, X, si, li = _problem(300, 128, 1100, "e4m3", 51)
     with pytest.raises(NotImplementedError):
         _gpu_step(xmc, W, X, si, li, "e4m3", 1, "reference")
 
