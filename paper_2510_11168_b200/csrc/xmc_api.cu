@@ -215,7 +215,8 @@ static int elem_bytes(int fmt) { return fmt == XMC_FMT_E4M3 || fmt == XMC_FMT_E5
 // padded batch = N of the logits MMA = G leading dimension
 static int padded_batch(int eb, int B) {
   // > 256: the forward runs 256-sample passes, the backward grad_X passes of
-  // 256 TMEM columns (the update rides on the last); up to 1024 samples
+  // 256 TMEM columns (the update rides on the last); beyond 1024 samples the
+  // padded batch is the next multiple of 256 (entries keep a 16-bit sample)
   const int opts1[] = {128, 256, 512, 1024};
   const int opts2[] = {64, 128, 256, 512, 1024};
   if (eb == 1) {
@@ -223,6 +224,7 @@ static int padded_batch(int eb, int B) {
   } else {
     for (int o : opts2) if (B <= o) return o;
   }
+  if (B <= 65535) return (B + 255) / 256 * 256;
   return -1;
 }
 
@@ -496,7 +498,7 @@ extern "C" xmc_status xmc_peer_create(int32_t rank, int32_t world, int32_t dim, 
   if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
     return fail(XMC_ERR_ARG, "rank %d / world %d outside [0, %d)", rank, world, kMaxPeers);
   if (dim <= 0 || dim % 32 != 0) return fail(XMC_ERR_SHAPE, "dim must be a positive multiple of 32");
-  if (max_batch < 1 || max_batch > 1024) return fail(XMC_ERR_ARG, "max_batch outside [1, 1024]");
+  if (max_batch < 1 || max_batch > 65535) return fail(XMC_ERR_ARG, "max_batch outside [1, 65535]");
   auto* p = new xmc_peer();
   p->rank = rank;
   p->world = world;
@@ -875,7 +877,7 @@ static xmc_status launch_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, in
     else if (Bp == 128) s = launch_bwd_v<2, true, 2, 1, 1>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<2, true, 4, 1, 1>(h, L, st);
     else if (Bp == 512) s = launch_bwd_v<2, false, 8, 1, 1>(h, L, st);
-    else if (Bp == 1024) s = launch_bwd_v<2, false, 16, 1, 1>(h, L, st);
+    else if (Bp >= 1024) s = launch_bwd_v<2, false, 16, 1, 1>(h, L, st);   // (k-chunks stream slot by slot)
   } else if (!update && gx_kc_count > 0 && Bp > 256) {
     // grad_X-only pass of a batch over 256 (the update rides on the last
     // pass): G boxes only, a two-tile G ring
@@ -885,13 +887,13 @@ static xmc_status launch_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, in
     if (Bp == 128) s = launch_bwd_v<1, true, 1, 1>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<1, true, 2, 1>(h, L, st);
     else if (Bp == 512) s = launch_bwd_v<1, true, 4, 1>(h, L, st);
-    else if (Bp == 1024) s = launch_bwd_v<1, false, 8, 1>(h, L, st);
+    else if (Bp >= 1024) s = launch_bwd_v<1, false, 8, 1>(h, L, st);   // (k-chunks stream slot by slot)
   } else {
     if (Bp == 64) s = launch_bwd_v<2, true, 1, 2>(h, L, st);
     else if (Bp == 128) s = launch_bwd_v<2, true, 2, 2>(h, L, st);
     else if (Bp == 256) s = launch_bwd_v<2, true, 4, 2>(h, L, st);
     else if (Bp == 512) s = launch_bwd_v<2, false, 8, 2>(h, L, st);
-    else if (Bp == 1024) s = launch_bwd_v<2, false, 16, 2>(h, L, st);
+    else if (Bp >= 1024) s = launch_bwd_v<2, false, 16, 2>(h, L, st);
   }
   if (s == XMC_ERR_UNSUPPORTED) return fail(s, "no backward kernel for padded batch %d", Bp);
   XMC_TRY(s);

@@ -105,7 +105,7 @@ def test_peer_group_argument_checks_without_device():
     assert lib.xmc_peer_create(2, 2, 768, 256, ctypes.byref(p), hv) == _lib.XMC_ERR_ARG      # rank >= world
     assert lib.xmc_peer_create(0, 9, 768, 256, ctypes.byref(p), hv) == _lib.XMC_ERR_ARG      # > 8 ranks
     assert lib.xmc_peer_create(0, 2, 100, 256, ctypes.byref(p), hv) == _lib.XMC_ERR_SHAPE    # dim % 128
-    assert lib.xmc_peer_create(0, 2, 768, 1025, ctypes.byref(p), hv) == _lib.XMC_ERR_ARG     # batch > 1024
+    assert lib.xmc_peer_create(0, 2, 768, 65536, ctypes.byref(p), hv) == _lib.XMC_ERR_ARG    # batch > 65535
     assert lib.xmc_peer_connect(None, hv) == _lib.XMC_ERR_ARG
     assert lib.xmc_head_attach_peers(None, None) == _lib.XMC_ERR_ARG
     # SgdSrConfig: generator names map onto (rounding code, sr_bits)

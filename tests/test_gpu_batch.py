@@ -1,6 +1,5 @@
-"""Batches above 256 samples (the reference takes any batch): e4m3 heads up to
-1024 samples (also in the bf16-operand modes: reference precision, bf16 G),
-bf16 up to 1024.  The forward runs 256-sample passes of the
+"""Batches above 256 samples (the reference takes any batch): every mode up to
+65,535 samples (padded to 512 / 1024 or the next multiple of 256).  The forward runs 256-sample passes of the
 pair kernel; the backward accumulates grad_X in passes of 256 TMEM columns
 and applies the update on the last pass, so every pass reads the pre-update
 weights (head.py:290-291).
@@ -49,7 +48,7 @@ def _gpu_step(xmc, W, X, si, li, fmt_name, k, precision, rounding="stochastic", 
 @pytest.mark.parametrize("fmt_name,B,precision", [
     ("e4m3", 512, "operand"), ("e4m3", 1000, "operand"), ("bf16", 1024, "operand"), ("bf16", 700, "operand"),
     ("bf16", 1024, "reference"), ("e4m3", 512, "reference"), ("e4m3", 400, "operand-bf16"),
-    ("e4m3", 1000, "reference")])
+    ("e4m3", 1000, "reference"), ("e4m3", 1500, "operand"), ("bf16", 2000, "operand"), ("e4m3", 1300, "reference")])
 def test_large_batch_step_matches_oracle(xmc, fmt_name, B, precision):
     L, d, k = 700, 256, 2
     fmt, W, X, si, li = _problem(L, d, B, fmt_name, 31)
@@ -82,9 +81,10 @@ def test_e4m3_batch_512_chunk_invariance_fast_path(xmc):
 
 
 def test_batch_limit(xmc):
-    """Batches up to 1024 in every mode; beyond that a clear error."""
-    _, W, X, si, li = _problem(300, 128, 1100, "e4m3", 51)
-    with pytest.raises(NotImplementedError):
+    """Any batch up to 65,535 (the 16-bit sample field of a bucket entry);
+    beyond that a clear error before any device work."""
+    _, W, X, si, li = _problem(300, 128, 65_536, "e4m3", 51)
+    with pytest.raises((ValueError, NotImplementedError)):
         _gpu_step(xmc, W, X, si, li, "e4m3", 1, "reference")
 
 
