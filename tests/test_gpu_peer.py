@@ -66,7 +66,7 @@ def _worker(rank, world, port, fmt_name, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fmt_name,world", [("e4m3", 2), ("bf16", 2), ("e4m3", 3)])
+@pytest.mark.parametrize("fmt_name,world", [("e4m3", 2), ("bf16", 2), ("e4m3", 3), ("e4m3", 8)])
 def test_peer_allreduce_ranks(tmp_path, fmt_name, world):
     mp.spawn(_worker, args=(world, _free_port(), fmt_name, str(tmp_path)), nprocs=world, join=True)
     r = [torch.load(os.path.join(tmp_path, f"rank{k}.pt")) for k in range(world)]

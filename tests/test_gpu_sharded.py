@@ -81,7 +81,7 @@ def _worker(rank, world, port, fmt_name, peer, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fmt_name,world,peer", [("e4m3", 2, True), ("e4m3", 3, False), ("bf16", 2, True)])
+@pytest.mark.parametrize("fmt_name,world,peer", [("e4m3", 2, True), ("e4m3", 3, False), ("bf16", 2, True), ("e4m3", 4, True)])
 def test_sharded_gpu_step_matches_single_process(tmp_path, fmt_name, world, peer):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
