@@ -59,10 +59,12 @@ def summarize(path):
                     v /= 1000.0
                 elif u == "byte":
                     v /= 1e6
-                elif u == "msecond" and k == "duration_us":
+                elif u in ("msecond", "ms") and k == "duration_us":
                     v *= 1000.0
-                elif u == "nsecond" and k == "duration_us":
+                elif u in ("nsecond", "ns") and k == "duration_us":
                     v /= 1000.0
+                elif u in ("second", "s") and k == "duration_us":
+                    v *= 1e6
                 if k == "dram_TBps":
                     v = v if u == "Tbyte/s" else (v / 1000.0 if u == "Gbyte/s" else v)
                 if k == "sm_clock_mhz":
