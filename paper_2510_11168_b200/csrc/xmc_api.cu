@@ -266,6 +266,7 @@ struct xmc_head {
   int64_t* chunk_dev;  // [k+1] chunk starts (local rows) + [k+1] tile bases
   int32_t* status;     // [4]
   int R_step;          // grad_X partial slots written by the current step's backward
+  int64_t g_row_off = 0;  // first G buffer row of the next backward launch (a sub-range of the chunk)
   uint8_t* xq_topk;    // Xq rows of the current top-k launch (sample offset applied)
   uint8_t* wm;         // [max_chunk_rows + 128][d] masked W chunk (dropout only)
   uint32_t* keep;      // [max_chunk_rows + 128][d / 32] dropout keep bits (dropout only)
@@ -761,7 +762,7 @@ static xmc_status setup_bwd(xmc_head* h, void* Wc, void* comp, int64_t row0, int
   XMC_TRY(make_map(&L->tws, Wc, h->eb, D, rows, D, 32));
   const int64_t tiles = cdiv(rows, 128);
   const int R = static_cast<int>(std::min<int64_t>(h->R, tiles));
-  XMC_TRY(make_map(&L->tg, h->gbuf, beb, ldg, rows, ldg, 128));
+  XMC_TRY(make_map(&L->tg, h->gbuf + h->g_row_off * ldg * beb, beb, ldg, rows, ldg, 128));
   XMC_TRY(make_map(&L->tx, h->xqt, beb, Bp, D, Bp, 128));
   BwdParams& p = L->p;
   p = BwdParams{};
@@ -926,11 +927,28 @@ static xmc_status run_backward(xmc_head* h, void* Wc, void* comp, int64_t row0, 
 // The backward of one chunk (local rows [r0, r0 + rows)), G in gbuf:
 // grad_X partials from Wgx (W, or the masked dropout copy at its chunk base)
 // and, if update, the update of W (dW masked by keep under dropout).
+static xmc_status zero_gx_ws(xmc_head* h, int Bp, cudaStream_t st);
+
 static xmc_status chunk_backward(xmc_head* h, void* W, const void* Wgx, void* comp, int64_t r0, int64_t rows,
                                  int Bp, bool gx, bool update, bool gx_overwrite, const xmc_step_args* a,
                                  cudaStream_t st, const uint32_t* keep = nullptr, float drop_scale = 1.0f) {
   const int D = h->desc.dim, eb = h->eb;
   uint8_t* Wr = static_cast<uint8_t*>(W) + r0 * D * eb;
+  // top-p% head-Kahan whose compensated prefix ends inside this chunk: the
+  // rows without a compensation run first on the plain kernel (their W and G
+  // are the ones the forward left in L2), then the prefix on the Kahan one
+  const int64_t ce = h->comp_rows;
+  if (gx && update && comp && keep == nullptr && Wgx == Wr && ce > r0 && ce < r0 + rows) {
+    const int64_t rb = r0 + rows - ce;
+    const bool ow_b = gx_overwrite && cdiv(rb, 128) >= h->R_step;
+    if (gx_overwrite && !ow_b) XMC_TRY(zero_gx_ws(h, Bp, st));
+    h->g_row_off = ce - r0;
+    const xmc_status sb = run_backward(h, static_cast<uint8_t*>(W) + ce * D * eb, comp, ce, rb, Bp, true, true, ow_b,
+                                       a, st);
+    h->g_row_off = 0;
+    XMC_TRY(sb);
+    return run_backward(h, Wr, comp, r0, ce - r0, Bp, true, true, false, a, st);
+  }
   if (Wgx == Wr || !gx) return run_backward(h, Wr, comp, r0, rows, Bp, gx, update, gx_overwrite, a, st, keep, drop_scale);
   XMC_TRY(run_backward(h, const_cast<void*>(Wgx), nullptr, r0, rows, Bp, true, false, gx_overwrite, a, st));
   return update ? launch_bwd(h, Wr, comp, r0, rows, Bp, true, 0, 0, false, a, st, keep, drop_scale) : XMC_OK;
