@@ -16,7 +16,7 @@ L, d = 3000, 256
 bad = 0
 for fmt_name, prec, gfmt, kahan, drop, B, rounding in itertools.product(
         ["e4m3", "bf16"], ["operand", "reference"], ["e5m2", "e4m3", "bf16"], [None, "bf16", "fp32"],
-        [0.0, 0.2], [100, 256, 512], ["stochastic", "nearest"]):
+        [0.0, 0.2], [100, 256, 512, 1500], ["stochastic", "nearest"]):
     if fmt_name == "bf16" and gfmt != "e5m2":
         continue   # a bf16 head's G is always bf16
     if prec == "reference" and gfmt != "e5m2":
