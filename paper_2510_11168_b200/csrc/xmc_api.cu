@@ -1156,7 +1156,11 @@ __global__ void __launch_bounds__(256) topk_merge_kernel(const float* __restrict
                                                          int64_t* __restrict__ out_l) {
   __shared__ float ss[256 * kTopK];
   __shared__ int32_t sl[256 * kTopK];
-  const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int s = blockIdx.x, tid = threadIdx.x;
+  // every (CTA, warp) slot list arrives sorted (descending, ties by label):
+  // thread t merges slots t, t + 256, ... with two-pointer merges
+  const float* a = cs + static_cast<size_t>(s) * nslots * kTopK;
+  const int32_t* b = cl + static_cast<size_t>(s) * nslots * kTopK;
   float ls[kTopK];
   int32_t ll[kTopK];
 #pragma unroll
@@ -1164,47 +1168,74 @@ __global__ void __launch_bounds__(256) topk_merge_kernel(const float* __restrict
     ls[i] = -INFINITY;
     ll[i] = 0x7fffffff;
   }
-  const int n = nslots * kTopK;
-  const float* a = cs + static_cast<size_t>(s) * n;
-  const int32_t* b = cl + static_cast<size_t>(s) * n;
-  for (int i = tid; i < n; i += blockDim.x) topk_insert(ls, ll, a[i], b[i]);
+  for (int sl0 = tid; sl0 < nslots; sl0 += blockDim.x) {
+    float bs[kTopK];
+    int32_t bl[kTopK];
+#pragma unroll
+    for (int i = 0; i < kTopK; ++i) {
+      bs[i] = a[sl0 * kTopK + i];
+      bl[i] = b[sl0 * kTopK + i];
+    }
+    float ms[kTopK];
+    int32_t ml[kTopK];
+    int ia = 0, ib = 0;
+#pragma unroll
+    for (int i = 0; i < kTopK; ++i) {
+      // (register arrays indexed by the merge cursors: selects over the 8 entries)
+      float av = -INFINITY, bv = -INFINITY;
+      int32_t al = 0x7fffffff, blv = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < kTopK; ++j) {
+        if (j == ia) { av = ls[j]; al = ll[j]; }
+        if (j == ib) { bv = bs[j]; blv = bl[j]; }
+      }
+      const bool ta = !topk_better(bv, blv, av, al);
+      ms[i] = ta ? av : bv;
+      ml[i] = ta ? al : blv;
+      ia += ta ? 1 : 0;
+      ib += ta ? 0 : 1;
+    }
+#pragma unroll
+    for (int i = 0; i < kTopK; ++i) {
+      ls[i] = ms[i];
+      ll[i] = ml[i];
+    }
+  }
 #pragma unroll
   for (int i = 0; i < kTopK; ++i) {
     ss[tid * kTopK + i] = ls[i];
     sl[tid * kTopK + i] = ll[i];
   }
   __syncthreads();
-  if (tid >= 32) return;
-  // warp 0: lane l folds the lists of threads l, l+32, ... into its own
-  for (int t = tid + 32; t < blockDim.x; t += 32)
-    for (int i = 0; i < kTopK; ++i) topk_insert(ls, ll, ss[t * kTopK + i], sl[t * kTopK + i]);
-  // k rounds of a warp-wide best-of-heads selection
-  int head = 0;
-  for (int r = 0; r < k; ++r) {
-    float v = -INFINITY;
-    int32_t lv = 0x7fffffff;
+  // tree of pairwise merges in shared memory (8 levels of "top kTopK of two
+  // sorted lists") instead of one warp folding 256 lists serially
+  for (int w = blockDim.x >> 1; w >= 1; w >>= 1) {
+    if (tid < w) {
+      const int a0 = tid * kTopK, b0 = (tid + w) * kTopK;
+      float ms[kTopK];
+      int32_t ml[kTopK];
+      int ia = 0, ib = 0;
 #pragma unroll
-    for (int i = 0; i < kTopK; ++i)
-      if (i == head) {
-        v = ls[i];
-        lv = ll[i];
+      for (int i = 0; i < kTopK; ++i) {
+        const float av = ss[a0 + ia], bv = ss[b0 + ib];
+        const int32_t al = sl[a0 + ia], bl = sl[b0 + ib];
+        const bool ta = !topk_better(bv, bl, av, al);   // ties keep A (labels are unique)
+        ms[i] = ta ? av : bv;
+        ml[i] = ta ? al : bl;
+        ia += ta ? 1 : 0;
+        ib += ta ? 0 : 1;
       }
-    float bv = v;
-    int32_t bl = lv;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int32_t ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      if (topk_better(ov, ol, bv, bl)) {
-        bv = ov;
-        bl = ol;
+      for (int i = 0; i < kTopK; ++i) {
+        ss[a0 + i] = ms[i];
+        sl[a0 + i] = ml[i];
       }
     }
-    if (v == bv && lv == bl) ++head;   // labels are unique: exactly one lane owns the winner
-    if (lane == 0) {
-      out_s[static_cast<size_t>(s) * k + r] = bv;
-      out_l[static_cast<size_t>(s) * k + r] = bl;
-    }
+    __syncthreads();
+  }
+  if (tid < k) {
+    out_s[static_cast<size_t>(s) * k + tid] = ss[tid];
+    out_l[static_cast<size_t>(s) * k + tid] = sl[tid];
   }
 }
 
