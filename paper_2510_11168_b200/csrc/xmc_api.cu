@@ -1314,16 +1314,20 @@ extern "C" xmc_status xmc_head_topk(xmc_head_t h, const void* W, const float* X,
       }
       return r == XMC_ERR_UNSUPPORTED ? fail(r, "no top-k kernel for padded batch %d", Bp) : r;
     };
-    // Prologue on every 32nd work unit (a strided label sample): its top-8
+    // Prologue on every 16th work unit (a strided label sample): its top-8
     // per sample bounds the final 8th score from below, so the full pass
     // skips almost every block in its pre-filter (the lists of one warp see
     // too few labels to warm up on their own)
-    // (stride sweep at C4, same box: 8 / 16 / 32 / 64 / none = 0.697 / 0.657 /
-    // 0.644 / 0.669 / 0.93 ms)
-    constexpr int kPreStride = 32;
+    // (the prologue keeps only each list's maximum; stride sweep at C4, same
+    // box: 4 / 8 / 16 / 32 = 0.590 / 0.546 / 0.533 / 0.541 ms)
+#ifndef XMC_TOPK_PRESTRIDE
+#define XMC_TOPK_PRESTRIDE 16
+#endif
+    constexpr int kPreStride = XMC_TOPK_PRESTRIDE;
     if (p.num_tiles >= 1024) {
       FwdParams q = p;
       q.unit_mul = kPreStride;
+      q.topk_max_only = 1;
       XMC_TRY(run(q));
       topk_merge_kernel<<<p.B, 256, 0, st>>>(p.cand_s, p.cand_l, nslots, kTopK, h->topk_pre_s, h->topk_pre_l);
       CUDA_TRY(cudaGetLastError());

@@ -68,6 +68,7 @@ struct FwdParams {
   int32_t* cand_l;
   int32_t unit_mul;          // TOPK prologue: only every unit_mul-th work unit (a strided label sample)
   const float* topk_bound;   // TOPK: [B][8] top-8 scores of that sample (slot 7 <= the final 8th), or null
+  int32_t topk_max_only;     // TOPK prologue: each lane list keeps only the maximum score of its labels
   int64_t label0;            // global label of local row 0 of this launch
   int32_t* status;           // nonzero abort bits -> no-op; NaN logits latch ST 4
   int32_t sample0;           // first sample of this pass (batch split into BN-wide passes); entries of
@@ -380,6 +381,27 @@ XMC_DEV void fwd_body(const CUtensorMap& tm_w, const CUtensorMap& tm_x, const Fw
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, r);
         tmem_ld_wait();
+        if (p.topk_max_only) {
+          // prologue: only a lower bound is needed.  The maxima of disjoint
+          // label groups are distinct scores, so the 8th largest of them
+          // cannot exceed the final 8th score.  Column max over the warp's
+          // 32 rows by a reduce-scatter butterfly (lane c ends with sample
+          // col0 + c): 31 shuffles instead of the 80 of the transpose.
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = lane < vrows ? __uint_as_float(r[i]) : -INFINITY;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < o; ++i) {
+              const float recv = __shfl_xor_sync(0xffffffffu, up ? v[i] : v[i + o], o);
+              v[i] = fmaxf(up ? v[i + o] : v[i], recv);
+            }
+          }
+          ls[cc][0] = fmaxf(ls[cc][0], v[0]);
+          continue;
+        }
         {
           // lane = row here: r[c] = score(row, sample col0 + c)
           bool cand = false;
