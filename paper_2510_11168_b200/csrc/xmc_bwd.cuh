@@ -744,40 +744,52 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // groups per accumulator: the column groups of one plane (reference
     // precision with N = 128 groups); group gi writes columns (gi % gpp) x N
     const int gpp = p.gx_cols / (gsz * C::kBoxK) > 0 ? p.gx_cols / (gsz * C::kBoxK) : 1;
+    // Lean bookkeeping (the reference-precision backward issues 12 k-chunks a
+    // tile and was bound by this warp's instruction stream, ~230 instructions
+    // per k-chunk with runtime divisions): descriptors are affine in the smem
+    // address (built once, advanced by byte offset >> 4) and the group /
+    // window positions are running counters instead of % and /.
+    const uint64_t dG0 = umma_desc_sw128(smem_u32(k_s), 16, 1024);                  // dW A: G, K-major
+    const uint64_t dX0 = XT_RES ? umma_desc_sw128(smem_u32(xt_s), 16, 1024)         // dW B: Xq^T, K-major
+                                : umma_desc_sw128(smem_u32(k_s) + C::kBox, 16, 1024);
+    const uint64_t dGt0 = umma_desc_sw128(smem_u32(k_s), C::kKSlot, 1024);          // grad_X B: G, MN-major
+    int win_pos = 0, win_idx = 0;   // it % gx_win, it / gx_win
     for (int it = 0; it < (FAST ? 0 : ntl); ++it) {
       mbar_wait(&w_full[ws], wph);
       mbar_wait(&t_empty[ds], dph ^ 1);
       tc_fence_after();
       // grad_X A operand: the W stage, or (kW8) the bf16 tile the epilogue converted
       const uint32_t w_addr = C::kW8 ? smem_u32(op_s) : smem_u32(w_s + ws * C::kWStride);
+      const uint64_t dA0 = umma_desc_sw128(w_addr, C::kBox, 1024);                  // grad_X A: W^T, MN-major
       const uint32_t d_dw = tmem_base + ds * 128;
       bool op_ready = !C::kW8;
+      // a new accumulation window starts once the epilogue drained the last one
+      const bool fresh = win_pos == 0;
+      int gpos = 0, gi = 0, gcol = 0;   // gk % gsz, gk / gsz, (gk / gsz) % gpp
+      bool gpast = false;               // gk / gsz >= gpp
       int xk = kb;   // Xq^T k-chunk of G k-chunk kc (the planes repeat it)
       while (xk >= p.xt_kc) xk -= p.xt_kc;
       for (int kc = kb; kc < ke; ++kc) {
         mbar_wait(&k_full[ks], kph);
         const int gk = kc - p.gx_kc0;
         const bool in_gx = do_gx && gk >= 0 && gk < p.gx_kc_count;
-        const bool gx_last = in_gx && gk % gsz == gsz - 1;   // a grad_X group's G boxes are all in
+        const bool gx_last = in_gx && gpos == gsz - 1;   // a grad_X group's G boxes are all in
         if (C::kW8 && gx_last && !op_ready) {
           mbar_wait(op_full, static_cast<uint32_t>(it) & 1u);
           op_ready = true;
         }
-        // a new accumulation window starts once the epilogue drained the last one
-        const bool fresh = it % gx_win == 0;
-        if (gx_last && fresh && it > 0 && gk < gsz)   // the window's first group
-          mbar_wait(gxw_empty, static_cast<uint32_t>(it / gx_win - 1) & 1u);
+        if (gx_last && fresh && it > 0 && gi == 0)   // the window's first group
+          mbar_wait(gxw_empty, static_cast<uint32_t>(win_idx - 1) & 1u);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t g_addr = smem_u32(k_s + ks * C::kKSlot);
-          const uint32_t x_addr = XT_RES ? smem_u32(xt_s + xk * C::kBox) : g_addr + C::kBox;
           if (p.do_update) {
+            const uint64_t ad = dG0 + ((static_cast<uint32_t>(ks) * C::kKSlot) >> 4);
+            const uint64_t bd = dX0 + (XT_RES ? ((static_cast<uint32_t>(xk) * C::kBox) >> 4)
+                                              : ((static_cast<uint32_t>(ks) * C::kKSlot) >> 4));
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              const uint64_t ad = umma_desc_sw128(g_addr + k * 32, 16, 1024);
-              const uint64_t bd = umma_desc_sw128(x_addr + k * 32, 16, 1024);
-              if constexpr (EB == 1) mma_f8(d_dw, ad, bd, idesc_dw, (kc | k) != 0);
-              else mma_f16(d_dw, ad, bd, idesc_dw, (kc | k) != 0);
+              if constexpr (EB == 1) mma_f8(d_dw, ad + 2 * k, bd + 2 * k, idesc_dw, (kc | k) != 0);
+              else mma_f16(d_dw, ad + 2 * k, bd + 2 * k, idesc_dw, (kc | k) != 0);
             }
           }
           // dW complete -> hand it to the update epilogue before the grad_X
@@ -790,25 +802,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           // W (A operand) is then read from smem once per group.  Groups of
           // the reference-precision planes accumulate into the same columns.
           if (gx_last) {
-            const int gi = gk / gsz;
-            const bool acc0 = !fresh || gi >= gpp;
-            const uint32_t d_gx = tmem_gx + (gi % gpp) * gsz * C::kBoxK;
-            const int s0 = ks - gk % gsz;   // ring slot of the group's first k-chunk
+            const bool acc0 = !fresh || gpast;
+            const uint32_t d_gx = tmem_gx + gcol * gsz * C::kBoxK;
+            const int s0 = ks - gpos;   // ring slot of the group's first k-chunk
             if (s0 >= 0) {
-              const uint32_t g0 = smem_u32(k_s + s0 * C::kKSlot);
+              const uint64_t bd0 = dGt0 + ((static_cast<uint32_t>(s0) * C::kKSlot) >> 4);
 #pragma unroll
               for (int k = 0; k < 128 / C::kKmma; ++k) {
-                const uint64_t ad = umma_desc_sw128(w_addr + k * C::kKmma * 128, C::kBox, 1024);
-                const uint64_t bd = umma_desc_sw128(g0 + k * C::kKmma * 128, C::kKSlot, 1024);
-                if constexpr (EB == 1) mma_f8(d_gx, ad, bd, idesc_gx, acc0 || k != 0);
-                else mma_f16(d_gx, ad, bd, idesc_gx, acc0 || k != 0);
+                constexpr uint32_t kStep = (C::kKmma * 128) >> 4;   // K rows of one MMA, MN-major
+                if constexpr (EB == 1) mma_f8(d_gx, dA0 + k * kStep, bd0 + k * kStep, idesc_gx, acc0 || k != 0);
+                else mma_f16(d_gx, dA0 + k * kStep, bd0 + k * kStep, idesc_gx, acc0 || k != 0);
               }
               for (int s = s0; s <= ks; ++s) mma_commit(&k_empty[s]);
             } else {
               // the group wraps around the ring: one N = kBoxK MMA group per
               // k-chunk into its TMEM columns
               const uint32_t idesc_c = umma_idesc(xf, gf, true, true, 128, C::kBoxK);
-              for (int c = 0; c <= gk % gsz; ++c) {
+              for (int c = 0; c <= gpos; ++c) {
                 const int sc = s0 + c < 0 ? s0 + c + KS : s0 + c;
                 const uint32_t gc = smem_u32(k_s + sc * C::kKSlot);
 #pragma unroll
@@ -829,16 +839,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (!(C::kOutBuf || C::kW8) && kc == ke - 1) mma_commit(&t_full[ds]);
         }
         __syncwarp();
+        if (in_gx && ++gpos == gsz) {
+          gpos = 0;
+          ++gi;
+          if (++gcol == gpp) { gcol = 0; gpast = true; }
+        }
         if (++xk == p.xt_kc) xk = 0;
         if (++ks == KS) { ks = 0; kph ^= 1; }
       }
+      if (++win_pos == gx_win) { win_pos = 0; ++win_idx; }   // now (it + 1) % gx_win, (it + 1) / gx_win
       if (elect_one()) {
         if constexpr (C::kW8) {
           if (conv) mma_commit(op_empty);   // the stage itself is released by the epilogue
         } else {
           mma_commit(&w_empty[ws]);
         }
-        if (do_gx && (it + 1) % gx_win == 0 && it + 1 < ntl) mma_commit(gxw_full);
+        if (do_gx && win_pos == 0 && it + 1 < ntl) mma_commit(gxw_full);
       }
       __syncwarp();
       if (++ws == WS) { ws = 0; wph ^= 1; }
