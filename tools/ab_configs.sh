@@ -1,0 +1,11 @@
+#!/usr/bin/env bash
+# Same-box A/B of library builds over the other BASELINE shapes / modes.
+#   tools/ab_configs.sh "base cur"
+libs=${1:?tags}
+for cfg in "c2:--labels 131073 --batch 512 --fmt bf16" "c3:--labels 670091" "c5r0:--labels 1077981 --batch 128" "c4b512:--batch 512" "c4kahan_top10:--kahan bf16 --kahan-labels 281228" "c4kahan_all:--kahan bf16" "c4kahan_fp32:--kahan fp32" "c4ref_rtn:--precision reference --rounding nearest"; do
+  t=${cfg%%:*}; args=${cfg#*:}
+  for l in $libs; do
+    XMC_LIB_PATH=paper_2510_11168_b200/libxmc_b200_$l.so timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu --ref-steps 0 --bf16g-steps 0 --e2e-steps 2 $args 2>/dev/null | tail -1 | \
+      python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$l', '$t', round(d['value']), round(d['ms_per_step'],4), {k: round(v,4) for k,v in d['roofline']['step_kernel_ms'].items()})"
+  done
+done
