@@ -64,7 +64,7 @@ def parse():
                     help="top-p%% head-Kahan: only the first N (frequency-sorted) labels carry a compensation")
     ap.add_argument("--ref-steps", type=int, default=5,
                     help="timed steps of the reference-precision mode reported beside the headline (0: skip)")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--bf16g-steps", type=int, default=5,
                     help="timed steps of the bf16-G mode (the paper's BF16 logit gradients) reported beside "
                          "the headline (0: skip)")
