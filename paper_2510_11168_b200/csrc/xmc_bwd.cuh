@@ -754,6 +754,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                 : umma_desc_sw128(smem_u32(k_s) + C::kBox, 16, 1024);
     const uint64_t dGt0 = umma_desc_sw128(smem_u32(k_s), C::kKSlot, 1024);          // grad_X B: G, MN-major
     int win_pos = 0, win_idx = 0;   // it % gx_win, it / gx_win
+    // groups of two k-chunks cover the whole tile from k-chunk 0, never wrap
+    // the ring and never straddle an Xq^T plane boundary
+    const bool pair_groups = gsz == 2 && do_gx && p.do_update && kb == 0 && p.gx_kc0 == 0 &&
+                             p.gx_kc_count == ke && ke % 2 == 0 && KS % 2 == 0 && p.xt_kc % 2 == 0;
     for (int it = 0; it < (FAST ? 0 : ntl); ++it) {
       mbar_wait(&w_full[ws], wph);
       mbar_wait(&t_empty[ds], dph ^ 1);
@@ -769,7 +773,65 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       bool gpast = false;               // gk / gsz >= gpp
       int xk = kb;   // Xq^T k-chunk of G k-chunk kc (the planes repeat it)
       while (xk >= p.xt_kc) xk -= p.xt_kc;
-      for (int kc = kb; kc < ke; ++kc) {
+      if (pair_groups) {
+        // every k-chunk in a grad_X group of two (reference-precision planes,
+        // bf16 G of an e4m3 head): one pass per group, i.e. half the waits,
+        // fences, elections and counter updates per MMA of the loop below;
+        // same MMAs, same order per accumulator, same commits
+        for (int kc = 0; kc < ke; kc += 2) {
+          mbar_wait(&k_full[ks], kph);
+          mbar_wait(&k_full[ks + 1], kph);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              const uint64_t ad = dG0 + ((static_cast<uint32_t>(ks + b) * C::kKSlot) >> 4);
+              const uint64_t bd = dX0 + (XT_RES ? ((static_cast<uint32_t>(xk + b) * C::kBox) >> 4)
+                                                : ((static_cast<uint32_t>(ks + b) * C::kKSlot) >> 4));
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                if constexpr (EB == 1) mma_f8(d_dw, ad + 2 * k, bd + 2 * k, idesc_dw, ((kc + b) | k) != 0);
+                else mma_f16(d_dw, ad + 2 * k, bd + 2 * k, idesc_dw, ((kc + b) | k) != 0);
+              }
+            }
+            if ((C::kOutBuf || C::kW8) && kc + 2 == ke) mma_commit(&t_full[ds]);
+          }
+          __syncwarp();
+          // the grad_X group: the operand tile converted (kW8), the window's
+          // accumulator drained (first group of a window)
+          if (C::kW8 && !op_ready) {
+            mbar_wait(op_full, static_cast<uint32_t>(it) & 1u);
+            op_ready = true;
+            tc_fence_after();
+          }
+          if (fresh && it > 0 && gi == 0) {
+            mbar_wait(gxw_empty, static_cast<uint32_t>(win_idx - 1) & 1u);
+            tc_fence_after();
+          }
+          if (elect_one()) {
+            const bool acc0 = !fresh || gpast;
+            const uint32_t d_gx = tmem_gx + gcol * 2 * C::kBoxK;
+            const uint64_t bd0 = dGt0 + ((static_cast<uint32_t>(ks) * C::kKSlot) >> 4);
+#pragma unroll
+            for (int k = 0; k < 128 / C::kKmma; ++k) {
+              constexpr uint32_t kStep = (C::kKmma * 128) >> 4;
+              if constexpr (EB == 1) mma_f8(d_gx, dA0 + k * kStep, bd0 + k * kStep, idesc_gx, acc0 || k != 0);
+              else mma_f16(d_gx, dA0 + k * kStep, bd0 + k * kStep, idesc_gx, acc0 || k != 0);
+            }
+            mma_commit(&k_empty[ks]);
+            mma_commit(&k_empty[ks + 1]);
+            if (!(C::kOutBuf || C::kW8) && kc + 2 == ke) mma_commit(&t_full[ds]);
+          }
+          __syncwarp();
+          ++gi;
+          if (++gcol == gpp) { gcol = 0; gpast = true; }
+          xk += 2;
+          if (xk == p.xt_kc) xk = 0;
+          ks += 2;
+          if (ks == KS) { ks = 0; kph ^= 1; }
+        }
+      }
+      for (int kc = pair_groups ? ke : kb; kc < ke; ++kc) {
         mbar_wait(&k_full[ks], kph);
         const int gk = kc - p.gx_kc0;
         const bool in_gx = do_gx && gk >= 0 && gk < p.gx_kc_count;
